@@ -1,0 +1,55 @@
+# Build for the B200-native curve-alignment library (sm_100a only).
+#   make            -> product library + harness + oracle (+ reference oracle if /root/reference exists)
+#   make lib        -> paper_2501_17779_b200/libcurvalign_cuda.so
+NVCC     ?= /usr/local/cuda/bin/nvcc
+CXX      ?= g++
+ARCH     := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+PKG      := paper_2501_17779_b200
+CSRC     := $(PKG)/csrc
+BUILD    := build
+REF      ?= /root/reference
+
+KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h include/curvalign_cuda.h
+
+.PHONY: all lib synth dropin oracle ref clean
+all: lib synth oracle ref
+
+lib: $(PKG)/libcurvalign_cuda.so
+synth: $(PKG)/libcurvalign_synth.so
+dropin: $(PKG)/libcurvalign.so
+
+$(BUILD)/kernels.o: $(CSRC)/kernels.cu $(KERNEL_HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_kernels.log || (cat $(BUILD)/ptxas_kernels.log; exit 1)
+
+$(BUILD)/capi.o: $(CSRC)/capi.cpp $(CSRC)/kernels.h include/curvalign_cuda.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(BUILD)/probe.o: $(CSRC)/probe.cu include/curvalign_cuda.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/capi.o $(BUILD)/probe.o
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
+
+# Synthetic workload generators (bench harness; host only).
+$(PKG)/libcurvalign_synth.so: $(CSRC)/synth.cpp
+	$(CXX) -O2 -std=c++20 -fPIC -shared -Wall -o $@ $< -lpthread
+
+# C++ drop-in for the reference API (namespace curvalign), on top of the C ABI.
+DROPIN_SRCS := $(wildcard $(CSRC)/dropin/*.cpp)
+$(PKG)/libcurvalign.so: $(DROPIN_SRCS) $(wildcard include/curvalign/*.hpp) $(PKG)/libcurvalign_cuda.so
+	$(CXX) -O2 -std=c++20 -fPIC -shared -Wall -Iinclude -o $@ $(DROPIN_SRCS) \
+	    -L$(PKG) -lcurvalign_cuda -Wl,-rpath,'$$ORIGIN'
+
+oracle:
+	$(MAKE) -C oracle oracle
+
+ref:
+	@if [ -d $(REF)/proj/src ]; then $(MAKE) -C oracle ref REF=$(REF); else echo "reference sources absent: using prebuilt oracle/_ref if present"; fi
+
+clean:
+	rm -rf $(BUILD) $(PKG)/*.so
+	$(MAKE) -C oracle clean

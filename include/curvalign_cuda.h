@@ -1,0 +1,149 @@
+/* curvalign_cuda.h — C ABI of the B200-native (sm_100a) curve-alignment library
+ * libcurvalign_cuda.so (paper_2501_17779_b200/).
+ *
+ * This is the drop-in boundary for the reference's hot path (arXiv 2501.17779,
+ * "FFT-based alignment of 2d closed curves"; reference C++ API in
+ * /root/reference/proj/include/curvalign/). Plain pointers and sizes only: no
+ * C++ or torch types cross it. The C++ API of the reference (namespace
+ * curvalign: align_fft, preprocess, resample_uniform, srv_transform, ...) is
+ * re-declared in the include/curvalign/ headers and implemented on top of these entry
+ * points (paper_2501_17779_b200/csrc/dropin.cpp); INTEGRATION.md shows the
+ * ctypes / C++ bindings a maintainer adds.
+ *
+ * Data layout. A curve of n nodes is n interleaved (x, y) doubles — the layout
+ * of curvalign::Point2 (proj/include/curvalign/geometry.hpp:9-33) and of
+ * std::span<const Point2>::data(), so reference buffers pass through unchanged.
+ * Batches are contiguous: pairs * n * 2 doubles. Ragged batches of raw curves
+ * use an offsets array: curve c is points [offsets[c], offsets[c+1]).
+ *
+ * Conventions (identical to the reference):
+ *  - shift m pairs c1[l] with c2[(l + m) mod N]            rigid_align.hpp:12-13
+ *  - rotation R(theta) = [[cos, sin], [-sin, cos]] (clockwise); the aligned
+ *    curve is aligned[l] = R(theta) c2[(l + shift) mod N]    geometry.hpp:48-73
+ *  - best shift = smallest m with |D_m| >= max|D| - 1e-12 max(1, max|D|),
+ *    D_m = sum_l conj(z1_l) z2_{(l+m) mod N}                 rigid_align.cpp:31-47
+ *  - energy = max(0, h (|c1|^2 + |c2|^2) - 2 h trace), h = 1/N  rigid_align.cpp:56-59
+ *
+ * Errors. Every entry point returns a cva_status. Batched device entry points
+ * validate what they can on the host (CVA_INVALID_ARGUMENT) and report
+ * data-dependent failures per pair in cva_alignment.status (e.g. coincident
+ * adjacent nodes -> CVA_INVALID_ARGUMENT, as proj/src/curve.cpp:58 throws),
+ * with NaN theta/energy for that pair, like distance_matrix's NaN cells
+ * (proj/src/elastic.cpp:210-217). cva_last_error() returns a thread-local
+ * message for the last failing call on the calling thread.
+ *
+ * Streams. `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ * stream). Device entry points are asynchronous on that stream; *_host entry
+ * points are synchronous. All entry points are thread-safe (the twiddle-table
+ * cache is guarded per device).
+ */
+#ifndef CURVALIGN_CUDA_H
+#define CURVALIGN_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CVA_ABI_VERSION 1
+
+typedef enum cva_status {
+  CVA_OK = 0,
+  CVA_INVALID_ARGUMENT = 1, /* reference throws std::invalid_argument */
+  CVA_RUNTIME_ERROR = 2,    /* reference throws std::runtime_error (singular spline) */
+  CVA_BAD_ALLOC = 3,        /* reference throws std::bad_alloc */
+  CVA_CUDA_ERROR = 4,       /* no device / launch failure / kernel fault */
+  CVA_UNSUPPORTED = 5       /* size outside what this build's kernels cover */
+} cva_status;
+
+/* One alignment result; mirrors curvalign::RigidAlignment
+ * (proj/include/curvalign/rigid_align.hpp:16-23). 48 bytes. */
+typedef struct cva_alignment {
+  int64_t shift;      /* m */
+  double t0;          /* m / N */
+  double theta;       /* Rotation2 angle, (-pi, pi] */
+  double trace;       /* tr(R A^T) at the optimum = |D_m| */
+  double energy;      /* mismatch energy */
+  int32_t degenerate; /* rotation underdetermined (D_m == 0) */
+  int32_t status;     /* cva_status of this pair */
+} cva_alignment;
+
+int cva_abi_version(void);
+const char* cva_last_error(void);
+/* Number of visible CUDA devices (0 when none); never fails. */
+int cva_device_count(void);
+/* Largest raw node count a single curve may have in the resampling kernels. */
+int64_t cva_max_resample_nodes(void);
+
+/* ---------------------------------------------------------------------------
+ * Hot-path batch entry points (device pointers, asynchronous on `stream`).
+ * ------------------------------------------------------------------------- */
+
+/* align_fft over a batch of pre-sampled pairs (proj/src/rigid_align.cpp:204-208).
+ * c1, c2: pairs x n points. out: pairs results. aligned (nullable): pairs x n
+ * points, aligned[l] = R c2[(l + shift) mod n]. Requires n >= 4. */
+int cva_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                    cva_alignment* out, double* aligned, void* stream);
+
+/* preprocess (proj/src/curve.cpp:93-97) of a ragged batch of raw curves.
+ * resample != 0: periodic-cubic-spline arc-length resampling to n_out nodes,
+ * then center, then normalize; out is curves x n_out points.
+ * resample == 0: center + normalize only; out has the input's ragged layout.
+ * max_n_in: largest curve size in the batch (host-known; bounds shared memory).
+ * status (nullable): per-curve cva_status. */
+int cva_preprocess_batch(const double* points, const int64_t* offsets, int64_t curves,
+                         int64_t max_n_in, int64_t n_out, int resample, double* out,
+                         int32_t* status, void* stream);
+
+/* resample_uniform (proj/src/curve.cpp:67-91) of a ragged batch: periodic cubic
+ * spline through the raw nodes on chordal arc length, sampled at t_l = l/n_out.
+ * No centering / normalisation. out is curves x n_out points. */
+int cva_resample_batch(const double* points, const int64_t* offsets, int64_t curves,
+                       int64_t max_n_in, int64_t n_out, double* out, int32_t* status,
+                       void* stream);
+
+/* Fused C1 path: pair p = (curve 2p, curve 2p+1) of the ragged raw batch;
+ * preprocess both to n_out nodes (resample != 0) then align_fft. aligned
+ * (nullable): pairs x n_out points. */
+int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int64_t pairs,
+                               int64_t max_n_in, int64_t n_out, int resample,
+                               cva_alignment* out, double* aligned, void* stream);
+
+/* SRV-space alignment: align_fft(srv_center(srv_transform(c1)).q,
+ * srv_center(srv_transform(c2)).q) (proj/src/srv.cpp:71-98; the (t0,R) step
+ * pattern of proj/src/elastic.cpp:138-139). aligned_q (nullable): the rotated,
+ * shifted centered SRV of c2. Requires n >= 8. */
+int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                        cva_alignment* out, double* aligned_q, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Host-buffer entry points (synchronous; host <-> device copies included).
+ * These are what the C++ drop-in API (include/curvalign/ headers) calls.
+ * ------------------------------------------------------------------------- */
+
+int cva_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                         cva_alignment* out, double* aligned);
+int cva_preprocess_batch_host(const double* points, const int64_t* offsets, int64_t curves,
+                              int64_t n_out, int resample, double* out, int32_t* status);
+int cva_resample_batch_host(const double* points, const int64_t* offsets, int64_t curves,
+                            int64_t n_out, double* out, int32_t* status);
+int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets, int64_t pairs,
+                                    int64_t n_out, int resample, cva_alignment* out,
+                                    double* aligned);
+int cva_srv_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                             cva_alignment* out, double* aligned_q);
+
+/* ---------------------------------------------------------------------------
+ * Diagnostics (not on the hot path).
+ * ------------------------------------------------------------------------- */
+
+/* Measured FP64 FMA throughput of the current device (dependent DFMA chains,
+ * 8 per thread, CUDA-event timed), for the FP64 roofline denominator. */
+int cva_probe_fp64_tflops(double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CURVALIGN_CUDA_H */

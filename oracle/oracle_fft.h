@@ -1,0 +1,31 @@
+/* TEST INFRASTRUCTURE ONLY — CPU oracle (see oracle/README.md). Never linked into
+ * the product library.
+ *
+ * Plain-C complex DFT of any length n, used (a) by the FFTW-API shim that lets
+ * the reference's own sources compile (oracle/shim/fftw3.h) and (b) by the C
+ * restatement of the reference's FFT correlation (oracle/curvalign_oracle.c).
+ *
+ *   sign = -1:  X[k] = sum_j x[j] exp(-2 pi i j k / n)     (forward, unnormalised)
+ *   sign = +1:  x[j] = sum_k X[k] exp(+2 pi i j k / n)     (backward, unnormalised)
+ *
+ * Power-of-two n: iterative radix-2 with directly evaluated twiddles.
+ * Other n: Bluestein chirp-z over a power-of-two convolution.
+ */
+#ifndef CURVALIGN_ORACLE_FFT_H
+#define CURVALIGN_ORACLE_FFT_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* In-place transform of n interleaved complex values (re, im). Returns 0 on
+ * success, -1 on allocation failure. */
+int offt_dft(double* data, size_t n, int sign);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

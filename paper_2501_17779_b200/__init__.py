@@ -1,0 +1,39 @@
+"""B200-native (sm_100a) batched FFT alignment of closed planar curves.
+
+A from-scratch GPU implementation of the hot path of arXiv 2501.17779
+("FFT-based alignment of 2d closed curves"): arc-length spline resampling ->
+center/normalize -> FFT cross-correlation over all cyclic shifts -> tie-broken
+argmax -> rotation, energy and aligned curve, plus the SRV-space variant.
+The compute lives in libcurvalign_cuda.so (hand-written CUDA for sm_100a behind
+the C ABI in include/curvalign_cuda.h); this package is the Python host mirror
+of the reference's API (proj/include/curvalign/*.hpp).
+"""
+from .api import (  # noqa: F401
+    RigidAlignment,
+    align_fft,
+    align_fft_batch,
+    aligned_curve,
+    decode_results,
+    preprocess,
+    preprocess_align_batch,
+    preprocess_batch,
+    ragged,
+    resample_batch,
+    resample_uniform,
+    srv_align_batch,
+)
+
+__all__ = [
+    "RigidAlignment",
+    "align_fft",
+    "align_fft_batch",
+    "aligned_curve",
+    "decode_results",
+    "preprocess",
+    "preprocess_align_batch",
+    "preprocess_batch",
+    "ragged",
+    "resample_batch",
+    "resample_uniform",
+    "srv_align_batch",
+]

@@ -1,0 +1,288 @@
+"""Python host mirror of the reference's alignment API over the C ABI.
+
+Names and argument meaning follow /root/reference/proj/include/curvalign/:
+``align_fft`` (rigid_align.hpp:44-51), ``preprocess`` (curve.hpp:47-48),
+``srv_transform``/``srv_center`` pattern (srv.hpp:23-27). Errors map to the
+exception classes the reference throws (std::invalid_argument -> ValueError,
+std::runtime_error -> RuntimeError, std::bad_alloc -> MemoryError).
+
+Two calling conventions:
+
+* numpy arrays (host memory): the synchronous ``*_host`` C entry points copy
+  to the GPU, run the kernels and copy back;
+* torch CUDA tensors (device memory): the asynchronous device entry points run
+  on torch's current stream; results stay on the device.
+
+Curves are ``(n, 2)`` float64 arrays (x, y) — the byte layout of
+``curvalign::Point2`` — and batches are ``(pairs, n, 2)``.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from ._native import ALIGNMENT_DTYPE, check
+
+try:  # torch is plumbing only (device memory + streams)
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+
+@dataclass
+class RigidAlignment:
+    """Mirror of curvalign::RigidAlignment (rigid_align.hpp:16-23)."""
+
+    shift: int
+    t0: float
+    theta: float
+    trace: float
+    energy: float
+    degenerate: bool
+
+
+def _is_cuda_tensor(x) -> bool:
+    return torch is not None and isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _f64c(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a is not None and a.size else (a.ctypes.data if a is not None else 0)
+
+
+def _tptr(t) -> int:
+    return 0 if t is None else t.data_ptr()
+
+
+def _stream_of(t) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def decode_results(raw) -> np.ndarray:
+    """Alignment results (device tensor of bytes or numpy buffer) -> structured array."""
+    if _is_cuda_tensor(raw):
+        raw = raw.cpu().numpy()
+    return np.frombuffer(np.ascontiguousarray(raw).tobytes(), dtype=ALIGNMENT_DTYPE)
+
+
+def _result_from_record(r) -> RigidAlignment:
+    return RigidAlignment(
+        shift=int(r["shift"]),
+        t0=float(r["t0"]),
+        theta=float(r["theta"]),
+        trace=float(r["trace"]),
+        energy=float(r["energy"]),
+        degenerate=bool(r["degenerate"]),
+    )
+
+
+def _raise_pair_status(res: np.ndarray) -> None:
+    bad = np.nonzero(res["status"] != 0)[0]
+    if bad.size:
+        st = int(res["status"][bad[0]])
+        msg = f"pair {int(bad[0])}: status {st}"
+        if st == _native.CVA_INVALID_ARGUMENT:
+            raise ValueError(msg)
+        if st == _native.CVA_RUNTIME_ERROR:
+            raise RuntimeError(msg)
+        raise _native.CurvalignError(msg)
+
+
+# --------------------------------------------------------------- align_fft
+
+
+def align_fft_batch(c1, c2, return_aligned: bool = False):
+    """align_fft over a batch of pre-sampled pairs (rigid_align.cpp:204-208).
+
+    c1, c2: ``(pairs, n, 2)`` float64, numpy (host) or CUDA tensor (device).
+    Returns ``(results, aligned)``: a structured array (host) or a ``(pairs, 48)``
+    uint8 device tensor (decode with :func:`decode_results`), and the aligned
+    curves ``R c2[(l + shift) mod n]`` or None.
+    """
+    lib = _native.load()
+    if _is_cuda_tensor(c1):
+        if c1.shape != c2.shape or c1.dim() != 3 or c1.shape[2] != 2:
+            raise ValueError("align: node count mismatch")
+        c1 = c1.contiguous().to(torch.float64)
+        c2 = c2.contiguous().to(torch.float64)
+        pairs, n = c1.shape[0], c1.shape[1]
+        out = torch.empty((pairs, 48), dtype=torch.uint8, device=c1.device)
+        al = torch.empty_like(c2) if return_aligned else None
+        check(lib.cva_align_batch(c1.data_ptr(), c2.data_ptr(), pairs, n, out.data_ptr(),
+                                  _tptr(al), _stream_of(c1)))
+        return out, al
+    a, b = _f64c(c1), _f64c(c2)
+    if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 2:
+        raise ValueError("align: node count mismatch")
+    pairs, n = a.shape[0], a.shape[1]
+    res = np.zeros(pairs, dtype=ALIGNMENT_DTYPE)
+    al = np.empty_like(b) if return_aligned else None
+    check(lib.cva_align_batch_host(_ptr(a), _ptr(b), pairs, n, res.ctypes.data,
+                                   al.ctypes.data if al is not None else 0))
+    return res, al
+
+
+def align_fft(c1, c2) -> RigidAlignment:
+    """Single-pair drop-in for curvalign::align_fft (rigid_align.hpp:45,50)."""
+    a, b = _f64c(c1), _f64c(c2)
+    if a.ndim != 2 or b.ndim != 2 or a.shape[0] != b.shape[0]:
+        raise ValueError("align: node count mismatch")
+    res, _ = align_fft_batch(a[None], b[None])
+    _raise_pair_status(res)
+    return _result_from_record(res[0])
+
+
+def aligned_curve(c1, c2):
+    """align_fft plus the aligned second curve R c2[(l + shift) mod N]."""
+    a, b = _f64c(c1), _f64c(c2)
+    if a.ndim != 2 or b.ndim != 2 or a.shape[0] != b.shape[0]:
+        raise ValueError("align: node count mismatch")
+    res, al = align_fft_batch(a[None], b[None], return_aligned=True)
+    _raise_pair_status(res)
+    return _result_from_record(res[0]), al[0]
+
+
+# -------------------------------------------------------------- preprocess
+
+
+def ragged(curves) -> tuple[np.ndarray, np.ndarray]:
+    """List of (n_i, 2) arrays -> (points (sum n_i, 2), offsets (len+1,) int64)."""
+    offs = np.zeros(len(curves) + 1, dtype=np.int64)
+    for i, c in enumerate(curves):
+        offs[i + 1] = offs[i] + np.asarray(c).shape[0]
+    pts = np.concatenate([_f64c(c).reshape(-1, 2) for c in curves]) if curves else np.zeros((0, 2))
+    return np.ascontiguousarray(pts), offs
+
+
+def preprocess_batch(points, offsets, n_out: int, resample: bool = True, max_n_in: int = 0):
+    """preprocess (curve.cpp:93-97) of a ragged batch: returns (curves, status).
+
+    numpy inputs: curves is ``(count, n_out, 2)`` (resample) or the input's
+    ragged ``(total, 2)`` layout (no resample). CUDA tensors: same on device.
+    """
+    lib = _native.load()
+    if _is_cuda_tensor(points):
+        count = offsets.shape[0] - 1
+        total = points.shape[0]
+        out = torch.empty((count, n_out, 2) if resample else (total, 2), dtype=torch.float64,
+                          device=points.device)
+        st = torch.empty(count, dtype=torch.int32, device=points.device)
+        check(lib.cva_preprocess_batch(points.data_ptr(), offsets.data_ptr(), count, int(max_n_in),
+                                       int(n_out), 1 if resample else 0, out.data_ptr(),
+                                       st.data_ptr(), _stream_of(points)))
+        return out, st
+    pts = _f64c(points)
+    offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    count = offs.shape[0] - 1
+    out = np.empty((count, n_out, 2) if resample else pts.shape, dtype=np.float64)
+    st = np.zeros(count, dtype=np.int32)
+    check(lib.cva_preprocess_batch_host(_ptr(pts), offs.ctypes.data, count, int(n_out),
+                                        1 if resample else 0, out.ctypes.data, st.ctypes.data))
+    return out, st
+
+
+def preprocess(curve, n_out: int, resample: bool = True) -> np.ndarray:
+    """Drop-in for curvalign::preprocess (curve.hpp:47-48): (n, 2) -> (n_out or n, 2)."""
+    c = _f64c(curve)
+    if c.ndim != 2 or c.shape[1] != 2:
+        raise ValueError("curve: expected (n, 2) nodes")
+    if resample and n_out < 8:
+        raise ValueError("resample: need at least 8 output nodes")
+    pts, offs = ragged([c])
+    out, st = preprocess_batch(pts, offs, n_out, resample)
+    if st[0] == _native.CVA_INVALID_ARGUMENT:
+        raise ValueError("curve: invalid input (too few / non-finite / coincident nodes)")
+    if st[0] != 0:
+        raise RuntimeError(f"preprocess: status {int(st[0])}")
+    return out[0] if resample else out
+
+
+def resample_batch(points, offsets, n_out: int, max_n_in: int = 0):
+    """resample_uniform (curve.cpp:67-91) of a ragged batch: returns (curves, status)."""
+    lib = _native.load()
+    if _is_cuda_tensor(points):
+        count = offsets.shape[0] - 1
+        out = torch.empty((count, n_out, 2), dtype=torch.float64, device=points.device)
+        st = torch.empty(count, dtype=torch.int32, device=points.device)
+        check(lib.cva_resample_batch(points.data_ptr(), offsets.data_ptr(), count, int(max_n_in),
+                                     int(n_out), out.data_ptr(), st.data_ptr(), _stream_of(points)))
+        return out, st
+    pts = _f64c(points)
+    offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    count = offs.shape[0] - 1
+    out = np.empty((count, n_out, 2), dtype=np.float64)
+    st = np.zeros(count, dtype=np.int32)
+    check(lib.cva_resample_batch_host(_ptr(pts), offs.ctypes.data, count, int(n_out),
+                                      out.ctypes.data, st.ctypes.data))
+    return out, st
+
+
+def resample_uniform(curve, n_out: int) -> np.ndarray:
+    """Drop-in for curvalign::resample_uniform (curve.hpp:44-45)."""
+    c = _f64c(curve)
+    if c.ndim != 2 or c.shape[1] != 2:
+        raise ValueError("curve: expected (n, 2) nodes")
+    if n_out < 8:
+        raise ValueError("resample: need at least 8 output nodes")
+    pts, offs = ragged([c])
+    out, st = resample_batch(pts, offs, n_out)
+    if st[0] == _native.CVA_INVALID_ARGUMENT:
+        raise ValueError("curve: invalid input (too few / non-finite / coincident nodes)")
+    if st[0] != 0:
+        raise RuntimeError(f"resample: status {int(st[0])}")
+    return out[0]
+
+
+def preprocess_align_batch(points, offsets, n_out: int, max_n_in: int = 0,
+                           return_aligned: bool = False):
+    """Fused C1 path: pair p = (curve 2p, curve 2p+1): preprocess both to n_out
+    nodes and align. Returns (results, aligned) like :func:`align_fft_batch`."""
+    lib = _native.load()
+    if _is_cuda_tensor(points):
+        pairs = (offsets.shape[0] - 1) // 2
+        out = torch.empty((pairs, 48), dtype=torch.uint8, device=points.device)
+        al = (torch.empty((pairs, n_out, 2), dtype=torch.float64, device=points.device)
+              if return_aligned else None)
+        check(lib.cva_preprocess_align_batch(points.data_ptr(), offsets.data_ptr(), pairs,
+                                             int(max_n_in), int(n_out), 1, out.data_ptr(),
+                                             _tptr(al), _stream_of(points)))
+        return out, al
+    pts = _f64c(points)
+    offs = np.ascontiguousarray(np.asarray(offsets, dtype=np.int64))
+    pairs = (offs.shape[0] - 1) // 2
+    res = np.zeros(pairs, dtype=ALIGNMENT_DTYPE)
+    al = np.empty((pairs, n_out, 2)) if return_aligned else None
+    check(lib.cva_preprocess_align_batch_host(_ptr(pts), offs.ctypes.data, pairs, int(n_out), 1,
+                                              res.ctypes.data,
+                                              al.ctypes.data if al is not None else 0))
+    return res, al
+
+
+def srv_align_batch(c1, c2, return_aligned: bool = False):
+    """SRV-space alignment: align_fft(srv_center(srv_transform(c1)).q,
+    srv_center(srv_transform(c2)).q) per pair (srv.cpp:71-98, elastic.cpp:138-139)."""
+    lib = _native.load()
+    if _is_cuda_tensor(c1):
+        c1 = c1.contiguous()
+        c2 = c2.contiguous()
+        pairs, n = c1.shape[0], c1.shape[1]
+        out = torch.empty((pairs, 48), dtype=torch.uint8, device=c1.device)
+        al = torch.empty_like(c2) if return_aligned else None
+        check(lib.cva_srv_align_batch(c1.data_ptr(), c2.data_ptr(), pairs, n, out.data_ptr(),
+                                      _tptr(al), _stream_of(c1)))
+        return out, al
+    a, b = _f64c(c1), _f64c(c2)
+    if a.shape != b.shape or a.ndim != 3:
+        raise ValueError("srv: size mismatch")
+    pairs, n = a.shape[0], a.shape[1]
+    res = np.zeros(pairs, dtype=ALIGNMENT_DTYPE)
+    al = np.empty_like(b) if return_aligned else None
+    check(lib.cva_srv_align_batch_host(_ptr(a), _ptr(b), pairs, n, res.ctypes.data,
+                                       al.ctypes.data if al is not None else 0))
+    return res, al

@@ -1,0 +1,365 @@
+// extern "C" entry points of libcurvalign_cuda.so (declared in include/curvalign_cuda.h).
+//
+// Host-side validation mirrors the reference's std::invalid_argument checks
+// (proj/src/rigid_align.cpp:18-21, proj/src/curve.cpp:10-15, :68-69,
+// proj/src/srv.cpp:72); data-dependent failures are reported per pair by the
+// kernels. There is no CPU fallback: without a CUDA device every compute entry
+// point fails with CVA_CUDA_ERROR.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/curvalign_cuda.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+  g_last_error = msg;
+  return status;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(CVA_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// Twiddle tables w_N^k, one per (device, N), built once and kept for the process.
+std::mutex g_tw_mu;
+std::map<std::pair<int, int>, double2*> g_tw;
+
+int get_twiddles(int n, cudaStream_t stream, const double2** out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(g_tw_mu);
+  auto it = g_tw.find({dev, n});
+  if (it != g_tw.end()) {
+    *out = it->second;
+    return CVA_OK;
+  }
+  double2* tw = nullptr;
+  e = cudaMalloc(&tw, sizeof(double2) * (size_t)n);
+  if (e != cudaSuccess) return fail(CVA_BAD_ALLOC, "twiddle table allocation failed");
+  e = cva::launch_tw_init(tw, n, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e != cudaSuccess) {
+    cudaFree(tw);
+    return cuda_fail(e, "twiddle init");
+  }
+  g_tw[{dev, n}] = tw;
+  *out = tw;
+  return CVA_OK;
+}
+
+int require_device() {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) return fail(CVA_CUDA_ERROR, "no CUDA device available");
+  return CVA_OK;
+}
+
+int smem_limit() {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  return v;
+}
+
+// FFT sizes the shared-memory kernels cover in this build.
+int check_fft_size(int64_t n) {
+  if (n < 4) return fail(CVA_INVALID_ARGUMENT, "align: need at least 4 nodes");
+  if (!is_pow2(n) || n > 2048)
+    return fail(CVA_UNSUPPORTED, "align: this build's shared-memory FFT covers N = 2^p <= 2048");
+  return CVA_OK;
+}
+
+int check_resample_nmax(int64_t nmax, int64_t n_out, size_t smem) {
+  if (nmax > cva::max_chunked_nodes() || smem > (size_t)smem_limit())
+    return fail(CVA_UNSUPPORTED, "resample: curve has more raw nodes than the shared-memory "
+                                 "resampler holds (n_in=" + std::to_string(nmax) +
+                                     ", n_out=" + std::to_string(n_out) + ")");
+  return CVA_OK;
+}
+
+int64_t host_max_n(const int64_t* offsets, int64_t curves) {
+  int64_t m = 0;
+  for (int64_t c = 0; c < curves; ++c) m = std::max(m, offsets[c + 1] - offsets[c]);
+  return m;
+}
+
+int device_max_n(const int64_t* d_offsets, int64_t curves, cudaStream_t s, int64_t* out) {
+  std::vector<int64_t> h((size_t)curves + 1);
+  cudaError_t e = cudaMemcpyAsync(h.data(), d_offsets, sizeof(int64_t) * h.size(),
+                                  cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "offsets D2H");
+  *out = host_max_n(h.data(), curves);
+  return CVA_OK;
+}
+
+int finish(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  return CVA_OK;
+}
+
+// RAII device buffer for the *_host entry points.
+struct DevBuf {
+  void* p = nullptr;
+  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int cva_abi_version(void) { return CVA_ABI_VERSION; }
+
+const char* cva_last_error(void) { return g_last_error.c_str(); }
+
+int cva_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int64_t cva_max_resample_nodes(void) { return cva::max_chunked_nodes(); }
+
+int cva_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                    cva_alignment* out, double* aligned, void* stream) {
+  if (int rc = check_fft_size(n)) return rc;
+  if (pairs < 0) return fail(CVA_INVALID_ARGUMENT, "align: negative pair count");
+  if (pairs == 0) return CVA_OK;
+  if (!c1 || !c2 || !out) return fail(CVA_INVALID_ARGUMENT, "align: null pointer");
+  if (int rc = require_device()) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const double2* tw = nullptr;
+  if (int rc = get_twiddles((int)n, s, &tw)) return rc;
+  return finish(cva::launch_align((const double2*)c1, (const double2*)c2, pairs, (int)n, tw, out,
+                                  (double2*)aligned, s),
+                "align launch");
+}
+
+int cva_preprocess_batch(const double* points, const int64_t* offsets, int64_t curves,
+                         int64_t max_n_in, int64_t n_out, int resample, double* out,
+                         int32_t* status, void* stream) {
+  if (curves < 0) return fail(CVA_INVALID_ARGUMENT, "preprocess: negative curve count");
+  if (curves == 0) return CVA_OK;
+  if (!points || !offsets || !out) return fail(CVA_INVALID_ARGUMENT, "preprocess: null pointer");
+  if (resample && n_out < 8)
+    return fail(CVA_INVALID_ARGUMENT, "resample: need at least 8 output nodes");
+  if (int rc = require_device()) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!resample)
+    return finish(cva::launch_preprocess_center((const double2*)points, offsets, curves,
+                                                (double2*)out, status, s),
+                  "preprocess launch");
+  if (max_n_in <= 0)
+    if (int rc = device_max_n(offsets, curves, s, &max_n_in)) return rc;
+  const int nmax = (int)std::max<int64_t>(max_n_in, 4);
+  if (int rc = check_resample_nmax(nmax, n_out, cva::resample_smem_bytes(nmax, (int)n_out)))
+    return rc;
+  return finish(cva::launch_preprocess_resample((const double2*)points, offsets, curves, nmax,
+                                                (int)n_out, 1, (double2*)out, status, s),
+                "preprocess launch");
+}
+
+int cva_resample_batch(const double* points, const int64_t* offsets, int64_t curves,
+                       int64_t max_n_in, int64_t n_out, double* out, int32_t* status,
+                       void* stream) {
+  if (curves < 0) return fail(CVA_INVALID_ARGUMENT, "resample: negative curve count");
+  if (curves == 0) return CVA_OK;
+  if (!points || !offsets || !out) return fail(CVA_INVALID_ARGUMENT, "resample: null pointer");
+  if (n_out < 8) return fail(CVA_INVALID_ARGUMENT, "resample: need at least 8 output nodes");
+  if (int rc = require_device()) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (max_n_in <= 0)
+    if (int rc = device_max_n(offsets, curves, s, &max_n_in)) return rc;
+  const int nmax = (int)std::max<int64_t>(max_n_in, 4);
+  if (int rc = check_resample_nmax(nmax, n_out, cva::resample_smem_bytes(nmax, (int)n_out)))
+    return rc;
+  return finish(cva::launch_preprocess_resample((const double2*)points, offsets, curves, nmax,
+                                                (int)n_out, 0, (double2*)out, status, s),
+                "resample launch");
+}
+
+int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int64_t pairs,
+                               int64_t max_n_in, int64_t n_out, int resample, cva_alignment* out,
+                               double* aligned, void* stream) {
+  if (pairs < 0) return fail(CVA_INVALID_ARGUMENT, "align: negative pair count");
+  if (pairs == 0) return CVA_OK;
+  if (!points || !offsets || !out) return fail(CVA_INVALID_ARGUMENT, "align: null pointer");
+  if (!resample)
+    return fail(CVA_UNSUPPORTED,
+                "preprocess_align: resample=0 pairs have per-curve sizes; use "
+                "cva_preprocess_batch + cva_align_batch");
+  if (n_out < 8) return fail(CVA_INVALID_ARGUMENT, "resample: need at least 8 output nodes");
+  if (int rc = check_fft_size(n_out)) return rc;
+  if (int rc = require_device()) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (max_n_in <= 0)
+    if (int rc = device_max_n(offsets, 2 * pairs, s, &max_n_in)) return rc;
+  const int nmax = (int)std::max<int64_t>(max_n_in, 4);
+  if (int rc = check_resample_nmax(nmax, n_out,
+                                   cva::preprocess_align_smem_bytes(nmax, (int)n_out)))
+    return rc;
+  const double2* tw = nullptr;
+  if (int rc = get_twiddles((int)n_out, s, &tw)) return rc;
+  return finish(cva::launch_preprocess_align((const double2*)points, offsets, pairs, nmax,
+                                             (int)n_out, tw, out, (double2*)aligned, s),
+                "preprocess_align launch");
+}
+
+int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                        cva_alignment* out, double* aligned_q, void* stream) {
+  if (n < 8) return fail(CVA_INVALID_ARGUMENT, "curve: too few nodes");  // srv.cpp:72
+  if (int rc = check_fft_size(n)) return rc;
+  if (pairs < 0) return fail(CVA_INVALID_ARGUMENT, "srv: negative pair count");
+  if (pairs == 0) return CVA_OK;
+  if (!c1 || !c2 || !out) return fail(CVA_INVALID_ARGUMENT, "srv: null pointer");
+  if (int rc = require_device()) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const double2* tw = nullptr;
+  if (int rc = get_twiddles((int)n, s, &tw)) return rc;
+  return finish(cva::launch_srv_align((const double2*)c1, (const double2*)c2, pairs, (int)n, tw,
+                                      out, (double2*)aligned_q, s),
+                "srv_align launch");
+}
+
+// ------------------------------------------------------------- host entries
+
+int cva_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                         cva_alignment* out, double* aligned) {
+  if (int rc = check_fft_size(n)) return rc;
+  if (pairs <= 0) return pairs == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative pair count");
+  if (int rc = require_device()) return rc;
+  const size_t cb = sizeof(double) * 2 * (size_t)(pairs * n);
+  DevBuf d1, d2, dout, dal;
+  if (d1.alloc(cb) || d2.alloc(cb) || dout.alloc(sizeof(cva_alignment) * pairs) ||
+      (aligned && dal.alloc(cb)))
+    return fail(CVA_BAD_ALLOC, "device allocation failed");
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  if (int rc = cva_align_batch((const double*)d1.p, (const double*)d2.p, pairs, n,
+                               (cva_alignment*)dout.p, aligned ? (double*)dal.p : nullptr, s))
+    return rc;
+  e = cudaMemcpyAsync(out, dout.p, sizeof(cva_alignment) * pairs, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && aligned) e = cudaMemcpyAsync(aligned, dal.p, cb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return finish(e, "align_batch_host");
+}
+
+namespace {
+// resample: 0 = center+normalize, 1 = resample+center+normalize, 2 = resample only
+int preprocess_host_impl(const double* points, const int64_t* offsets, int64_t curves,
+                         int64_t n_out, int resample, double* out, int32_t* status) {
+  if (curves <= 0) return curves == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative curve count");
+  if (int rc = require_device()) return rc;
+  const int64_t total = offsets[curves] - offsets[0];
+  if (offsets[0] != 0) return fail(CVA_INVALID_ARGUMENT, "offsets[0] must be 0");
+  const size_t ib = sizeof(double) * 2 * (size_t)total;
+  const size_t ob = resample ? sizeof(double) * 2 * (size_t)(curves * n_out) : ib;
+  DevBuf dp, doff, dout, dst;
+  if (dp.alloc(ib) || doff.alloc(sizeof(int64_t) * (curves + 1)) || dout.alloc(ob) ||
+      dst.alloc(sizeof(int32_t) * curves))
+    return fail(CVA_BAD_ALLOC, "device allocation failed");
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaMemcpyAsync(dp.p, points, ib, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(doff.p, offsets, sizeof(int64_t) * (curves + 1), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  const int rc = resample == 2
+                     ? cva_resample_batch((const double*)dp.p, (const int64_t*)doff.p, curves,
+                                          host_max_n(offsets, curves), n_out, (double*)dout.p,
+                                          (int32_t*)dst.p, s)
+                     : cva_preprocess_batch((const double*)dp.p, (const int64_t*)doff.p, curves,
+                                            host_max_n(offsets, curves), n_out, resample,
+                                            (double*)dout.p, (int32_t*)dst.p, s);
+  if (rc) return rc;
+  e = cudaMemcpyAsync(out, dout.p, ob, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && status)
+    e = cudaMemcpyAsync(status, dst.p, sizeof(int32_t) * curves, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return finish(e, "preprocess_batch_host");
+}
+}  // namespace
+
+int cva_preprocess_batch_host(const double* points, const int64_t* offsets, int64_t curves,
+                              int64_t n_out, int resample, double* out, int32_t* status) {
+  return preprocess_host_impl(points, offsets, curves, n_out, resample ? 1 : 0, out, status);
+}
+
+int cva_resample_batch_host(const double* points, const int64_t* offsets, int64_t curves,
+                            int64_t n_out, double* out, int32_t* status) {
+  return preprocess_host_impl(points, offsets, curves, n_out, 2, out, status);
+}
+
+int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets, int64_t pairs,
+                                    int64_t n_out, int resample, cva_alignment* out,
+                                    double* aligned) {
+  if (pairs <= 0) return pairs == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative pair count");
+  if (int rc = require_device()) return rc;
+  if (offsets[0] != 0) return fail(CVA_INVALID_ARGUMENT, "offsets[0] must be 0");
+  const int64_t total = offsets[2 * pairs];
+  const size_t ib = sizeof(double) * 2 * (size_t)total;
+  const size_t ab = sizeof(double) * 2 * (size_t)(pairs * n_out);
+  DevBuf dp, doff, dout, dal;
+  if (dp.alloc(ib) || doff.alloc(sizeof(int64_t) * (2 * pairs + 1)) ||
+      dout.alloc(sizeof(cva_alignment) * pairs) || (aligned && dal.alloc(ab)))
+    return fail(CVA_BAD_ALLOC, "device allocation failed");
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaMemcpyAsync(dp.p, points, ib, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(doff.p, offsets, sizeof(int64_t) * (2 * pairs + 1), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  if (int rc = cva_preprocess_align_batch((const double*)dp.p, (const int64_t*)doff.p, pairs,
+                                          host_max_n(offsets, 2 * pairs), n_out, resample,
+                                          (cva_alignment*)dout.p, aligned ? (double*)dal.p : nullptr, s))
+    return rc;
+  e = cudaMemcpyAsync(out, dout.p, sizeof(cva_alignment) * pairs, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && aligned) e = cudaMemcpyAsync(aligned, dal.p, ab, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return finish(e, "preprocess_align_batch_host");
+}
+
+int cva_srv_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                             cva_alignment* out, double* aligned_q) {
+  if (n < 8) return fail(CVA_INVALID_ARGUMENT, "curve: too few nodes");
+  if (int rc = check_fft_size(n)) return rc;
+  if (pairs <= 0) return pairs == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative pair count");
+  if (int rc = require_device()) return rc;
+  const size_t cb = sizeof(double) * 2 * (size_t)(pairs * n);
+  DevBuf d1, d2, dout, dal;
+  if (d1.alloc(cb) || d2.alloc(cb) || dout.alloc(sizeof(cva_alignment) * pairs) ||
+      (aligned_q && dal.alloc(cb)))
+    return fail(CVA_BAD_ALLOC, "device allocation failed");
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  if (int rc = cva_srv_align_batch((const double*)d1.p, (const double*)d2.p, pairs, n,
+                                   (cva_alignment*)dout.p, aligned_q ? (double*)dal.p : nullptr, s))
+    return rc;
+  e = cudaMemcpyAsync(out, dout.p, sizeof(cva_alignment) * pairs, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && aligned_q)
+    e = cudaMemcpyAsync(aligned_q, dal.p, cb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return finish(e, "srv_align_batch_host");
+}
+
+}  // extern "C"

@@ -1,0 +1,344 @@
+// sm_100a kernels of the curve-alignment hot path and their host launchers.
+//
+//   tw_init_kernel              twiddle table w_N^k = exp(-2 pi i k / N) (sincospi)
+//   align_kernel                align_fft on pre-sampled pairs       (rigid_align.cpp:204-208)
+//   preprocess_resample_kernel  resample -> center -> normalize       (curve.cpp:93-97)
+//   preprocess_center_kernel    center -> normalize (resample=false)   (curve.cpp:93-97)
+//   preprocess_align_kernel     fused C1 path: both preprocesses + align_fft of one pair
+//   srv_align_kernel            srv_transform -> srv_center -> align_fft (srv.cpp:71-98)
+//
+// One CTA per pair (or per curve); all intermediate data stays in shared memory,
+// so each pair reads its raw input from HBM once and writes only its result and
+// aligned curve.
+#include <cuda_runtime.h>
+
+#include "../../include/curvalign_cuda.h"
+#include "align.cuh"
+#include "cva_common.cuh"
+#include "fft.cuh"
+#include "kernels.h"
+#include "spline.cuh"
+
+namespace cva {
+
+constexpr int kThreads = 256;
+constexpr int kRedSlots = 64;
+
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
+
+__global__ void tw_init_kernel(double2* tw, int N) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < N) {
+    double s, c;
+    // exp(-2 pi i k / N) = cospi(2k/N) - i sinpi(2k/N); 2k/N exact for N = 2^p
+    sincospi(2.0 * (double)k / (double)N, &s, &c);
+    tw[k] = make_double2(c, -s);
+  }
+}
+
+__device__ __forceinline__ void load_curve(const double2* __restrict__ g, double2* sm, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = __ldg(&g[i]);
+}
+
+__device__ __forceinline__ int block_any_nonfinite(const double2* sm, int n, double2* red) {
+  int bad = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double2 p = sm[i];
+    bad |= !(isfinite(p.x) && isfinite(p.y));
+  }
+  return block_or(bad, red);
+}
+
+// Shared-memory layout for resampling one curve of up to nmax raw nodes.
+struct ResampleSmem {
+  double2* xy;      // nmax
+  double* s;        // nmax + 1 (padded to even)
+  double2* m;       // nmax
+  ChunkEnds* ends;  // kThreads
+  static __host__ __device__ size_t bytes(int nmax) {
+    return sizeof(double2) * (size_t)nmax + sizeof(double) * (size_t)((nmax + 2) & ~1) +
+           sizeof(double2) * (size_t)nmax + sizeof(ChunkEnds) * kThreads;
+  }
+  __device__ void carve(char* base, int nmax) {
+    xy = reinterpret_cast<double2*>(base);
+    s = reinterpret_cast<double*>(xy + nmax);
+    m = reinterpret_cast<double2*>(s + ((nmax + 2) & ~1));
+    ends = reinterpret_cast<ChunkEnds*>(m + nmax);
+  }
+};
+
+// raw curve (global, n nodes) -> preprocess(raw, n_out, true) in out_sm.
+// Returns block-uniform status.
+__device__ inline int block_resample_preprocess(const double2* __restrict__ raw, int n, int n_out,
+                                                const ResampleSmem& R, double2* out_sm,
+                                                double2* red, bool center_normalize = true) {
+  if (n < 4 || n_out < 8) return kInvalid;  // validate_curve(c, 4), n_out >= 8 (curve.cpp:68-69)
+  load_curve(raw, R.xy, n);
+  __syncthreads();
+  int bad = block_any_nonfinite(R.xy, n, red);
+  if (bad) return kInvalid;
+  block_arc_length(R.xy, n, R.s, red, &bad);
+  if (bad) return kInvalid;
+  block_spline_solve(R.s, R.xy, R.m, n, R.ends, red);
+  block_spline_eval(R.s, R.xy, R.m, n, n_out, out_sm);
+  if (center_normalize) block_center_normalize(out_sm, n_out, red, &bad);
+  return bad ? kInvalid : kOk;
+}
+
+__device__ inline void write_bad_alignment(cva_alignment* out, int status) {
+  cva_alignment r;
+  r.shift = 0;
+  r.t0 = 0.0;
+  r.theta = qnan();
+  r.trace = qnan();
+  r.energy = qnan();
+  r.degenerate = 0;
+  r.status = status;
+  *out = r;
+}
+
+__device__ inline void fill_nan(double2* g, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) g[i] = make_double2(qnan(), qnan());
+}
+
+// ------------------------------------------------------------------ kernels
+
+__global__ void __launch_bounds__(kThreads) align_kernel(const double2* __restrict__ c1,
+                                                         const double2* __restrict__ c2, int N,
+                                                         const double2* __restrict__ tw,
+                                                         cva_alignment* __restrict__ out,
+                                                         double2* __restrict__ aligned) {
+  extern __shared__ __align__(16) char smem_raw[];
+  __shared__ double2 red[kRedSlots];
+  double2* A = reinterpret_cast<double2*>(smem_raw);
+  double2* B = A + N;
+  double2* C = B + N;
+  double2* D = C + N;
+  const int64_t p = blockIdx.x;
+  load_curve(c1 + p * N, A, N);
+  load_curve(c2 + p * N, B, N);
+  __syncthreads();
+  const double s1 = block_sum_norm2(A, N, red);
+  const double s2 = block_sum_norm2(B, N, red);
+  block_align_tail(A, B, C, D, N, tw, s1, s2, out + p, aligned ? aligned + p * N : nullptr, red);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    preprocess_resample_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off,
+                               int nmax, int n_out, int center_normalize,
+                               double2* __restrict__ out, int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) char smem_raw[];
+  __shared__ double2 red[kRedSlots];
+  ResampleSmem R;
+  R.carve(smem_raw, nmax);
+  double2* obuf = reinterpret_cast<double2*>(smem_raw + ResampleSmem::bytes(nmax));
+  const int64_t c = blockIdx.x;
+  const int64_t b0 = off[c];
+  const int n = (int)(off[c + 1] - b0);
+  const int st = block_resample_preprocess(pts + b0, n, n_out, R, obuf, red, center_normalize != 0);
+  double2* o = out + c * n_out;
+  if (st == kOk) {
+    for (int i = threadIdx.x; i < n_out; i += blockDim.x) o[i] = obuf[i];
+  } else {
+    fill_nan(o, n_out);
+  }
+  if (status && threadIdx.x == 0) status[c] = st;
+}
+
+// center + normalize in place in global memory (no resampling; any n >= 3).
+__global__ void __launch_bounds__(kThreads)
+    preprocess_center_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off,
+                             double2* __restrict__ out, int32_t* __restrict__ status) {
+  __shared__ double2 red[kRedSlots];
+  const int64_t c = blockIdx.x;
+  const int64_t b0 = off[c];
+  const int n = (int)(off[c + 1] - b0);
+  const double2* in = pts + b0;
+  double2* o = out + b0;
+  int bad = n < 3;  // validate_curve(c) default min_nodes = 3 (curve.hpp:29)
+  if (!bad) {
+    double2 acc = make_double2(0, 0);
+    int nf = 0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double2 q = __ldg(&in[i]);
+      nf |= !(isfinite(q.x) && isfinite(q.y));
+      acc = cadd(acc, q);
+    }
+    bad = block_or(nf, red);
+    acc = block_sum2(acc, red);
+    const double invn = 1.0 / (double)n;
+    const double2 g = make_double2(invn * acc.x, invn * acc.y);
+    double len = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double2 p0 = csub(__ldg(&in[i]), g), p1 = csub(__ldg(&in[i + 1 == n ? 0 : i + 1]), g);
+      const double dx = p1.x - p0.x, dy = p1.y - p0.y;
+      len += sqrt(fma(dx, dx, dy * dy));
+    }
+    len = block_sum(len, red);
+    bad |= !(len > 0.0);
+    if (!bad) {
+      const double sc = 1.0 / len;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) o[i] = cscale(csub(__ldg(&in[i]), g), sc);
+    }
+  }
+  if (bad) fill_nan(o, n > 0 ? n : 0);
+  if (status && threadIdx.x == 0) status[c] = bad ? kInvalid : kOk;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    preprocess_align_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off,
+                            int nmax, int N, const double2* __restrict__ tw,
+                            cva_alignment* __restrict__ out, double2* __restrict__ aligned) {
+  extern __shared__ __align__(16) char smem_raw[];
+  __shared__ double2 red[kRedSlots];
+  double2* Z1 = reinterpret_cast<double2*>(smem_raw);
+  double2* Z2 = Z1 + N;
+  char* work = reinterpret_cast<char*>(Z2 + N);  // resample arrays, later FFT scratch
+  ResampleSmem R;
+  R.carve(work, nmax);
+  const int64_t p = blockIdx.x;
+  const int64_t a0 = off[2 * p], a1 = off[2 * p + 1], b1 = off[2 * p + 2];
+  int st = block_resample_preprocess(pts + a0, (int)(a1 - a0), N, R, Z1, red);
+  if (st == kOk) st = block_resample_preprocess(pts + a1, (int)(b1 - a1), N, R, Z2, red);
+  double2* al = aligned ? aligned + p * N : nullptr;
+  if (st != kOk) {
+    if (threadIdx.x == 0) write_bad_alignment(out + p, st);
+    if (al) fill_nan(al, N);
+    return;
+  }
+  const double s1 = block_sum_norm2(Z1, N, red);
+  const double s2 = block_sum_norm2(Z2, N, red);
+  double2* W1 = reinterpret_cast<double2*>(work);
+  double2* W2 = W1 + N;
+  block_align_tail(Z1, Z2, W1, W2, N, tw, s1, s2, out + p, al, red);
+}
+
+// q_l = d_l / sqrt(|d_l|), d_l = (N/2)(c[l+1] - c[l-1]); 0 if |d_l| < 1e-8 N (srv.cpp:71-88)
+__device__ inline void block_srv(const double2* c, double2* q, int N) {
+  const double nn = (double)N;
+  const double eps = 1e-8 * nn;
+  for (int l = threadIdx.x; l < N; l += blockDim.x) {
+    const double2 nx = c[l + 1 == N ? 0 : l + 1], pv = c[l == 0 ? N - 1 : l - 1];
+    const double2 d = make_double2((nn / 2.0) * (nx.x - pv.x), (nn / 2.0) * (nx.y - pv.y));
+    const double mag = sqrt(fma(d.x, d.x, d.y * d.y));
+    q[l] = mag < eps ? make_double2(0.0, 0.0) : cscale(d, 1.0 / sqrt(mag));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) srv_align_kernel(const double2* __restrict__ c1,
+                                                             const double2* __restrict__ c2, int N,
+                                                             const double2* __restrict__ tw,
+                                                             cva_alignment* __restrict__ out,
+                                                             double2* __restrict__ aligned) {
+  extern __shared__ __align__(16) char smem_raw[];
+  __shared__ double2 red[kRedSlots];
+  double2* A = reinterpret_cast<double2*>(smem_raw);
+  double2* B = A + N;
+  double2* Q1 = B + N;
+  double2* Q2 = Q1 + N;
+  const int64_t p = blockIdx.x;
+  load_curve(c1 + p * N, A, N);
+  load_curve(c2 + p * N, B, N);
+  __syncthreads();
+  const int bad = block_any_nonfinite(A, N, red) | block_any_nonfinite(B, N, red);
+  double2* al = aligned ? aligned + p * N : nullptr;
+  if (bad) {
+    if (threadIdx.x == 0) write_bad_alignment(out + p, kInvalid);
+    if (al) fill_nan(al, N);
+    return;
+  }
+  block_srv(A, Q1, N);
+  block_srv(B, Q2, N);
+  __syncthreads();
+  // srv_center (srv.cpp:90-98)
+  double2 m1 = make_double2(0, 0), m2 = make_double2(0, 0);
+  for (int l = threadIdx.x; l < N; l += blockDim.x) {
+    m1 = cadd(m1, Q1[l]);
+    m2 = cadd(m2, Q2[l]);
+  }
+  m1 = block_sum2(m1, red);
+  m2 = block_sum2(m2, red);
+  const double invn = 1.0 / (double)N;
+  m1 = cscale(m1, invn);
+  m2 = cscale(m2, invn);
+  for (int l = threadIdx.x; l < N; l += blockDim.x) {
+    Q1[l] = csub(Q1[l], m1);
+    Q2[l] = csub(Q2[l], m2);
+  }
+  __syncthreads();
+  const double s1 = block_sum_norm2(Q1, N, red);
+  const double s2 = block_sum_norm2(Q2, N, red);
+  block_align_tail(Q1, Q2, A, B, N, tw, s1, s2, out + p, al, red);
+}
+
+// ------------------------------------------------------------ host launchers
+
+size_t align_smem_bytes(int N) { return 4 * sizeof(double2) * (size_t)N; }
+size_t resample_smem_bytes(int nmax, int n_out) {
+  return ResampleSmem::bytes(nmax) + sizeof(double2) * (size_t)n_out;
+}
+size_t preprocess_align_smem_bytes(int nmax, int N) {
+  const size_t work = ResampleSmem::bytes(nmax);
+  const size_t fft_scratch = 2 * sizeof(double2) * (size_t)N;
+  return 2 * sizeof(double2) * (size_t)N + (work > fft_scratch ? work : fft_scratch);
+}
+
+static cudaError_t set_smem(const void* fn, size_t bytes) {
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+cudaError_t launch_tw_init(double2* tw, int N, cudaStream_t s) {
+  tw_init_kernel<<<(N + 255) / 256, 256, 0, s>>>(tw, N);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_align(const double2* c1, const double2* c2, int64_t pairs, int N,
+                         const double2* tw, cva_alignment* out, double2* aligned, cudaStream_t s) {
+  const size_t sm = align_smem_bytes(N);
+  cudaError_t e = set_smem((const void*)align_kernel, sm);
+  if (e != cudaSuccess) return e;
+  align_kernel<<<(unsigned)pairs, kThreads, sm, s>>>(c1, c2, N, tw, out, aligned);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_preprocess_resample(const double2* pts, const int64_t* off, int64_t curves,
+                                       int nmax, int n_out, int center_normalize, double2* out,
+                                       int32_t* status, cudaStream_t s) {
+  const size_t sm = resample_smem_bytes(nmax, n_out);
+  cudaError_t e = set_smem((const void*)preprocess_resample_kernel, sm);
+  if (e != cudaSuccess) return e;
+  preprocess_resample_kernel<<<(unsigned)curves, kThreads, sm, s>>>(pts, off, nmax, n_out,
+                                                                     center_normalize, out, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_preprocess_center(const double2* pts, const int64_t* off, int64_t curves,
+                                     double2* out, int32_t* status, cudaStream_t s) {
+  preprocess_center_kernel<<<(unsigned)curves, kThreads, 0, s>>>(pts, off, out, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_preprocess_align(const double2* pts, const int64_t* off, int64_t pairs,
+                                    int nmax, int N, const double2* tw, cva_alignment* out,
+                                    double2* aligned, cudaStream_t s) {
+  const size_t sm = preprocess_align_smem_bytes(nmax, N);
+  cudaError_t e = set_smem((const void*)preprocess_align_kernel, sm);
+  if (e != cudaSuccess) return e;
+  preprocess_align_kernel<<<(unsigned)pairs, kThreads, sm, s>>>(pts, off, nmax, N, tw, out,
+                                                                 aligned);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_srv_align(const double2* c1, const double2* c2, int64_t pairs, int N,
+                             const double2* tw, cva_alignment* out, double2* aligned,
+                             cudaStream_t s) {
+  const size_t sm = align_smem_bytes(N);
+  cudaError_t e = set_smem((const void*)srv_align_kernel, sm);
+  if (e != cudaSuccess) return e;
+  srv_align_kernel<<<(unsigned)pairs, kThreads, sm, s>>>(c1, c2, N, tw, out, aligned);
+  return cudaGetLastError();
+}
+
+int max_chunked_nodes() { return kThreads * kMaxChunk; }
+
+}  // namespace cva

@@ -1,0 +1,304 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle and the
+reference's golden vectors.
+
+Acceptance rule (BASELINE.json north_star), written out here:
+  (i)   shift identical, unless the oracle's |D| at the two shifts agree within
+        1e-12 relative (a documented near-tie);
+  (ii)  |theta_gpu - theta_ref| mod 2 pi <= 1e-10;
+  (iii) aligned coordinates: max |a_gpu - a_ref| <= 1e-10 max |a_ref|;
+  (iv)  energy: |e_gpu - e_ref| <= 1e-10 max(e_ref, 1e-6 h (s1 + s2))  (the
+        identity e = h(s1+s2) - 2h trace cancels; floor per SURVEY.md P8).
+"""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2501_17779_b200 as cva
+from paper_2501_17779_b200 import _native, synth
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+PI = np.pi
+THETA_TOL = 1e-10
+COORD_TOL = 1e-10
+ENERGY_TOL = 1e-10
+
+
+def gold(name):
+    return np.load(os.path.join(GOLD, name))
+
+
+def wrap(a):
+    return (np.asarray(a) + PI) % (2 * PI) - PI
+
+
+def tau(c1, c2, m):
+    """|D_m| = |sum_l conj(z1_l) z2_{l+m}| computed directly (naive, exact order-free)."""
+    z1 = c1[:, 0] + 1j * c1[:, 1]
+    z2 = c2[:, 0] + 1j * c2[:, 1]
+    return abs(np.sum(np.conj(z1) * np.roll(z2, -m)))
+
+
+def check_pair(g, r, c1, c2, al_g=None, al_r=None):
+    """g: GPU record, r: oracle/reference record, c1/c2: the aligned inputs."""
+    assert int(g["status"]) == 0
+    n = c1.shape[0]
+    if int(g["shift"]) != int(r["shift"]):
+        t1, t2 = tau(c1, c2, int(g["shift"])), tau(c1, c2, int(r["shift"]))
+        assert abs(t1 - t2) <= 1e-12 * max(t1, t2), "shift differs outside the near-tie band"
+        return "near-tie"
+    assert abs(wrap(float(g["theta"]) - float(r["theta"]))) <= THETA_TOL
+    h = 1.0 / n
+    floor = 1e-6 * h * (np.sum(c1 ** 2) + np.sum(c2 ** 2))
+    assert abs(float(g["energy"]) - float(r["energy"])) <= ENERGY_TOL * max(float(r["energy"]), floor)
+    assert abs(float(g["trace"]) - float(r["trace"])) <= 1e-12 * max(1.0, float(r["trace"]))
+    assert float(g["t0"]) == pytest.approx(int(g["shift"]) / n, abs=0)
+    if al_g is not None:
+        assert np.abs(al_g - al_r).max() <= COORD_TOL * np.abs(al_r).max()
+    return "ok"
+
+
+# ----------------------------------------------------- reference known answers
+
+
+@pytest.mark.parametrize("case", ["limacon", "fourier", "bumps", "circle", "reflect", "hippo_rot"])
+def test_kat_cases(cuda, case):
+    g = gold("rigid_align_kat.npz")
+    if case == "circle":
+        c1 = c2 = g["circle"]
+    elif case == "hippo_rot":
+        c1, c2 = g["hippo_c1"], g["hippo_c2"]
+    else:
+        c1, c2 = g[f"{case}_c1"], g[f"{case}_c2"]
+    key = {"circle": "circle_res", "hippo_rot": "hippo_rot"}.get(case, f"{case}_res")
+    res, al = cva.align_fft_batch(c1[None], c2[None], return_aligned=True)
+    ref = g[key][0]
+    check_pair(res[0], ref, c1, c2)
+    if case == "limacon":  # test_rigid_align.cpp:153-168
+        assert res[0]["shift"] == 29 and abs(res[0]["theta"]) < 1e-9 and res[0]["energy"] < 1e-15
+    if case in ("fourier", "bumps"):  # :178-185
+        assert res[0]["t0"] == pytest.approx(0.25, abs=1e-12)
+        assert res[0]["theta"] == pytest.approx(PI / 3, abs=1e-9)
+        assert res[0]["energy"] < 1e-12
+    if case == "circle":  # :170-176 tie-break to shift 0
+        assert res[0]["shift"] == 0 and abs(res[0]["theta"]) < 1e-9
+    if case == "reflect":  # :237-246
+        assert res[0]["energy"] > 1e-6
+
+
+@pytest.mark.parametrize("n", [8, 64, 128, 1024])
+def test_random_pairs_match_reference(cuda, n):  # test_rigid_align.cpp:133-151
+    g = gold("rigid_align_kat.npz")
+    a, b = g[f"rand{n}_c1"], g[f"rand{n}_c2"]
+    res, al = cva.align_fft_batch(a[None], b[None], return_aligned=True)
+    check_pair(res[0], g[f"rand{n}_res"][0], a, b)
+    check_pair(res[0], g[f"rand{n}_res_naive"][0], a, b)
+
+
+@pytest.mark.parametrize("n", [20, 101])
+def test_non_pow2_reported_unsupported(cuda, n):
+    """Any-N FFT is SURVEY §8(f) item 1 ("next"); until it lands the library
+    must refuse loudly rather than return a wrong answer."""
+    g = gold("rigid_align_kat.npz")
+    with pytest.raises(_native.CurvalignError):
+        cva.align_fft_batch(g[f"rand{n}_c1"][None], g[f"rand{n}_c2"][None])
+
+
+def test_energy_matches_direct_residual(cuda):  # test_rigid_align.cpp:187-197
+    rng = np.random.default_rng(57)
+    a, b = rng.uniform(-1, 1, (64, 2)), rng.uniform(-1, 1, (64, 2))
+    r, al = cva.aligned_curve(a, b)
+    direct = np.mean(np.sum((a - al) ** 2, 1))
+    assert r.energy == pytest.approx(direct, rel=1e-9)
+
+
+def test_shift_covariance(cuda, oracle):  # test_rigid_align.cpp:222-235
+    rng = np.random.default_rng(71)
+    a, b = rng.uniform(-1, 1, (64, 2)), rng.uniform(-1, 1, (64, 2))
+    base = cva.align_fft(a, b)
+    bs = np.roll(b, -17, axis=0)  # c2s[l] = c2[(l + 17) % n]
+    sh = cva.align_fft(a, bs)
+    assert sh.shift == (base.shift + 64 - 17) % 64
+    assert sh.theta == pytest.approx(base.theta, abs=1e-10)
+    assert sh.energy == pytest.approx(base.energy, rel=1e-10)
+
+
+def test_validation_errors(cuda):  # test_rigid_align.cpp:248-257
+    with pytest.raises(ValueError):
+        cva.align_fft(np.zeros((32, 2)), np.zeros((64, 2)))
+    with pytest.raises(ValueError):
+        cva.align_fft(np.zeros((3, 2)), np.zeros((3, 2)))
+
+
+# ------------------------------------------------------------------ preprocess
+
+
+def test_preprocess_kat(cuda):  # test_curve_core.cpp:154-232
+    g = gold("curve_core_kat.npz")
+    np.testing.assert_allclose(cva.preprocess(g["hippo100"], 128), g["hippo100_prep128"], atol=1e-14)
+    np.testing.assert_allclose(cva.preprocess(g["hippo100"], 64, resample=False),
+                               g["hippo100_prep_noresample"], atol=1e-15)
+    np.testing.assert_allclose(cva.preprocess(g["square"], 8), g["square_prep8"], atol=1e-14)
+    np.testing.assert_allclose(cva.resample_uniform(g["nonuniform_circle"], 256),
+                               g["nonuniform_circle_r256"], atol=1e-13)
+    np.testing.assert_allclose(cva.resample_uniform(g["gon128"], 128), g["gon128_r128"], atol=1e-13)
+    np.testing.assert_allclose(cva.resample_uniform(g["square"], 8), g["square_resampled8"], atol=1e-14)
+
+
+def test_preprocess_matches_oracle_ragged(cuda, oracle):
+    pts, offs, _, _ = synth.ragged_pairs(3, 48, 1024)
+    out, st = cva.preprocess_batch(pts, offs, 1024)
+    assert (st == 0).all()
+    for c in range(0, 96, 7):
+        want = oracle.preprocess(pts[offs[c]:offs[c + 1]], 1024)
+        assert np.abs(out[c] - want).max() <= 1e-13 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("n_in", [4, 5, 7, 8, 9, 16, 31, 33, 100, 257, 511, 513, 1000, 3000, 4096])
+def test_resample_sizes(cuda, oracle, n_in):
+    """Ragged sizes around every chunking boundary of the partition solver."""
+    rng = np.random.default_rng(n_in)
+    phi = np.sort(rng.uniform(0, 2 * PI, n_in))
+    r = 1 + 0.3 * np.cos(3 * phi + 0.2)
+    raw = np.stack([r * np.cos(phi), r * np.sin(phi)], 1)
+    for n_out in (8, 100, 1024):
+        got = cva.resample_uniform(raw, n_out)
+        want = oracle.resample_uniform(raw, n_out)
+        assert np.abs(got - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+
+
+def test_preprocess_invalid_curves(cuda):
+    good = np.stack([np.cos(np.arange(40) * 0.157), np.sin(np.arange(40) * 0.157)], 1)
+    dup = good.copy()
+    dup[5] = dup[4]  # coincident adjacent nodes (curve.cpp:58)
+    nan = good.copy()
+    nan[3, 0] = np.nan  # non-finite (curve.cpp:11-14)
+    pts, offs = cva.ragged([good, dup, nan, good[:3]])
+    out, st = cva.preprocess_batch(pts, offs, 64)
+    assert list(st) == [0, 1, 1, 1]
+    assert np.isfinite(out[0]).all() and np.isnan(out[1]).all()
+    with pytest.raises(ValueError):
+        cva.preprocess(dup, 64)
+
+
+# ---------------------------------------------------------- BASELINE configs
+
+
+def test_c0_full(cuda, oracle):
+    g = gold("configs_sample.npz")
+    pts = np.concatenate([g["c0_c1"], g["c0_c2"]])
+    offs = np.array([0, 256, 512], np.int64)
+    prep, st = cva.preprocess_batch(pts, offs, 0, resample=False)
+    assert (st == 0).all()
+    c1, c2 = prep[:256], prep[256:]
+    res, al = cva.align_fft_batch(c1[None], c2[None], return_aligned=True)
+    check_pair(res[0], g["c0_res"][0], c1, c2, al[0], g["c0_aligned"][0])
+    assert res[0]["shift"] == g["c0_k"][0]  # the planted shift is recovered
+
+
+def test_c1_golden_sample(cuda):
+    g = gold("configs_sample.npz")
+    res, al = cva.preprocess_align_batch(g["c1_points"], g["c1_offsets"], 1024, return_aligned=True)
+    offs = g["c1_offsets"]
+    for p in range(len(res)):
+        c1 = cva.preprocess(g["c1_points"][offs[2 * p]:offs[2 * p + 1]], 1024)
+        c2 = cva.preprocess(g["c1_points"][offs[2 * p + 1]:offs[2 * p + 2]], 1024)
+        check_pair(res[p], g["c1_res"][p], c1, c2, al[p], g["c1_aligned"][p])
+
+
+def test_c1_live_vs_oracle(cuda, oracle):
+    pts, offs, k, th = synth.ragged_pairs(2024, 96, 1024)
+    res, al = cva.preprocess_align_batch(pts, offs, 1024, return_aligned=True)
+    ro, ao = oracle.batch(pts, offs, 1024, mode=0, threads=os.cpu_count() or 1, aligned=True)
+    prep, _ = cva.preprocess_batch(pts, offs, 1024)
+    kinds = [check_pair(res[p], ro[p], prep[2 * p], prep[2 * p + 1], al[p], ao[p]) for p in range(96)]
+    assert kinds.count("ok") >= 95
+    # split path (preprocess then align) is the same computation, bitwise
+    r2, a2 = cva.align_fft_batch(prep[0::2], prep[1::2], return_aligned=True)
+    np.testing.assert_array_equal(r2, res)
+    np.testing.assert_array_equal(a2, al)
+
+
+def test_c1_full_size_properties(cuda, oracle):
+    """All 4096 C1 pairs on the GPU; a 96-pair subset against the oracle and
+    size-independent properties over the whole batch."""
+    import torch
+
+    cfg = synth.CONFIGS["c1"]
+    pts, offs, k, th = synth.ragged_pairs(1, cfg["pairs"], cfg["N"])
+    dp = torch.from_numpy(pts).cuda()
+    do = torch.from_numpy(offs).cuda()
+    raw, dal = cva.preprocess_align_batch(dp, do, 1024, max_n_in=int(np.diff(offs).max()), return_aligned=True)
+    res = cva.decode_results(raw)
+    al = dal.cpu().numpy()
+    assert (res["status"] == 0).all()
+    assert (res["energy"] >= 0).all() and np.isfinite(res["energy"]).all()
+    dk = np.minimum((res["shift"] - k) % 1024, (k - res["shift"]) % 1024)
+    assert dk.max() <= 4 and np.abs(wrap(res["theta"] - th)).max() < 0.05
+    # deterministic: a second run is bitwise identical
+    raw2, _ = cva.preprocess_align_batch(dp, do, 1024, max_n_in=int(np.diff(offs).max()))
+    torch.cuda.synchronize()
+    assert torch.equal(raw, raw2)
+    # energy is the residual of the returned aligned curve (checksum over all pairs)
+    prep, _ = cva.preprocess_batch(dp, do, 1024, max_n_in=int(np.diff(offs).max()))
+    c1 = prep[0::2].cpu().numpy()
+    direct = np.mean(np.sum((c1 - al) ** 2, axis=2), axis=1)
+    h = 1.0 / 1024
+    floor = 1e-6 * h * (np.sum(c1 ** 2, axis=(1, 2)) * 2)
+    assert (np.abs(direct - res["energy"]) <= 1e-9 * np.maximum(res["energy"], floor)).all()
+    # oracle subset
+    sel = np.arange(0, cfg["pairs"], 43)
+    sub_offs = [0]
+    sub_pts = []
+    for p in sel:
+        for c in (2 * p, 2 * p + 1):
+            sub_pts.append(pts[offs[c]:offs[c + 1]])
+            sub_offs.append(sub_offs[-1] + offs[c + 1] - offs[c])
+    ro, ao = oracle.batch(np.concatenate(sub_pts), np.array(sub_offs), 1024, mode=0,
+                          threads=os.cpu_count() or 1, aligned=True)
+    p2 = prep.cpu().numpy()
+    for i, p in enumerate(sel):
+        check_pair(res[p], ro[i], p2[2 * p], p2[2 * p + 1], al[p], ao[i])
+
+
+def test_c4_golden_and_live(cuda, oracle):
+    g = gold("configs_sample.npz")
+    res, al = cva.srv_align_batch(g["c4_c1"], g["c4_c2"], return_aligned=True)
+    for p in range(2):
+        q1 = oracle.srv_center(oracle.srv_transform(g["c4_c1"][p]))
+        q2 = oracle.srv_center(oracle.srv_transform(g["c4_c2"][p]))
+        check_pair(res[p], g["c4_res"][p], q1, q2, al[p], g["c4_aligned"][p])
+    s1, s2, k, th, u = synth.srv_pairs(5, 24, 2048)
+    res, al = cva.srv_align_batch(s1, s2, return_aligned=True)
+    pts = np.concatenate([np.concatenate([s1[p], s2[p]]) for p in range(24)])
+    offs = np.arange(0, 48 * 2048 + 1, 2048, dtype=np.int64)
+    ro, ao = oracle.batch(pts, offs, 2048, mode=2, threads=os.cpu_count() or 1, aligned=True)
+    for p in range(24):
+        q1 = oracle.srv_center(oracle.srv_transform(s1[p]))
+        q2 = oracle.srv_center(oracle.srv_transform(s2[p]))
+        check_pair(res[p], ro[p], q1, q2, al[p], ao[p])
+
+
+def test_c2_sample_allpairs(cuda):
+    """C2 sample: 6 curves, all 36 ordered pairs vs the reference's matrix."""
+    g = gold("configs_sample.npz")
+    prep, st = cva.preprocess_batch(g["c2_points"], g["c2_offsets"], 512)
+    assert (st == 0).all()
+    np.testing.assert_allclose(prep, g["c2_prep"], atol=1e-13)
+    i, j = np.meshgrid(np.arange(6), np.arange(6), indexing="ij")
+    res, _ = cva.align_fft_batch(prep[i.ravel()], prep[j.ravel()])
+    np.testing.assert_array_equal(res["shift"].reshape(6, 6), g["c2_shift"])
+    e = res["energy"].reshape(6, 6)
+    assert np.all(np.abs(e - g["c2_energy"]) <= 1e-10 * np.maximum(g["c2_energy"], 1e-6 / 512))
+
+
+def test_align_idempotent(cuda):
+    """Aligning c1 against its own aligned partner gives shift 0 and theta 0."""
+    c1, c2, _, _ = synth.uniform_pairs(4, 8, 512)
+    r, al = cva.align_fft_batch(c1, c2, return_aligned=True)
+    r2, _ = cva.align_fft_batch(c1, al)
+    assert (r2["shift"] == 0).all()
+    assert np.abs(wrap(r2["theta"])).max() < 1e-10
+    np.testing.assert_allclose(r2["energy"], r["energy"], rtol=1e-9, atol=1e-15)

@@ -1,0 +1,166 @@
+"""Generate tests/golden/*.npz from the REFERENCE's own code (oracle/_ref).
+
+Run here (where /root/reference exists and `make ref` built oracle/_ref):
+    python tools/make_golden.py
+Each fixture holds inputs plus the reference's outputs for them; the oracle
+(tests/test_oracle_pins.py) and the GPU path (tests/test_gpu_*.py) are checked
+against these files. Cases restate the reference's own known-answer tests
+(proj/tests/test_rigid_align.cpp, test_curve_core.cpp, test_srv.cpp,
+test_synthetic.cpp) plus small seeded samples of the BASELINE configs.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+from pyoracle import ALIGNMENT_DTYPE, Reference  # noqa: E402
+
+from paper_2501_17779_b200 import synth  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+PI = np.pi
+
+
+def rec(a):
+    return np.array([tuple(a)], dtype=ALIGNMENT_DTYPE)
+
+
+def aligned_of(c2, r):
+    n = c2.shape[0]
+    c, s = np.cos(r["theta"]), np.sin(r["theta"])
+    q = c2[(np.arange(n) + int(r["shift"])) % n]
+    return np.stack([c * q[:, 0] + s * q[:, 1], -s * q[:, 0] + c * q[:, 1]], 1)
+
+
+def main():
+    R = Reference()
+    os.makedirs(OUT, exist_ok=True)
+    kat = {}
+
+    # --- rigid_align known answers (proj/tests/test_rigid_align.cpp)
+    diamond = np.array([[1, 0], [0, 1], [-1, 0], [0, -1]], float)
+    kat["diamond"] = diamond
+    kat["diamond_A1"] = R.cross_correlation_matrix(diamond, diamond, 1)  # :47-56
+
+    lim = R.gen_curve("limacon", 96)  # :153-168
+    lim2 = np.empty_like(lim)
+    for l in range(96):
+        lim2[(l + 29) % 96] = lim[l]
+    kat["limacon_c1"], kat["limacon_c2"] = lim, lim2
+    kat["limacon_res"] = rec(R.align(lim, lim2))
+
+    circ = R.gen_curve("circle", 64)  # :170-176
+    kat["circle"] = circ
+    kat["circle_res"] = rec(R.align(circ, circ))
+
+    f1 = R.gen_curve("fourier_random", 256, 5)  # :178-185
+    f2 = R.transform_curve(f1, 0.25, PI / 3.0)
+    kat["fourier_c1"], kat["fourier_c2"] = f1, f2
+    kat["fourier_res"] = rec(R.align(f1, f2))
+
+    b1 = R.gen_curve("bumps", 256)  # test_synthetic.cpp:100-107
+    b2 = R.transform_curve(b1, 0.25, PI / 3.0)
+    kat["bumps_c1"], kat["bumps_c2"] = b1, b2
+    kat["bumps_res"] = rec(R.align(b1, b2))
+
+    h1 = R.gen_curve("hippopede", 128)  # :212-220
+    h2 = h1.copy()
+    c, s = np.cos(0.4), np.sin(0.4)
+    h2 = np.stack([c * h1[:, 0] - s * h1[:, 1], s * h1[:, 0] + c * h1[:, 1]], 1)
+    kat["hippo_c1"], kat["hippo_c2"] = h1, h2
+    kat["hippo_base"] = rec(R.align(h1, h1))
+    kat["hippo_rot"] = rec(R.align(h1, h2))
+
+    lr = R.gen_curve("limacon", 128)  # :237-246
+    lm = lr.copy()
+    lm[:, 1] = -lm[:, 1]
+    kat["reflect_c1"], kat["reflect_c2"] = lr, lm
+    kat["reflect_res"] = rec(R.align(lr, lm))
+
+    rng = np.random.default_rng(43)  # :133-151 (naive == fft); pow2 and non-pow2 n
+    for n in (8, 20, 64, 101, 128, 1024):
+        a = rng.uniform(-1, 1, (n, 2))
+        b = rng.uniform(-1, 1, (n, 2))
+        kat[f"rand{n}_c1"], kat[f"rand{n}_c2"] = a, b
+        kat[f"rand{n}_naive"] = R.correlation_all_shifts(a, b, fft=False)
+        kat[f"rand{n}_fft"] = R.correlation_all_shifts(a, b, fft=True)
+        kat[f"rand{n}_res"] = rec(R.align(a, b))
+        kat[f"rand{n}_res_naive"] = rec(R.align(a, b, fft=False))
+    np.savez_compressed(os.path.join(OUT, "rigid_align_kat.npz"), **kat)
+
+    # --- curve core / spline known answers (proj/tests/test_curve_core.cpp)
+    cc = {}
+    sq = np.array([[0, 0], [1, 0], [1, 1], [0, 1]], float)
+    rect = np.array([[0, 0], [2, 0], [2, 1], [0, 1]], float)
+    cc["square"], cc["rect"] = sq, rect
+    cc["square_s"], cc["square_len"] = R.arc_length_params(sq)
+    cc["rect_s"], cc["rect_len"] = R.arc_length_params(rect)
+    cc["square_resampled8"] = R.resample_uniform(sq, 8)
+    cc["square_prep8"] = R.preprocess(sq, 8)
+    x = np.array([0.0, 0.2, 0.45, 0.7, 1.0])
+    y = np.array([1.0, -0.5, 2.0, 0.25, 1.0])
+    xq = np.linspace(-0.3, 1.3, 41)
+    cc["spline_x"], cc["spline_y"], cc["spline_xq"] = x, y, xq
+    cc["spline_val"] = R.spline(x, y, xq)
+    nonu = np.array([[np.cos(2 * PI * (t + 0.15 * t * (1 - t))), np.sin(2 * PI * (t + 0.15 * t * (1 - t)))]
+                     for t in np.arange(64) / 64.0])
+    cc["nonuniform_circle"] = nonu
+    cc["nonuniform_circle_r256"] = R.resample_uniform(nonu, 256)
+    gon = np.array([[np.cos(2 * PI * i / 128), np.sin(2 * PI * i / 128)] for i in range(128)])
+    cc["gon128"] = gon
+    cc["gon128_r128"] = R.resample_uniform(gon, 128)
+    hip = R.gen_curve("hippopede", 100)
+    cc["hippo100"] = hip
+    cc["hippo100_prep128"] = R.preprocess(hip, 128)
+    cc["hippo100_prep_noresample"] = R.preprocess(hip, 64, resample=False)
+    clover = R.gen_curve("clover", 200)
+    cc["clover200"] = clover
+    cc["clover200_s"], _ = R.arc_length_params(clover)
+    np.savez_compressed(os.path.join(OUT, "curve_core_kat.npz"), **cc)
+
+    # --- srv (proj/tests/test_srv.cpp:80-128)
+    sv = {}
+    circ_p = R.preprocess(R.gen_curve("circle", 512), 256)
+    sv["circle_prep256"] = circ_p
+    sv["circle_q"] = R.srv_transform(circ_p)
+    bp = R.preprocess(R.gen_curve("bumps", 256), 128)
+    sv["bumps_prep128"] = bp
+    sv["bumps_qc"] = R.srv_center(R.srv_transform(bp))
+    np.savez_compressed(os.path.join(OUT, "srv_kat.npz"), **sv)
+
+    # --- BASELINE config samples (seeded synthetic inputs, reference outputs)
+    cfg = {}
+    c1, c2, k, th = synth.uniform_pairs(7, 1, 256, modes=7, sigma=1e-3)  # C0
+    pts = np.concatenate([c1[0], c2[0]])
+    offs = np.array([0, 256, 512], np.int64)
+    res, al = R.batch(pts, offs, 256, mode=0, resample=False, aligned=True)
+    cfg["c0_c1"], cfg["c0_c2"], cfg["c0_k"], cfg["c0_theta"] = c1[0], c2[0], k, th
+    cfg["c0_res"], cfg["c0_aligned"] = res, al
+    pts, offs, k, th = synth.ragged_pairs(11, 4, 1024)  # C1 sample
+    res, al = R.batch(pts, offs, 1024, mode=0, resample=True, aligned=True)
+    cfg["c1_points"], cfg["c1_offsets"], cfg["c1_k"], cfg["c1_theta"] = pts, offs, k, th
+    cfg["c1_res"], cfg["c1_aligned"] = res, al
+    cpts, coffs = synth.ragged_curves(13, 6)  # C2 sample: 6 curves -> 36 ordered pairs at N=512
+    prep = np.stack([R.preprocess(cpts[coffs[i]:coffs[i + 1]], 512) for i in range(6)])
+    e, kk, tt = R.allpairs(prep, 0, 6)
+    cfg["c2_points"], cfg["c2_offsets"], cfg["c2_prep"] = cpts, coffs, prep
+    cfg["c2_energy"], cfg["c2_shift"], cfg["c2_theta"] = e, kk, tt
+    s1, s2, k, th, u = synth.srv_pairs(17, 2, 2048)  # C4 sample
+    pts = np.concatenate([s1[0], s2[0], s1[1], s2[1]])
+    offs = np.array([0, 2048, 4096, 6144, 8192], np.int64)
+    res, al = R.batch(pts, offs, 2048, mode=2, aligned=True)
+    cfg["c4_c1"], cfg["c4_c2"], cfg["c4_res"], cfg["c4_aligned"] = s1, s2, res, al
+    np.savez_compressed(os.path.join(OUT, "configs_sample.npz"), **cfg)
+
+    for f in sorted(os.listdir(OUT)):
+        print(f, os.path.getsize(os.path.join(OUT, f)))
+
+
+if __name__ == "__main__":
+    main()
