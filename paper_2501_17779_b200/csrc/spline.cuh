@@ -22,6 +22,9 @@
 //   phase 3  each chunk re-solves its interior with known boundary values.
 // No truncation is involved, so the result equals the reference's up to
 // rounding (~1e-15 relative; the matrix is diagonally dominant with ratio 1/2).
+// Parity note: the system solved is the one the reference's code actually
+// solves, whose last row differs from the textbook periodic spline when
+// h_{n-2} != h_{n-1} (see phase 2 and DESIGN.md, parity trap P11).
 #pragma once
 
 #include "cva_common.cuh"
@@ -167,10 +170,23 @@ __device__ inline void block_spline_solve(const double* s, const double2* xy, do
     const double hL = knot_h(s, n, j - 1), hj = knot_h(s, n, j);
     const ChunkEnds e = ends[t], en = ends[kn];
     const double2 r = m[j];
+    double dj = 2.0 * (hL + hj), sj = hj;
+    if (t == K - 1) {
+      // Row n-1 as the reference actually solves it. Its Sherman-Morrison split
+      // (proj/src/spline.cpp:20-26, :43-46) takes u[n-1] = b[n-1] and
+      // v[n-1] = a[n-1]/g where the cyclic corner is a[n-1] / b[0], so with
+      // non-uniform knots the last row reads
+      //   h_{n-2} m_{n-2} + (2(h_{n-2}+h_{n-1}) + h_{n-1}(h_{n-1}-h_{n-2}) / (2(h_{n-1}+h_0))) m_{n-1}
+      //     + h_{n-2} m_0 = r_{n-1}
+      // (scaled by 6). Identical to the textbook row when h_{n-2} = h_{n-1}.
+      const double h0 = knot_h(s, n, 0);
+      sj = hL;
+      dj = 2.0 * (hL + hj) + hj * (hj - hL) / (2.0 * (hj + h0));
+    }
     ra = hL * e.vLl;
-    rd = 2.0 * (hL + hj) + hL * e.vRl + hj * en.vLf;
-    rc = hj * en.vRf;
-    rr = make_double2(r.x - hL * e.v0l.x - hj * en.v0f.x, r.y - hL * e.v0l.y - hj * en.v0f.y);
+    rd = dj + hL * e.vRl + sj * en.vLf;
+    rc = sj * en.vRf;
+    rr = make_double2(r.x - hL * e.v0l.x - sj * en.v0f.x, r.y - hL * e.v0l.y - sj * en.v0f.y);
   }
   // PCR storage reuses `ends` (>= K * 48 bytes needed, ChunkEnds is 64 bytes)
   double* pa = reinterpret_cast<double*>(ends);
