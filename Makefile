@@ -10,7 +10,7 @@ CSRC     := $(PKG)/csrc
 BUILD    := build
 REF      ?= /root/reference
 
-KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h include/curvalign_cuda.h
+KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h $(CSRC)/fused.h include/curvalign_cuda.h
 
 .PHONY: all lib synth dropin oracle ref clean
 all: lib synth oracle ref
@@ -23,7 +23,11 @@ $(BUILD)/kernels.o: $(CSRC)/kernels.cu $(KERNEL_HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_kernels.log || (cat $(BUILD)/ptxas_kernels.log; exit 1)
 
-$(BUILD)/capi.o: $(CSRC)/capi.cpp $(CSRC)/kernels.h include/curvalign_cuda.h
+$(BUILD)/fused.o: $(CSRC)/fused.cu $(KERNEL_HDRS) $(CSRC)/fused.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_fused.log || (cat $(BUILD)/ptxas_fused.log; exit 1)
+
+$(BUILD)/capi.o: $(CSRC)/capi.cpp $(CSRC)/kernels.h $(CSRC)/fused.h include/curvalign_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 
@@ -31,7 +35,7 @@ $(BUILD)/probe.o: $(CSRC)/probe.cu include/curvalign_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/capi.o $(BUILD)/probe.o
+$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/fused.o $(BUILD)/capi.o $(BUILD)/probe.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
 
 # Synthetic workload generators (bench harness; host only).

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/curvalign_cuda.h"
+#include "fused.h"
 #include "kernels.h"
 
 namespace {
@@ -84,6 +85,29 @@ int check_fft_size(int64_t n) {
   return CVA_OK;
 }
 
+// Stream-ordered scratch (cudaMallocAsync on the call's stream, freed after the
+// kernels on the same stream): safe for concurrent calls on different streams.
+// The device's default pool keeps freed blocks cached.
+std::mutex g_pool_mu;
+std::map<int, bool> g_pool_ready;
+
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  {
+    std::lock_guard<std::mutex> lock(g_pool_mu);
+    if (!g_pool_ready[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      g_pool_ready[dev] = true;
+    }
+  }
+  return cudaMallocAsync(p, bytes ? bytes : 16, s);
+}
+
 int check_resample_nmax(int64_t nmax, int64_t n_out, size_t smem) {
   if (nmax > cva::max_chunked_nodes() || smem > (size_t)smem_limit())
     return fail(CVA_UNSUPPORTED, "resample: curve has more raw nodes than the shared-memory "
@@ -111,6 +135,23 @@ int device_max_n(const int64_t* d_offsets, int64_t curves, cudaStream_t s, int64
 int finish(cudaError_t e, const char* what) {
   if (e != cudaSuccess) return cuda_fail(e, what);
   return CVA_OK;
+}
+
+// v2 shared-memory resampler when the batch fits it, else the general v1 kernel.
+int resample_dispatch(const double* points, const int64_t* offsets, int64_t curves,
+                      int64_t max_n_in, int64_t n_out, int center_normalize, double* out,
+                      int32_t* status, cudaStream_t s) {
+  const int nmax = (int)std::max<int64_t>(max_n_in, 4);
+  if (nmax <= cva::v2_max_raw_nodes() && n_out <= 2048)
+    return finish(cva::launch_v2_preprocess((const double2*)points, offsets, curves, (int)n_out,
+                                            center_normalize, (double2*)out, status, s),
+                  "preprocess launch");
+  if (int rc = check_resample_nmax(nmax, n_out, cva::resample_smem_bytes(nmax, (int)n_out)))
+    return rc;
+  return finish(cva::launch_preprocess_resample((const double2*)points, offsets, curves, nmax,
+                                                (int)n_out, center_normalize, (double2*)out,
+                                                status, s),
+                "preprocess launch");
 }
 
 // RAII device buffer for the *_host entry points.
@@ -148,8 +189,8 @@ int cva_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
   if (int rc = get_twiddles((int)n, s, &tw)) return rc;
-  return finish(cva::launch_align((const double2*)c1, (const double2*)c2, pairs, (int)n, tw, out,
-                                  (double2*)aligned, s),
+  return finish(cva::launch_v2_align((const double2*)c1, (const double2*)c2, pairs, (int)n, tw,
+                                     out, (double2*)aligned, s),
                 "align launch");
 }
 
@@ -169,12 +210,7 @@ int cva_preprocess_batch(const double* points, const int64_t* offsets, int64_t c
                   "preprocess launch");
   if (max_n_in <= 0)
     if (int rc = device_max_n(offsets, curves, s, &max_n_in)) return rc;
-  const int nmax = (int)std::max<int64_t>(max_n_in, 4);
-  if (int rc = check_resample_nmax(nmax, n_out, cva::resample_smem_bytes(nmax, (int)n_out)))
-    return rc;
-  return finish(cva::launch_preprocess_resample((const double2*)points, offsets, curves, nmax,
-                                                (int)n_out, 1, (double2*)out, status, s),
-                "preprocess launch");
+  return resample_dispatch(points, offsets, curves, max_n_in, n_out, 1, out, status, s);
 }
 
 int cva_resample_batch(const double* points, const int64_t* offsets, int64_t curves,
@@ -188,12 +224,7 @@ int cva_resample_batch(const double* points, const int64_t* offsets, int64_t cur
   cudaStream_t s = (cudaStream_t)stream;
   if (max_n_in <= 0)
     if (int rc = device_max_n(offsets, curves, s, &max_n_in)) return rc;
-  const int nmax = (int)std::max<int64_t>(max_n_in, 4);
-  if (int rc = check_resample_nmax(nmax, n_out, cva::resample_smem_bytes(nmax, (int)n_out)))
-    return rc;
-  return finish(cva::launch_preprocess_resample((const double2*)points, offsets, curves, nmax,
-                                                (int)n_out, 0, (double2*)out, status, s),
-                "resample launch");
+  return resample_dispatch(points, offsets, curves, max_n_in, n_out, 0, out, status, s);
 }
 
 int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int64_t pairs,
@@ -213,11 +244,38 @@ int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int
   if (max_n_in <= 0)
     if (int rc = device_max_n(offsets, 2 * pairs, s, &max_n_in)) return rc;
   const int nmax = (int)std::max<int64_t>(max_n_in, 4);
+  const double2* tw = nullptr;
+  if (int rc = get_twiddles((int)n_out, s, &tw)) return rc;
+  if (nmax <= cva::v2_max_raw_nodes()) {
+    const size_t ab = sizeof(double2) * (size_t)(pairs * n_out);
+    if (cva::v2_resample_align_supported((int)n_out)) {
+      // fused kernel; the aligned rows double as the second curve's staging buffer
+      void* ws = nullptr;
+      if (!aligned && scratch_alloc(&ws, ab, s) != cudaSuccess)
+        return fail(CVA_BAD_ALLOC, "scratch allocation failed");
+      cudaError_t e = cva::launch_v2_resample_align((const double2*)points, offsets, pairs,
+                                                    (int)n_out, tw, out,
+                                                    aligned ? (double2*)aligned : (double2*)ws, s);
+      if (ws) cudaFreeAsync(ws, s);
+      return finish(e, "resample_align launch");
+    }
+    // other N: preprocess into scratch, then align
+    void* ws = nullptr;
+    if (scratch_alloc(&ws, 2 * ab, s) != cudaSuccess)
+      return fail(CVA_BAD_ALLOC, "scratch allocation failed");
+    cudaError_t e = cva::launch_v2_preprocess((const double2*)points, offsets, 2 * pairs,
+                                              (int)n_out, 1, (double2*)ws, nullptr, s);
+    // pair p = prepared rows 2p, 2p+1: strided views via a second launch on
+    // de-interleaved halves is avoided by aligning row pairs in place
+    if (e == cudaSuccess)
+      e = cva::launch_v2_align_interleaved((const double2*)ws, pairs, (int)n_out, tw, out,
+                                           (double2*)aligned, s);
+    cudaFreeAsync(ws, s);
+    return finish(e, "preprocess+align launch");
+  }
   if (int rc = check_resample_nmax(nmax, n_out,
                                    cva::preprocess_align_smem_bytes(nmax, (int)n_out)))
     return rc;
-  const double2* tw = nullptr;
-  if (int rc = get_twiddles((int)n_out, s, &tw)) return rc;
   return finish(cva::launch_preprocess_align((const double2*)points, offsets, pairs, nmax,
                                              (int)n_out, tw, out, (double2*)aligned, s),
                 "preprocess_align launch");
@@ -234,9 +292,13 @@ int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
   if (int rc = get_twiddles((int)n, s, &tw)) return rc;
-  return finish(cva::launch_srv_align((const double2*)c1, (const double2*)c2, pairs, (int)n, tw,
-                                      out, (double2*)aligned_q, s),
-                "srv_align launch");
+  void* ws = nullptr;
+  if (scratch_alloc(&ws, 2 * sizeof(double2) * (size_t)(pairs * n), s) != cudaSuccess)
+    return fail(CVA_BAD_ALLOC, "scratch allocation failed");
+  cudaError_t e = cva::launch_v2_srv_align((const double2*)c1, (const double2*)c2, pairs, (int)n,
+                                           tw, out, (double2*)aligned_q, (double2*)ws, s);
+  cudaFreeAsync(ws, s);
+  return finish(e, "srv_align launch");
 }
 
 // ------------------------------------------------------------- host entries

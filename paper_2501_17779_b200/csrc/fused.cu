@@ -1,0 +1,287 @@
+// v2 sm_100a kernels (256 threads, 2 CTAs per SM): the fused C1 path and the
+// shared-memory preprocess / align / SRV-align kernels built from resample.cuh
+// and pairfft.cuh. kernels.cu keeps the general v1 kernels for sizes outside
+// these bounds (raw curves > 3072 nodes, N > 2048).
+#include <cuda_runtime.h>
+
+#include "../../include/curvalign_cuda.h"
+#include "fused.h"
+#include "pairfft.cuh"
+#include "resample.cuh"
+
+namespace cva {
+namespace v2 {
+
+constexpr int kT = 256;
+constexpr size_t kRawBytes = sizeof(double2) * rs::kNMax + sizeof(double) * (rs::kNMax + 2);
+constexpr size_t kScrBytes = sizeof(double) * rs::kScratchDoubles;
+
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
+
+// Stream a raw curve into shared memory (read-once data: evict-first loads).
+__device__ __forceinline__ void load_raw(const double2* __restrict__ g, double2* sm, int n) {
+  for (int i = threadIdx.x; i < n; i += kT) sm[i] = __ldcs(&g[i]);
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p, int bytes) {
+  if (bytes >= 16)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes & ~15) : "memory");
+}
+
+__device__ inline void write_bad(cva_alignment* out, int status) {
+  cva_alignment r;
+  r.shift = 0;
+  r.t0 = 0.0;
+  r.theta = qnan();
+  r.trace = qnan();
+  r.energy = qnan();
+  r.degenerate = 0;
+  r.status = status;
+  *out = r;
+}
+
+// ---------------------------------------------------------------- fused C1
+
+// Pair p = (curve 2p, curve 2p+1) of the ragged raw batch: preprocess both to
+// N nodes (resample -> center -> normalize, curve.cpp:93-97) and align_fft
+// (rigid_align.cpp:204-208), all on chip. The second curve's resampled nodes
+// are staged in this pair's `aligned` row (L2), which the pair stage then
+// overwrites with the aligned curve.
+template <int N>
+__global__ void __launch_bounds__(kT, 2)
+    resample_align_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off,
+                          const double2* __restrict__ tw, cva_alignment* __restrict__ out,
+                          double2* __restrict__ aligned) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double2 red[16];
+  double2* xy = reinterpret_cast<double2*>(smem);
+  double* s = reinterpret_cast<double*>(xy + rs::kNMax);
+  double2* bufs = reinterpret_cast<double2*>(smem);  // aliases the raw region after resampling
+  double* scr = reinterpret_cast<double*>(smem + kRawBytes);
+  double2* Z1 = reinterpret_cast<double2*>(smem + kRawBytes + kScrBytes);
+
+  const int64_t p = blockIdx.x;
+  const int64_t a0 = off[2 * p], a1 = off[2 * p + 1], b1 = off[2 * p + 2];
+  const int na = (int)(a1 - a0), nb = (int)(b1 - a1);
+  double2* al = aligned + p * N;
+  if (threadIdx.x == 0) prefetch_l2(pts + a1, nb * (int)sizeof(double2));
+  if (na < 4 || nb < 4 || na > rs::kNMax || nb > rs::kNMax) {  // validate_curve(c, 4)
+    if (threadIdx.x == 0) write_bad(out + p, CVA_INVALID_ARGUMENT);
+    for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
+    return;
+  }
+  load_raw(pts + a0, xy, na);
+  __syncthreads();
+  const rs::CurveStats A = rs::resample_block<true>(xy, na, s, scr, red, Z1, N);
+  load_raw(pts + a1, xy, nb);
+  __syncthreads();
+  const rs::CurveStats B = rs::resample_block<true>(xy, nb, s, scr, red, al, N);
+  if (A.bad || B.bad) {
+    if (threadIdx.x == 0) write_bad(out + p, CVA_INVALID_ARGUMENT);
+    for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
+    return;
+  }
+  __syncthreads();
+  pf::PairIn in{Z1, al, A.centroid, B.centroid, A.inv_len, B.inv_len};
+  pf::pair_stage(in, bufs, N, tw, out + p, al, red);
+}
+
+// ------------------------------------------------------------- preprocess
+
+// preprocess(raw, n_out, true) (curve.cpp:93-97) or resample_uniform alone
+// (center_normalize == 0) for one curve per CTA; n_out <= 2048.
+template <bool kPow2>
+__global__ void __launch_bounds__(kT, 2)
+    preprocess_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off, int n_out,
+                      int center_normalize, double2* __restrict__ out,
+                      int32_t* __restrict__ status) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double2 red[16];
+  double2* xy = reinterpret_cast<double2*>(smem);
+  double* s = reinterpret_cast<double*>(xy + rs::kNMax);
+  double* scr = reinterpret_cast<double*>(smem + kRawBytes);
+  double2* Z = reinterpret_cast<double2*>(smem + kRawBytes + kScrBytes);
+  const int64_t c = blockIdx.x;
+  const int64_t b0 = off[c];
+  const int n = (int)(off[c + 1] - b0);
+  double2* o = out + c * n_out;
+  int bad = n < 4 || n > rs::kNMax;
+  rs::CurveStats st{};
+  if (!bad) {
+    load_raw(pts + b0, xy, n);
+    __syncthreads();
+    st = rs::resample_block<kPow2>(xy, n, s, scr, red, Z, n_out);
+    bad = st.bad;
+  }
+  if (bad) {
+    for (int l = threadIdx.x; l < n_out; l += kT) o[l] = make_double2(qnan(), qnan());
+  } else if (center_normalize) {
+    for (int l = threadIdx.x; l < n_out; l += kT) {
+      const double2 z = Z[l];
+      o[l] = make_double2((z.x - st.centroid.x) * st.inv_len, (z.y - st.centroid.y) * st.inv_len);
+    }
+  } else {
+    for (int l = threadIdx.x; l < n_out; l += kT) o[l] = Z[l];
+  }
+  if (status && threadIdx.x == 0) status[c] = bad ? CVA_INVALID_ARGUMENT : CVA_OK;
+}
+
+// ----------------------------------------------------------------- align
+
+// align_fft on pre-sampled pairs (rigid_align.cpp:204-208), N = 2^p <= 2048.
+// Pair p reads c1 + p * stride and c2 + p * stride (stride N: separate
+// batches; stride 2N with c2 = c1 + N: interleaved rows 2p, 2p+1).
+__global__ void __launch_bounds__(kT)
+    align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
+                 int64_t stride, const double2* __restrict__ tw, cva_alignment* __restrict__ out,
+                 double2* __restrict__ aligned) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double2 red[16];
+  const int64_t p = blockIdx.x;
+  pf::PairIn in{c1 + p * stride, c2 + p * stride, make_double2(0, 0), make_double2(0, 0), 1.0, 1.0};
+  pf::pair_stage(in, reinterpret_cast<double2*>(smem), N, tw, out + p,
+                 aligned ? aligned + p * N : nullptr, red);
+}
+
+// ------------------------------------------------------------------- SRV
+
+// q_l = d_l / sqrt(|d_l|), d_l = (N/2)(c[l+1] - c[l-1]); 0 if |d_l| < 1e-8 N (srv.cpp:71-88)
+__device__ __forceinline__ double2 srv_at(const double2* __restrict__ c, int l, int N) {
+  const double nn = (double)N;
+  const double2 nx = c[l + 1 == N ? 0 : l + 1], pv = c[l == 0 ? N - 1 : l - 1];
+  const double2 d = make_double2((nn / 2.0) * (nx.x - pv.x), (nn / 2.0) * (nx.y - pv.y));
+  const double mag = sqrt(fma(d.x, d.x, d.y * d.y));
+  if (mag < 1e-8 * nn) return make_double2(0.0, 0.0);
+  const double r = 1.0 / sqrt(mag);
+  return make_double2(r * d.x, r * d.y);
+}
+
+// SRV alignment (srv_transform -> srv_center -> align_fft, the (t0,R) step of
+// elastic.cpp:138-139). The centered SRVs are written to `qbuf` (this pair's
+// 2N scratch rows in global memory / L2) and aligned by the pair stage.
+__global__ void __launch_bounds__(kT)
+    srv_align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
+                     const double2* __restrict__ tw, cva_alignment* __restrict__ out,
+                     double2* __restrict__ aligned, double2* __restrict__ qbuf) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double2 red[16];
+  const int64_t p = blockIdx.x;
+  const double2* a = c1 + p * N;
+  const double2* b = c2 + p * N;
+  double2* q1 = qbuf + 2 * p * N;
+  double2* q2 = q1 + N;
+  int bad = 0;
+  double2 m1 = make_double2(0, 0), m2 = make_double2(0, 0);
+  for (int l = threadIdx.x; l < N; l += kT) {
+    const double2 u = a[l], v = b[l];
+    bad |= !(isfinite(u.x) && isfinite(u.y) && isfinite(v.x) && isfinite(v.y));
+    const double2 x = srv_at(a, l, N), y = srv_at(b, l, N);
+    q1[l] = x;
+    q2[l] = y;
+    m1 = cadd(m1, x);
+    m2 = cadd(m2, y);
+  }
+  double bs = bad ? 1.0 : 0.0;
+  rs::block_sum3(m1.x, m1.y, bs, red);
+  double m2y = m2.y, dummy = 0.0;
+  rs::block_sum3(m2.x, m2y, dummy, red);
+  double2* al = aligned ? aligned + p * N : nullptr;
+  if (bs != 0.0) {
+    if (threadIdx.x == 0) write_bad(out + p, CVA_INVALID_ARGUMENT);
+    if (al)
+      for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
+    return;
+  }
+  const double invn = 1.0 / (double)N;  // srv_center (srv.cpp:90-98)
+  pf::PairIn in{q1, q2, make_double2(invn * m1.x, invn * m1.y), make_double2(invn * m2.x, invn * m2y),
+                1.0, 1.0};
+  pf::pair_stage(in, reinterpret_cast<double2*>(smem), N, tw, out + p, al, red);
+}
+
+}  // namespace v2
+
+// ------------------------------------------------------------ launchers
+
+namespace {
+cudaError_t set_smem(const void* fn, size_t bytes) {
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+}  // namespace
+
+int v2_max_raw_nodes() { return rs::kNMax; }
+
+size_t v2_resample_align_smem(int N) {
+  const size_t fft = 4 * sizeof(double2) * (size_t)N;
+  const size_t raw = v2::kRawBytes > fft ? v2::kRawBytes : fft;
+  return raw + v2::kScrBytes + sizeof(double2) * (size_t)N;
+}
+size_t v2_preprocess_smem(int n_out) {
+  return v2::kRawBytes + v2::kScrBytes + sizeof(double2) * (size_t)n_out;
+}
+size_t v2_align_smem(int N) { return 4 * sizeof(double2) * (size_t)N; }
+
+bool v2_resample_align_supported(int N) { return N == 512 || N == 1024; }
+
+cudaError_t launch_v2_resample_align(const double2* pts, const int64_t* off, int64_t pairs, int N,
+                                     const double2* tw, cva_alignment* out, double2* aligned,
+                                     cudaStream_t s) {
+  const size_t sm = v2_resample_align_smem(N);
+  const void* fn = N == 512 ? (const void*)v2::resample_align_kernel<512>
+                            : (const void*)v2::resample_align_kernel<1024>;
+  cudaError_t e = set_smem(fn, sm);
+  if (e != cudaSuccess) return e;
+  if (N == 512)
+    v2::resample_align_kernel<512><<<(unsigned)pairs, v2::kT, sm, s>>>(pts, off, tw, out, aligned);
+  else
+    v2::resample_align_kernel<1024><<<(unsigned)pairs, v2::kT, sm, s>>>(pts, off, tw, out, aligned);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_v2_preprocess(const double2* pts, const int64_t* off, int64_t curves, int n_out,
+                                 int center_normalize, double2* out, int32_t* status,
+                                 cudaStream_t s) {
+  const size_t sm = v2_preprocess_smem(n_out);
+  const bool pow2 = (n_out & (n_out - 1)) == 0;
+  const void* fn = pow2 ? (const void*)v2::preprocess_kernel<true> : (const void*)v2::preprocess_kernel<false>;
+  cudaError_t e = set_smem(fn, sm);
+  if (e != cudaSuccess) return e;
+  if (pow2)
+    v2::preprocess_kernel<true><<<(unsigned)curves, v2::kT, sm, s>>>(pts, off, n_out, center_normalize,
+                                                                     out, status);
+  else
+    v2::preprocess_kernel<false><<<(unsigned)curves, v2::kT, sm, s>>>(pts, off, n_out,
+                                                                      center_normalize, out, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_v2_align(const double2* c1, const double2* c2, int64_t pairs, int N,
+                            const double2* tw, cva_alignment* out, double2* aligned,
+                            cudaStream_t s) {
+  const size_t sm = v2_align_smem(N);
+  cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
+  if (e != cudaSuccess) return e;
+  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, N, tw, out, aligned);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_v2_align_interleaved(const double2* rows, int64_t pairs, int N, const double2* tw,
+                                        cva_alignment* out, double2* aligned, cudaStream_t s) {
+  const size_t sm = v2_align_smem(N);
+  cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
+  if (e != cudaSuccess) return e;
+  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(rows, rows + N, N, 2 * (int64_t)N, tw, out,
+                                                        aligned);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_v2_srv_align(const double2* c1, const double2* c2, int64_t pairs, int N,
+                                const double2* tw, cva_alignment* out, double2* aligned,
+                                double2* qbuf, cudaStream_t s) {
+  const size_t sm = v2_align_smem(N);
+  cudaError_t e = set_smem((const void*)v2::srv_align_kernel, sm);
+  if (e != cudaSuccess) return e;
+  v2::srv_align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, tw, out, aligned, qbuf);
+  return cudaGetLastError();
+}
+
+}  // namespace cva

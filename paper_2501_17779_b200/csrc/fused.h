@@ -1,0 +1,33 @@
+// Host-side declarations of the v2 launchers (fused.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/curvalign_cuda.h"
+
+namespace cva {
+
+int v2_max_raw_nodes();
+size_t v2_resample_align_smem(int N);
+size_t v2_preprocess_smem(int n_out);
+size_t v2_align_smem(int N);
+bool v2_resample_align_supported(int N);
+
+cudaError_t launch_v2_resample_align(const double2* pts, const int64_t* off, int64_t pairs, int N,
+                                     const double2* tw, cva_alignment* out, double2* aligned,
+                                     cudaStream_t s);
+cudaError_t launch_v2_preprocess(const double2* pts, const int64_t* off, int64_t curves, int n_out,
+                                 int center_normalize, double2* out, int32_t* status,
+                                 cudaStream_t s);
+cudaError_t launch_v2_align(const double2* c1, const double2* c2, int64_t pairs, int N,
+                            const double2* tw, cva_alignment* out, double2* aligned,
+                            cudaStream_t s);
+cudaError_t launch_v2_align_interleaved(const double2* rows, int64_t pairs, int N, const double2* tw,
+                                        cva_alignment* out, double2* aligned, cudaStream_t s);
+cudaError_t launch_v2_srv_align(const double2* c1, const double2* c2, int64_t pairs, int N,
+                                const double2* tw, cva_alignment* out, double2* aligned,
+                                double2* qbuf, cudaStream_t s);
+
+}  // namespace cva

@@ -1,0 +1,256 @@
+// Pair stage of the alignment on one 256-thread CTA (v2): two concurrent
+// forward FFTs (one per 128-thread half, named barriers), the correlation
+// spectrum Z1 conj(Z2) fused into the first pass of the third FFT, a
+// deterministic two-phase argmax with the reference's tie band, and the
+// rotated, shifted aligned curve. Replaces correlation_all_shifts_fft +
+// pick_best + optimal_rotation_svd (proj/src/rigid_align.cpp:147-183, :31-61,
+// :82-102); the 4 real r2c + 4 real c2r FFTW transforms per pair become 3
+// complex transforms on z = x + i y.
+#pragma once
+
+#include <climits>
+
+#include "../../include/curvalign_cuda.h"
+#include "cva_common.cuh"
+#include "fft.cuh"
+
+namespace cva {
+namespace pf {
+
+constexpr int kT = 256;
+constexpr int kHalf = 128;
+constexpr double kTieRelTol = 1e-12;  // proj/src/rigid_align.cpp:16
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// One Stockham pass (see fft.cuh) reading through a functor.
+template <int R, int NT, typename Src>
+__device__ __forceinline__ void pass(Src src, double2* __restrict__ dst, int N, int Ns,
+                                     const double2* __restrict__ tw, int g) {
+  const int nb = N / R;
+  const int tws = N / (Ns * R);
+  for (int j = g; j < nb; j += NT) {
+    double2 v[R];
+    const int jm = j & (Ns - 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = src(j + r * nb);
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[r * jm * tws]));
+    }
+    dft_r<R>(v);
+    const int base = (j - jm) * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[base + r * Ns] = v[r];
+  }
+}
+
+// Forward FFT of length N (power of two) by NT threads (index g), first pass
+// reading through src0, then ping-ponging b0 -> b1 -> b0 ... Returns the
+// buffer holding the spectrum. sync() is the group barrier.
+template <int NT, typename Src, typename Sync>
+__device__ inline double2* group_fft(Src src0, double2* b0, double2* b1, int N,
+                                     const double2* __restrict__ tw, int g, Sync sync) {
+  const int maxR = N / NT >= 8 ? 8 : 4;
+  int Ns = 1;
+  double2* dst = b0;
+  double2* other = b1;
+  bool first = true;
+  while (Ns < N) {
+    const int rem = N / Ns;
+    const int R = (rem % 8 == 0 && maxR >= 8) ? 8 : (rem % 4 == 0 && maxR >= 4 ? 4 : 2);
+    if (first) {
+      if (R == 8) pass<8, NT>(src0, dst, N, Ns, tw, g);
+      else if (R == 4) pass<4, NT>(src0, dst, N, Ns, tw, g);
+      else pass<2, NT>(src0, dst, N, Ns, tw, g);
+      first = false;
+    } else {
+      const double2* in = other;
+      auto src = [in](int i) { return in[i]; };
+      if (R == 8) pass<8, NT>(src, dst, N, Ns, tw, g);
+      else if (R == 4) pass<4, NT>(src, dst, N, Ns, tw, g);
+      else pass<2, NT>(src, dst, N, Ns, tw, g);
+    }
+    sync();
+    Ns *= R;
+    double2* t = dst;
+    dst = other;
+    other = t;
+  }
+  return other;  // last written
+}
+
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
+
+struct PairIn {
+  const double2* z1;  // curve 1 samples (shared or global), uncentered
+  const double2* z2;  // curve 2 samples (global or shared), uncentered
+  double2 g1, g2;     // centroids subtracted on load
+  double sc1, sc2;    // scale applied after centering (1 for already-normalized input)
+};
+
+// Runs the pair stage. bufs: 4 * N double2 of shared memory (distinct from
+// the inputs). out: this pair's result (written by thread 0). aligned: this
+// pair's aligned curve (may alias in.z2: all reads happen before any write).
+// red: >= 16 double2 shared. Requires blockDim.x == 256, N power of two >= 8.
+__device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
+                                  const double2* __restrict__ tw, cva_alignment* out,
+                                  double2* aligned, double2* red) {
+  const int t = threadIdx.x;
+  const int grp = t / kHalf, g = t % kHalf;
+  double2* B0 = bufs;
+  double2* B1 = bufs + N;
+  double2* B2 = bufs + 2 * N;
+  double2* B3 = bufs + 3 * N;
+
+  // ---- two forward transforms of the normalized curves (normalization fused into the load)
+  double ss = 0.0;  // sum |z'|^2 of this group's curve (rigid_align.cpp:23-27)
+  double2* X;
+  {
+    const double2* src = grp == 0 ? in.z1 : in.z2;
+    const double2 c = grp == 0 ? in.g1 : in.g2;
+    const double sc = grp == 0 ? in.sc1 : in.sc2;
+    auto load = [&](int i) {
+      const double2 q = src[i];
+      const double2 z = make_double2((q.x - c.x) * sc, (q.y - c.y) * sc);
+      ss = fma(z.x, z.x, fma(z.y, z.y, ss));
+      return z;
+    };
+    auto sync = [grp]() { named_sync(1 + grp, kHalf); };
+    X = group_fft<kHalf>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, N, tw, g, sync);
+  }
+  __syncthreads();
+  // group 0's result is B0 or B1, group 1's is B2 or B3 (same pass count)
+  const bool in0 = (X == B0 || X == B2);
+  const double2* X1 = in0 ? B0 : B1;
+  const double2* X2 = in0 ? B2 : B3;
+  double2* F0 = in0 ? B1 : B0;
+  double2* F1 = in0 ? B3 : B2;
+
+  // ---- D_m = sum_l conj(z1_l) z2_{l+m} = IDFT(conj Z1 . Z2)_m = conj(FFT(Z1 conj Z2)_m) / N
+  auto prod = [X1, X2](int k) { return cmulconj(X1[k], X2[k]); };
+  auto sync_all = []() { __syncthreads(); };
+  const double2* F = group_fft<kT>(prod, F0, F1, N, tw, t, sync_all);
+
+  // ---- tie-broken argmax of |D_m| (rigid_align.cpp:31-47): max, then smallest index in band
+  const double invN = 1.0 / (double)N;
+  double best = -INFINITY;
+  for (int k = t; k < N; k += kT) {
+    const double2 f = F[k];
+    best = fmax(best, sqrt(fma(f.x, f.x, f.y * f.y)) * invN);
+  }
+  // block max of best and sums of s1 / s2 in one exchange
+  const int lane = t & 31, wid = t >> 5;
+  double s1 = grp == 0 ? ss : 0.0, s2 = grp == 1 ? ss : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (lane == 0) {
+    red[wid] = make_double2(best, s1);
+    red[8 + wid].x = s2;
+  }
+  __syncthreads();
+  best = -INFINITY;
+  s1 = s2 = 0.0;
+#pragma unroll
+  for (int w = 0; w < kT / 32; ++w) {
+    best = fmax(best, red[w].x);
+    s1 += red[w].y;
+    s2 += red[8 + w].x;
+  }
+  const double thr = best - kTieRelTol * fmax(1.0, fabs(best));
+  int cand = INT_MAX;
+  for (int k = t; k < N; k += kT) {
+    const double2 f = F[k];
+    if (sqrt(fma(f.x, f.x, f.y * f.y)) * invN >= thr) {
+      cand = k;
+      break;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
+  __shared__ int s_cand[8];
+  __shared__ int s_m;
+  __shared__ double2 s_rot;
+  if (lane == 0) s_cand[wid] = cand;
+  __syncthreads();
+  if (t == 0) {
+    int m = INT_MAX;
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) m = min(m, s_cand[w]);
+    cva_alignment r;
+    if (!isfinite(best) || m == INT_MAX) {
+      r.shift = 0;
+      r.t0 = 0.0;
+      r.theta = qnan();
+      r.trace = qnan();
+      r.energy = qnan();
+      r.degenerate = 0;
+      r.status = CVA_INVALID_ARGUMENT;  // non-finite correlation (rigid_align.cpp:83)
+      s_m = -1;
+    } else {
+      const double2 f = F[m];
+      const double trace = sqrt(fma(f.x, f.x, f.y * f.y)) * invN;
+      double theta = 0.0;
+      int degenerate = 0;
+      if (trace == 0.0)
+        degenerate = 1;  // rigid_align.cpp:86-88
+      else
+        theta = atan2(-f.y, f.x);  // arg D_m
+      double e = invN * (s1 + s2) - 2.0 * invN * trace;  // rigid_align.cpp:56-59
+      if (e < 0.0) e = 0.0;
+      r.shift = m;
+      r.t0 = (double)m * invN;
+      r.theta = theta;
+      r.trace = degenerate ? 0.0 : trace;
+      r.energy = e;
+      r.degenerate = degenerate;
+      r.status = CVA_OK;
+      s_m = m;
+      double sn, cs;
+      sincos(theta, &sn, &cs);
+      s_rot = make_double2(cs, sn);
+    }
+    *out = r;
+  }
+  __syncthreads();
+
+  // ---- aligned[l] = R(theta) z2'[(l + m) mod N]  (geometry.hpp:70-73; elastic.cpp:80)
+  if (aligned != nullptr) {
+    const int m = s_m;
+    constexpr int kMaxPer = 8;  // N <= 2048
+    double2 v[kMaxPer];
+    const double2 c = in.g2;
+    const double sc = in.sc2;
+    const double2 rot = s_rot;
+#pragma unroll
+    for (int q = 0; q < kMaxPer; ++q) {
+      const int j = t + q * kT;
+      if (j < N) {
+        const double2 z = in.z2[j];
+        const double2 p = make_double2((z.x - c.x) * sc, (z.y - c.y) * sc);
+        v[q] = m < 0 ? make_double2(qnan(), qnan())
+                     : make_double2(fma(rot.x, p.x, rot.y * p.y), fma(-rot.y, p.x, rot.x * p.y));
+      }
+    }
+    __syncthreads();  // in.z2 may alias `aligned`
+    const int mm = m < 0 ? 0 : m;
+#pragma unroll
+    for (int q = 0; q < kMaxPer; ++q) {
+      const int j = t + q * kT;
+      if (j < N) {
+        int l = j - mm;
+        if (l < 0) l += N;
+        aligned[l] = v[q];
+      }
+    }
+  }
+}
+
+}  // namespace pf
+}  // namespace cva

@@ -1,0 +1,435 @@
+// Arc-length spline resampling of one closed curve by one 256-thread CTA (v2).
+//
+// Replaces, per curve (reference file:line):
+//   arc_length_params              proj/src/curve.cpp:50-65
+//   PeriodicCubicSpline ctor/solve proj/src/spline.cpp:62-96, :16-58
+//   PeriodicCubicSpline::eval      proj/src/spline.cpp:98-117
+//   resample_uniform               proj/src/curve.cpp:67-91
+//   centroid / curve_length        proj/src/curve.cpp:17-32 (returned, applied by the caller)
+//
+// Layout: the raw curve (n <= kNMax nodes, 16 B each) and its knots s[0..n]
+// live in shared memory (24 B/node, 72 KB at the 3072-node maximum). Thread t
+// owns chunk [a_t, a_{t+1}) of K <= 256 knots (<= kCMax = 12 per chunk), and
+// keeps the chunk's right-hand sides and pivots in registers, so no per-knot
+// solver state is stored.
+//
+// The spline system is solved in the scaled unknowns mu = m / 6:
+//   h_{i-1} mu_{i-1} + 2 (h_{i-1} + h_i) mu_i + h_i mu_{i+1} = slope_i - slope_{i-1},
+//   slope_i = (y_{i+1} - y_i) / h_i,
+// and evaluated as  A y_i + B y_{i+1} + ((A^3 - A) mu_i + (B^3 - B) mu_{i+1}) h_i^2,
+// which is the reference's system and cubic (spline.cpp:80-92, :107-117) with
+// the factor 6 folded into mu.
+//
+// Solver (exact; no truncation):
+//   phase 1  each chunk eliminates its interior [a, b-1) by a forward Thomas
+//            sweep, expressing it through the interface unknowns w_{k-1}, w_k
+//            (= mu at the chunk's last knot b-1); the end values of the three
+//            back-substituted responses are accumulated as running sums.
+//   phase 2  the K interface rows form a cyclic tridiagonal system, solved by
+//            parallel cyclic reduction (log2 K steps, ping-pong buffers, one
+//            barrier per step, closed 2x2 solve at stride K/2).
+//   phase 3  each chunk re-sweeps its interior with the now-known boundary
+//            values and evaluates the resampled nodes inside its knot
+//            intervals during the back-substitution (no mu array is stored).
+//
+// Parity trap (P11): the reference's Sherman-Morrison split uses
+// u[n-1] = b[n-1], v[n-1] = a[n-1]/g where the cyclic corner is a[n-1], b[0]
+// (spline.cpp:20-26, :43-46), so the last row it solves is
+//   h_{n-2} mu_{n-2} + (2(h_{n-2}+h_{n-1}) + h_{n-1}(h_{n-1}-h_{n-2})/(2(h_{n-1}+h_0))) mu_{n-1}
+//     + h_{n-2} mu_0 = r_{n-1}.
+// That row is always an interface row here (chunk K-1 ends at n-1) and is
+// reproduced in phase 2.
+#pragma once
+
+#include "cva_common.cuh"
+
+namespace cva {
+namespace rs {
+
+constexpr int kT = 256;            // threads per CTA = max chunks
+constexpr int kCMax = 12;          // knots per chunk
+constexpr int kNMax = kT * kCMax;  // raw nodes per curve (3072)
+constexpr int kScratchDoubles = 10 * kT;  // PCR ping-pong (2 x 5 arrays); also F / W / MB
+
+__device__ __forceinline__ void bar_sync() { __syncthreads(); }
+
+__device__ __forceinline__ int num_chunks(int n) {
+  int K = 2;
+  while (K * 2 <= kT && K * 2 <= n / 2) K *= 2;
+  return K;
+}
+
+// Fast reciprocal: MUFU seed + 2 Newton steps (<= 1 ulp; the reference's
+// divisions are correctly rounded, the difference is far below the 1e-10 bar).
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// Block exclusive scan of one double per thread (kT threads); also returns the
+// total. red: >= 16 double2 of shared scratch.
+__device__ __forceinline__ double scan_excl(double v, double* total, double2* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  bar_sync();  // previous readers of red are done
+  double inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
+  }
+  if (lane == 31) red[wid].x = inc;
+  bar_sync();
+  double pre = 0.0, tot = 0.0;
+#pragma unroll
+  for (int w = 0; w < kT / 32; ++w) {
+    const double x = red[w].x;
+    if (w < wid) pre += x;
+    tot += x;
+  }
+  *total = tot;
+  return pre + inc - v;
+}
+
+// Sum of three doubles over the block (kT threads); every thread gets the sums.
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double2* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  bar_sync();
+  if (lane == 0) {
+    red[wid] = make_double2(a, b);
+    red[8 + wid].x = c;
+  }
+  bar_sync();
+  a = b = c = 0.0;
+#pragma unroll
+  for (int w = 0; w < kT / 32; ++w) {
+    a += red[w].x;
+    b += red[w].y;
+    c += red[8 + w].x;
+  }
+}
+
+struct CurveStats {
+  double2 centroid;  // vertex mean of the resampled nodes (curve.cpp:27-32)
+  double inv_len;    // 1 / polygon length incl. closing edge (curve.cpp:17-25, :41-48)
+  int bad;           // invalid input (too few / non-finite / coincident nodes)
+};
+
+// First sample index l in [0, N] with t_l = l / N >= x, t_l computed as the
+// reference does ((double)l / (double)N, curve.cpp:88). For N = 2^p, x * N is
+// exact and the answer is ceil(x N).
+template <bool kPow2>
+__device__ __forceinline__ int first_sample(double x, int N) {
+  const double nn = (double)N;
+  int l = (int)ceil(x * nn);
+  if (!kPow2) {
+    l = max(0, min(N, l));
+    while (l > 0 && (double)(l - 1) / nn >= x) --l;
+    while (l < N && (double)l / nn < x) ++l;
+  }
+  return l;
+}
+
+template <bool kPow2>
+__device__ __forceinline__ double sample_t(int l, int N, double invN) {
+  return kPow2 ? (double)l * invN : (double)l / (double)N;
+}
+
+// Resample the raw curve already in xy[0..n) (shared) at t_l = l/N, l < N, into
+// out[0..N) (shared or global), uncentered. Returns the centroid and 1/length of
+// the resampled polygon so that preprocess(c) = (out - centroid) * inv_len.
+// s: shared, >= n+1 doubles. scr: shared, kScratchDoubles. red: 16 double2.
+// Requires 4 <= n <= kNMax, N >= 8 (kPow2: N a power of two), blockDim.x == kT.
+template <bool kPow2>
+__device__ inline CurveStats resample_block(const double2* __restrict__ xy, int n, double* __restrict__ s,
+                                            double* __restrict__ scr, double2* __restrict__ red,
+                                            double2* __restrict__ out, const int N) {
+  const int t = threadIdx.x;
+  const int K = num_chunks(n);
+  const bool own = t < K;
+  const int a = own ? (t * n) / K : 0;
+  const int b = own ? ((t + 1) * n) / K : 0;
+  int bad = 0;
+
+  // ---- phase 0: chordal arc length, s[i] = S_i / S_n, s[n] = 1 (curve.cpp:50-65)
+  double acc = 0.0;
+  if (own) {
+    double2 p = xy[a];
+    for (int i = a; i < b; ++i) {
+      const double2 q = xy[i + 1 == n ? 0 : i + 1];
+      const double dx = q.x - p.x, dy = q.y - p.y;
+      const double d = sqrt(fma(dx, dx, dy * dy));
+      bad |= !(d > 0.0);
+      acc += d;
+      s[i + 1] = acc;
+      p = q;
+    }
+  }
+  double total;
+  const double off = scan_excl(acc, &total, red);
+  bad |= !isfinite(total);
+  const double inv_total = 1.0 / total;
+  if (own) {
+    for (int i = a; i < b; ++i) s[i + 1] = (s[i + 1] + off) * inv_total;
+  }
+  if (t == 0) s[0] = 0.0;
+  bar_sync();
+  if (t == 0) s[n] = 1.0;  // forced (curve.cpp:64); written after every chunk's store
+  bar_sync();
+
+  // ---- phase 1: rhs, forward sweep, chunk-end responses
+  double2 R[kCMax];  // right-hand sides, later forward values g
+  double IB[kCMax];  // 1 / pivot of interior rows
+  double2 v0f = make_double2(0, 0), v0l = make_double2(0, 0);
+  double vLf = 0, vLl = 0, vRf = 0, vRl = 0;
+  double hL = 0, hj = 0;  // h_{b-2}, h_{b-1}
+  double2 rj = make_double2(0, 0);  // rhs of the interface row b-1
+  const int M = b - 1 - a;  // interior knots (>= 1)
+  if (own) {
+    double si = s[a];
+    double hm = a == 0 ? s[n] - s[n - 1] : si - s[a - 1];
+    const double2 yp = xy[a == 0 ? n - 1 : a - 1];
+    double2 y0 = xy[a];
+    const double ihm = frcp(hm);
+    double2 slp = make_double2((y0.x - yp.x) * ihm, (y0.y - yp.y) * ihm);
+    double2 g = make_double2(0, 0);
+    double gL = 0, Q = 1.0, ib = 0;
+    double2 S = make_double2(0, 0);
+    double SL = 0;
+#pragma unroll
+    for (int j = 0; j < kCMax; ++j) {
+      if (j <= M) {
+        const int i = a + j;
+        const double sn = s[i + 1];
+        const double h = sn - si;
+        bad |= !(h > 0.0);  // strictly increasing knots (spline.cpp:66-68)
+        const double ih = frcp(h);
+        const double2 y1 = xy[i + 1 == n ? 0 : i + 1];
+        const double2 sl = make_double2((y1.x - y0.x) * ih, (y1.y - y0.y) * ih);
+        const double2 r = make_double2(sl.x - slp.x, sl.y - slp.y);
+        R[j] = r;
+        if (j < M) {  // interior row i
+          if (j == 0) {
+            ib = frcp(2.0 * (hm + h));
+            g = cscale(r, ib);
+            gL = -hm * ib;
+            S = g;
+            SL = gL;
+          } else {
+            const double cpr = hm * ib;
+            ib = frcp(fma(-hm, cpr, 2.0 * (hm + h)));
+            g = make_double2(fma(-hm, g.x, r.x) * ib, fma(-hm, g.y, r.y) * ib);
+            gL = -hm * gL * ib;
+            Q *= -cpr;
+            S.x = fma(g.x, Q, S.x);
+            S.y = fma(g.y, Q, S.y);
+            SL = fma(gL, Q, SL);
+          }
+          IB[j] = ib;
+          hL = h;  // h_L after the last interior row
+        } else {
+          hj = h;  // interface row: h_{b-1}
+          rj = r;
+        }
+        hm = h;
+        slp = sl;
+        y0 = y1;
+        si = sn;
+      }
+    }
+    v0l = g;
+    vLl = gL;
+    vRl = -hL * ib;
+    vRf = vRl * Q;
+    v0f = S;
+    vLf = SL;
+  }
+
+  // ---- phase 2: interface rows -> cyclic PCR
+  double* F = scr;  // [K][4]: v0f.x, v0f.y, vLf, vRf
+  if (own) {
+    F[4 * t + 0] = v0f.x;
+    F[4 * t + 1] = v0f.y;
+    F[4 * t + 2] = vLf;
+    F[4 * t + 3] = vRf;
+  }
+  bar_sync();
+  double ra = 0, rc = 0, rd = 1, rid = 1;
+  double2 rr = make_double2(0, 0);
+  if (own) {
+    const int tn = t + 1 == K ? 0 : t + 1;
+    const double2 nf = make_double2(F[4 * tn + 0], F[4 * tn + 1]);
+    const double nL = F[4 * tn + 2], nR = F[4 * tn + 3];
+    double dj = 2.0 * (hL + hj), sj = hj;
+    if (t == K - 1) {  // the reference's last row (see header, P11)
+      const double h0 = s[1] - s[0];
+      sj = hL;
+      dj = 2.0 * (hL + hj) + hj * (hj - hL) / (2.0 * (hj + h0));
+    }
+    const double2 r = rj;
+    ra = hL * vLl;
+    rd = dj + hL * vRl + sj * nL;
+    rc = sj * nR;
+    rr = make_double2(r.x - hL * v0l.x - sj * nf.x, r.y - hL * v0l.y - sj * nf.y);
+    rid = frcp(rd);
+  }
+  bar_sync();  // F fully consumed before the PCR buffers (aliasing it) are written
+  {
+    int buf = 0;
+    auto P = [&](int bsel, int arr) { return scr + (bsel * 5 + arr) * kT; };
+    if (own) {
+      P(0, 0)[t] = ra;
+      P(0, 1)[t] = rc;
+      P(0, 2)[t] = rid;
+      P(0, 3)[t] = rr.x;
+      P(0, 4)[t] = rr.y;
+    }
+    bar_sync();
+    for (int st = 1; st < K / 2; st *= 2) {
+      if (own) {
+        const int im = (t - st) & (K - 1), ip = (t + st) & (K - 1);
+        const double* A = P(buf, 0);
+        const double* C = P(buf, 1);
+        const double* ID = P(buf, 2);
+        const double al = -ra * ID[im], ga = -rc * ID[ip];
+        const double na = al * A[im], nc = ga * C[ip];
+        rd = rd + al * C[im] + ga * A[ip];
+        rr.x = rr.x + al * P(buf, 3)[im] + ga * P(buf, 3)[ip];
+        rr.y = rr.y + al * P(buf, 4)[im] + ga * P(buf, 4)[ip];
+        ra = na;
+        rc = nc;
+        rid = frcp(rd);
+        const int nb = buf ^ 1;
+        P(nb, 0)[t] = ra;
+        P(nb, 1)[t] = rc;
+        P(nb, 2)[t] = rid;
+        P(nb, 3)[t] = rr.x;
+        P(nb, 4)[t] = rr.y;
+      }
+      buf ^= 1;
+      bar_sync();
+    }
+    double2 w = make_double2(0, 0);
+    if (own) {
+      const int jp = (t + K / 2) & (K - 1);
+      const double ei = ra + rc, ej = P(buf, 0)[jp] + P(buf, 1)[jp];
+      const double dj = 1.0 / P(buf, 2)[jp];
+      const double2 rj = make_double2(P(buf, 3)[jp], P(buf, 4)[jp]);
+      const double idet = 1.0 / (rd * dj - ei * ej);
+      w = make_double2((rr.x * dj - ei * rj.x) * idet, (rr.y * dj - ei * rj.y) * idet);
+    }
+    // W and MB go to the buffer not read in the final step
+    double2* W = reinterpret_cast<double2*>(P(buf ^ 1, 0));
+    double2* MB = W + kT;
+    if (own) W[t] = w;
+    bar_sync();
+    double2 wl = make_double2(0, 0);
+    if (own) {
+      wl = W[t == 0 ? K - 1 : t - 1];
+      // mu at this chunk's first knot a (its first interior row), published for chunk t-1
+      MB[t] = make_double2(v0f.x + wl.x * vLf + w.x * vRf, v0f.y + wl.y * vLf + w.y * vRf);
+    }
+    bar_sync();
+
+    // ---- phase 3: interior re-solve + fused evaluation
+    double2 cacc = make_double2(0, 0);
+    if (own) {
+      const double2 mub = MB[t + 1 == K ? 0 : t + 1];
+      // forward with known boundary values (R[j] <- g_j)
+      double hm = a == 0 ? s[n] - s[n - 1] : s[a] - s[a - 1];
+      double2 g = make_double2(0, 0);
+#pragma unroll
+      for (int j = 0; j < kCMax; ++j) {
+        if (j < M) {
+          const int i = a + j;
+          const double h = s[i + 1] - s[i];
+          double2 r = R[j];
+          if (j == 0) {
+            r.x = fma(-hm, wl.x, r.x);
+            r.y = fma(-hm, wl.y, r.y);
+          }
+          if (j == M - 1) {
+            r.x = fma(-h, w.x, r.x);
+            r.y = fma(-h, w.y, r.y);
+          }
+          if (j == 0) {
+            g = cscale(r, IB[0]);
+          } else {
+            g = make_double2(fma(-hm, g.x, r.x) * IB[j], fma(-hm, g.y, r.y) * IB[j]);
+          }
+          R[j] = g;
+          hm = h;
+        }
+      }
+      // backward: intervals b-1, b-2, ..., a
+      const double invN = 1.0 / (double)N;
+      double s1 = s[b];
+      int hi = (t == K - 1) ? N : first_sample<kPow2>(s1, N);
+      double2 y1 = xy[b == n ? 0 : b];
+      double2 mu1 = mub;
+      double2 mu0 = w;
+#pragma unroll
+      for (int j = kCMax - 1; j >= 0; --j) {
+        if (j <= M) {
+          const int i = a + j;  // interval [s_i, s_{i+1})
+          const double s0 = s[i];
+          const double h = s1 - s0;
+          if (j < M) {
+            // mu_i = g_i - c'_i mu_{i+1}, c'_i = h_i / pivot_i
+            const double cpr = h * IB[j];
+            mu0 = (j == M - 1) ? R[j] : make_double2(fma(-cpr, mu1.x, R[j].x), fma(-cpr, mu1.y, R[j].y));
+          }
+          const double2 y0 = xy[i];
+          const int lo = first_sample<kPow2>(s0, N);
+          if (lo < hi) {
+            const double ih = frcp(h), h2 = h * h;
+            for (int l = lo; l < hi; ++l) {
+              const double tt = sample_t<kPow2>(l, N, invN);
+              const double A = (s1 - tt) * ih, B = (tt - s0) * ih;
+              const double ca = fma(A, A, -1.0) * A * h2, cb = fma(B, B, -1.0) * B * h2;
+              const double2 v = make_double2(fma(A, y0.x, fma(B, y1.x, fma(ca, mu0.x, cb * mu1.x))),
+                                             fma(A, y0.y, fma(B, y1.y, fma(ca, mu0.y, cb * mu1.y))));
+              out[l] = v;
+              cacc.x += v.x;
+              cacc.y += v.y;
+            }
+          }
+          hi = lo;
+          s1 = s0;
+          y1 = y0;
+          mu1 = mu0;
+        }
+      }
+    }
+    bar_sync();  // all samples written
+
+    // ---- polygon length of the resampled curve and centroid (one reduction)
+    double len = 0.0;
+    for (int l = t; l < N; l += kT) {
+      const double2 p = out[l], q = out[l + 1 == N ? 0 : l + 1];
+      const double dx = q.x - p.x, dy = q.y - p.y;
+      len += sqrt(fma(dx, dx, dy * dy));
+    }
+    double sx = cacc.x, sy = cacc.y;
+    double lb = len + (bad ? INFINITY : 0.0);
+    block_sum3(sx, sy, lb, red);
+    CurveStats cs;
+    const double invn = 1.0 / (double)N;
+    cs.centroid = make_double2(invn * sx, invn * sy);
+    cs.bad = !(lb > 0.0) || !isfinite(lb);
+    cs.inv_len = 1.0 / lb;
+    return cs;
+  }
+}
+
+}  // namespace rs
+}  // namespace cva
