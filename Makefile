@@ -4,7 +4,7 @@
 NVCC     ?= /usr/local/cuda/bin/nvcc
 CXX      ?= g++
 ARCH     := -gencode arch=compute_100a,code=sm_100a
-NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
+NVFLAGS  := $(ARCH) $(EXTRA) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 PKG      := paper_2501_17779_b200
 CSRC     := $(PKG)/csrc
 BUILD    := build

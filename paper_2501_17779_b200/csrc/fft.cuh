@@ -67,7 +67,7 @@ __device__ __forceinline__ void dft_r<8>(double2* v) { dft8(v); }
 
 // One Stockham pass of radix R over a length-N sequence, threads t in [0, T).
 template <int R>
-__device__ __forceinline__ void stockham_pass(const double2* __restrict__ in, double2* __restrict__ out,
+__device__ __forceinline__ void stockham_pass(const double2* in, double2* out,
                                               int N, int Ns, const double2* __restrict__ tw, int t,
                                               int T) {
   const int nb = N / R;

@@ -51,7 +51,7 @@ template <int N>
 __global__ void __launch_bounds__(kT, 2)
     resample_align_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off,
                           const double2* __restrict__ tw, cva_alignment* __restrict__ out,
-                          double2* __restrict__ aligned) {
+                          double2* aligned) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double2 red[16];
   double2* xy = reinterpret_cast<double2*>(smem);
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kT, 2)
 template <bool kPow2>
 __global__ void __launch_bounds__(kT, 2)
     preprocess_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off, int n_out,
-                      int center_normalize, double2* __restrict__ out,
+                      int center_normalize, double2* out,
                       int32_t* __restrict__ status) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double2 red[16];
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kT, 2)
 __global__ void __launch_bounds__(kT)
     align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
                  int64_t stride, const double2* __restrict__ tw, cva_alignment* __restrict__ out,
-                 double2* __restrict__ aligned) {
+                 double2* aligned) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double2 red[16];
   const int64_t p = blockIdx.x;
@@ -162,7 +162,7 @@ __device__ __forceinline__ double2 srv_at(const double2* __restrict__ c, int l, 
 __global__ void __launch_bounds__(kT)
     srv_align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
                      const double2* __restrict__ tw, cva_alignment* __restrict__ out,
-                     double2* __restrict__ aligned, double2* __restrict__ qbuf) {
+                     double2* aligned, double2* qbuf) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double2 red[16];
   const int64_t p = blockIdx.x;

@@ -27,7 +27,7 @@ __device__ __forceinline__ void named_sync(int id, int n) {
 
 // One Stockham pass (see fft.cuh) reading through a functor.
 template <int R, int NT, typename Src>
-__device__ __forceinline__ void pass(Src src, double2* __restrict__ dst, int N, int Ns,
+__device__ __forceinline__ void pass(Src src, double2* dst, int N, int Ns,
                                      const double2* __restrict__ tw, int g) {
   const int nb = N / R;
   const int tws = N / (Ns * R);

@@ -127,12 +127,14 @@ struct CurveStats {
 // First sample index l in [0, N] with t_l = l / N >= x, t_l computed as the
 // reference does ((double)l / (double)N, curve.cpp:88). For N = 2^p, x * N is
 // exact and the answer is ceil(x N).
+// Clamped to [0, N] so that garbage knots of an invalid curve (NaN / inf,
+// flagged separately) can never index outside the output.
 template <bool kPow2>
 __device__ __forceinline__ int first_sample(double x, int N) {
   const double nn = (double)N;
-  int l = (int)ceil(x * nn);
+  const double c = ceil(x * nn);
+  int l = c >= 0.0 ? (c <= nn ? (int)c : N) : 0;  // NaN -> 0
   if (!kPow2) {
-    l = max(0, min(N, l));
     while (l > 0 && (double)(l - 1) / nn >= x) --l;
     while (l < N && (double)l / nn < x) ++l;
   }
@@ -150,9 +152,11 @@ __device__ __forceinline__ double sample_t(int l, int N, double invN) {
 // s: shared, >= n+1 doubles. scr: shared, kScratchDoubles. red: 16 double2.
 // Requires 4 <= n <= kNMax, N >= 8 (kPow2: N a power of two), blockDim.x == kT.
 template <bool kPow2>
-__device__ inline CurveStats resample_block(const double2* __restrict__ xy, int n, double* __restrict__ s,
-                                            double* __restrict__ scr, double2* __restrict__ red,
-                                            double2* __restrict__ out, const int N) {
+// NOTE: no __restrict__ on these pointers: they carry data between threads
+// across __syncthreads(), and restrict lets the compiler forward stale loads
+// across the barrier.
+__device__ inline CurveStats resample_block(const double2* xy, int n, double* s, double* scr,
+                                            double2* red, double2* out, const int N) {
   const int t = threadIdx.x;
   const int K = num_chunks(n);
   const bool own = t < K;
