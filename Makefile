@@ -12,7 +12,17 @@ REF      ?= /root/reference
 
 KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h $(CSRC)/fused.h include/curvalign_cuda.h
 
-.PHONY: all lib synth dropin oracle ref clean
+.PHONY: all lib synth dropin oracle ref clean prof
+
+# Phase-timing build (tools/phase_timing.py): separate .so, never shipped.
+prof: $(PKG)/libcurvalign_cuda_prof.so
+$(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kernels.cu $(KERNEL_HDRS) $(CSRC)/prof.cuh
+	@mkdir -p $(BUILD)/prof
+	$(NVCC) $(NVFLAGS) -DCVA_PHASE_TIMING -c $(CSRC)/fused.cu -o $(BUILD)/prof/fused.o
+	$(NVCC) $(NVFLAGS) -c $(CSRC)/kernels.cu -o $(BUILD)/prof/kernels.o
+	$(NVCC) $(NVFLAGS) -x cu -c $(CSRC)/capi.cpp -o $(BUILD)/prof/capi.o
+	$(NVCC) $(NVFLAGS) -c $(CSRC)/probe.cu -o $(BUILD)/prof/probe.o
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(BUILD)/prof/*.o
 all: lib synth oracle ref
 
 lib: $(PKG)/libcurvalign_cuda.so

@@ -7,7 +7,14 @@
 #include "../../include/curvalign_cuda.h"
 #include "fused.h"
 #include "pairfft.cuh"
+#include "prof.cuh"
 #include "resample.cuh"
+
+#ifdef CVA_PHASE_TIMING
+extern "C" int cva_debug_set_prof(long long* p) {
+  return cudaMemcpyToSymbol(g_cva_prof, &p, sizeof(p)) == cudaSuccess ? 0 : 4;
+}
+#endif
 
 namespace cva {
 namespace v2 {
@@ -70,12 +77,15 @@ __global__ void __launch_bounds__(kT, 2)
     for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
     return;
   }
+  CVA_MARK(0);
   load_raw(pts + a0, xy, na);
   __syncthreads();
-  const rs::CurveStats A = rs::resample_block<true>(xy, na, s, scr, red, Z1, N);
+  CVA_MARK(1);
+  const rs::CurveStats A = rs::resample_block<true>(xy, na, s, scr, red, Z1, N, 2);
   load_raw(pts + a1, xy, nb);
   __syncthreads();
-  const rs::CurveStats B = rs::resample_block<true>(xy, nb, s, scr, red, al, N);
+  CVA_MARK(10);
+  const rs::CurveStats B = rs::resample_block<true>(xy, nb, s, scr, red, al, N, 11);
   if (A.bad || B.bad) {
     if (threadIdx.x == 0) write_bad(out + p, CVA_INVALID_ARGUMENT);
     for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
@@ -211,14 +221,14 @@ cudaError_t set_smem(const void* fn, size_t bytes) {
 int v2_max_raw_nodes() { return rs::kNMax; }
 
 size_t v2_resample_align_smem(int N) {
-  const size_t fft = 4 * sizeof(double2) * (size_t)N;
+  const size_t fft = 4 * sizeof(double2) * (size_t)pf::padded_len(N);
   const size_t raw = v2::kRawBytes > fft ? v2::kRawBytes : fft;
   return raw + v2::kScrBytes + sizeof(double2) * (size_t)N;
 }
 size_t v2_preprocess_smem(int n_out) {
   return v2::kRawBytes + v2::kScrBytes + sizeof(double2) * (size_t)n_out;
 }
-size_t v2_align_smem(int N) { return 4 * sizeof(double2) * (size_t)N; }
+size_t v2_align_smem(int N) { return 4 * sizeof(double2) * (size_t)pf::padded_len(N); }
 
 bool v2_resample_align_supported(int N) { return N == 512 || N == 1024; }
 

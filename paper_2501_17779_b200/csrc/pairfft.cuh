@@ -13,6 +13,7 @@
 #include "../../include/curvalign_cuda.h"
 #include "cva_common.cuh"
 #include "fft.cuh"
+#include "prof.cuh"
 
 namespace cva {
 namespace pf {
@@ -20,6 +21,11 @@ namespace pf {
 constexpr int kT = 256;
 constexpr int kHalf = 128;
 constexpr double kTieRelTol = 1e-12;  // proj/src/rigid_align.cpp:16
+
+// Shared-memory index with one pad slot every 8 double2 (128 B): Stockham
+// stores at stride R (first passes) become bank-conflict free.
+__device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
+__host__ __device__ constexpr int padded_len(int n) { return n + n / 8; }
 
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -43,7 +49,7 @@ __device__ __forceinline__ void pass(Src src, double2* dst, int N, int Ns,
     dft_r<R>(v);
     const int base = (j - jm) * R + jm;
 #pragma unroll
-    for (int r = 0; r < R; ++r) dst[base + r * Ns] = v[r];
+    for (int r = 0; r < R; ++r) dst[pad(base + r * Ns)] = v[r];
   }
 }
 
@@ -68,7 +74,7 @@ __device__ inline double2* group_fft(Src src0, double2* b0, double2* b1, int N,
       first = false;
     } else {
       const double2* in = other;
-      auto src = [in](int i) { return in[i]; };
+      auto src = [in](int i) { return in[pad(i)]; };
       if (R == 8) pass<8, NT>(src, dst, N, Ns, tw, g);
       else if (R == 4) pass<4, NT>(src, dst, N, Ns, tw, g);
       else pass<2, NT>(src, dst, N, Ns, tw, g);
@@ -91,7 +97,7 @@ struct PairIn {
   double sc1, sc2;    // scale applied after centering (1 for already-normalized input)
 };
 
-// Runs the pair stage. bufs: 4 * N double2 of shared memory (distinct from
+// Runs the pair stage. bufs: 4 * padded_len(N) double2 of shared memory (distinct from
 // the inputs). out: this pair's result (written by thread 0). aligned: this
 // pair's aligned curve (may alias in.z2: all reads happen before any write).
 // red: >= 16 double2 shared. Requires blockDim.x == 256, N power of two >= 8.
@@ -100,10 +106,11 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
                                   double2* aligned, double2* red) {
   const int t = threadIdx.x;
   const int grp = t / kHalf, g = t % kHalf;
+  const int NP = padded_len(N);
   double2* B0 = bufs;
-  double2* B1 = bufs + N;
-  double2* B2 = bufs + 2 * N;
-  double2* B3 = bufs + 3 * N;
+  double2* B1 = bufs + NP;
+  double2* B2 = bufs + 2 * NP;
+  double2* B3 = bufs + 3 * NP;
 
   // ---- two forward transforms of the normalized curves (normalization fused into the load)
   double ss = 0.0;  // sum |z'|^2 of this group's curve (rigid_align.cpp:23-27)
@@ -122,6 +129,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     X = group_fft<kHalf>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, N, tw, g, sync);
   }
   __syncthreads();
+  CVA_MARK(20);
   // group 0's result is B0 or B1, group 1's is B2 or B3 (same pass count)
   const bool in0 = (X == B0 || X == B2);
   const double2* X1 = in0 ? B0 : B1;
@@ -130,44 +138,50 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   double2* F1 = in0 ? B3 : B2;
 
   // ---- D_m = sum_l conj(z1_l) z2_{l+m} = IDFT(conj Z1 . Z2)_m = conj(FFT(Z1 conj Z2)_m) / N
-  auto prod = [X1, X2](int k) { return cmulconj(X1[k], X2[k]); };
+  auto prod = [X1, X2](int k) { return cmulconj(X1[pad(k)], X2[pad(k)]); };
   auto sync_all = []() { __syncthreads(); };
   const double2* F = group_fft<kT>(prod, F0, F1, N, tw, t, sync_all);
 
+  CVA_MARK(21);
   // ---- tie-broken argmax of |D_m| (rigid_align.cpp:31-47): max, then smallest index in band
+  // |D_m| = |F_m| / N. The max and the band test run on squared magnitudes;
+  // the band threshold is formed exactly as the reference does (on |D|).
   const double invN = 1.0 / (double)N;
-  double best = -INFINITY;
+  double best2 = -1.0;
   for (int k = t; k < N; k += kT) {
-    const double2 f = F[k];
-    best = fmax(best, sqrt(fma(f.x, f.x, f.y * f.y)) * invN);
+    const double2 f = F[pad(k)];
+    best2 = fmax(best2, fma(f.x, f.x, f.y * f.y));
   }
-  // block max of best and sums of s1 / s2 in one exchange
+  // block max of best2 and sums of s1 / s2 in one exchange
   const int lane = t & 31, wid = t >> 5;
   double s1 = grp == 0 ? ss : 0.0, s2 = grp == 1 ? ss : 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+    best2 = fmax(best2, __shfl_xor_sync(0xffffffffu, best2, o));
     s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     s2 += __shfl_xor_sync(0xffffffffu, s2, o);
   }
   if (lane == 0) {
-    red[wid] = make_double2(best, s1);
+    red[wid] = make_double2(best2, s1);
     red[8 + wid].x = s2;
   }
   __syncthreads();
-  best = -INFINITY;
+  best2 = -1.0;
   s1 = s2 = 0.0;
 #pragma unroll
   for (int w = 0; w < kT / 32; ++w) {
-    best = fmax(best, red[w].x);
+    best2 = fmax(best2, red[w].x);
     s1 += red[w].y;
     s2 += red[8 + w].x;
   }
+  const double best = sqrt(best2) * invN;  // NaN if the correlation is not finite
   const double thr = best - kTieRelTol * fmax(1.0, fabs(best));
+  const double thrN = thr * (double)N;
+  const double thr2 = thr > 0.0 ? thrN * thrN : -1.0;  // |F|^2 >= (thr N)^2  <=>  |D| >= thr
   int cand = INT_MAX;
   for (int k = t; k < N; k += kT) {
-    const double2 f = F[k];
-    if (sqrt(fma(f.x, f.x, f.y * f.y)) * invN >= thr) {
+    const double2 f = F[pad(k)];
+    if (fma(f.x, f.x, f.y * f.y) >= thr2) {
       cand = k;
       break;
     }
@@ -184,7 +198,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
 #pragma unroll
     for (int w = 0; w < kT / 32; ++w) m = min(m, s_cand[w]);
     cva_alignment r;
-    if (!isfinite(best) || m == INT_MAX) {
+    if (!isfinite(best) || best2 < 0.0 || m == INT_MAX) {
       r.shift = 0;
       r.t0 = 0.0;
       r.theta = qnan();
@@ -194,7 +208,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       r.status = CVA_INVALID_ARGUMENT;  // non-finite correlation (rigid_align.cpp:83)
       s_m = -1;
     } else {
-      const double2 f = F[m];
+      const double2 f = F[pad(m)];
       const double trace = sqrt(fma(f.x, f.x, f.y * f.y)) * invN;
       double theta = 0.0;
       int degenerate = 0;
@@ -220,6 +234,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   }
   __syncthreads();
 
+  CVA_MARK(22);
   // ---- aligned[l] = R(theta) z2'[(l + m) mod N]  (geometry.hpp:70-73; elastic.cpp:80)
   if (aligned != nullptr) {
     const int m = s_m;
@@ -250,6 +265,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       }
     }
   }
+  CVA_MARK(23);
 }
 
 }  // namespace pf

@@ -42,6 +42,7 @@
 #pragma once
 
 #include "cva_common.cuh"
+#include "prof.cuh"
 
 namespace cva {
 namespace rs {
@@ -68,6 +69,18 @@ __device__ __forceinline__ double frcp(double x) {
   r = fma(r, e, r);
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
+}
+
+// Fast sqrt: MUFU rsqrt seed, 2 Newton steps, one final correction (<= 1 ulp).
+__device__ __forceinline__ double fsqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double hx = 0.5 * x;
+  r = r * fma(-hx * r, r, 1.5);
+  r = r * fma(-hx * r, r, 1.5);
+  double y = x * r;
+  y = fma(fma(-y, y, x), 0.5 * r, y);
+  return x > 0.0 ? y : (x == 0.0 ? 0.0 : __longlong_as_double(0x7ff8000000000000ULL));
 }
 
 // Block exclusive scan of one double per thread (kT threads); also returns the
@@ -156,7 +169,8 @@ template <bool kPow2>
 // across __syncthreads(), and restrict lets the compiler forward stale loads
 // across the barrier.
 __device__ inline CurveStats resample_block(const double2* xy, int n, double* s, double* scr,
-                                            double2* red, double2* out, const int N) {
+                                            double2* red, double2* out, const int N,
+                                            const int pb = 0 /* phase-stamp base */) {
   const int t = threadIdx.x;
   const int K = num_chunks(n);
   const bool own = t < K;
@@ -167,15 +181,14 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
   // ---- phase 0: chordal arc length, s[i] = S_i / S_n, s[n] = 1 (curve.cpp:50-65)
   double acc = 0.0;
   if (own) {
-    double2 p = xy[a];
+#pragma unroll 4
     for (int i = a; i < b; ++i) {
-      const double2 q = xy[i + 1 == n ? 0 : i + 1];
+      const double2 p = xy[i], q = xy[i + 1 == n ? 0 : i + 1];
       const double dx = q.x - p.x, dy = q.y - p.y;
-      const double d = sqrt(fma(dx, dx, dy * dy));
+      const double d = fsqrt(fma(dx, dx, dy * dy));
       bad |= !(d > 0.0);
       acc += d;
       s[i + 1] = acc;
-      p = q;
     }
   }
   double total;
@@ -183,6 +196,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
   bad |= !isfinite(total);
   const double inv_total = 1.0 / total;
   if (own) {
+#pragma unroll 4
     for (int i = a; i < b; ++i) s[i + 1] = (s[i + 1] + off) * inv_total;
   }
   if (t == 0) s[0] = 0.0;
@@ -190,6 +204,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
   if (t == 0) s[n] = 1.0;  // forced (curve.cpp:64); written after every chunk's store
   bar_sync();
 
+  CVA_MARK(pb + 0);
   // ---- phase 1: rhs, forward sweep, chunk-end responses
   double2 R[kCMax];  // right-hand sides, later forward values g
   double IB[kCMax];  // 1 / pivot of interior rows
@@ -258,6 +273,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
     vLf = SL;
   }
 
+  CVA_MARK(pb + 1);
   // ---- phase 2: interface rows -> cyclic PCR
   double* F = scr;  // [K][4]: v0f.x, v0f.y, vLf, vRf
   if (own) {
@@ -344,6 +360,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
     }
     bar_sync();
 
+    CVA_MARK(pb + 2);
     // ---- phase 3: interior re-solve + fused evaluation
     double2 cacc = make_double2(0, 0);
     if (own) {
@@ -374,10 +391,14 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
           hm = h;
         }
       }
-      // backward: intervals b-1, b-2, ..., a
+      CVA_MARK(pb + 5);
+      // backward: intervals b-1, b-2, ..., a; the chunk's samples are walked
+      // downwards from the last one below s_b (sample l lies in interval i iff
+      // s_i <= t_l < s_{i+1}, the reference's upper_bound rule, spline.cpp:98-105)
       const double invN = 1.0 / (double)N;
       double s1 = s[b];
-      int hi = (t == K - 1) ? N : first_sample<kPow2>(s1, N);
+      int l = ((t == K - 1) ? N : first_sample<kPow2>(s1, N)) - 1;
+      double tl = sample_t<kPow2>(l, N, invN);
       double2 y1 = xy[b == n ? 0 : b];
       double2 mu1 = mub;
       double2 mu0 = w;
@@ -393,39 +414,41 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
             mu0 = (j == M - 1) ? R[j] : make_double2(fma(-cpr, mu1.x, R[j].x), fma(-cpr, mu1.y, R[j].y));
           }
           const double2 y0 = xy[i];
-          const int lo = first_sample<kPow2>(s0, N);
-          if (lo < hi) {
+          if (l >= 0 && tl >= s0) {
             const double ih = frcp(h), h2 = h * h;
-            for (int l = lo; l < hi; ++l) {
-              const double tt = sample_t<kPow2>(l, N, invN);
-              const double A = (s1 - tt) * ih, B = (tt - s0) * ih;
+            do {
+              const double A = (s1 - tl) * ih, B = (tl - s0) * ih;
               const double ca = fma(A, A, -1.0) * A * h2, cb = fma(B, B, -1.0) * B * h2;
               const double2 v = make_double2(fma(A, y0.x, fma(B, y1.x, fma(ca, mu0.x, cb * mu1.x))),
                                              fma(A, y0.y, fma(B, y1.y, fma(ca, mu0.y, cb * mu1.y))));
               out[l] = v;
               cacc.x += v.x;
               cacc.y += v.y;
-            }
+              --l;
+              tl = sample_t<kPow2>(l, N, invN);
+            } while (l >= 0 && tl >= s0);
           }
-          hi = lo;
           s1 = s0;
           y1 = y0;
           mu1 = mu0;
         }
       }
     }
+    CVA_MARK(pb + 6);
     bar_sync();  // all samples written
+    CVA_MARK(pb + 3);
 
     // ---- polygon length of the resampled curve and centroid (one reduction)
     double len = 0.0;
     for (int l = t; l < N; l += kT) {
       const double2 p = out[l], q = out[l + 1 == N ? 0 : l + 1];
       const double dx = q.x - p.x, dy = q.y - p.y;
-      len += sqrt(fma(dx, dx, dy * dy));
+      len += fsqrt(fma(dx, dx, dy * dy));
     }
     double sx = cacc.x, sy = cacc.y;
     double lb = len + (bad ? INFINITY : 0.0);
     block_sum3(sx, sy, lb, red);
+    CVA_MARK(pb + 4);
     CurveStats cs;
     const double invn = 1.0 / (double)N;
     cs.centroid = make_double2(invn * sx, invn * sy);

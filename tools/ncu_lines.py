@@ -34,10 +34,11 @@ def sass_page(report, kernel):
     return recs
 
 
-def line_map(lib, kernel):
+def line_map(lib, kernel, recs=None):
+    """addr -> file:line for the function whose SASS matches the ncu page."""
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
-    m = {}
+    maps, ops = {}, {}
     for cub in glob.glob(os.path.join(tmp, "*.cubin")):
         txt = subprocess.run(["nvdisasm", "-gi", "-c", cub], capture_output=True, text=True).stdout
         cur_fn, loc, fresh = None, None, True
@@ -45,6 +46,9 @@ def line_map(lib, kernel):
             f = re.match(r"\s*\.text\.(\S+):", ln)
             if f:
                 cur_fn = f.group(1)
+                if kernel in cur_fn:
+                    maps.setdefault(cur_fn, {})
+                    ops.setdefault(cur_fn, [])
                 continue
             g = re.search(r'//## File "([^"]+)", line (\d+)', ln)
             if g:
@@ -52,12 +56,17 @@ def line_map(lib, kernel):
                     loc = f"{os.path.basename(g.group(1))}:{g.group(2)}"
                     fresh = False
                 continue
-            a = re.match(r"\s*/\*([0-9a-f]{4,})\*/", ln)
+            a = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s+(.*?);", ln)
             if a:
                 fresh = True
                 if cur_fn and kernel in cur_fn:
-                    m[int(a.group(1), 16)] = loc
-    return m
+                    maps[cur_fn][int(a.group(1), 16)] = loc
+                    ops[cur_fn].append(a.group(2).split()[0])
+    if recs is None or len(maps) <= 1:
+        return next(iter(maps.values()), {})
+    want = [r["Source"].split()[0] for r in recs]
+    best = max(maps, key=lambda fn: (len(ops[fn]) == len(want), sum(a == b for a, b in zip(ops[fn], want))))
+    return maps[best]
 
 
 def main():
@@ -68,7 +77,7 @@ def main():
     ap.add_argument("--top", type=int, default=40)
     a = ap.parse_args()
     recs = sass_page(a.report, a.kernel)
-    lm = line_map(a.lib, a.kernel.split("::")[-1])
+    lm = line_map(a.lib, a.kernel.split("::")[-1], recs)
     samp = collections.Counter()
     inst = collections.Counter()
     tot_s = tot_i = 0
