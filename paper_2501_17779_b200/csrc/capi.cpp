@@ -78,10 +78,13 @@ int smem_limit() {
 }
 
 // FFT sizes the shared-memory kernels cover in this build.
+// Shared-memory pair kernels: power-of-two N <= 2048, other N zero-padded to a
+// power of two M >= 2N (pairfft.cuh), so N <= 1024.
 int check_fft_size(int64_t n) {
   if (n < 4) return fail(CVA_INVALID_ARGUMENT, "align: need at least 4 nodes");
-  if (!is_pow2(n) || n > 2048)
-    return fail(CVA_UNSUPPORTED, "align: this build's shared-memory FFT covers N = 2^p <= 2048");
+  if (n > 2048 || cva::v2_fft_len((int)n) > 2048)
+    return fail(CVA_UNSUPPORTED, "align: the shared-memory pair kernels cover N <= 2048 "
+                                 "(powers of two) and N <= 1024 otherwise");
   return CVA_OK;
 }
 
@@ -188,7 +191,7 @@ int cva_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n
   if (int rc = require_device()) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
-  if (int rc = get_twiddles((int)n, s, &tw)) return rc;
+  if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
   return finish(cva::launch_v2_align((const double2*)c1, (const double2*)c2, pairs, (int)n, tw,
                                      out, (double2*)aligned, s),
                 "align launch");
@@ -245,7 +248,7 @@ int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int
     if (int rc = device_max_n(offsets, 2 * pairs, s, &max_n_in)) return rc;
   const int nmax = (int)std::max<int64_t>(max_n_in, 4);
   const double2* tw = nullptr;
-  if (int rc = get_twiddles((int)n_out, s, &tw)) return rc;
+  if (int rc = get_twiddles(cva::v2_fft_len((int)n_out), s, &tw)) return rc;
   if (nmax <= cva::v2_max_raw_nodes()) {
     const size_t ab = sizeof(double2) * (size_t)(pairs * n_out);
     if (cva::v2_resample_align_supported((int)n_out)) {
@@ -273,12 +276,19 @@ int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int
     cudaFreeAsync(ws, s);
     return finish(e, "preprocess+align launch");
   }
-  if (int rc = check_resample_nmax(nmax, n_out,
-                                   cva::preprocess_align_smem_bytes(nmax, (int)n_out)))
+  // raw curves beyond the v2 resampler: general resampler into scratch, then align
+  if (int rc = check_resample_nmax(nmax, n_out, cva::resample_smem_bytes(nmax, (int)n_out)))
     return rc;
-  return finish(cva::launch_preprocess_align((const double2*)points, offsets, pairs, nmax,
-                                             (int)n_out, tw, out, (double2*)aligned, s),
-                "preprocess_align launch");
+  void* ws = nullptr;
+  if (scratch_alloc(&ws, 2 * sizeof(double2) * (size_t)(pairs * n_out), s) != cudaSuccess)
+    return fail(CVA_BAD_ALLOC, "scratch allocation failed");
+  cudaError_t e = cva::launch_preprocess_resample((const double2*)points, offsets, 2 * pairs, nmax,
+                                                  (int)n_out, 1, (double2*)ws, nullptr, s);
+  if (e == cudaSuccess)
+    e = cva::launch_v2_align_interleaved((const double2*)ws, pairs, (int)n_out, tw, out,
+                                         (double2*)aligned, s);
+  cudaFreeAsync(ws, s);
+  return finish(e, "preprocess+align launch");
 }
 
 int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
@@ -291,7 +301,7 @@ int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64
   if (int rc = require_device()) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
-  if (int rc = get_twiddles((int)n, s, &tw)) return rc;
+  if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
   void* ws = nullptr;
   if (scratch_alloc(&ws, 2 * sizeof(double2) * (size_t)(pairs * n), s) != cudaSuccess)
     return fail(CVA_BAD_ALLOC, "scratch allocation failed");

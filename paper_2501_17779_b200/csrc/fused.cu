@@ -228,7 +228,8 @@ size_t v2_resample_align_smem(int N) {
 size_t v2_preprocess_smem(int n_out) {
   return v2::kRawBytes + v2::kScrBytes + sizeof(double2) * (size_t)n_out;
 }
-size_t v2_align_smem(int N) { return 4 * sizeof(double2) * (size_t)pf::padded_len(N); }
+size_t v2_align_smem(int N) { return 4 * sizeof(double2) * (size_t)pf::padded_len(pf::fft_len(N)); }
+int v2_fft_len(int N) { return pf::fft_len(N); }
 
 bool v2_resample_align_supported(int N) { return N == 512 || N == 1024; }
 

@@ -13,6 +13,7 @@ int v2_max_raw_nodes();
 size_t v2_resample_align_smem(int N);
 size_t v2_preprocess_smem(int n_out);
 size_t v2_align_smem(int N);
+int v2_fft_len(int N);  // power-of-two transform length used for N data points
 bool v2_resample_align_supported(int N);
 
 cudaError_t launch_v2_resample_align(const double2* pts, const int64_t* off, int64_t pairs, int N,

@@ -97,16 +97,32 @@ struct PairIn {
   double sc1, sc2;    // scale applied after centering (1 for already-normalized input)
 };
 
-// Runs the pair stage. bufs: 4 * padded_len(N) double2 of shared memory (distinct from
-// the inputs). out: this pair's result (written by thread 0). aligned: this
-// pair's aligned curve (may alias in.z2: all reads happen before any write).
-// red: >= 16 double2 shared. Requires blockDim.x == 256, N power of two >= 8.
+// FFT length for N data points: N itself when N is a power of two, else the
+// smallest power of two M >= 2N. In the padded case the circular correlation
+// of length N is the first N lags of the length-M circular correlation of
+// a = [z1, 0...] and b = [z2, z2, 0...]: for m < N and l < N, l + m < 2N <= M,
+// so no term wraps and b_{l+m} = z2_{(l+m) mod N}. This gives any N >= 4 (the
+// reference's FFTW path accepts any length) with power-of-two
+// transforms only.
+__host__ __device__ inline int fft_len(int N) {
+  if ((N & (N - 1)) == 0) return N;
+  int M = 1;
+  while (M < 2 * N) M <<= 1;
+  return M;
+}
+
+// Runs the pair stage. bufs: 4 * padded_len(M) double2 of shared memory (distinct from
+// the inputs), M = fft_len(N), tw the length-M twiddle table. out: this pair's
+// result (written by thread 0). aligned: this pair's aligned curve (may alias
+// in.z2: all reads happen before any write). red: >= 16 double2 shared.
+// Requires blockDim.x == 256, N >= 4, M <= 2048.
 __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
                                   const double2* __restrict__ tw, cva_alignment* out,
                                   double2* aligned, double2* red) {
   const int t = threadIdx.x;
   const int grp = t / kHalf, g = t % kHalf;
-  const int NP = padded_len(N);
+  const int M = fft_len(N);
+  const int NP = padded_len(M);
   double2* B0 = bufs;
   double2* B1 = bufs + NP;
   double2* B2 = bufs + 2 * NP;
@@ -119,14 +135,18 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     const double2* src = grp == 0 ? in.z1 : in.z2;
     const double2 c = grp == 0 ? in.g1 : in.g2;
     const double sc = grp == 0 ? in.sc1 : in.sc2;
+    // group 0: a = [z1, 0...]; group 1: b = [z2, z2, 0...] (M == N: plain z)
+    const int lim = (grp == 0 || M == N) ? N : 2 * N;
     auto load = [&](int i) {
-      const double2 q = src[i];
+      if (i >= lim) return make_double2(0.0, 0.0);
+      const int k = i < N ? i : i - N;
+      const double2 q = src[k];
       const double2 z = make_double2((q.x - c.x) * sc, (q.y - c.y) * sc);
-      ss = fma(z.x, z.x, fma(z.y, z.y, ss));
+      if (i < N) ss = fma(z.x, z.x, fma(z.y, z.y, ss));
       return z;
     };
     auto sync = [grp]() { named_sync(1 + grp, kHalf); };
-    X = group_fft<kHalf>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, N, tw, g, sync);
+    X = group_fft<kHalf>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, M, tw, g, sync);
   }
   __syncthreads();
   CVA_MARK(20);
@@ -140,13 +160,14 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   // ---- D_m = sum_l conj(z1_l) z2_{l+m} = IDFT(conj Z1 . Z2)_m = conj(FFT(Z1 conj Z2)_m) / N
   auto prod = [X1, X2](int k) { return cmulconj(X1[pad(k)], X2[pad(k)]); };
   auto sync_all = []() { __syncthreads(); };
-  const double2* F = group_fft<kT>(prod, F0, F1, N, tw, t, sync_all);
+  const double2* F = group_fft<kT>(prod, F0, F1, M, tw, t, sync_all);
 
   CVA_MARK(21);
   // ---- tie-broken argmax of |D_m| (rigid_align.cpp:31-47): max, then smallest index in band
   // |D_m| = |F_m| / N. The max and the band test run on squared magnitudes;
   // the band threshold is formed exactly as the reference does (on |D|).
-  const double invN = 1.0 / (double)N;
+  const double invN = 1.0 / (double)N;  // h = 1/N (rigid_align.cpp:56)
+  const double invM = 1.0 / (double)M;  // D_m = conj(F_m) / M
   double best2 = -1.0;
   for (int k = t; k < N; k += kT) {
     const double2 f = F[pad(k)];
@@ -174,9 +195,9 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     s1 += red[w].y;
     s2 += red[8 + w].x;
   }
-  const double best = sqrt(best2) * invN;  // NaN if the correlation is not finite
+  const double best = sqrt(best2) * invM;  // NaN if the correlation is not finite
   const double thr = best - kTieRelTol * fmax(1.0, fabs(best));
-  const double thrN = thr * (double)N;
+  const double thrN = thr * (double)M;
   const double thr2 = thr > 0.0 ? thrN * thrN : -1.0;  // |F|^2 >= (thr N)^2  <=>  |D| >= thr
   int cand = INT_MAX;
   for (int k = t; k < N; k += kT) {
@@ -209,7 +230,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       s_m = -1;
     } else {
       const double2 f = F[pad(m)];
-      const double trace = sqrt(fma(f.x, f.x, f.y * f.y)) * invN;
+      const double trace = sqrt(fma(f.x, f.x, f.y * f.y)) * invM;
       double theta = 0.0;
       int degenerate = 0;
       if (trace == 0.0)
@@ -219,7 +240,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       double e = invN * (s1 + s2) - 2.0 * invN * trace;  // rigid_align.cpp:56-59
       if (e < 0.0) e = 0.0;
       r.shift = m;
-      r.t0 = (double)m * invN;
+      r.t0 = (double)m / (double)N;  // rigid_align.cpp:52
       r.theta = theta;
       r.trace = degenerate ? 0.0 : trace;
       r.energy = e;

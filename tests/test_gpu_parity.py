@@ -79,11 +79,6 @@ def test_kat_cases(cuda, case):
     else:
         c1, c2 = g[f"{case}_c1"], g[f"{case}_c2"]
     key = {"circle": "circle_res", "hippo_rot": "hippo_rot"}.get(case, f"{case}_res")
-    n = c1.shape[0]
-    if n & (n - 1):  # any-N FFT is SURVEY §8(f) item 1; refused loudly until then
-        with pytest.raises(_native.CurvalignError):
-            cva.align_fft_batch(c1[None], c2[None])
-        return
     res, al = cva.align_fft_batch(c1[None], c2[None], return_aligned=True)
     ref = g[key][0]
     check_pair(res[0], ref, c1, c2)
@@ -99,7 +94,7 @@ def test_kat_cases(cuda, case):
         assert res[0]["energy"] > 1e-6
 
 
-@pytest.mark.parametrize("n", [8, 64, 128, 1024])
+@pytest.mark.parametrize("n", [8, 20, 64, 101, 128, 1024])
 def test_random_pairs_match_reference(cuda, n):  # test_rigid_align.cpp:133-151
     g = gold("rigid_align_kat.npz")
     a, b = g[f"rand{n}_c1"], g[f"rand{n}_c2"]
@@ -108,13 +103,29 @@ def test_random_pairs_match_reference(cuda, n):  # test_rigid_align.cpp:133-151
     check_pair(res[0], g[f"rand{n}_res_naive"][0], a, b)
 
 
-@pytest.mark.parametrize("n", [20, 101])
-def test_non_pow2_reported_unsupported(cuda, n):
-    """Any-N FFT is SURVEY §8(f) item 1 ("next"); until it lands the library
-    must refuse loudly rather than return a wrong answer."""
-    g = gold("rigid_align_kat.npz")
+@pytest.mark.parametrize("n", [4, 5, 6, 7, 9, 33, 37, 48, 60, 96, 100, 127, 255, 256, 257, 1000, 1023, 2048])
+def test_any_n_matches_oracle(cuda, oracle, n):
+    """Any N >= 4 (the reference's FFTW path takes any length; its
+    tests use N = 20, 33, 40, 48, 60, 96, 100, 101, 127, 255): non-powers of two
+    run as zero-padded power-of-two correlations."""
+    rng = np.random.default_rng(1000 + n)
+    a = rng.uniform(-1, 1, (3, n, 2))
+    b = np.stack([np.roll(a[0], 3 % n, 0), rng.uniform(-1, 1, (n, 2)), a[2] * 0.5])
+    res, al = cva.align_fft_batch(a, b, return_aligned=True)
+    for p in range(3):
+        r = oracle.align(a[p], b[p])
+        want_al = np.empty_like(b[p])
+        c, sn = np.cos(r["theta"]), np.sin(r["theta"])
+        q = b[p][(np.arange(n) + int(r["shift"])) % n]
+        want_al[:, 0], want_al[:, 1] = c * q[:, 0] + sn * q[:, 1], -sn * q[:, 0] + c * q[:, 1]
+        check_pair(res[p], r, a[p], b[p], al[p], want_al)
+
+
+def test_beyond_shared_memory_refused(cuda):
+    """N past the shared-memory pair kernels is refused loudly (large-N path: §8 C3)."""
+    z = np.zeros((1, 1500, 2))
     with pytest.raises(_native.CurvalignError):
-        cva.align_fft_batch(g[f"rand{n}_c1"][None], g[f"rand{n}_c2"][None])
+        cva.align_fft_batch(z, z)
 
 
 def test_energy_matches_direct_residual(cuda):  # test_rigid_align.cpp:187-197
