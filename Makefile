@@ -16,12 +16,13 @@ KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h $(CSRC)/fused.h inclu
 
 # Phase-timing build (tools/phase_timing.py): separate .so, never shipped.
 prof: $(PKG)/libcurvalign_cuda_prof.so
-$(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kernels.cu $(KERNEL_HDRS) $(CSRC)/prof.cuh
+$(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kernels.cu $(CSRC)/allpairs.cu $(KERNEL_HDRS) $(CSRC)/prof.cuh
 	@mkdir -p $(BUILD)/prof
 	$(NVCC) $(NVFLAGS) -DCVA_PHASE_TIMING -c $(CSRC)/fused.cu -o $(BUILD)/prof/fused.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/kernels.cu -o $(BUILD)/prof/kernels.o
 	$(NVCC) $(NVFLAGS) -x cu -c $(CSRC)/capi.cpp -o $(BUILD)/prof/capi.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/probe.cu -o $(BUILD)/prof/probe.o
+	$(NVCC) $(NVFLAGS) -c $(CSRC)/allpairs.cu -o $(BUILD)/prof/allpairs.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(BUILD)/prof/*.o
 all: lib synth oracle ref
 
@@ -37,6 +38,10 @@ $(BUILD)/fused.o: $(CSRC)/fused.cu $(KERNEL_HDRS) $(CSRC)/fused.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_fused.log || (cat $(BUILD)/ptxas_fused.log; exit 1)
 
+$(BUILD)/allpairs.o: $(CSRC)/allpairs.cu $(KERNEL_HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_allpairs.log || (cat $(BUILD)/ptxas_allpairs.log; exit 1)
+
 $(BUILD)/capi.o: $(CSRC)/capi.cpp $(CSRC)/kernels.h $(CSRC)/fused.h include/curvalign_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
@@ -45,7 +50,7 @@ $(BUILD)/probe.o: $(CSRC)/probe.cu include/curvalign_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/fused.o $(BUILD)/capi.o $(BUILD)/probe.o
+$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/fused.o $(BUILD)/allpairs.o $(BUILD)/capi.o $(BUILD)/probe.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
 
 # Synthetic workload generators (bench harness; host only).

@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c1", choices=["c1"])
+    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c4"],
+                    help="c1 is the headline (BASELINE metric); c2/c4 are secondary workloads")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -195,10 +196,108 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def run_secondary(args):
+    """C2 (all pairs, N=512, FP64-bound) and C4 (SRV pairs, N=2048, HBM-bound):
+    same JSON contract, device-timed, inputs resident."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2501_17779_b200 as cva
+    from paper_2501_17779_b200 import _native, synth
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _native.load()
+    stream = torch.cuda.current_stream(dev)
+    fp64 = ctypes_probe(lib)
+    if args.config == "c2":
+        cfg = synth.CONFIGS["c2"]
+        M, N = cfg["curves"], cfg["N"]
+        pts, offs = synth.ragged_curves(args.seed, M)
+        dp, do = torch.from_numpy(pts).to(dev), torch.from_numpy(offs).to(dev)
+        mx = int(np.diff(offs).max())
+        r0, r1 = rank * M // world, (rank + 1) * M // world
+        prep = torch.empty((M, N, 2), dtype=torch.float64, device=dev)
+        e = torch.empty((r1 - r0, M), dtype=torch.float64, device=dev)
+        k = torch.empty((r1 - r0, M), dtype=torch.int32, device=dev)
+        th = torch.empty((r1 - r0, M), dtype=torch.float64, device=dev)
+
+        def step():
+            _native.check(lib.cva_preprocess_batch(dp.data_ptr(), do.data_ptr(), M, mx, N, 1, prep.data_ptr(), 0,
+                                                   stream.cuda_stream))
+            _native.check(lib.cva_allpairs(prep.data_ptr(), M, N, r0, r1, e.data_ptr(), k.data_ptr(), th.data_ptr(),
+                                           stream.cuda_stream))
+        units = (r1 - r0) * M
+        workload = f"C2: all ordered pairs of {M} curves (raw n_in~U{{300..3000}}), N={N}, rows sharded"
+        flops_unit = 5 * N * math.log2(N)
+        bound = "fp64"
+    else:
+        cfg = synth.CONFIGS["c4"]
+        P, N = cfg["pairs"], cfg["N"]
+        c1, c2, _, _, _ = synth.srv_pairs(args.seed + 1000 * rank, P, N)
+        d1, d2 = torch.from_numpy(c1).to(dev), torch.from_numpy(c2).to(dev)
+        out = torch.empty((P, 48), dtype=torch.uint8, device=dev)
+        al = torch.empty_like(d2)
+
+        def step():
+            _native.check(lib.cva_srv_align_batch(d1.data_ptr(), d2.data_ptr(), P, N, out.data_ptr(), al.data_ptr(),
+                                                  stream.cuda_stream))
+        units = P
+        workload = f"C4: {P} SRV pairs/GPU, N={N}, srv_transform+srv_center+align_fft+aligned q"
+        bytes_unit = 16 * 2 * N + 16 * N + 48
+        bound = "hbm"
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item()) / args.steps
+    total_units = units * world
+    value = total_units / (ms_step * 1e-3)
+    launch_s = (ms / args.steps) * 1e-3
+    if bound == "fp64":
+        ach = units * flops_unit / launch_s / 1e12
+        roof = {"bound": "fp64", "achieved": ach, "peak": fp64, "unit": "TFLOP/s", "frac": ach / fp64 if fp64 else None,
+                "traffic": None, "peak_source": "measured here (cva_probe_fp64_tflops)",
+                "note": "5 N log2 N flops per pair (one transform per cell; spectra amortised)"}
+    else:
+        hbm_peak, peak_kind = load_peaks()
+        ach = units * bytes_unit / launch_s / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                "traffic": None, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": f"aligned curve pairs/sec (fp64, {args.config})", "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak" if args.config == "c4" else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, csrc/synth.cpp)",
+            "config": {"workload": workload}, "roofline": roof, "cpu_baseline": None, "e2e": None,
+            "gpu_launches": args.steps * (2 if args.config == "c2" else 1), "clocks": clk.summary()}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference_arm(args)
+        return
+    if args.config != "c1":
+        run_secondary(args)
         return
 
     import torch

@@ -117,6 +117,15 @@ int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int
 int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
                         cva_alignment* out, double* aligned_q, void* stream);
 
+/* All ordered pairs of `count` pre-sampled curves of n nodes (BASELINE config
+ * C2; the cells of distance_matrix, proj/src/elastic.cpp:176-236, each an
+ * align_fft). Rows [row_begin, row_end) of the count x count matrices:
+ * energy[r][j] (f64), shift[r][j] (i32), theta[r][j] (f64) for pair
+ * (curve row_begin + r, curve j), row-major. Each curve's spectrum is computed
+ * once and reused across its row and column. Multi-GPU callers shard rows. */
+int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_begin, int64_t row_end,
+                 double* energy, int32_t* shift, double* theta, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Host-buffer entry points (synchronous; host <-> device copies included).
  * These are what the C++ drop-in API (include/curvalign/ headers) calls.
@@ -133,6 +142,8 @@ int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets
                                     double* aligned);
 int cva_srv_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
                              cva_alignment* out, double* aligned_q);
+int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t row_begin,
+                      int64_t row_end, double* energy, int32_t* shift, double* theta);
 
 /* ---------------------------------------------------------------------------
  * Diagnostics (not on the hot path).

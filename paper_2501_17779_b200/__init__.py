@@ -11,6 +11,7 @@ of the reference's API (proj/include/curvalign/*.hpp).
 from .api import (  # noqa: F401
     RigidAlignment,
     align_fft,
+    allpairs,
     align_fft_batch,
     aligned_curve,
     decode_results,
@@ -26,6 +27,7 @@ from .api import (  # noqa: F401
 __all__ = [
     "RigidAlignment",
     "align_fft",
+    "allpairs",
     "align_fft_batch",
     "aligned_curve",
     "decode_results",

@@ -286,3 +286,38 @@ def srv_align_batch(c1, c2, return_aligned: bool = False):
     check(lib.cva_srv_align_batch_host(_ptr(a), _ptr(b), pairs, n, res.ctypes.data,
                                        al.ctypes.data if al is not None else 0))
     return res, al
+
+
+# --------------------------------------------------------------- all pairs
+
+
+def allpairs(curves, row_begin: int = 0, row_end: int | None = None):
+    """All ordered pairs of pre-sampled curves (BASELINE config C2).
+
+    curves: ``(count, n, 2)`` float64 (preprocessed). Returns
+    ``(energy, shift, theta)`` matrices of rows [row_begin, row_end) x count,
+    cell (r, j) = align_fft(curves[row_begin + r], curves[j]). numpy in ->
+    numpy out (synchronous); CUDA tensor in -> CUDA tensors out (stream-ordered).
+    """
+    lib = _native.load()
+    if _is_cuda_tensor(curves):
+        c = curves.contiguous()
+        count, n = c.shape[0], c.shape[1]
+        re = count if row_end is None else row_end
+        rows = re - row_begin
+        e = torch.empty((rows, count), dtype=torch.float64, device=c.device)
+        k = torch.empty((rows, count), dtype=torch.int32, device=c.device)
+        th = torch.empty((rows, count), dtype=torch.float64, device=c.device)
+        check(lib.cva_allpairs(c.data_ptr(), count, n, row_begin, re, e.data_ptr(), k.data_ptr(),
+                               th.data_ptr(), _stream_of(c)))
+        return e, k, th
+    c = _f64c(curves)
+    count, n = c.shape[0], c.shape[1]
+    re = count if row_end is None else row_end
+    rows = re - row_begin
+    e = np.empty((rows, count))
+    k = np.empty((rows, count), dtype=np.int32)
+    th = np.empty((rows, count))
+    check(lib.cva_allpairs_host(_ptr(c), count, n, row_begin, re, e.ctypes.data, k.ctypes.data,
+                                th.ctypes.data))
+    return e, k, th

@@ -311,6 +311,47 @@ int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64
   return finish(e, "srv_align launch");
 }
 
+int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_begin, int64_t row_end,
+                 double* energy, int32_t* shift, double* theta, void* stream) {
+  if (int rc = check_fft_size(n)) return rc;
+  if (count < 0 || row_begin < 0 || row_end > count || row_begin > row_end)
+    return fail(CVA_INVALID_ARGUMENT, "allpairs: bad row range");
+  if (row_end == row_begin || count == 0) return CVA_OK;
+  if (!curves || !energy || !shift || !theta) return fail(CVA_INVALID_ARGUMENT, "allpairs: null pointer");
+  if (int rc = require_device()) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int M = cva::v2_fft_len((int)n);
+  const double2* tw = nullptr;
+  if (int rc = get_twiddles(M, s, &tw)) return rc;
+  if (cva::allpairs_fast_supported((int)n)) {
+    // spectra once per curve (kept L2-resident), then one warp per cell
+    void* ws = nullptr;
+    const size_t zbytes = sizeof(double2) * (size_t)(count * M);
+    if (scratch_alloc(&ws, zbytes + sizeof(double) * (size_t)count, s) != cudaSuccess)
+      return fail(CVA_BAD_ALLOC, "scratch allocation failed");
+    double2* za = (double2*)ws;
+    double* ss = (double*)((char*)ws + zbytes);
+    cudaError_t e = cva::launch_spectra((const double2*)curves, count, (int)n, tw, za, za, ss, s);
+    if (e == cudaSuccess)
+      e = cva::launch_allpairs(za, za, ss, count, row_begin, row_end, tw, energy, shift, theta, s);
+    cudaFreeAsync(ws, s);
+    return finish(e, "allpairs launch");
+  }
+  // general N: one CTA per cell through the pair kernel, row by row
+  void* ws = nullptr;
+  if (scratch_alloc(&ws, sizeof(cva_alignment) * (size_t)count, s) != cudaSuccess)
+    return fail(CVA_BAD_ALLOC, "scratch allocation failed");
+  cudaError_t e = cudaSuccess;
+  for (int64_t i = row_begin; i < row_end && e == cudaSuccess; ++i) {
+    const int64_t o = (i - row_begin) * count;
+    e = cva::launch_v2_align_row((const double2*)curves + i * n, (const double2*)curves, count, (int)n, tw,
+                                 (cva_alignment*)ws, s);
+    if (e == cudaSuccess) e = cva::launch_unpack_row((const cva_alignment*)ws, count, energy + o, shift + o, theta + o, s);
+  }
+  cudaFreeAsync(ws, s);
+  return finish(e, "allpairs launch");
+}
+
 // ------------------------------------------------------------- host entries
 
 int cva_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
@@ -407,6 +448,30 @@ int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets
   if (e == cudaSuccess && aligned) e = cudaMemcpyAsync(aligned, dal.p, ab, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   return finish(e, "preprocess_align_batch_host");
+}
+
+int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t row_begin,
+                      int64_t row_end, double* energy, int32_t* shift, double* theta) {
+  if (int rc = check_fft_size(n)) return rc;
+  if (count < 0 || row_begin < 0 || row_end > count || row_begin > row_end)
+    return fail(CVA_INVALID_ARGUMENT, "allpairs: bad row range");
+  if (int rc = require_device()) return rc;
+  const int64_t cells = (row_end - row_begin) * count;
+  DevBuf dc, de, dk, dt;
+  if (dc.alloc(sizeof(double2) * (size_t)(count * n)) || de.alloc(sizeof(double) * cells) ||
+      dk.alloc(sizeof(int32_t) * cells) || dt.alloc(sizeof(double) * cells))
+    return fail(CVA_BAD_ALLOC, "device allocation failed");
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaMemcpyAsync(dc.p, curves, sizeof(double2) * (size_t)(count * n), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  if (int rc = cva_allpairs((const double*)dc.p, count, n, row_begin, row_end, (double*)de.p,
+                            (int32_t*)dk.p, (double*)dt.p, s))
+    return rc;
+  e = cudaMemcpyAsync(energy, de.p, sizeof(double) * cells, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(shift, dk.p, sizeof(int32_t) * cells, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(theta, dt.p, sizeof(double) * cells, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return finish(e, "allpairs_host");
 }
 
 int cva_srv_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,

@@ -143,12 +143,12 @@ __global__ void __launch_bounds__(kT, 2)
 // batches; stride 2N with c2 = c1 + N: interleaved rows 2p, 2p+1).
 __global__ void __launch_bounds__(kT)
     align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
-                 int64_t stride, const double2* __restrict__ tw, cva_alignment* __restrict__ out,
-                 double2* aligned) {
+                 int64_t stride1, int64_t stride2, const double2* __restrict__ tw,
+                 cva_alignment* __restrict__ out, double2* aligned) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double2 red[16];
   const int64_t p = blockIdx.x;
-  pf::PairIn in{c1 + p * stride, c2 + p * stride, make_double2(0, 0), make_double2(0, 0), 1.0, 1.0};
+  pf::PairIn in{c1 + p * stride1, c2 + p * stride2, make_double2(0, 0), make_double2(0, 0), 1.0, 1.0};
   pf::pair_stage(in, reinterpret_cast<double2*>(smem), N, tw, out + p,
                  aligned ? aligned + p * N : nullptr, red);
 }
@@ -271,7 +271,7 @@ cudaError_t launch_v2_align(const double2* c1, const double2* c2, int64_t pairs,
   const size_t sm = v2_align_smem(N);
   cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
   if (e != cudaSuccess) return e;
-  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, N, tw, out, aligned);
+  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, N, N, tw, out, aligned);
   return cudaGetLastError();
 }
 
@@ -280,8 +280,37 @@ cudaError_t launch_v2_align_interleaved(const double2* rows, int64_t pairs, int 
   const size_t sm = v2_align_smem(N);
   cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
   if (e != cudaSuccess) return e;
-  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(rows, rows + N, N, 2 * (int64_t)N, tw, out,
-                                                        aligned);
+  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(rows, rows + N, N, 2 * (int64_t)N,
+                                                        2 * (int64_t)N, tw, out, aligned);
+  return cudaGetLastError();
+}
+
+// One row of an all-pairs matrix: pair j = (row, curves[j]) for j < count.
+cudaError_t launch_v2_align_row(const double2* row, const double2* curves, int64_t count, int N,
+                                const double2* tw, cva_alignment* out, cudaStream_t s) {
+  const size_t sm = v2_align_smem(N);
+  cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
+  if (e != cudaSuccess) return e;
+  v2::align_kernel<<<(unsigned)count, v2::kT, sm, s>>>(row, curves, N, 0, N, tw, out, nullptr);
+  return cudaGetLastError();
+}
+
+namespace v2 {
+__global__ void unpack_row_kernel(const cva_alignment* __restrict__ in, int64_t count, double* energy,
+                                  int32_t* shift, double* theta) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < count) {
+    const cva_alignment r = in[j];
+    energy[j] = r.energy;
+    shift[j] = (int32_t)r.shift;
+    theta[j] = r.theta;
+  }
+}
+}  // namespace v2
+
+cudaError_t launch_unpack_row(const cva_alignment* in, int64_t count, double* energy, int32_t* shift,
+                              double* theta, cudaStream_t s) {
+  v2::unpack_row_kernel<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(in, count, energy, shift, theta);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,20 @@ cudaError_t launch_v2_align(const double2* c1, const double2* c2, int64_t pairs,
                             cudaStream_t s);
 cudaError_t launch_v2_align_interleaved(const double2* rows, int64_t pairs, int N, const double2* tw,
                                         cva_alignment* out, double2* aligned, cudaStream_t s);
+cudaError_t launch_v2_align_row(const double2* row, const double2* curves, int64_t count, int N,
+                                const double2* tw, cva_alignment* out, cudaStream_t s);
+cudaError_t launch_unpack_row(const cva_alignment* in, int64_t count, double* energy, int32_t* shift,
+                              double* theta, cudaStream_t s);
+
+// all-pairs (allpairs.cu)
+size_t allpairs_spectra_smem(int N);
+cudaError_t launch_spectra(const double2* curves, int64_t count, int N, const double2* tw, double2* za,
+                           double2* zb, double* ss, cudaStream_t s);
+bool allpairs_fast_supported(int N);
+cudaError_t launch_allpairs(const double2* za, const double2* zb, const double* ss, int64_t count,
+                            int64_t row_begin, int64_t row_end, const double2* tw, double* energy,
+                            int32_t* shift, double* theta, cudaStream_t s);
+
 cudaError_t launch_v2_srv_align(const double2* c1, const double2* c2, int64_t pairs, int N,
                                 const double2* tw, cva_alignment* out, double2* aligned,
                                 double2* qbuf, cudaStream_t s);

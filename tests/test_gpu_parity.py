@@ -327,3 +327,48 @@ def test_align_idempotent(cuda):
     assert (r2["shift"] == 0).all()
     assert np.abs(wrap(r2["theta"])).max() < 1e-10
     np.testing.assert_allclose(r2["energy"], r["energy"], rtol=1e-9, atol=1e-15)
+
+
+@pytest.mark.parametrize("n", [512, 96])
+def test_allpairs_matches_oracle(cuda, oracle, n):
+    """C2 kernel (spectrum reuse; N=512 warp path, other N general path) vs align_fft per cell."""
+    rng = np.random.default_rng(n)
+    m = 11
+    base = rng.uniform(-1, 1, (m, n, 2))
+    base[3] = np.roll(base[1], 17, 0)  # an exact shifted copy
+    e, k, th = cva.allpairs(base, 2, 9)
+    assert e.shape == (7, m)
+    for r in range(7):
+        for j in range(m):
+            want = oracle.align(base[2 + r], base[j])
+            g = np.zeros(1, dtype=_native.ALIGNMENT_DTYPE)[0]
+            g["shift"], g["theta"], g["energy"] = k[r, j], th[r, j], e[r, j]
+            g["trace"], g["t0"] = want["trace"], int(k[r, j]) / n
+            check_pair(g, want, base[2 + r], base[j])
+
+
+def test_c2_full_size(cuda, oracle):
+    """All 2048^2 ordered pairs of the C2 workload at N=512: oracle on sampled
+    cells, exact properties on all (diagonal zero, symmetry of energies)."""
+    import torch
+
+    cfg = synth.CONFIGS["c2"]
+    pts, offs = synth.ragged_curves(3, cfg["curves"])
+    dp, do = torch.from_numpy(pts).cuda(), torch.from_numpy(offs).cuda()
+    prep, st = cva.preprocess_batch(dp, do, cfg["N"], max_n_in=int(np.diff(offs).max()))
+    assert int(st.abs().sum()) == 0
+    e, k, th = cva.allpairs(prep)
+    e, k, th = e.cpu().numpy(), k.cpu().numpy(), th.cpu().numpy()
+    p = prep.cpu().numpy()
+    M = cfg["curves"]
+    assert e.shape == (M, M) and np.isfinite(e).all() and (e >= 0).all()
+    assert (k.diagonal() == 0).all() and np.abs(wrap(th.diagonal())).max() < 1e-12
+    # energy is symmetric in exact arithmetic (align(j,i) is the inverse rigid motion)
+    assert np.abs(e - e.T).max() <= 1e-12
+    rng = np.random.default_rng(0)
+    for _ in range(64):
+        i, j = rng.integers(0, M, 2)
+        want = oracle.align(p[i], p[j])
+        g = np.zeros(1, dtype=_native.ALIGNMENT_DTYPE)[0]
+        g["shift"], g["theta"], g["energy"], g["trace"], g["t0"] = k[i, j], th[i, j], e[i, j], want["trace"], k[i, j] / 512
+        check_pair(g, want, p[i], p[j])
