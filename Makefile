@@ -10,7 +10,7 @@ CSRC     := $(PKG)/csrc
 BUILD    := build
 REF      ?= /root/reference
 
-KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h $(CSRC)/fused.h include/curvalign_cuda.h
+KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h $(CSRC)/fused.h $(CSRC)/largen.h include/curvalign_cuda.h
 
 .PHONY: all lib synth dropin oracle ref clean prof
 
@@ -23,6 +23,7 @@ $(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kern
 	$(NVCC) $(NVFLAGS) -x cu -c $(CSRC)/capi.cpp -o $(BUILD)/prof/capi.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/probe.cu -o $(BUILD)/prof/probe.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/allpairs.cu -o $(BUILD)/prof/allpairs.o
+	$(NVCC) $(NVFLAGS) -c $(CSRC)/largen.cu -o $(BUILD)/prof/largen.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(BUILD)/prof/*.o
 all: lib synth oracle ref
 
@@ -42,6 +43,10 @@ $(BUILD)/allpairs.o: $(CSRC)/allpairs.cu $(KERNEL_HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_allpairs.log || (cat $(BUILD)/ptxas_allpairs.log; exit 1)
 
+$(BUILD)/largen.o: $(CSRC)/largen.cu $(KERNEL_HDRS) $(CSRC)/largen.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_largen.log || (cat $(BUILD)/ptxas_largen.log; exit 1)
+
 $(BUILD)/capi.o: $(CSRC)/capi.cpp $(CSRC)/kernels.h $(CSRC)/fused.h include/curvalign_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
@@ -50,7 +55,7 @@ $(BUILD)/probe.o: $(CSRC)/probe.cu include/curvalign_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/fused.o $(BUILD)/allpairs.o $(BUILD)/capi.o $(BUILD)/probe.o
+$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/fused.o $(BUILD)/allpairs.o $(BUILD)/largen.o $(BUILD)/capi.o $(BUILD)/probe.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
 
 # Synthetic workload generators (bench harness; host only).

@@ -82,7 +82,9 @@ int64_t cva_max_resample_nodes(void);
 
 /* align_fft over a batch of pre-sampled pairs (proj/src/rigid_align.cpp:204-208).
  * c1, c2: pairs x n points. out: pairs results. aligned (nullable): pairs x n
- * points, aligned[l] = R c2[(l + shift) mod n]. Requires n >= 4. */
+ * points, aligned[l] = R c2[(l + shift) mod n]. Any n >= 4: n <= 2048 runs in
+ * shared memory (non-powers of two zero-padded), larger n through the
+ * L2-chunked multi-pass transform. */
 int cva_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
                     cva_alignment* out, double* aligned, void* stream);
 
@@ -109,6 +111,13 @@ int cva_resample_batch(const double* points, const int64_t* offsets, int64_t cur
 int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int64_t pairs,
                                int64_t max_n_in, int64_t n_out, int resample,
                                cva_alignment* out, double* aligned, void* stream);
+
+/* preprocess(resample = false) of both curves (center, then normalize to unit
+ * length; proj/src/curve.cpp:93-97) fused with align_fft, for equal-size pairs
+ * (BASELINE configs C0 and C3). Any N >= 4; large N runs the L2-chunked
+ * multi-pass transform. aligned (nullable): pairs x n points. */
+int cva_preprocess_align_uniform(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                 cva_alignment* out, double* aligned, void* stream);
 
 /* SRV-space alignment: align_fft(srv_center(srv_transform(c1)).q,
  * srv_center(srv_transform(c2)).q) (proj/src/srv.cpp:71-98; the (t0,R) step
@@ -142,6 +151,8 @@ int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets
                                     double* aligned);
 int cva_srv_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
                              cva_alignment* out, double* aligned_q);
+int cva_preprocess_align_uniform_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                      cva_alignment* out, double* aligned);
 int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t row_begin,
                       int64_t row_end, double* energy, int32_t* shift, double* theta);
 

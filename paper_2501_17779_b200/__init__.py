@@ -17,6 +17,7 @@ from .api import (  # noqa: F401
     decode_results,
     preprocess,
     preprocess_align_batch,
+    preprocess_align_uniform,
     preprocess_batch,
     ragged,
     resample_batch,
@@ -33,6 +34,7 @@ __all__ = [
     "decode_results",
     "preprocess",
     "preprocess_align_batch",
+    "preprocess_align_uniform",
     "preprocess_batch",
     "ragged",
     "resample_batch",

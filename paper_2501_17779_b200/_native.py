@@ -78,6 +78,8 @@ SIGNATURES = {
     ),
     "cva_srv_align_batch_host": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "cva_probe_fp64_tflops": (c_int, [c_void_p]),
+    "cva_preprocess_align_uniform": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
+    "cva_preprocess_align_uniform_host": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "cva_allpairs": (
         c_int,
         [c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p],

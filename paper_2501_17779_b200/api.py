@@ -321,3 +321,27 @@ def allpairs(curves, row_begin: int = 0, row_end: int | None = None):
     check(lib.cva_allpairs_host(_ptr(c), count, n, row_begin, re, e.ctypes.data, k.ctypes.data,
                                 th.ctypes.data))
     return e, k, th
+
+
+def preprocess_align_uniform(c1, c2, return_aligned: bool = False):
+    """preprocess(resample=false) of both curves + align_fft for equal-size
+    pairs (BASELINE C0 / C3). Same conventions as :func:`align_fft_batch`."""
+    lib = _native.load()
+    if _is_cuda_tensor(c1):
+        c1 = c1.contiguous()
+        c2 = c2.contiguous()
+        pairs, n = c1.shape[0], c1.shape[1]
+        out = torch.empty((pairs, 48), dtype=torch.uint8, device=c1.device)
+        al = torch.empty_like(c2) if return_aligned else None
+        check(lib.cva_preprocess_align_uniform(c1.data_ptr(), c2.data_ptr(), pairs, n, out.data_ptr(),
+                                               _tptr(al), _stream_of(c1)))
+        return out, al
+    a, b = _f64c(c1), _f64c(c2)
+    if a.shape != b.shape or a.ndim != 3:
+        raise ValueError("align: node count mismatch")
+    pairs, n = a.shape[0], a.shape[1]
+    res = np.zeros(pairs, dtype=ALIGNMENT_DTYPE)
+    al = np.empty_like(b) if return_aligned else None
+    check(lib.cva_preprocess_align_uniform_host(_ptr(a), _ptr(b), pairs, n, res.ctypes.data,
+                                                al.ctypes.data if al is not None else 0))
+    return res, al

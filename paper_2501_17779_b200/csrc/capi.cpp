@@ -19,6 +19,7 @@
 #include "../../include/curvalign_cuda.h"
 #include "fused.h"
 #include "kernels.h"
+#include "largen.h"
 
 namespace {
 
@@ -79,11 +80,21 @@ int smem_limit() {
 
 // FFT sizes the shared-memory kernels cover in this build.
 // Shared-memory pair kernels: power-of-two N <= 2048, other N zero-padded to a
-// power of two M >= 2N (pairfft.cuh), so N <= 1024.
+// power of two M >= 2N (pairfft.cuh), so N <= 1024. Larger N: largen.cu.
+constexpr int64_t kMaxLargeN = 1 << 22;
+
+bool small_fft(int64_t n) { return n <= 2048 && cva::v2_fft_len((int)n) <= 2048; }
+
 int check_fft_size(int64_t n) {
   if (n < 4) return fail(CVA_INVALID_ARGUMENT, "align: need at least 4 nodes");
-  if (n > 2048 || cva::v2_fft_len((int)n) > 2048)
-    return fail(CVA_UNSUPPORTED, "align: the shared-memory pair kernels cover N <= 2048 "
+  if (n > kMaxLargeN) return fail(CVA_UNSUPPORTED, "align: N beyond 4M nodes");
+  return CVA_OK;
+}
+
+int check_small_fft(int64_t n) {
+  if (int rc = check_fft_size(n)) return rc;
+  if (!small_fft(n))
+    return fail(CVA_UNSUPPORTED, "this entry point's shared-memory kernels cover N <= 2048 "
                                  "(powers of two) and N <= 1024 otherwise");
   return CVA_OK;
 }
@@ -140,6 +151,18 @@ int finish(cudaError_t e, const char* what) {
   return CVA_OK;
 }
 
+int large_align(const double* c1, const double* c2, int64_t pairs, int64_t n, int normalize,
+                cva_alignment* out, double* aligned, const double2* tw, cudaStream_t s) {
+  const int64_t chunk = std::min<int64_t>(pairs, cva::large_chunk_pairs((int)n));
+  void* ws = nullptr;
+  if (scratch_alloc(&ws, cva::large_workspace_bytes(chunk, (int)n), s) != cudaSuccess)
+    return fail(CVA_BAD_ALLOC, "large-N workspace allocation failed");
+  cudaError_t e = cva::launch_large_align((const double2*)c1, (const double2*)c2, pairs, (int)n, normalize, tw,
+                                          out, (double2*)aligned, ws, chunk, s);
+  cudaFreeAsync(ws, s);
+  return finish(e, "large-N align launch");
+}
+
 // v2 shared-memory resampler when the batch fits it, else the general v1 kernel.
 int resample_dispatch(const double* points, const int64_t* offsets, int64_t curves,
                       int64_t max_n_in, int64_t n_out, int center_normalize, double* out,
@@ -192,6 +215,7 @@ int cva_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
   if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
+  if (!small_fft(n)) return large_align(c1, c2, pairs, n, 0, out, aligned, tw, s);
   return finish(cva::launch_v2_align((const double2*)c1, (const double2*)c2, pairs, (int)n, tw,
                                      out, (double2*)aligned, s),
                 "align launch");
@@ -238,10 +262,10 @@ int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int
   if (!points || !offsets || !out) return fail(CVA_INVALID_ARGUMENT, "align: null pointer");
   if (!resample)
     return fail(CVA_UNSUPPORTED,
-                "preprocess_align: resample=0 pairs have per-curve sizes; use "
-                "cva_preprocess_batch + cva_align_batch");
+                "preprocess_align: resample=0 takes equal-size pairs; use "
+                "cva_preprocess_align_uniform");
   if (n_out < 8) return fail(CVA_INVALID_ARGUMENT, "resample: need at least 8 output nodes");
-  if (int rc = check_fft_size(n_out)) return rc;
+  if (int rc = check_small_fft(n_out)) return rc;
   if (int rc = require_device()) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if (max_n_in <= 0)
@@ -291,10 +315,24 @@ int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int
   return finish(e, "preprocess+align launch");
 }
 
+int cva_preprocess_align_uniform(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                 cva_alignment* out, double* aligned, void* stream) {
+  if (n < 4) return fail(CVA_INVALID_ARGUMENT, "align: need at least 4 nodes");
+  if (int rc = check_fft_size(n)) return rc;
+  if (pairs < 0) return fail(CVA_INVALID_ARGUMENT, "align: negative pair count");
+  if (pairs == 0) return CVA_OK;
+  if (!c1 || !c2 || !out) return fail(CVA_INVALID_ARGUMENT, "align: null pointer");
+  if (int rc = require_device()) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const double2* tw = nullptr;
+  if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
+  return large_align(c1, c2, pairs, n, 1, out, aligned, tw, s);
+}
+
 int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
                         cva_alignment* out, double* aligned_q, void* stream) {
   if (n < 8) return fail(CVA_INVALID_ARGUMENT, "curve: too few nodes");  // srv.cpp:72
-  if (int rc = check_fft_size(n)) return rc;
+  if (int rc = check_small_fft(n)) return rc;
   if (pairs < 0) return fail(CVA_INVALID_ARGUMENT, "srv: negative pair count");
   if (pairs == 0) return CVA_OK;
   if (!c1 || !c2 || !out) return fail(CVA_INVALID_ARGUMENT, "srv: null pointer");
@@ -313,7 +351,7 @@ int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64
 
 int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_begin, int64_t row_end,
                  double* energy, int32_t* shift, double* theta, void* stream) {
-  if (int rc = check_fft_size(n)) return rc;
+  if (int rc = check_small_fft(n)) return rc;
   if (count < 0 || row_begin < 0 || row_end > count || row_begin > row_end)
     return fail(CVA_INVALID_ARGUMENT, "allpairs: bad row range");
   if (row_end == row_begin || count == 0) return CVA_OK;
@@ -452,7 +490,7 @@ int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets
 
 int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t row_begin,
                       int64_t row_end, double* energy, int32_t* shift, double* theta) {
-  if (int rc = check_fft_size(n)) return rc;
+  if (int rc = check_small_fft(n)) return rc;
   if (count < 0 || row_begin < 0 || row_end > count || row_begin > row_end)
     return fail(CVA_INVALID_ARGUMENT, "allpairs: bad row range");
   if (int rc = require_device()) return rc;
@@ -474,10 +512,33 @@ int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t ro
   return finish(e, "allpairs_host");
 }
 
+int cva_preprocess_align_uniform_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                      cva_alignment* out, double* aligned) {
+  if (n < 4) return fail(CVA_INVALID_ARGUMENT, "align: need at least 4 nodes");
+  if (int rc = check_fft_size(n)) return rc;
+  if (pairs <= 0) return pairs == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative pair count");
+  if (int rc = require_device()) return rc;
+  const size_t cb = sizeof(double) * 2 * (size_t)(pairs * n);
+  DevBuf d1, d2, dout, dal;
+  if (d1.alloc(cb) || d2.alloc(cb) || dout.alloc(sizeof(cva_alignment) * pairs) || (aligned && dal.alloc(cb)))
+    return fail(CVA_BAD_ALLOC, "device allocation failed");
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  if (int rc = cva_preprocess_align_uniform((const double*)d1.p, (const double*)d2.p, pairs, n,
+                                            (cva_alignment*)dout.p, aligned ? (double*)dal.p : nullptr, s))
+    return rc;
+  e = cudaMemcpyAsync(out, dout.p, sizeof(cva_alignment) * pairs, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && aligned) e = cudaMemcpyAsync(aligned, dal.p, cb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return finish(e, "preprocess_align_uniform_host");
+}
+
 int cva_srv_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
                              cva_alignment* out, double* aligned_q) {
   if (n < 8) return fail(CVA_INVALID_ARGUMENT, "curve: too few nodes");
-  if (int rc = check_fft_size(n)) return rc;
+  if (int rc = check_small_fft(n)) return rc;
   if (pairs <= 0) return pairs == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative pair count");
   if (int rc = require_device()) return rc;
   const size_t cb = sizeof(double) * 2 * (size_t)(pairs * n);

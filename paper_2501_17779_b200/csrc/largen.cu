@@ -1,0 +1,391 @@
+// Large-N alignment (BASELINE config C3: N = 65536; any N whose transform
+// length exceeds the shared-memory pair kernels, e.g. the reference tests'
+// N = 4097). A curve is 1 MB at N = 65536, beyond one CTA's shared memory, so
+// the three transforms run as batched multi-pass radix-16 Stockham kernels over
+// global buffers; the host processes pairs in chunks whose working set stays
+// resident in the 126 MB L2, so HBM sees the inputs, the aligned output and
+// little else.
+//
+// Per chunk of P pairs (M = fft_len(N), data in the length-M padded form of
+// pairfft.cuh: a = [z1', 0...], b = [z2', z2', 0...]):
+//   stats_kernel      centroid / 1/length of each curve (curve.cpp:27-48) when
+//                     the preprocess (resample=false) is fused, else identity
+//   lpass<kLoadA/B>   first radix-16 pass reading the curves, normalising on load
+//   lpass<kPlain>     remaining passes of the two forward transforms
+//   lpass<kProduct>   first pass of the correlation transform on Z1 conj(Z2)
+//   lmax_kernel       per-block max of |F|^2
+//   lpick_kernel      global max, reference tie band, smallest index -> result
+//   aligned_kernel    aligned[l] = R(theta) z2'[(l + m) mod N]
+#include <cuda_runtime.h>
+
+#include <climits>
+
+#include "../../include/curvalign_cuda.h"
+#include "cva_common.cuh"
+#include "fft.cuh"
+#include "largen.h"
+#include "pairfft.cuh"
+
+namespace cva {
+namespace ln {
+
+constexpr int kT = 256;
+
+__device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
+
+// 16-point DFT as 4 x 4 (radix-4 twice with the W16 twiddles in between).
+__device__ __forceinline__ void dft16(double2* v) {
+  // columns: v[c + 4 r], r = 0..3 -> DFT4 over r for each c
+#pragma unroll
+  for (int c = 0; c < 4; ++c) dft4(v[c], v[c + 4], v[c + 8], v[c + 12]);
+  // twiddles W16^(c * k1)
+  constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
+  constexpr double r2 = 0.70710678118654752440;
+  const double2 w[4][4] = {
+      {{1, 0}, {1, 0}, {1, 0}, {1, 0}},
+      {{1, 0}, {c1, -s1}, {r2, -r2}, {s1, -c1}},
+      {{1, 0}, {r2, -r2}, {0, -1}, {-r2, -r2}},
+      {{1, 0}, {s1, -c1}, {-r2, -r2}, {-c1, s1}},
+  };
+#pragma unroll
+  for (int k1 = 1; k1 < 4; ++k1)
+#pragma unroll
+    for (int c = 1; c < 4; ++c) v[c + 4 * k1] = cmul(v[c + 4 * k1], w[k1][c]);
+  // rows: for each k1, DFT4 over c -> output index k1 + 4 k2
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+  // v[4 k1 + k2] holds X[k1 + 4 k2]; transpose into natural order
+  double2 t[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) t[i] = v[i];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
+}
+
+template <int R>
+__device__ __forceinline__ void dft_any(double2* v) {
+  if constexpr (R == 16)
+    dft16(v);
+  else
+    dft_r<R>(v);
+}
+
+enum Load { kPlain = 0, kLoadA = 1, kLoadB = 2, kProduct = 3 };
+
+struct CurveNorm {
+  double2 g;
+  double sc;
+};
+
+// One Stockham pass of radix R over `nseq` sequences of length M (stride M).
+// kLoadA / kLoadB: the pass reads curve c (N nodes) through its normalisation
+// into the padded length-M form (first pass only, Ns = 1). kProduct: reads
+// x1[k] conj(x2[k]) of two spectra (first pass only).
+template <int R, int kMode>
+__global__ void __launch_bounds__(kT)
+    lpass(const double2* __restrict__ in, const double2* __restrict__ in2, double2* out, int M, int N,
+          int Ns, const double2* __restrict__ tw, const CurveNorm* __restrict__ norm, int64_t nseq) {
+  const int nb = M / R;
+  const int64_t gid = (int64_t)blockIdx.x * kT + threadIdx.x;
+  const int64_t seq = gid / nb;
+  if (seq >= nseq) return;
+  const int j = (int)(gid - seq * nb);
+  const int jm = j & (Ns - 1);
+  double2 v[R];
+  if (kMode == kLoadA || kMode == kLoadB) {
+    const double2* z = in + seq * N;
+    const CurveNorm cn = norm[seq];
+    const int lim = (kMode == kLoadA || M == N) ? N : 2 * N;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = j + r * nb;
+      if (i < lim) {
+        const double2 q = __ldg(&z[i < N ? i : i - N]);
+        v[r] = make_double2((q.x - cn.g.x) * cn.sc, (q.y - cn.g.y) * cn.sc);
+      } else {
+        v[r] = make_double2(0.0, 0.0);
+      }
+    }
+  } else if (kMode == kProduct) {
+    const double2* a = in + seq * M;
+    const double2* b = in2 + seq * M;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = cmulconj(__ldg(&a[j + r * nb]), __ldg(&b[j + r * nb]));
+  } else {
+    const double2* x = in + seq * M;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = __ldg(&x[j + r * nb]);
+  }
+  if (Ns > 1) {
+    const int tws = M / (Ns * R);
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[(int64_t)r * jm * tws]));
+  }
+  dft_any<R>(v);
+  double2* o = out + seq * M;
+  const int base = (j - jm) * R + jm;
+#pragma unroll
+  for (int r = 0; r < R; ++r) o[base + r * Ns] = v[r];
+}
+
+// centroid and 1/length of each curve (center then normalize, curve.cpp:27-48),
+// plus sum |z'|^2 (rigid_align.cpp:23-27). identity: keep the curve as given.
+__global__ void __launch_bounds__(kT)
+    stats_kernel(const double2* __restrict__ curves, int N, int normalize, CurveNorm* norm, double* ss,
+                 int32_t* bad) {
+  __shared__ double2 red[64];
+  const double2* z = curves + (int64_t)blockIdx.x * N;
+  double2 acc = make_double2(0, 0);
+  int nf = 0;
+  for (int i = threadIdx.x; i < N; i += kT) {
+    const double2 q = __ldg(&z[i]);
+    nf |= !(isfinite(q.x) && isfinite(q.y));
+    acc = cadd(acc, q);
+  }
+  nf = block_or(nf, red);
+  double2 g = make_double2(0, 0);
+  double sc = 1.0;
+  if (normalize) {
+    acc = block_sum2(acc, red);
+    const double invn = 1.0 / (double)N;
+    g = make_double2(invn * acc.x, invn * acc.y);
+    double len = 0.0;
+    for (int i = threadIdx.x; i < N; i += kT) {
+      const double2 p0 = csub(__ldg(&z[i]), g), p1 = csub(__ldg(&z[i + 1 == N ? 0 : i + 1]), g);
+      const double dx = p1.x - p0.x, dy = p1.y - p0.y;
+      len += sqrt(fma(dx, dx, dy * dy));
+    }
+    len = block_sum(len, red);
+    nf |= !(len > 0.0);
+    sc = 1.0 / len;
+  }
+  double s = 0.0;
+  for (int i = threadIdx.x; i < N; i += kT) {
+    const double2 q = __ldg(&z[i]);
+    const double x = (q.x - g.x) * sc, y = (q.y - g.y) * sc;
+    s = fma(x, x, fma(y, y, s));
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) {
+    norm[blockIdx.x] = CurveNorm{g, sc};
+    ss[blockIdx.x] = s;
+    bad[blockIdx.x] = nf;
+  }
+}
+
+// per-block max of |F|^2 over the first N lags; grid (blocks_per_seq, nseq)
+__global__ void __launch_bounds__(kT)
+    lmax_kernel(const double2* __restrict__ F, int M, int N, double* bmax) {
+  __shared__ double2 red[64];
+  const double2* f = F + (int64_t)blockIdx.y * M;
+  double m = -1.0;
+  for (int k = blockIdx.x * kT + threadIdx.x; k < N; k += gridDim.x * kT) {
+    const double2 v = __ldg(&f[k]);
+    m = fmax(m, fma(v.x, v.x, v.y * v.y));
+  }
+  m = block_max(m, red);
+  if (threadIdx.x == 0) bmax[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = m;
+}
+
+// one CTA per pair: reference tie band (rigid_align.cpp:31-61) on |D| = |F| / M
+__global__ void __launch_bounds__(kT)
+    lpick_kernel(const double2* __restrict__ F, int M, int N, const double* __restrict__ bmax, int nblk,
+                 const double* __restrict__ ss1, const double* __restrict__ ss2, const int32_t* bad1,
+                 const int32_t* bad2, cva_alignment* out, double2* rot) {
+  __shared__ double2 red[64];
+  const int64_t p = blockIdx.x;
+  const double2* f = F + p * M;
+  double best2 = -1.0;
+  for (int b = threadIdx.x; b < nblk; b += kT) best2 = fmax(best2, bmax[p * nblk + b]);
+  best2 = block_max(best2, red);
+  const double invM = 1.0 / (double)M, invN = 1.0 / (double)N;
+  const double best = sqrt(best2) * invM;
+  const double thr = best - pf::kTieRelTol * fmax(1.0, fabs(best));
+  const double thrN = thr * (double)M;
+  const double thr2 = thr > 0.0 ? thrN * thrN : -1.0;
+  int cand = INT_MAX;
+  for (int k = threadIdx.x; k < N; k += kT) {
+    const double2 v = __ldg(&f[k]);
+    if (fma(v.x, v.x, v.y * v.y) >= thr2) {
+      cand = k;
+      break;
+    }
+  }
+  const int m = block_min_int(cand, red);
+  if (threadIdx.x == 0) {
+    cva_alignment r;
+    if (bad1[p] || bad2[p] || !isfinite(best) || best2 < 0.0 || m == INT_MAX) {
+      r.shift = 0;
+      r.t0 = 0.0;
+      r.theta = r.trace = r.energy = qnan();
+      r.degenerate = 0;
+      r.status = CVA_INVALID_ARGUMENT;
+      rot[p] = make_double2(qnan(), qnan());
+    } else {
+      const double2 v = f[m];
+      const double trace = sqrt(fma(v.x, v.x, v.y * v.y)) * invM;
+      const int degenerate = trace == 0.0;
+      const double theta = degenerate ? 0.0 : atan2(-v.y, v.x);
+      double e = invN * (ss1[p] + ss2[p]) - 2.0 * invN * trace;
+      if (e < 0.0) e = 0.0;
+      r.shift = m;
+      r.t0 = (double)m / (double)N;
+      r.theta = theta;
+      r.trace = degenerate ? 0.0 : trace;
+      r.energy = e;
+      r.degenerate = degenerate;
+      r.status = CVA_OK;
+      double sn, cs;
+      sincos(theta, &sn, &cs);
+      rot[p] = make_double2(cs, sn);
+    }
+    out[p] = r;
+  }
+}
+
+// aligned[l] = R(theta) z2'[(l + m) mod N]; grid (blocks, pairs)
+__global__ void __launch_bounds__(kT)
+    aligned_kernel(const double2* __restrict__ c2, int N, const CurveNorm* __restrict__ norm2,
+                   const cva_alignment* __restrict__ res, const double2* __restrict__ rot, double2* aligned) {
+  const int64_t p = blockIdx.y;
+  const int64_t m = res[p].shift;
+  const double2 r = rot[p];
+  const CurveNorm cn = norm2[p];
+  const double2* z = c2 + p * N;
+  double2* a = aligned + p * N;
+  for (int l = blockIdx.x * kT + threadIdx.x; l < N; l += gridDim.x * kT) {
+    int64_t j = l + m;
+    if (j >= N) j -= N;
+    const double2 q = __ldg(&z[j]);
+    const double2 v = make_double2((q.x - cn.g.x) * cn.sc, (q.y - cn.g.y) * cn.sc);
+    a[l] = make_double2(fma(r.x, v.x, r.y * v.y), fma(-r.y, v.x, r.x * v.y));
+  }
+}
+
+}  // namespace ln
+
+// ------------------------------------------------------------------ host
+
+namespace {
+
+template <int R, int kMode>
+cudaError_t pass(const double2* in, const double2* in2, double2* out, int M, int N, int Ns,
+                 const double2* tw, const ln::CurveNorm* norm, int64_t nseq, cudaStream_t s) {
+  const int64_t threads = nseq * (M / R);
+  ln::lpass<R, kMode><<<(unsigned)((threads + ln::kT - 1) / ln::kT), ln::kT, 0, s>>>(in, in2, out, M, N, Ns, tw,
+                                                                                     norm, nseq);
+  return cudaGetLastError();
+}
+
+template <int kMode>
+cudaError_t pass_r(int R, const double2* in, const double2* in2, double2* out, int M, int N, int Ns,
+                   const double2* tw, const ln::CurveNorm* norm, int64_t nseq, cudaStream_t s) {
+  switch (R) {
+    case 16: return pass<16, kMode>(in, in2, out, M, N, Ns, tw, norm, nseq, s);
+    case 8: return pass<8, kMode>(in, in2, out, M, N, Ns, tw, norm, nseq, s);
+    case 4: return pass<4, kMode>(in, in2, out, M, N, Ns, tw, norm, nseq, s);
+    default: return pass<2, kMode>(in, in2, out, M, N, Ns, tw, norm, nseq, s);
+  }
+}
+
+// Forward FFT of nseq sequences: first pass in mode `first` (from `src`), the
+// rest ping-ponging a -> b. Returns the buffer holding the spectra.
+template <int kFirst>
+cudaError_t fft_many(const double2* src, const double2* src2, double2* a, double2* b, int M, int N,
+                     const double2* tw, const ln::CurveNorm* norm, int64_t nseq, cudaStream_t s,
+                     double2** result) {
+  int Ns = 1;
+  double2* dst = a;
+  double2* other = b;
+  bool first = true;
+  cudaError_t e = cudaSuccess;
+  while (Ns < M && e == cudaSuccess) {
+    const int rem = M / Ns;
+    const int R = rem >= 16 ? 16 : rem;
+    if (first)
+      e = pass_r<kFirst>(R, src, src2, dst, M, N, Ns, tw, norm, nseq, s);
+    else
+      e = pass_r<ln::kPlain>(R, other, nullptr, dst, M, N, Ns, tw, norm, nseq, s);
+    first = false;
+    Ns *= R;
+    double2* t = dst;
+    dst = other;
+    other = t;
+  }
+  *result = other;
+  return e;
+}
+
+}  // namespace
+
+size_t large_workspace_bytes(int64_t chunk, int N) {
+  const int M = pf::fft_len(N);
+  const size_t seq = sizeof(double2) * (size_t)M;
+  const int nblk = (N + ln::kT * 4 - 1) / (ln::kT * 4);
+  return 4 * seq * (size_t)chunk                      // two ping-pong pairs of spectra
+         + 2 * sizeof(ln::CurveNorm) * (size_t)chunk  // norms
+         + 2 * sizeof(double) * (size_t)chunk         // sums of squares
+         + 2 * sizeof(int32_t) * (size_t)chunk + 16   // bad flags
+         + sizeof(double2) * (size_t)chunk            // rotations
+         + sizeof(double) * (size_t)(chunk * nblk) + 256;
+}
+
+int64_t large_chunk_pairs(int N) {
+  // ~96 MB working set: 4 spectra of 16 M bytes per pair at N = 65536
+  const int M = pf::fft_len(N);
+  const int64_t per = 4 * (int64_t)sizeof(double2) * M;
+  int64_t c = (96ll << 20) / per;
+  return c < 1 ? 1 : c;
+}
+
+cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pairs, int N, int normalize,
+                               const double2* tw, cva_alignment* out, double2* aligned, void* ws,
+                               int64_t chunk, cudaStream_t s) {
+  const int M = pf::fft_len(N);
+  const int nblk = (N + ln::kT * 4 - 1) / (ln::kT * 4);
+  char* w = (char*)ws;
+  auto take = [&](size_t bytes) {
+    char* p = w;
+    w += (bytes + 255) & ~size_t(255);
+    return (void*)p;
+  };
+  double2* A = (double2*)take(sizeof(double2) * (size_t)M * chunk);
+  double2* B = (double2*)take(sizeof(double2) * (size_t)M * chunk);
+  double2* C = (double2*)take(sizeof(double2) * (size_t)M * chunk);
+  double2* D = (double2*)take(sizeof(double2) * (size_t)M * chunk);
+  ln::CurveNorm* n1 = (ln::CurveNorm*)take(sizeof(ln::CurveNorm) * chunk);
+  ln::CurveNorm* n2 = (ln::CurveNorm*)take(sizeof(ln::CurveNorm) * chunk);
+  double* s1 = (double*)take(sizeof(double) * chunk);
+  double* s2 = (double*)take(sizeof(double) * chunk);
+  int32_t* b1 = (int32_t*)take(sizeof(int32_t) * chunk);
+  int32_t* b2 = (int32_t*)take(sizeof(int32_t) * chunk);
+  double2* rot = (double2*)take(sizeof(double2) * chunk);
+  double* bmax = (double*)take(sizeof(double) * chunk * nblk);
+  cudaError_t e = cudaSuccess;
+  for (int64_t p0 = 0; p0 < pairs && e == cudaSuccess; p0 += chunk) {
+    const int64_t P = pairs - p0 < chunk ? pairs - p0 : chunk;
+    const double2* z1 = c1 + p0 * N;
+    const double2* z2 = c2 + p0 * N;
+    ln::stats_kernel<<<(unsigned)P, ln::kT, 0, s>>>(z1, N, normalize, n1, s1, b1);
+    ln::stats_kernel<<<(unsigned)P, ln::kT, 0, s>>>(z2, N, normalize, n2, s2, b2);
+    double2 *Z1 = nullptr, *Z2 = nullptr, *F = nullptr;
+    e = fft_many<ln::kLoadA>(z1, nullptr, A, B, M, N, tw, n1, P, s, &Z1);
+    if (e == cudaSuccess) e = fft_many<ln::kLoadB>(z2, nullptr, C, D, M, N, tw, n2, P, s, &Z2);
+    if (e != cudaSuccess) break;
+    double2* fa = (Z1 == A) ? B : A;  // free buffers for the correlation transform
+    double2* fb = (Z2 == C) ? D : C;
+    e = fft_many<ln::kProduct>(Z1, Z2, fa, fb, M, N, tw, nullptr, P, s, &F);
+    if (e != cudaSuccess) break;
+    ln::lmax_kernel<<<dim3((unsigned)nblk, (unsigned)P), ln::kT, 0, s>>>(F, M, N, bmax);
+    ln::lpick_kernel<<<(unsigned)P, ln::kT, 0, s>>>(F, M, N, bmax, nblk, s1, s2, b1, b2, out + p0, rot);
+    if (aligned)
+      ln::aligned_kernel<<<dim3((unsigned)((N + 4 * ln::kT - 1) / (4 * ln::kT)), (unsigned)P), ln::kT, 0, s>>>(
+          z2, N, n2, out + p0, rot, aligned + p0 * N);
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+}  // namespace cva

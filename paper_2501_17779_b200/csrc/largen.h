@@ -1,0 +1,24 @@
+// Host-side declarations of the large-N path (largen.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+#include "../../include/curvalign_cuda.h"
+
+namespace cva {
+
+// Workspace for `chunk` pairs of N-node curves and the pair count per chunk
+// that keeps the chunk's working set L2-resident.
+size_t large_workspace_bytes(int64_t chunk, int N);
+int64_t large_chunk_pairs(int N);
+
+// align_fft (normalize = 0) or preprocess(resample=false) + align_fft
+// (normalize = 1) for pairs of N-node curves whose transform length exceeds the
+// shared-memory kernels. tw: twiddles of length fft_len(N). aligned nullable.
+cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pairs, int N, int normalize,
+                               const double2* tw, cva_alignment* out, double2* aligned, void* ws,
+                               int64_t chunk, cudaStream_t s);
+
+}  // namespace cva

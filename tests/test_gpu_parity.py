@@ -121,11 +121,64 @@ def test_any_n_matches_oracle(cuda, oracle, n):
         check_pair(res[p], r, a[p], b[p], al[p], want_al)
 
 
-def test_beyond_shared_memory_refused(cuda):
-    """N past the shared-memory pair kernels is refused loudly (large-N path: §8 C3)."""
-    z = np.zeros((1, 1500, 2))
-    with pytest.raises(_native.CurvalignError):
-        cva.align_fft_batch(z, z)
+@pytest.mark.parametrize("n", [1500, 2049, 4096, 4097, 8192, 65536])
+def test_large_n_matches_oracle(cuda, oracle, n):
+    """Transform lengths past shared memory run the L2-chunked multi-pass path
+    (N = 4097 is the reference's own largest test size, acceptance.cpp:97-98)."""
+    rng = np.random.default_rng(n)
+    phi = 2 * PI * np.arange(n) / n
+    r = 1 + 0.2 * np.cos(3 * phi + 0.3) + 0.05 * np.sin(7 * phi)
+    a = np.stack([r * np.cos(phi), r * np.sin(phi)], 1)
+    k = int(rng.integers(0, n))
+    th = 0.7
+    b = np.roll(a, k, 0) @ np.array([[np.cos(th), np.sin(th)], [-np.sin(th), np.cos(th)]]) + 1e-4 * rng.standard_normal((n, 2))
+    A, B = np.stack([a, b]), np.stack([b, a])
+    res, al = cva.align_fft_batch(A, B, return_aligned=True)
+    for p in range(2):
+        want = oracle.align(A[p], B[p])
+        c, sn = np.cos(want["theta"]), np.sin(want["theta"])
+        q = B[p][(np.arange(n) + int(want["shift"])) % n]
+        wal = np.stack([c * q[:, 0] + sn * q[:, 1], -sn * q[:, 0] + c * q[:, 1]], 1)
+        check_pair(res[p], want, A[p], B[p], al[p], wal)
+
+
+def test_c3_full_size(cuda, oracle):
+    """C3: 256 pairs at N = 65536 (center + normalize + align fused); oracle on a
+    subset, planted shift / rotation recovered on all."""
+    import torch
+
+    cfg = synth.CONFIGS["c3"]
+    c1, c2, k, th = synth.uniform_pairs(3, cfg["pairs"], cfg["N"], cfg["modes"], cfg["amp"], cfg["amp_exp"],
+                                        cfg["sigma"])
+    raw, al = cva.preprocess_align_uniform(torch.from_numpy(c1).cuda(), torch.from_numpy(c2).cuda(),
+                                           return_aligned=True)
+    res = cva.decode_results(raw)
+    assert (res["status"] == 0).all()
+    assert (res["shift"] == k).all()
+    assert np.abs(wrap(res["theta"] - th)).max() < 1e-3
+    al = al.cpu().numpy()
+    for p in (0, 101, 255):
+        u = oracle.preprocess(c1[p], 0, resample=False)
+        v = oracle.preprocess(c2[p], 0, resample=False)
+        want = oracle.align(u, v)
+        c, sn = np.cos(want["theta"]), np.sin(want["theta"])
+        q = v[(np.arange(cfg["N"]) + int(want["shift"])) % cfg["N"]]
+        wal = np.stack([c * q[:, 0] + sn * q[:, 1], -sn * q[:, 0] + c * q[:, 1]], 1)
+        check_pair(res[p], want, u, v, al[p], wal)
+
+
+def test_uniform_small_n_matches_split_path(cuda):
+    """preprocess_align_uniform at small N equals preprocess(resample=False) + align."""
+    c1, c2, _, _ = synth.uniform_pairs(5, 6, 256, sigma=1e-3)
+    r1, a1 = cva.preprocess_align_uniform(c1, c2, return_aligned=True)
+    pts, offs = cva.ragged(list(c1) + list(c2))
+    prep, _ = cva.preprocess_batch(pts, offs, 0, resample=False)
+    p1, p2 = prep[: 6 * 256].reshape(6, 256, 2), prep[6 * 256:].reshape(6, 256, 2)
+    r2, a2 = cva.align_fft_batch(p1, p2, return_aligned=True)
+    np.testing.assert_array_equal(r1["shift"], r2["shift"])
+    assert np.abs(wrap(r1["theta"] - r2["theta"])).max() < 1e-12
+    np.testing.assert_allclose(r1["energy"], r2["energy"], rtol=1e-10, atol=1e-16)
+    np.testing.assert_allclose(a1, a2, atol=1e-13)
 
 
 def test_energy_matches_direct_residual(cuda):  # test_rigid_align.cpp:187-197
