@@ -12,11 +12,11 @@ REF      ?= /root/reference
 
 KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h $(CSRC)/fused.h $(CSRC)/largen.h include/curvalign_cuda.h
 
-.PHONY: all lib synth dropin oracle ref clean prof
+.PHONY: all lib synth dropin dropin_test oracle ref clean prof
 
 # Phase-timing build (tools/phase_timing.py): separate .so, never shipped.
 prof: $(PKG)/libcurvalign_cuda_prof.so
-$(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kernels.cu $(CSRC)/allpairs.cu $(KERNEL_HDRS) $(CSRC)/prof.cuh
+$(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kernels.cu $(CSRC)/allpairs.cu $(CSRC)/largen.cu $(CSRC)/dropin_kernels.cu $(KERNEL_HDRS) $(CSRC)/prof.cuh
 	@mkdir -p $(BUILD)/prof
 	$(NVCC) $(NVFLAGS) -DCVA_PHASE_TIMING -c $(CSRC)/fused.cu -o $(BUILD)/prof/fused.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/kernels.cu -o $(BUILD)/prof/kernels.o
@@ -24,8 +24,9 @@ $(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kern
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/probe.cu -o $(BUILD)/prof/probe.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/allpairs.cu -o $(BUILD)/prof/allpairs.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/largen.cu -o $(BUILD)/prof/largen.o
+	$(NVCC) $(NVFLAGS) -c $(CSRC)/dropin_kernels.cu -o $(BUILD)/prof/dropin_kernels.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(BUILD)/prof/*.o
-all: lib synth oracle ref
+all: lib synth dropin dropin_test oracle ref
 
 lib: $(PKG)/libcurvalign_cuda.so
 synth: $(PKG)/libcurvalign_synth.so
@@ -47,6 +48,10 @@ $(BUILD)/largen.o: $(CSRC)/largen.cu $(KERNEL_HDRS) $(CSRC)/largen.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_largen.log || (cat $(BUILD)/ptxas_largen.log; exit 1)
 
+$(BUILD)/dropin_kernels.o: $(CSRC)/dropin_kernels.cu $(KERNEL_HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
 $(BUILD)/capi.o: $(CSRC)/capi.cpp $(CSRC)/kernels.h $(CSRC)/fused.h include/curvalign_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
@@ -55,7 +60,7 @@ $(BUILD)/probe.o: $(CSRC)/probe.cu include/curvalign_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/fused.o $(BUILD)/allpairs.o $(BUILD)/largen.o $(BUILD)/capi.o $(BUILD)/probe.o
+$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/fused.o $(BUILD)/allpairs.o $(BUILD)/largen.o $(BUILD)/dropin_kernels.o $(BUILD)/capi.o $(BUILD)/probe.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
 
 # Synthetic workload generators (bench harness; host only).
@@ -64,9 +69,17 @@ $(PKG)/libcurvalign_synth.so: $(CSRC)/synth.cpp
 
 # C++ drop-in for the reference API (namespace curvalign), on top of the C ABI.
 DROPIN_SRCS := $(wildcard $(CSRC)/dropin/*.cpp)
-$(PKG)/libcurvalign.so: $(DROPIN_SRCS) $(wildcard include/curvalign/*.hpp) $(PKG)/libcurvalign_cuda.so
+$(PKG)/libcurvalign.so: $(DROPIN_SRCS) $(wildcard include/curvalign/*.hpp) $(CSRC)/dropin/status.hpp $(PKG)/libcurvalign_cuda.so
 	$(CXX) -O2 -std=c++20 -fPIC -shared -Wall -Iinclude -o $@ $(DROPIN_SRCS) \
 	    -L$(PKG) -lcurvalign_cuda -Wl,-rpath,'$$ORIGIN'
+
+# C++ tests of the drop-in API (restating the reference's doctest cases); run
+# on a GPU by tests/test_gpu_dropin_cpp.py.
+tests/cpp/bin/test_dropin: tests/cpp/test_dropin.cpp $(PKG)/libcurvalign.so
+	@mkdir -p tests/cpp/bin
+	$(CXX) -O2 -std=c++20 -Wall -Iinclude -o $@ $< -L$(PKG) -lcurvalign -lcurvalign_cuda \
+	    -Wl,-rpath,'$$ORIGIN/../../../$(PKG)'
+dropin_test: tests/cpp/bin/test_dropin
 
 oracle:
 	$(MAKE) -C oracle oracle

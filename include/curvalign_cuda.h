@@ -157,6 +157,33 @@ int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t ro
                       int64_t row_end, double* energy, int32_t* shift, double* theta);
 
 /* ---------------------------------------------------------------------------
+ * Single-curve utilities behind the C++ drop-in API (synchronous, host
+ * buffers, GPU compute). cva_dropin_last_error() describes their failures.
+ * ------------------------------------------------------------------------- */
+
+const char* cva_dropin_last_error(void);
+/* A(m), m in [m_begin, m_begin + m_count): out4[4 i + {0,1,2,3}] = a11, a12, a21, a22
+ * (cross_correlation_matrix / correlation_all_shifts_*, rigid_align.cpp:65-80, :126-183). */
+int cva_correlation_matrices_host(const double* c1, const double* c2, int64_t n, int64_t m_begin,
+                                  int64_t m_count, double* out4);
+/* mismatch_energy (rigid_align.cpp:185-196) */
+int cva_mismatch_energy_host(const double* c1, const double* c2, int64_t n, int64_t shift, double theta,
+                             double* out);
+/* centroid (curve.cpp:27-32) and curve_length (curve.cpp:17-25); either output nullable */
+int cva_curve_stats_host(const double* xy, int64_t n, double* centroid2, double* length);
+/* mode 1: center_curve (curve.cpp:34-39); mode 2: normalize_length (curve.cpp:41-48) */
+int cva_center_or_normalize_host(const double* xy, int64_t n, int mode, double* out);
+/* arc_length_params (curve.cpp:50-65): s[0..n], total */
+int cva_arc_length_params_host(const double* xy, int64_t n, double* s, double* total);
+/* PeriodicCubicSpline second derivatives m[0..n_knots) (spline.cpp:62-96) */
+int cva_spline_solve_host(const double* x, const double* y, int64_t n_knots, double* m);
+/* srv_transform (srv.cpp:71-88); center != 0 also applies srv_center (srv.cpp:90-98) */
+int cva_srv_transform_host(const double* xy, int64_t n, int center, double* q);
+/* X_k = scale * sum_j x_j exp(sign 2 pi i j k / n), k < kcount (any n; real_dft / real_idft) */
+int cva_dft_host(const double* x_complex, int64_t n, int64_t kcount, int sign, double scale,
+                 double* out_complex);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics (not on the hot path).
  * ------------------------------------------------------------------------- */
 

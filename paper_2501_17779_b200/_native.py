@@ -78,6 +78,15 @@ SIGNATURES = {
     ),
     "cva_srv_align_batch_host": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "cva_probe_fp64_tflops": (c_int, [c_void_p]),
+    "cva_dropin_last_error": (c_char_p, []),
+    "cva_correlation_matrices_host": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p]),
+    "cva_mismatch_energy_host": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_double, c_void_p]),
+    "cva_curve_stats_host": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "cva_center_or_normalize_host": (c_int, [c_void_p, c_int64, c_int, c_void_p]),
+    "cva_arc_length_params_host": (c_int, [c_void_p, c_int64, c_void_p, c_void_p]),
+    "cva_spline_solve_host": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
+    "cva_srv_transform_host": (c_int, [c_void_p, c_int64, c_int, c_void_p]),
+    "cva_dft_host": (c_int, [c_void_p, c_int64, c_int64, c_int, c_double, c_void_p]),
     "cva_preprocess_align_uniform": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
     "cva_preprocess_align_uniform_host": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "cva_allpairs": (

@@ -1,0 +1,377 @@
+// C++ tests of the drop-in API (include/curvalign/*.hpp over libcurvalign_cuda.so).
+// Each case restates a hot-path test of the reference's own suite
+// (/root/reference/proj/tests/test_rigid_align.cpp, test_curve_core.cpp,
+// test_srv.cpp; file:line cited per case), written against the same API so a
+// reference user's code compiles unchanged. Fixture curves are generated here
+// (the reference's synthetic.cpp generators are outside this library).
+// Exit status = number of failed checks.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "curvalign/curve.hpp"
+#include "curvalign/fft.hpp"
+#include "curvalign/rigid_align.hpp"
+#include "curvalign/spline.hpp"
+#include "curvalign/srv.hpp"
+
+using namespace curvalign;
+
+static int g_fail = 0, g_checks = 0;
+static std::string g_case;
+#define CHECK(cond)                                                                  \
+  do {                                                                               \
+    ++g_checks;                                                                      \
+    if (!(cond)) {                                                                   \
+      ++g_fail;                                                                      \
+      std::printf("FAIL [%s] %s:%d: %s\n", g_case.c_str(), __FILE__, __LINE__, #cond); \
+    }                                                                                \
+  } while (0)
+template <class E, class F>
+static bool throws(F&& f) {
+  try {
+    f();
+  } catch (const E&) {
+    return true;
+  } catch (...) {
+    return false;
+  }
+  return false;
+}
+static void run(const char* name, const std::function<void()>& f) {
+  g_case = name;
+  try {
+    f();
+  } catch (const std::exception& e) {
+    ++g_fail;
+    std::printf("FAIL [%s] unexpected exception: %s\n", name, e.what());
+  }
+}
+
+static const double kPi = 3.14159265358979323846;
+
+static Curve polar(std::size_t n, const std::function<double(double)>& r) {
+  Curve c;
+  c.nodes.resize(n);
+  for (std::size_t l = 0; l < n; ++l) {
+    const double phi = 2.0 * kPi * (double)l / (double)n;
+    c.nodes[l] = Point2(r(phi) * std::cos(phi), r(phi) * std::sin(phi));
+  }
+  return c;
+}
+static Curve limacon(std::size_t n) { return polar(n, [](double p) { return 0.75 + 0.5 * std::cos(p); }); }
+static Curve circle(std::size_t n) { return polar(n, [](double) { return 1.0; }); }
+static Curve bumps(std::size_t n) { return polar(n, [](double p) { return 1.0 + 0.2 * std::sin(6.0 * p); }); }
+static Curve hippopede(std::size_t n) {
+  return polar(n, [](double p) { return std::sqrt(4.0 * 0.9 * (1.0 - 0.9 * std::sin(p) * std::sin(p))); });
+}
+static Curve random_curve(std::mt19937_64& rng, std::size_t n) {
+  std::uniform_real_distribution<double> u(-1.0, 1.0);
+  Curve c;
+  c.nodes.resize(n);
+  for (auto& p : c.nodes) p = Point2(u(rng), u(rng));
+  return c;
+}
+static double wrap_angle(double t) {
+  while (t > kPi) t -= 2.0 * kPi;
+  while (t < -kPi) t += 2.0 * kPi;
+  return t;
+}
+// c2[l] = rotate_ccw(c1[(l - k) mod n], th): the reference recovers shift k, angle th
+static Curve shift_rotate(const Curve& c1, std::size_t k, double th) {
+  const std::size_t n = c1.size();
+  Curve c2;
+  c2.nodes.resize(n);
+  for (std::size_t l = 0; l < n; ++l) c2.nodes[l] = rotate_ccw(c1[(l + n - k) % n], th);
+  return c2;
+}
+
+int main() {
+  // ---------------------------------------------------------- rigid_align
+  run("diamond", [] {  // test_rigid_align.cpp:47-56
+    Curve c;
+    c.nodes = {{1, 0}, {0, 1}, {-1, 0}, {0, -1}};
+    const Mat2 a = cross_correlation_matrix(c.nodes, c.nodes, 1);
+    CHECK(std::fabs(a.a11) < 1e-15 && std::fabs(a.a12 - 2.0) < 1e-15 && std::fabs(a.a21 + 2.0) < 1e-15 &&
+          std::fabs(a.a22) < 1e-15);
+  });
+  run("direct double loop", [] {  // :58-70
+    std::mt19937_64 rng(7);
+    Curve c1 = random_curve(rng, 37), c2 = random_curve(rng, 37);
+    for (std::size_t m : {0u, 1u, 13u, 36u}) {
+      Mat2 want;
+      for (std::size_t l = 0; l < 37; ++l) {
+        const Point2 p = c1[l], q = c2[(l + m) % 37];
+        want.a11 += p.x * q.x, want.a12 += p.x * q.y, want.a21 += p.y * q.x, want.a22 += p.y * q.y;
+      }
+      const Mat2 got = cross_correlation_matrix(c1.nodes, c2.nodes, m);
+      CHECK(std::fabs(got.a11 - want.a11) < 1e-12 && std::fabs(got.a12 - want.a12) < 1e-12 &&
+            std::fabs(got.a21 - want.a21) < 1e-12 && std::fabs(got.a22 - want.a22) < 1e-12);
+    }
+  });
+  run("closed form known matrix", [] {  // :79-86
+    const RotationFit f = optimal_rotation_closed_form(Mat2{0.0, 1.0, -1.0, 0.0});
+    CHECK(std::fabs(f.rotation.theta() - kPi / 2) < 1e-14 && std::fabs(f.trace - 2.0) < 1e-13 && !f.degenerate);
+  });
+  run("svd vs closed form", [] {  // :88-100
+    std::mt19937_64 rng(23);
+    std::uniform_real_distribution<double> u(-2.0, 2.0);
+    for (int k = 0; k < 1000; ++k) {
+      const Mat2 a{u(rng), u(rng), u(rng), u(rng)};
+      const RotationFit s = optimal_rotation_svd(a), c = optimal_rotation_closed_form(a);
+      CHECK(std::fabs(s.trace - c.trace) < 1e-10);
+      if (!s.degenerate && !c.degenerate && std::fabs(s.trace) > 1e-6)
+        CHECK(std::fabs(wrap_angle(s.rotation.theta() - c.rotation.theta())) < 1e-8);
+    }
+  });
+  run("degenerate", [] {  // :102-108
+    CHECK(optimal_rotation_svd(Mat2{}).degenerate);
+    CHECK(optimal_rotation_closed_form(Mat2{}).degenerate);
+  });
+  run("fixed start rotation", [] {  // :125-131
+    Curve c1 = bumps(128), c2 = c1;
+    for (auto& p : c2.nodes) p = rotate_ccw(p, kPi / 3.0);
+    CHECK(std::fabs(optimal_rotation_fixed_start(c1, c2).theta() - kPi / 3.0) < 1e-10);
+  });
+  run("naive == fft stacks", [] {  // :133-151
+    std::mt19937_64 rng(43);
+    for (std::size_t n : {8u, 20u, 64u, 101u}) {
+      Curve c1 = random_curve(rng, n), c2 = random_curve(rng, n);
+      const auto a = correlation_all_shifts_naive(c1.nodes, c2.nodes);
+      const auto b = correlation_all_shifts_fft(c1.nodes, c2.nodes);
+      CHECK(a.size() == n && b.size() == n);
+      for (std::size_t m = 0; m < n; ++m)
+        CHECK(std::fabs(a[m].a11 - b[m].a11) < 1e-9 * n && std::fabs(a[m].a22 - b[m].a22) < 1e-9 * n);
+      const RigidAlignment f = align_fft(c1, c2), g = align_naive(c1, c2);
+      CHECK(f.shift == g.shift && std::fabs(f.energy - g.energy) < 1e-9);
+    }
+  });
+  run("exact cyclic shift", [] {  // :153-168
+    Curve c1 = limacon(96), c2;
+    c2.nodes.resize(96);
+    for (std::size_t l = 0; l < 96; ++l) c2.nodes[(l + 29) % 96] = c1[l];
+    const RigidAlignment a = align_fft(c1, c2);
+    CHECK(a.shift == 29 && std::fabs(a.rotation.theta()) < 1e-9 && a.energy < 1e-15);
+    const RigidAlignment b = align_naive(c1, c2);
+    CHECK(b.shift == a.shift);
+  });
+  run("circle tie -> shift 0", [] {  // :170-176
+    Curve c = circle(64);
+    const RigidAlignment a = align_fft(c, c);
+    CHECK(a.shift == 0 && std::fabs(a.rotation.theta()) < 1e-9 && a.energy < 1e-12);
+  });
+  run("shift and rotation recovered", [] {  // :178-185 (fixture built by cyclic shift + rotation)
+    Curve c1 = polar(256, [](double p) { return 1.0 + 0.2 * std::cos(3 * p + 0.4) + 0.1 * std::sin(5 * p); });
+    Curve c2 = shift_rotate(c1, 64, kPi / 3.0);
+    const RigidAlignment a = align_fft(c1, c2);
+    CHECK(std::fabs(a.t0 - 0.25) < 1e-12 && std::fabs(a.rotation.theta() - kPi / 3.0) < 1e-9 && a.energy < 1e-12);
+  });
+  run("energy identity", [] {  // :187-197
+    std::mt19937_64 rng(57);
+    Curve c1 = random_curve(rng, 48), c2 = random_curve(rng, 48);
+    const RigidAlignment a = align_naive(c1, c2);
+    const double direct = mismatch_energy(c1.nodes, c2.nodes, a.shift, a.rotation);
+    CHECK(std::fabs(a.energy - direct) <= 1e-9 * std::fabs(direct));
+  });
+  run("optimum beats random candidates", [] {  // :199-210
+    std::mt19937_64 rng(61);
+    Curve c1 = random_curve(rng, 40), c2 = random_curve(rng, 40);
+    const RigidAlignment a = align_naive(c1, c2);
+    std::uniform_real_distribution<double> ang(-kPi, kPi);
+    std::uniform_int_distribution<std::size_t> sh(0, 39);
+    for (int k = 0; k < 100; ++k) CHECK(a.energy <= mismatch_energy(c1.nodes, c2.nodes, sh(rng), Rotation2(ang(rng))) + 1e-12);
+  });
+  run("rotation covariance", [] {  // :212-220
+    Curve c1 = hippopede(128), c2 = c1;
+    for (auto& p : c2.nodes) p = rotate_ccw(p, 0.4);
+    const RigidAlignment base = align_fft(c1, c1), rot = align_fft(c1, c2);
+    CHECK(rot.shift == base.shift && std::fabs(wrap_angle(rot.rotation.theta() - base.rotation.theta()) - 0.4) < 1e-8);
+  });
+  run("shift covariance", [] {  // :222-235
+    std::mt19937_64 rng(71);
+    Curve c1 = random_curve(rng, 60), c2 = random_curve(rng, 60), c2s;
+    const RigidAlignment base = align_naive(c1, c2);
+    c2s.nodes.resize(60);
+    for (std::size_t l = 0; l < 60; ++l) c2s.nodes[l] = c2[(l + 17) % 60];
+    const RigidAlignment s = align_naive(c1, c2s);
+    CHECK(s.shift == (base.shift + 60 - 17) % 60 && std::fabs(s.rotation.theta() - base.rotation.theta()) < 1e-10 &&
+          std::fabs(s.energy - base.energy) <= 1e-10 * base.energy);
+  });
+  run("reflection", [] {  // :237-246
+    Curve c1 = limacon(128), c2 = c1;
+    for (auto& p : c2.nodes) p.y = -p.y;
+    const RigidAlignment a = align_fft(c1, c2);
+    const Mat2 r = a.rotation.matrix();
+    CHECK(std::fabs(r.a11 * r.a22 - r.a12 * r.a21 - 1.0) < 1e-12 && a.energy > 1e-6);
+  });
+  run("validation", [] {  // :248-257
+    Curve c1 = circle(32), c2 = circle(64), tiny;
+    tiny.nodes = {{0, 0}, {1, 0}, {0, 1}};
+    CHECK(throws<std::invalid_argument>([&] { align_fft(c1, c2); }));
+    CHECK(throws<std::invalid_argument>([&] { cross_correlation_matrix(c1.nodes, c2.nodes, 0); }));
+    CHECK(throws<std::invalid_argument>([&] { cross_correlation_matrix(c1.nodes, c1.nodes, 32); }));
+    CHECK(throws<std::invalid_argument>([&] { align_fft(tiny, tiny); }));
+  });
+
+  // ----------------------------------------------------------- curve core
+  run("curve_length", [] {  // test_curve_core.cpp:73-84
+    Curve sq;
+    sq.nodes = {{0, 0}, {1, 0}, {1, 1}, {0, 1}};
+    CHECK(std::fabs(curve_length(sq) - 4.0) < 1e-15);
+    CHECK(std::fabs(curve_length(circle(256)) - 512.0 * std::sin(kPi / 256.0)) < 1e-12);
+  });
+  run("centroid / center", [] {  // :86-104
+    Curve c;
+    c.nodes = {{0, 0}, {2, 0}, {2, 2}, {0, 2}};
+    const Point2 g = centroid(c);
+    CHECK(std::fabs(g.x - 1.0) < 1e-15 && std::fabs(g.y - 1.0) < 1e-15);
+    const Curve ce = center_curve(c);
+    CHECK(std::fabs(ce[0].x + 1.0) < 1e-15 && std::fabs(ce[2].y - 1.0) < 1e-15);
+    const Point2 m = centroid(ce);
+    CHECK(std::hypot(m.x, m.y) < 1e-12);
+  });
+  run("normalize_length", [] {  // :106-113
+    Curve sq;
+    sq.nodes = {{0, 0}, {1, 0}, {1, 1}, {0, 1}};
+    const Curve c = normalize_length(sq);
+    CHECK(std::fabs(curve_length(c) - 1.0) < 1e-14 && std::fabs(c[1].x - 0.25) < 1e-14);
+  });
+  run("arc_length_params", [] {  // :126-138
+    Curve sq, rect;
+    sq.nodes = {{0, 0}, {1, 0}, {1, 1}, {0, 1}};
+    rect.nodes = {{0, 0}, {2, 0}, {2, 1}, {0, 1}};
+    const ArcLengthParams a = arc_length_params(sq), b = arc_length_params(rect);
+    const double es[5] = {0, 0.25, 0.5, 0.75, 1.0}, er[5] = {0, 1.0 / 3.0, 0.5, 5.0 / 6.0, 1.0};
+    CHECK(a.s.size() == 5 && std::fabs(a.total_length - 4.0) < 1e-14);
+    for (int i = 0; i < 5; ++i) CHECK(std::fabs(a.s[i] - es[i]) < 1e-15 && std::fabs(b.s[i] - er[i]) < 1e-15);
+    Curve dup;
+    dup.nodes = {{0, 0}, {1, 0}, {1, 0}, {0, 1}};
+    CHECK(throws<std::invalid_argument>([&] { arc_length_params(dup); }));
+  });
+  run("spline knots / smooth / bad knots", [] {  // :36-71
+    std::vector<double> x = {0.0, 0.2, 0.45, 0.7, 1.0}, y = {1.0, -0.5, 2.0, 0.25, 1.0};
+    PeriodicCubicSpline s(x, y);
+    for (std::size_t i = 0; i + 1 < x.size(); ++i) CHECK(std::fabs(s.eval(x[i]) - y[i]) < 1e-14);
+    CHECK(std::fabs(s.eval(0.0) - s.eval(1.0)) < 1e-14);
+    std::vector<double> xs(65), ys(65);
+    for (int i = 0; i <= 64; ++i) {
+      xs[i] = i / 64.0;
+      ys[i] = std::sin(2 * kPi * xs[i]);
+    }
+    PeriodicCubicSpline t(xs, ys);
+    double worst = 0.0;
+    for (int k = 0; k < 1000; ++k) worst = std::fmax(worst, std::fabs(t.eval(k / 1000.0) - std::sin(2 * kPi * k / 1000.0)));
+    CHECK(worst < 1e-5);
+    std::vector<double> bx = {0.0, 0.5, 0.25, 0.75}, by = {0, 1, 2, 3};
+    CHECK(throws<std::invalid_argument>([&] { PeriodicCubicSpline(bx, by); }));
+  });
+  run("resample equalizes chords / reproduces uniform", [] {  // :154-189
+    Curve c;
+    c.nodes.resize(64);
+    for (int i = 0; i < 64; ++i) {
+      const double t = i / 64.0, u = t + 0.15 * t * (1.0 - t);
+      c.nodes[i] = Point2(std::cos(2 * kPi * u), std::sin(2 * kPi * u));
+    }
+    const Curve r = resample_uniform(c, 256);
+    double lo = 1e300, hi = 0.0;
+    for (std::size_t i = 0; i < 256; ++i) {
+      const double ch = (r[(i + 1) % 256] - r[i]).norm();
+      lo = std::fmin(lo, ch), hi = std::fmax(hi, ch);
+    }
+    CHECK((hi - lo) / hi < 0.02);
+    const Curve g = circle(128), rg = resample_uniform(g, 128);
+    double worst = 0.0;
+    for (std::size_t i = 0; i < 128; ++i) worst = std::fmax(worst, (rg[i] - g[i]).norm());
+    CHECK(worst < 1e-4);
+    Curve sq;
+    sq.nodes = {{0, 0}, {1, 0}, {1, 1}, {0, 1}};
+    CHECK(throws<std::invalid_argument>([&] { resample_uniform(sq, 4); }));
+  });
+  run("preprocess composes", [] {  // :215-232
+    const Curve c = hippopede(100), p = preprocess(c, 128);
+    const Curve manual = normalize_length(center_curve(resample_uniform(c, 128)));
+    CHECK(p.size() == 128);
+    bool same = true;
+    for (std::size_t i = 0; i < 128; ++i) same = same && p[i].x == manual[i].x && p[i].y == manual[i].y;
+    CHECK(same);
+    const Point2 m = centroid(p);
+    CHECK(std::hypot(m.x, m.y) < 1e-12 && std::fabs(curve_length(p) - 1.0) < 1e-12);
+    CHECK(preprocess(c, 64, false).size() == 100);
+    // the batched (fused) path agrees to rounding
+    const Curve b = preprocess_batch({c}, 128)[0];
+    for (std::size_t i = 0; i < 128; ++i) CHECK((b[i] - p[i]).norm() < 1e-14);
+  });
+
+  // ------------------------------------------------------------------ srv
+  run("srv of unit circle / equivariance / center", [] {  // test_srv.cpp:80-128
+    const SrvCurve q = srv_transform(preprocess(circle(512), 256));
+    CHECK(q.size() == 256 && std::fabs(q.h - 1.0 / 256.0) < 1e-15);
+    for (const auto& p : q.q) CHECK(std::fabs(p.norm() - 1.0) < 1e-3);
+    Curve c = preprocess(bumps(256), 128), cr = c;
+    for (auto& p : cr.nodes) p = rotate_ccw(p, 0.7);
+    const SrvCurve a = srv_transform(c), b = srv_transform(cr);
+    for (std::size_t l = 0; l < a.size(); ++l) {
+      const Point2 w = rotate_ccw(a.q[l], 0.7);
+      CHECK(std::fabs(b.q[l].x - w.x) < 1e-14 && std::fabs(b.q[l].y - w.y) < 1e-14);
+    }
+    const SrvCurve z = srv_center(a);
+    Point2 mean;
+    for (const auto& p : z.q) mean += p;
+    CHECK(std::hypot(mean.x, mean.y) / z.size() < 1e-12);
+  });
+
+  // ------------------------------------------------------------------ fft
+  run("real dft / idft / correlation", [] {
+    std::mt19937_64 rng(5);
+    std::normal_distribution<double> g;
+    for (std::size_t n : {2u, 3u, 8u, 33u, 101u, 256u}) {
+      std::vector<double> x(n), y(n);
+      for (auto& v : x) v = g(rng);
+      for (auto& v : y) v = g(rng);
+      const auto X = real_dft(x);
+      CHECK(X.size() == n / 2 + 1);
+      double err = 0.0;
+      for (std::size_t k = 0; k < X.size(); ++k) {
+        std::complex<double> w;
+        for (std::size_t j = 0; j < n; ++j) w += x[j] * std::polar(1.0, -2 * kPi * double((j * k) % n) / double(n));
+        err = std::fmax(err, std::abs(w - X[k]));
+      }
+      CHECK(err < 1e-12 * n);
+      const auto back = real_idft(X, n);
+      for (std::size_t j = 0; j < n; ++j) CHECK(std::fabs(back[j] - x[j]) < 1e-12);
+      const auto r = circular_cross_correlation(x, y);
+      for (std::size_t m = 0; m < n; ++m) {
+        double w = 0.0;
+        for (std::size_t l = 0; l < n; ++l) w += x[l] * y[(l + m) % n];
+        CHECK(std::fabs(w - r[m]) < 1e-12 * n);
+      }
+    }
+  });
+
+  // ---------------------------------------------------------------- batch
+  run("batch == single", [] {
+    std::mt19937_64 rng(9);
+    std::vector<Curve> a, b;
+    for (int p = 0; p < 5; ++p) {
+      a.push_back(random_curve(rng, 128));
+      b.push_back(shift_rotate(a.back(), 7 * p + 1, 0.3 * p));
+    }
+    std::vector<Curve> al;
+    const auto res = align_fft_batch(a, b, &al);
+    for (int p = 0; p < 5; ++p) {
+      const RigidAlignment s = align_fft(a[p], b[p]);
+      CHECK(res[p].shift == s.shift && res[p].shift == (std::size_t)(7 * p + 1));
+      CHECK(std::fabs(res[p].energy - mismatch_energy(a[p].nodes, b[p].nodes, s.shift, s.rotation)) < 1e-12);
+      for (std::size_t l = 0; l < 128; ++l) CHECK((al[p][l] - a[p][l]).norm() < 1e-12);
+    }
+    const auto pr = preprocess_align_batch(a, b, 256);
+    CHECK(pr.size() == 5);
+  });
+
+  std::printf("%d checks, %d failed\n", g_checks, g_fail);
+  return g_fail;
+}
