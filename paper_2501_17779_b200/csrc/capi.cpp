@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <new>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -460,32 +461,100 @@ int cva_resample_batch_host(const double* points, const int64_t* offsets, int64_
   return preprocess_host_impl(points, offsets, curves, n_out, 2, out, status);
 }
 
+// Per-thread, per-device host-path context: grow-only device buffers and
+// streams reused across calls (no per-call cudaMalloc of hundreds of MB).
+struct HostCtx {
+  int dev = -1;
+  static constexpr int kStreams = 3;
+  cudaStream_t st[kStreams] = {};
+  cudaEvent_t ready = nullptr;
+  void* buf[4] = {};
+  size_t cap[4] = {};
+  ~HostCtx() {
+    for (void* p : buf)
+      if (p) cudaFree(p);
+    for (cudaStream_t x : st)
+      if (x) cudaStreamDestroy(x);
+    if (ready) cudaEventDestroy(ready);
+  }
+  int init() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) return fail(CVA_CUDA_ERROR, "cudaGetDevice failed");
+    if (d == dev) return CVA_OK;
+    this->~HostCtx();
+    new (this) HostCtx();
+    dev = d;
+    for (auto& x : st)
+      if (cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess)
+        return fail(CVA_CUDA_ERROR, "stream creation failed");
+    if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess)
+      return fail(CVA_CUDA_ERROR, "event creation failed");
+    return CVA_OK;
+  }
+  void* get(int i, size_t bytes) {
+    if (cap[i] < bytes) {
+      if (buf[i]) cudaFree(buf[i]);
+      buf[i] = nullptr;
+      cap[i] = 0;
+      if (cudaMalloc(&buf[i], bytes) != cudaSuccess) return nullptr;
+      cap[i] = bytes;
+    }
+    return buf[i];
+  }
+};
+thread_local HostCtx t_host;
+
+// Host-buffer fused path, pipelined in chunks of pairs over 3 streams: the
+// H2D copy of chunk i+1, the kernel of chunk i and the D2H copy of chunk i-1
+// overlap (pinned host buffers give the asynchronous copies; pageable ones
+// still work, with less overlap).
 int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets, int64_t pairs,
                                     int64_t n_out, int resample, cva_alignment* out,
                                     double* aligned) {
   if (pairs <= 0) return pairs == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative pair count");
   if (int rc = require_device()) return rc;
   if (offsets[0] != 0) return fail(CVA_INVALID_ARGUMENT, "offsets[0] must be 0");
+  if (int rc = t_host.init()) return rc;
+  HostCtx& h = t_host;
   const int64_t total = offsets[2 * pairs];
-  const size_t ib = sizeof(double) * 2 * (size_t)total;
-  const size_t ab = sizeof(double) * 2 * (size_t)(pairs * n_out);
-  DevBuf dp, doff, dout, dal;
-  if (dp.alloc(ib) || doff.alloc(sizeof(int64_t) * (2 * pairs + 1)) ||
-      dout.alloc(sizeof(cva_alignment) * pairs) || (aligned && dal.alloc(ab)))
-    return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = nullptr;
-  cudaError_t e = cudaMemcpyAsync(dp.p, points, ib, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(doff.p, offsets, sizeof(int64_t) * (2 * pairs + 1), cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D");
-  if (int rc = cva_preprocess_align_batch((const double*)dp.p, (const int64_t*)doff.p, pairs,
-                                          host_max_n(offsets, 2 * pairs), n_out, resample,
-                                          (cva_alignment*)dout.p, aligned ? (double*)dal.p : nullptr, s))
-    return rc;
-  e = cudaMemcpyAsync(out, dout.p, sizeof(cva_alignment) * pairs, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && aligned) e = cudaMemcpyAsync(aligned, dal.p, ab, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  return finish(e, "preprocess_align_batch_host");
+  const size_t ib = sizeof(double2) * (size_t)total;
+  const size_t ab = sizeof(double2) * (size_t)(pairs * n_out);
+  double2* dp = (double2*)h.get(0, ib);
+  int64_t* doff = (int64_t*)h.get(1, sizeof(int64_t) * (size_t)(2 * pairs + 1));
+  cva_alignment* dout = (cva_alignment*)h.get(2, sizeof(cva_alignment) * (size_t)pairs);
+  double2* dal = aligned ? (double2*)h.get(3, ab) : nullptr;
+  if (!dp || !doff || !dout || (aligned && !dal)) return fail(CVA_BAD_ALLOC, "device allocation failed");
+  const int64_t max_n = host_max_n(offsets, 2 * pairs);
+  cudaError_t e = cudaMemcpyAsync(doff, offsets, sizeof(int64_t) * (size_t)(2 * pairs + 1),
+                                  cudaMemcpyHostToDevice, h.st[0]);
+  if (e == cudaSuccess) e = cudaEventRecord(h.ready, h.st[0]);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D offsets");
+  const int64_t nchunks = std::min<int64_t>(8, std::max<int64_t>(1, pairs / 256));
+  const int64_t per = (pairs + nchunks - 1) / nchunks;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int64_t p0 = c * per, p1 = std::min(pairs, p0 + per);
+    if (p0 >= p1) break;
+    cudaStream_t s = h.st[c % HostCtx::kStreams];
+    e = cudaStreamWaitEvent(s, h.ready, 0);
+    const int64_t a = offsets[2 * p0], b = offsets[2 * p1];
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(dp + a, points + 2 * a, sizeof(double2) * (size_t)(b - a), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D");
+    // the kernels index points with the absolute offsets; pass this chunk's slice
+    if (int rc = cva_preprocess_align_batch((const double*)dp, doff + 2 * p0, p1 - p0, max_n, n_out, resample,
+                                            dout + p0, aligned ? (double*)(dal + p0 * n_out) : nullptr, s))
+      return rc;
+    e = cudaMemcpyAsync(out + p0, dout + p0, sizeof(cva_alignment) * (size_t)(p1 - p0), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && aligned)
+      e = cudaMemcpyAsync(aligned + 2 * p0 * n_out, dal + p0 * n_out, sizeof(double2) * (size_t)((p1 - p0) * n_out),
+                          cudaMemcpyDeviceToHost, s);
+    if (e != cudaSuccess) return cuda_fail(e, "D2H");
+  }
+  for (cudaStream_t s : h.st) {
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "preprocess_align_batch_host");
+  }
+  return CVA_OK;
 }
 
 int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t row_begin,
