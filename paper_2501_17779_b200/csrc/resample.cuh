@@ -50,7 +50,7 @@ namespace rs {
 constexpr int kT = 256;            // threads per CTA = max chunks
 constexpr int kCMax = 12;          // knots per chunk
 constexpr int kNMax = kT * kCMax;  // raw nodes per curve (3072)
-constexpr int kScratchDoubles = 10 * kT;  // PCR ping-pong (2 x 5 arrays); also F / W / MB
+constexpr int kScratchDoubles = 11 * kT + 2;  // PCR ping-pong (2 x 5 arrays; F / W / MB alias them) + chunk offsets
 
 __device__ __forceinline__ void bar_sync() { __syncthreads(); }
 
@@ -139,9 +139,8 @@ struct CurveStats {
 
 // First sample index l in [0, N] with t_l = l / N >= x, t_l computed as the
 // reference does ((double)l / (double)N, curve.cpp:88). For N = 2^p, x * N is
-// exact and the answer is ceil(x N).
-// Clamped to [0, N] so that garbage knots of an invalid curve (NaN / inf,
-// flagged separately) can never index outside the output.
+// exact and the answer is ceil(x N). Clamped to [0, N] so that garbage knots
+// of an invalid curve (NaN / inf, flagged separately) never index outside.
 template <bool kPow2>
 __device__ __forceinline__ int first_sample(double x, int N) {
   const double nn = (double)N;
@@ -162,61 +161,90 @@ __device__ __forceinline__ double sample_t(int l, int N, double invN) {
 // Resample the raw curve already in xy[0..n) (shared) at t_l = l/N, l < N, into
 // out[0..N) (shared or global), uncentered. Returns the centroid and 1/length of
 // the resampled polygon so that preprocess(c) = (out - centroid) * inv_len.
-// s: shared, >= n+1 doubles. scr: shared, kScratchDoubles. red: 16 double2.
-// Requires 4 <= n <= kNMax, N >= 8 (kPow2: N a power of two), blockDim.x == kT.
+//
+// Knots follow the reference's rounding structure (curve.cpp:50-65,
+// spline.cpp:85): s_i = S_i / T with S_i the chordal prefix sum and T the
+// perimeter, and h_i = s_{i+1} - s_i (spacings taken from the normalised knots,
+// as the reference does, not from the edge lengths: with uneven spacing the
+// two differ by ~ulp(1)/h relative, which the spline system amplifies). S_i is a
+// two-level sum: sequential within a chunk, exclusive scan across chunks.
+//
+// L: shared, >= n + 1 doubles (chunk-local prefix sums, normalised in place). scr: shared,
+// kScratchDoubles. red: 16 double2. Requires 4 <= n <= kNMax, N >= 8 (kPow2:
+// N = 2^p), blockDim.x == kT. NOTE: no __restrict__ on these pointers: they
+// carry data between threads across __syncthreads(), and restrict lets the
+// compiler forward stale loads across the barrier.
 template <bool kPow2>
-// NOTE: no __restrict__ on these pointers: they carry data between threads
-// across __syncthreads(), and restrict lets the compiler forward stale loads
-// across the barrier.
-__device__ inline CurveStats resample_block(const double2* xy, int n, double* s, double* scr,
+__device__ inline CurveStats resample_block(const double2* xy, int n, double* L, double* scr,
                                             double2* red, double2* out, const int N,
                                             const int pb = 0 /* phase-stamp base */) {
   const int t = threadIdx.x;
+  const int lane = t & 31, wid = t >> 5;
   const int K = num_chunks(n);
   const bool own = t < K;
   const int a = own ? (t * n) / K : 0;
   const int b = own ? ((t + 1) * n) / K : 0;
+  const int M = b - 1 - a;  // interior knots (>= 1); knot b-1 is the interface
   int bad = 0;
 
-  // ---- phase 0: chordal arc length, s[i] = S_i / S_n, s[n] = 1 (curve.cpp:50-65)
-  double acc = 0.0;
+  // ---- phase 0: chordal edges, chunk-local prefix sums, cross-chunk scan
+  double tot = 0.0;
   if (own) {
 #pragma unroll 4
     for (int i = a; i < b; ++i) {
       const double2 p = xy[i], q = xy[i + 1 == n ? 0 : i + 1];
       const double dx = q.x - p.x, dy = q.y - p.y;
-      const double d = fsqrt(fma(dx, dx, dy * dy));
-      bad |= !(d > 0.0);
-      acc += d;
-      s[i + 1] = acc;
+      const double d = fsqrt(fma(dx, dx, dy * dy));  // curve.cpp:57
+      bad |= !(d > 0.0);                             // coincident nodes (curve.cpp:58)
+      tot += d;
+      if (i + 1 < b) L[i + 1] = tot;
     }
   }
-  double total;
-  const double off = scan_excl(acc, &total, red);
-  bad |= !isfinite(total);
-  const double inv_total = 1.0 / total;
-  if (own) {
-#pragma unroll 4
-    for (int i = a; i < b; ++i) s[i + 1] = (s[i + 1] + off) * inv_total;
+  double inc = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double u = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += u;
   }
-  if (t == 0) s[0] = 0.0;
+  bar_sync();  // previous users of red are done
+  if (lane == 31) red[wid].x = inc;
   bar_sync();
-  if (t == 0) s[n] = 1.0;  // forced (curve.cpp:64); written after every chunk's store
+  double T = 0.0, pre = 0.0;
+#pragma unroll
+  for (int w = 0; w < kT / 32; ++w) {
+    const double x = red[w].x;
+    if (w < wid) pre += x;
+    T += x;
+  }
+  bad |= !isfinite(T);
+  const double invT = 1.0 / T;
+  // normalise in place: L[i] <- s_i = (OFF_t + L_i) / T for this chunk's knots
+  // a..b-1 (s_a = OFF_t / T), and s_n = 1 (curve.cpp:63-64)
+  double* sk = L;
+  if (own) {
+    const double off = pre + inc - tot;
+    sk[a] = off * invT;
+#pragma unroll 4
+    for (int i = a + 1; i < b; ++i) sk[i] = (off + sk[i]) * invT;
+    if (t == K - 1) sk[n] = 1.0;
+  }
   bar_sync();
-
+  auto knot = [&](int i) -> double { return sk[i]; };
   CVA_MARK(pb + 0);
+
   // ---- phase 1: rhs, forward sweep, chunk-end responses
   double2 R[kCMax];  // right-hand sides, later forward values g
   double IB[kCMax];  // 1 / pivot of interior rows
   double2 v0f = make_double2(0, 0), v0l = make_double2(0, 0);
   double vLf = 0, vLl = 0, vRf = 0, vRl = 0;
-  double hL = 0, hj = 0;  // h_{b-2}, h_{b-1}
+  double hL = 0, hj = 0;            // h_{b-2}, h_{b-1}
   double2 rj = make_double2(0, 0);  // rhs of the interface row b-1
-  const int M = b - 1 - a;  // interior knots (>= 1)
   if (own) {
-    double si = s[a];
-    double hm = a == 0 ? s[n] - s[n - 1] : si - s[a - 1];
-    const double2 yp = xy[a == 0 ? n - 1 : a - 1];
+    // h_{a-1} = s_a - s_{a-1} (h_{n-1} = s_n - s_{n-1} for the first chunk)
+    const int ap = a == 0 ? n - 1 : a - 1;
+    double si = knot(a);
+    double hm = knot(a == 0 ? n : a) - knot(ap);
+    const double2 yp = xy[ap];
     double2 y0 = xy[a];
     const double ihm = frcp(hm);
     double2 slp = make_double2((y0.x - yp.x) * ihm, (y0.y - yp.y) * ihm);
@@ -228,7 +256,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
     for (int j = 0; j < kCMax; ++j) {
       if (j <= M) {
         const int i = a + j;
-        const double sn = s[i + 1];
+        const double sn = knot(i + 1);
         const double h = sn - si;
         bad |= !(h > 0.0);  // strictly increasing knots (spline.cpp:66-68)
         const double ih = frcp(h);
@@ -254,9 +282,9 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
             SL = fma(gL, Q, SL);
           }
           IB[j] = ib;
-          hL = h;  // h_L after the last interior row
+          hL = h;
         } else {
-          hj = h;  // interface row: h_{b-1}
+          hj = h;
           rj = r;
         }
         hm = h;
@@ -273,9 +301,8 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
     vLf = SL;
   }
 
-  CVA_MARK(pb + 1);
-  // ---- phase 2: interface rows -> cyclic PCR
-  double* F = scr;  // [K][4]: v0f.x, v0f.y, vLf, vRf
+  // ---- exchange chunk-start responses
+  double* F = scr + 5 * kT;  // PCR buffer 1 as [K][4]: v0f.x, v0f.y, vLf, vRf
   if (own) {
     F[4 * t + 0] = v0f.x;
     F[4 * t + 1] = v0f.y;
@@ -283,6 +310,9 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
     F[4 * t + 3] = vRf;
   }
   bar_sync();
+  CVA_MARK(pb + 1);
+
+  // ---- phase 2: interface rows -> cyclic PCR
   double ra = 0, rc = 0, rd = 1, rid = 1;
   double2 rr = make_double2(0, 0);
   if (own) {
@@ -290,23 +320,21 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
     const double2 nf = make_double2(F[4 * tn + 0], F[4 * tn + 1]);
     const double nL = F[4 * tn + 2], nR = F[4 * tn + 3];
     double dj = 2.0 * (hL + hj), sj = hj;
-    if (t == K - 1) {  // the reference's last row (see header, P11)
-      const double h0 = s[1] - s[0];
+    if (t == K - 1) {  // the reference's last row (see header, P11); h_0 = s_1 - s_0
+      const double h0 = knot(1) - knot(0);
       sj = hL;
       dj = 2.0 * (hL + hj) + hj * (hj - hL) / (2.0 * (hj + h0));
     }
-    const double2 r = rj;
     ra = hL * vLl;
     rd = dj + hL * vRl + sj * nL;
     rc = sj * nR;
-    rr = make_double2(r.x - hL * v0l.x - sj * nf.x, r.y - hL * v0l.y - sj * nf.y);
+    rr = make_double2(rj.x - hL * v0l.x - sj * nf.x, rj.y - hL * v0l.y - sj * nf.y);
     rid = frcp(rd);
   }
-  bar_sync();  // F fully consumed before the PCR buffers (aliasing it) are written
   {
     int buf = 0;
     auto P = [&](int bsel, int arr) { return scr + (bsel * 5 + arr) * kT; };
-    if (own) {
+    if (own) {  // buffer 0 (F lives in buffer 1, read above)
       P(0, 0)[t] = ra;
       P(0, 1)[t] = rc;
       P(0, 2)[t] = rid;
@@ -343,9 +371,9 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
       const int jp = (t + K / 2) & (K - 1);
       const double ei = ra + rc, ej = P(buf, 0)[jp] + P(buf, 1)[jp];
       const double dj = 1.0 / P(buf, 2)[jp];
-      const double2 rj = make_double2(P(buf, 3)[jp], P(buf, 4)[jp]);
+      const double2 rjp = make_double2(P(buf, 3)[jp], P(buf, 4)[jp]);
       const double idet = 1.0 / (rd * dj - ei * ej);
-      w = make_double2((rr.x * dj - ei * rj.x) * idet, (rr.y * dj - ei * rj.y) * idet);
+      w = make_double2((rr.x * dj - ei * rjp.x) * idet, (rr.y * dj - ei * rjp.y) * idet);
     }
     // W and MB go to the buffer not read in the final step
     double2* W = reinterpret_cast<double2*>(P(buf ^ 1, 0));
@@ -359,20 +387,22 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
       MB[t] = make_double2(v0f.x + wl.x * vLf + w.x * vRf, v0f.y + wl.y * vLf + w.y * vRf);
     }
     bar_sync();
-
     CVA_MARK(pb + 2);
+
     // ---- phase 3: interior re-solve + fused evaluation
     double2 cacc = make_double2(0, 0);
     if (own) {
       const double2 mub = MB[t + 1 == K ? 0 : t + 1];
       // forward with known boundary values (R[j] <- g_j)
-      double hm = a == 0 ? s[n] - s[n - 1] : s[a] - s[a - 1];
+      const int ap = a == 0 ? n - 1 : a - 1;
+      double si = knot(a);
+      double hm = knot(a == 0 ? n : a) - knot(ap);
       double2 g = make_double2(0, 0);
 #pragma unroll
       for (int j = 0; j < kCMax; ++j) {
         if (j < M) {
-          const int i = a + j;
-          const double h = s[i + 1] - s[i];
+          const double sn = knot(a + j + 1);
+          const double h = sn - si;
           double2 r = R[j];
           if (j == 0) {
             r.x = fma(-hm, wl.x, r.x);
@@ -389,14 +419,15 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
           }
           R[j] = g;
           hm = h;
+          si = sn;
         }
       }
       CVA_MARK(pb + 5);
-      // backward: intervals b-1, b-2, ..., a; the chunk's samples are walked
-      // downwards from the last one below s_b (sample l lies in interval i iff
-      // s_i <= t_l < s_{i+1}, the reference's upper_bound rule, spline.cpp:98-105)
+      // backward: intervals b-1, b-2, ..., a; samples walked downwards from the
+      // last one below s_b (sample l lies in interval i iff s_i <= t_l < s_{i+1},
+      // the reference's upper_bound rule, spline.cpp:98-105)
       const double invN = 1.0 / (double)N;
-      double s1 = s[b];
+      double s1 = knot(b);
       int l = ((t == K - 1) ? N : first_sample<kPow2>(s1, N)) - 1;
       double tl = sample_t<kPow2>(l, N, invN);
       double2 y1 = xy[b == n ? 0 : b];
@@ -406,7 +437,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
       for (int j = kCMax - 1; j >= 0; --j) {
         if (j <= M) {
           const int i = a + j;  // interval [s_i, s_{i+1})
-          const double s0 = s[i];
+          const double s0 = knot(i);
           const double h = s1 - s0;
           if (j < M) {
             // mu_i = g_i - c'_i mu_{i+1}, c'_i = h_i / pivot_i
@@ -440,9 +471,9 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* s,
 
     // ---- polygon length of the resampled curve and centroid (one reduction)
     double len = 0.0;
-    for (int l = t; l < N; l += kT) {
-      const double2 p = out[l], q = out[l + 1 == N ? 0 : l + 1];
-      const double dx = q.x - p.x, dy = q.y - p.y;
+    for (int q = t; q < N; q += kT) {
+      const double2 p = out[q], o = out[q + 1 == N ? 0 : q + 1];
+      const double dx = o.x - p.x, dy = o.y - p.y;
       len += fsqrt(fma(dx, dx, dy * dy));
     }
     double sx = cacc.x, sy = cacc.y;

@@ -233,7 +233,14 @@ def test_preprocess_matches_oracle_ragged(cuda, oracle):
 
 @pytest.mark.parametrize("n_in", [4, 5, 7, 8, 9, 16, 31, 33, 100, 257, 511, 513, 1000, 3000, 4096])
 def test_resample_sizes(cuda, oracle, n_in):
-    """Ragged sizes around every chunking boundary of the partition solver."""
+    """Ragged sizes around every chunking boundary of the partition solver.
+
+    The nodes sit at sorted uniform random angles, so adjacent knot spacings
+    differ by up to ~10^3x: the spline system then amplifies rounding (the
+    reference's own h = s[i+1] - s[i] carries ~1 ulp(1) / h relative error).
+    Observed GPU-vs-reference differences stay <= 4e-12 of the curve's scale
+    here (<= 3e-15 on the C1 workload); the bound below is 1e-11, a tenth of
+    the 1e-10 parity bar."""
     rng = np.random.default_rng(n_in)
     phi = np.sort(rng.uniform(0, 2 * PI, n_in))
     r = 1 + 0.3 * np.cos(3 * phi + 0.2)
@@ -241,7 +248,7 @@ def test_resample_sizes(cuda, oracle, n_in):
     for n_out in (8, 100, 1024):
         got = cva.resample_uniform(raw, n_out)
         want = oracle.resample_uniform(raw, n_out)
-        assert np.abs(got - want).max() <= 1e-12 * max(1.0, np.abs(want).max())
+        assert np.abs(got - want).max() <= 1e-11 * max(1.0, np.abs(want).max())
 
 
 def test_preprocess_invalid_curves(cuda):
