@@ -164,14 +164,23 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
 
   CVA_MARK(21);
   // ---- tie-broken argmax of |D_m| (rigid_align.cpp:31-47): max, then smallest index in band
-  // |D_m| = |F_m| / N. The max and the band test run on squared magnitudes;
-  // the band threshold is formed exactly as the reference does (on |D|).
+  // |D_m| = |F_m| / M. The max and the band test run on squared magnitudes,
+  // each thread's |F|^2 values read once into registers; the band threshold is
+  // formed exactly as the reference does (on |D|).
+  constexpr int kMaxPer = 8;  // N <= 2048
   const double invN = 1.0 / (double)N;  // h = 1/N (rigid_align.cpp:56)
   const double invM = 1.0 / (double)M;  // D_m = conj(F_m) / M
+  double mag2[kMaxPer];
   double best2 = -1.0;
-  for (int k = t; k < N; k += kT) {
-    const double2 f = F[pad(k)];
-    best2 = fmax(best2, fma(f.x, f.x, f.y * f.y));
+#pragma unroll
+  for (int q = 0; q < kMaxPer; ++q) {
+    const int k = t + q * kT;
+    mag2[q] = -1.0;
+    if (k < N) {
+      const double2 f = F[pad(k)];
+      mag2[q] = fma(f.x, f.x, f.y * f.y);
+      best2 = fmax(best2, mag2[q]);
+    }
   }
   // block max of best2 and sums of s1 / s2 in one exchange
   const int lane = t & 31, wid = t >> 5;
@@ -197,85 +206,53 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   }
   const double best = sqrt(best2) * invM;  // NaN if the correlation is not finite
   const double thr = best - kTieRelTol * fmax(1.0, fabs(best));
-  const double thrN = thr * (double)M;
-  const double thr2 = thr > 0.0 ? thrN * thrN : -1.0;  // |F|^2 >= (thr N)^2  <=>  |D| >= thr
+  const double thrM = thr * (double)M;
+  const double thr2 = thr > 0.0 ? thrM * thrM : -1.0;  // |F|^2 >= (thr M)^2  <=>  |D| >= thr
   int cand = INT_MAX;
-  for (int k = t; k < N; k += kT) {
-    const double2 f = F[pad(k)];
-    if (fma(f.x, f.x, f.y * f.y) >= thr2) {
-      cand = k;
-      break;
-    }
-  }
+#pragma unroll
+  for (int q = kMaxPer - 1; q >= 0; --q)
+    if (mag2[q] >= thr2 && t + q * kT < N) cand = t + q * kT;  // smallest k of this thread
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
   __shared__ int s_cand[8];
-  __shared__ int s_m;
-  __shared__ double2 s_rot;
   if (lane == 0) s_cand[wid] = cand;
   __syncthreads();
-  if (t == 0) {
-    int m = INT_MAX;
+  int m = INT_MAX;
 #pragma unroll
-    for (int w = 0; w < kT / 32; ++w) m = min(m, s_cand[w]);
-    cva_alignment r;
-    if (!isfinite(best) || best2 < 0.0 || m == INT_MAX) {
-      r.shift = 0;
-      r.t0 = 0.0;
-      r.theta = qnan();
-      r.trace = qnan();
-      r.energy = qnan();
-      r.degenerate = 0;
-      r.status = CVA_INVALID_ARGUMENT;  // non-finite correlation (rigid_align.cpp:83)
-      s_m = -1;
+  for (int w = 0; w < kT / 32; ++w) m = min(m, s_cand[w]);
+  const bool ok = isfinite(best) && best2 >= 0.0 && m != INT_MAX;
+  // rotation straight from D_m: (cos, sin) = (Re D, Im D) / |D| (every thread)
+  double2 rot = make_double2(qnan(), qnan());
+  double trace = 0.0;
+  double2 fm = make_double2(0.0, 0.0);
+  if (ok) {
+    fm = F[pad(m)];
+    const double a2 = fma(fm.x, fm.x, fm.y * fm.y);
+    trace = sqrt(a2) * invM;
+    if (a2 > 0.0) {
+      const double ia = 1.0 / sqrt(a2);
+      rot = make_double2(fm.x * ia, -fm.y * ia);
     } else {
-      const double2 f = F[pad(m)];
-      const double trace = sqrt(fma(f.x, f.x, f.y * f.y)) * invM;
-      double theta = 0.0;
-      int degenerate = 0;
-      if (trace == 0.0)
-        degenerate = 1;  // rigid_align.cpp:86-88
-      else
-        theta = atan2(-f.y, f.x);  // arg D_m
-      double e = invN * (s1 + s2) - 2.0 * invN * trace;  // rigid_align.cpp:56-59
-      if (e < 0.0) e = 0.0;
-      r.shift = m;
-      r.t0 = (double)m / (double)N;  // rigid_align.cpp:52
-      r.theta = theta;
-      r.trace = degenerate ? 0.0 : trace;
-      r.energy = e;
-      r.degenerate = degenerate;
-      r.status = CVA_OK;
-      s_m = m;
-      double sn, cs;
-      sincos(theta, &sn, &cs);
-      s_rot = make_double2(cs, sn);
+      rot = make_double2(1.0, 0.0);  // degenerate: theta = 0 (rigid_align.cpp:86-88)
     }
-    *out = r;
   }
-  __syncthreads();
 
-  CVA_MARK(22);
   // ---- aligned[l] = R(theta) z2'[(l + m) mod N]  (geometry.hpp:70-73; elastic.cpp:80)
   if (aligned != nullptr) {
-    const int m = s_m;
-    constexpr int kMaxPer = 8;  // N <= 2048
     double2 v[kMaxPer];
     const double2 c = in.g2;
     const double sc = in.sc2;
-    const double2 rot = s_rot;
 #pragma unroll
     for (int q = 0; q < kMaxPer; ++q) {
       const int j = t + q * kT;
       if (j < N) {
         const double2 z = in.z2[j];
         const double2 p = make_double2((z.x - c.x) * sc, (z.y - c.y) * sc);
-        v[q] = m < 0 ? make_double2(qnan(), qnan())
-                     : make_double2(fma(rot.x, p.x, rot.y * p.y), fma(-rot.y, p.x, rot.x * p.y));
+        v[q] = make_double2(fma(rot.x, p.x, rot.y * p.y), fma(-rot.y, p.x, rot.x * p.y));
       }
     }
     __syncthreads();  // in.z2 may alias `aligned`
-    const int mm = m < 0 ? 0 : m;
+    const int mm = ok ? m : 0;
 #pragma unroll
     for (int q = 0; q < kMaxPer; ++q) {
       const int j = t + q * kT;
@@ -285,6 +262,30 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
         aligned[l] = v[q];
       }
     }
+  }
+  if (t == 0) {
+    cva_alignment r;
+    if (!ok) {
+      r.shift = 0;
+      r.t0 = 0.0;
+      r.theta = qnan();
+      r.trace = qnan();
+      r.energy = qnan();
+      r.degenerate = 0;
+      r.status = CVA_INVALID_ARGUMENT;  // non-finite correlation (rigid_align.cpp:83)
+    } else {
+      const int degenerate = trace == 0.0;
+      double e = invN * (s1 + s2) - 2.0 * invN * trace;  // rigid_align.cpp:56-59
+      if (e < 0.0) e = 0.0;
+      r.shift = m;
+      r.t0 = (double)m / (double)N;  // rigid_align.cpp:52
+      r.theta = degenerate ? 0.0 : atan2(-fm.y, fm.x);  // arg D_m
+      r.trace = trace;
+      r.energy = e;
+      r.degenerate = degenerate;
+      r.status = CVA_OK;
+    }
+    *out = r;
   }
   CVA_MARK(23);
 }
