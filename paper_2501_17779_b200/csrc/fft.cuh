@@ -56,6 +56,29 @@ __device__ __forceinline__ void dft8(double2* v) {
   v[7] = csub(e3, t3);
 }
 
+// 16-point DFT as 4 x 4: X[k1 + 4 k2] = sum_n2 W4^{n2 k2} W16^{n2 k1} sum_n1 x[n2 + 4 n1] W4^{n1 k1}.
+// Leaves X[k1 + 4 k2] in v[4 k1 + k2] (no register transpose): read outputs
+// through dft16_slot(k).
+__device__ __forceinline__ void dft16(double2* v) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) dft4(v[c], v[c + 4], v[c + 8], v[c + 12]);
+  constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
+  constexpr double r2 = 0.70710678118654752440;
+  // v[c + 4 k1] *= W16^{c k1}
+  v[5] = cmul(v[5], make_double2(c1, -s1));
+  v[6] = cmul(v[6], make_double2(r2, -r2));
+  v[7] = cmul(v[7], make_double2(s1, -c1));
+  v[9] = cmul(v[9], make_double2(r2, -r2));
+  v[10] = cmul_mi(v[10]);
+  v[11] = cmul(v[11], make_double2(-r2, -r2));
+  v[13] = cmul(v[13], make_double2(s1, -c1));
+  v[14] = cmul(v[14], make_double2(-r2, -r2));
+  v[15] = cmul(v[15], make_double2(-c1, s1));
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+}
+__host__ __device__ constexpr int dft16_slot(int k) { return 4 * (k & 3) + (k >> 2); }
+
 template <int R>
 __device__ __forceinline__ void dft_r(double2* v);
 template <>
@@ -64,6 +87,13 @@ template <>
 __device__ __forceinline__ void dft_r<4>(double2* v) { dft4(v[0], v[1], v[2], v[3]); }
 template <>
 __device__ __forceinline__ void dft_r<8>(double2* v) { dft8(v); }
+template <>
+__device__ __forceinline__ void dft_r<16>(double2* v) { dft16(v); }
+// register holding output k of dft_r<R>
+template <int R>
+__host__ __device__ constexpr int dft_slot(int k) {
+  return R == 16 ? dft16_slot(k) : k;
+}
 
 // One Stockham pass of radix R over a length-N sequence, threads t in [0, T).
 template <int R>

@@ -33,43 +33,9 @@ constexpr int kT = 256;
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
 
-// 16-point DFT as 4 x 4 (radix-4 twice with the W16 twiddles in between).
-__device__ __forceinline__ void dft16(double2* v) {
-  // columns: v[c + 4 r], r = 0..3 -> DFT4 over r for each c
-#pragma unroll
-  for (int c = 0; c < 4; ++c) dft4(v[c], v[c + 4], v[c + 8], v[c + 12]);
-  // twiddles W16^(c * k1)
-  constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
-  constexpr double r2 = 0.70710678118654752440;
-  const double2 w[4][4] = {
-      {{1, 0}, {1, 0}, {1, 0}, {1, 0}},
-      {{1, 0}, {c1, -s1}, {r2, -r2}, {s1, -c1}},
-      {{1, 0}, {r2, -r2}, {0, -1}, {-r2, -r2}},
-      {{1, 0}, {s1, -c1}, {-r2, -r2}, {-c1, s1}},
-  };
-#pragma unroll
-  for (int k1 = 1; k1 < 4; ++k1)
-#pragma unroll
-    for (int c = 1; c < 4; ++c) v[c + 4 * k1] = cmul(v[c + 4 * k1], w[k1][c]);
-  // rows: for each k1, DFT4 over c -> output index k1 + 4 k2
-#pragma unroll
-  for (int k1 = 0; k1 < 4; ++k1) dft4(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
-  // v[4 k1 + k2] holds X[k1 + 4 k2]; transpose into natural order
-  double2 t[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) t[i] = v[i];
-#pragma unroll
-  for (int k1 = 0; k1 < 4; ++k1)
-#pragma unroll
-    for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
-}
-
 template <int R>
 __device__ __forceinline__ void dft_any(double2* v) {
-  if constexpr (R == 16)
-    dft16(v);
-  else
-    dft_r<R>(v);
+  dft_r<R>(v);
 }
 
 enum Load { kPlain = 0, kLoadA = 1, kLoadB = 2, kProduct = 3 };
@@ -127,7 +93,7 @@ __global__ void __launch_bounds__(kT)
   double2* o = out + seq * M;
   const int base = (j - jm) * R + jm;
 #pragma unroll
-  for (int r = 0; r < R; ++r) o[base + r * Ns] = v[r];
+  for (int r = 0; r < R; ++r) o[base + r * Ns] = v[dft_slot<R>(r)];
 }
 
 // centroid and 1/length of each curve (center then normalize, curve.cpp:27-48),

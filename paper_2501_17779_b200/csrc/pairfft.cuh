@@ -49,24 +49,28 @@ __device__ __forceinline__ void pass(Src src, double2* dst, int N, int Ns,
     dft_r<R>(v);
     const int base = (j - jm) * R + jm;
 #pragma unroll
-    for (int r = 0; r < R; ++r) dst[pad(base + r * Ns)] = v[r];
+    for (int r = 0; r < R; ++r) dst[pad(base + r * Ns)] = v[dft_slot<R>(r)];
   }
 }
 
 // Forward FFT of length N (power of two) by NT threads (index g), first pass
 // reading through src0, then ping-ponging b0 -> b1 -> b0 ... Returns the
 // buffer holding the spectrum. sync() is the group barrier.
+// Radix plan: radix 8 while it keeps every thread of the group busy, then 4 / 2
+// (1024 points, 128 threads: 8 x 8 x 8 x 2). Radix 16 was measured slower here
+// (register spills at the 128-register cap, half the threads idle).
+
 template <int NT, typename Src, typename Sync>
 __device__ inline double2* group_fft(Src src0, double2* b0, double2* b1, int N,
                                      const double2* __restrict__ tw, int g, Sync sync) {
-  const int maxR = N / NT >= 8 ? 8 : 4;
   int Ns = 1;
   double2* dst = b0;
   double2* other = b1;
   bool first = true;
+  const int maxR = N / NT >= 8 ? 8 : 4;
   while (Ns < N) {
     const int rem = N / Ns;
-    const int R = (rem % 8 == 0 && maxR >= 8) ? 8 : (rem % 4 == 0 && maxR >= 4 ? 4 : 2);
+    const int R = (rem % 8 == 0 && maxR >= 8) ? 8 : (rem % 4 == 0 ? 4 : 2);
     if (first) {
       if (R == 8) pass<8, NT>(src0, dst, N, Ns, tw, g);
       else if (R == 4) pass<4, NT>(src0, dst, N, Ns, tw, g);
