@@ -327,7 +327,22 @@ int cva_preprocess_align_uniform(const double* c1, const double* c2, int64_t pai
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
   if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
-  return large_align(c1, c2, pairs, n, 1, out, aligned, tw, s);
+  if (!small_fft(n)) return large_align(c1, c2, pairs, n, 1, out, aligned, tw, s);
+  // shared-memory path: per-curve stats, then the pair kernel normalising on load
+  void* ws = nullptr;
+  const size_t nb = sizeof(double4) * (size_t)(2 * pairs), bb = sizeof(int32_t) * (size_t)(2 * pairs);
+  const size_t sb = cva::curve_stats_workspace(pairs);
+  if (scratch_alloc(&ws, nb + bb + sb + 512, s) != cudaSuccess) return fail(CVA_BAD_ALLOC, "scratch allocation failed");
+  double4* norm = (double4*)ws;
+  int32_t* bad = (int32_t*)((char*)ws + nb);
+  void* part = (char*)ws + ((nb + bb + 255) & ~size_t(255));
+  cudaError_t e = cva::launch_curve_stats((const double2*)c1, pairs, (int)n, 1, norm, bad, part, s);
+  if (e == cudaSuccess) e = cva::launch_curve_stats((const double2*)c2, pairs, (int)n, 1, norm + pairs, bad + pairs, part, s);
+  if (e == cudaSuccess)
+    e = cva::launch_v2_align_norm((const double2*)c1, (const double2*)c2, pairs, (int)n, tw, norm, norm + pairs, bad,
+                                  bad + pairs, out, (double2*)aligned, s);
+  cudaFreeAsync(ws, s);
+  return finish(e, "preprocess_align_uniform launch");
 }
 
 int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,

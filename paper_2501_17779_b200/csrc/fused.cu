@@ -141,14 +141,31 @@ __global__ void __launch_bounds__(kT, 2)
 // align_fft on pre-sampled pairs (rigid_align.cpp:204-208), N = 2^p <= 2048.
 // Pair p reads c1 + p * stride and c2 + p * stride (stride N: separate
 // batches; stride 2N with c2 = c1 + N: interleaved rows 2p, 2p+1).
+// Optional per-curve normalisation (centroid x, y, 1/length, -) and invalid
+// flags fuse preprocess(resample=false) into the load (cva_preprocess_align_uniform).
 __global__ void __launch_bounds__(kT)
     align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
                  int64_t stride1, int64_t stride2, const double2* __restrict__ tw,
-                 cva_alignment* __restrict__ out, double2* aligned) {
+                 cva_alignment* __restrict__ out, double2* aligned, const double4* __restrict__ norm1,
+                 const double4* __restrict__ norm2, const int32_t* __restrict__ bad1,
+                 const int32_t* __restrict__ bad2) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double2 red[16];
   const int64_t p = blockIdx.x;
   pf::PairIn in{c1 + p * stride1, c2 + p * stride2, make_double2(0, 0), make_double2(0, 0), 1.0, 1.0};
+  if (norm1) {
+    if (bad1[p] || bad2[p]) {
+      if (threadIdx.x == 0) write_bad(out + p, CVA_INVALID_ARGUMENT);
+      if (aligned)
+        for (int l = threadIdx.x; l < N; l += kT) aligned[p * N + l] = make_double2(qnan(), qnan());
+      return;
+    }
+    const double4 a = norm1[p], b = norm2[p];
+    in.g1 = make_double2(a.x, a.y);
+    in.sc1 = a.z;
+    in.g2 = make_double2(b.x, b.y);
+    in.sc2 = b.z;
+  }
   pf::pair_stage(in, reinterpret_cast<double2*>(smem), N, tw, out + p,
                  aligned ? aligned + p * N : nullptr, red);
 }
@@ -271,7 +288,19 @@ cudaError_t launch_v2_align(const double2* c1, const double2* c2, int64_t pairs,
   const size_t sm = v2_align_smem(N);
   cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
   if (e != cudaSuccess) return e;
-  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, N, N, tw, out, aligned);
+  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, N, N, tw, out, aligned, nullptr, nullptr,
+                                                        nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_v2_align_norm(const double2* c1, const double2* c2, int64_t pairs, int N, const double2* tw,
+                                 const double4* norm1, const double4* norm2, const int32_t* bad1,
+                                 const int32_t* bad2, cva_alignment* out, double2* aligned, cudaStream_t s) {
+  const size_t sm = v2_align_smem(N);
+  cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
+  if (e != cudaSuccess) return e;
+  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, N, N, tw, out, aligned, norm1, norm2, bad1,
+                                                        bad2);
   return cudaGetLastError();
 }
 
@@ -281,7 +310,8 @@ cudaError_t launch_v2_align_interleaved(const double2* rows, int64_t pairs, int 
   cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
   if (e != cudaSuccess) return e;
   v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(rows, rows + N, N, 2 * (int64_t)N,
-                                                        2 * (int64_t)N, tw, out, aligned);
+                                                        2 * (int64_t)N, tw, out, aligned, nullptr, nullptr,
+                                                        nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -291,7 +321,8 @@ cudaError_t launch_v2_align_row(const double2* row, const double2* curves, int64
   const size_t sm = v2_align_smem(N);
   cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
   if (e != cudaSuccess) return e;
-  v2::align_kernel<<<(unsigned)count, v2::kT, sm, s>>>(row, curves, N, 0, N, tw, out, nullptr);
+  v2::align_kernel<<<(unsigned)count, v2::kT, sm, s>>>(row, curves, N, 0, N, tw, out, nullptr, nullptr,
+                                                        nullptr, nullptr, nullptr);
   return cudaGetLastError();
 }
 

@@ -27,6 +27,9 @@ cudaError_t launch_v2_align(const double2* c1, const double2* c2, int64_t pairs,
                             cudaStream_t s);
 cudaError_t launch_v2_align_interleaved(const double2* rows, int64_t pairs, int N, const double2* tw,
                                         cva_alignment* out, double2* aligned, cudaStream_t s);
+cudaError_t launch_v2_align_norm(const double2* c1, const double2* c2, int64_t pairs, int N, const double2* tw,
+                                 const double4* norm1, const double4* norm2, const int32_t* bad1,
+                                 const int32_t* bad2, cva_alignment* out, double2* aligned, cudaStream_t s);
 cudaError_t launch_v2_align_row(const double2* row, const double2* curves, int64_t count, int N,
                                 const double2* tw, cva_alignment* out, cudaStream_t s);
 cudaError_t launch_unpack_row(const cva_alignment* in, int64_t count, double* energy, int32_t* shift,

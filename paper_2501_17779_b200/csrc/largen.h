@@ -21,4 +21,10 @@ cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pai
                                const double2* tw, cva_alignment* out, double2* aligned, void* ws,
                                int64_t chunk, cudaStream_t s);
 
+// Per-curve centroid / 1/length (normalize = 1; else identity) and invalid
+// flags, as (gx, gy, sc, 0) per curve; ws >= curve_stats_workspace(count).
+size_t curve_stats_workspace(int64_t curves);
+cudaError_t launch_curve_stats(const double2* curves, int64_t count, int N, int normalize, double4* norm,
+                               int32_t* bad, void* ws, cudaStream_t s);
+
 }  // namespace cva
