@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(kT, 2)
 // batches; stride 2N with c2 = c1 + N: interleaved rows 2p, 2p+1).
 // Optional per-curve normalisation (centroid x, y, 1/length, -) and invalid
 // flags fuse preprocess(resample=false) into the load (cva_preprocess_align_uniform).
-__global__ void __launch_bounds__(kT)
+template <bool kIP>
+__global__ void __launch_bounds__(kT, kIP ? 2 : 3)
     align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
                  int64_t stride1, int64_t stride2, const double2* __restrict__ tw,
                  cva_alignment* __restrict__ out, double2* aligned, const double4* __restrict__ norm1,
@@ -166,8 +167,8 @@ __global__ void __launch_bounds__(kT)
     in.g2 = make_double2(b.x, b.y);
     in.sc2 = b.z;
   }
-  pf::pair_stage(in, reinterpret_cast<double2*>(smem), N, tw, out + p,
-                 aligned ? aligned + p * N : nullptr, red);
+  pf::pair_stage<kIP>(in, reinterpret_cast<double2*>(smem), N, tw, out + p,
+                      aligned ? aligned + p * N : nullptr, red);
 }
 
 // ------------------------------------------------------------------- SRV
@@ -186,7 +187,8 @@ __device__ __forceinline__ double2 srv_at(const double2* __restrict__ c, int l, 
 // SRV alignment (srv_transform -> srv_center -> align_fft, the (t0,R) step of
 // elastic.cpp:138-139). The centered SRVs are written to `qbuf` (this pair's
 // 2N scratch rows in global memory / L2) and aligned by the pair stage.
-__global__ void __launch_bounds__(kT)
+template <bool kIP>
+__global__ void __launch_bounds__(kT, kIP ? 2 : 3)
     srv_align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
                      const double2* __restrict__ tw, cva_alignment* __restrict__ out,
                      double2* aligned, double2* qbuf) {
@@ -222,7 +224,7 @@ __global__ void __launch_bounds__(kT)
   const double invn = 1.0 / (double)N;  // srv_center (srv.cpp:90-98)
   pf::PairIn in{q1, q2, make_double2(invn * m1.x, invn * m1.y), make_double2(invn * m2.x, invn * m2y),
                 1.0, 1.0};
-  pf::pair_stage(in, reinterpret_cast<double2*>(smem), N, tw, out + p, al, red);
+  pf::pair_stage<kIP>(in, reinterpret_cast<double2*>(smem), N, tw, out + p, al, red);
 }
 
 }  // namespace v2
@@ -237,6 +239,25 @@ cudaError_t set_smem(const void* fn, size_t bytes) {
 
 int v2_max_raw_nodes() { return rs::kNMax; }
 
+// In-place transforms (half the buffers) once four buffers would exceed ~75 KB,
+// so the pair kernels keep >= 2-3 CTAs per SM (N = 2048: 147 KB -> 74 KB).
+bool v2_inplace(int N) { return pf::fft_len(N) == 2048; }
+
+static cudaError_t launch_align_kernel(unsigned grid, size_t sm, cudaStream_t s, const double2* c1,
+                                       const double2* c2, int N, int64_t st1, int64_t st2, const double2* tw,
+                                       cva_alignment* out, double2* aligned, const double4* n1, const double4* n2,
+                                       const int32_t* b1, const int32_t* b2) {
+  const bool ip = v2_inplace(N);
+  const void* fn = ip ? (const void*)v2::align_kernel<true> : (const void*)v2::align_kernel<false>;
+  cudaError_t e = set_smem(fn, sm);
+  if (e != cudaSuccess) return e;
+  if (ip)
+    v2::align_kernel<true><<<grid, v2::kT, sm, s>>>(c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
+  else
+    v2::align_kernel<false><<<grid, v2::kT, sm, s>>>(c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
+  return cudaGetLastError();
+}
+
 size_t v2_resample_align_smem(int N) {
   const size_t fft = 4 * sizeof(double2) * (size_t)pf::padded_len(N);
   const size_t raw = v2::kRawBytes > fft ? v2::kRawBytes : fft;
@@ -245,7 +266,9 @@ size_t v2_resample_align_smem(int N) {
 size_t v2_preprocess_smem(int n_out) {
   return v2::kRawBytes + v2::kScrBytes + sizeof(double2) * (size_t)n_out;
 }
-size_t v2_align_smem(int N) { return 4 * sizeof(double2) * (size_t)pf::padded_len(pf::fft_len(N)); }
+size_t v2_align_smem(int N) {
+  return (v2_inplace(N) ? 2 : 4) * sizeof(double2) * (size_t)pf::padded_len(pf::fft_len(N));
+}
 int v2_fft_len(int N) { return pf::fft_len(N); }
 
 bool v2_resample_align_supported(int N) { return N == 512 || N == 1024; }
@@ -286,44 +309,30 @@ cudaError_t launch_v2_align(const double2* c1, const double2* c2, int64_t pairs,
                             const double2* tw, cva_alignment* out, double2* aligned,
                             cudaStream_t s) {
   const size_t sm = v2_align_smem(N);
-  cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
-  if (e != cudaSuccess) return e;
-  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, N, N, tw, out, aligned, nullptr, nullptr,
-                                                        nullptr, nullptr);
-  return cudaGetLastError();
+  return launch_align_kernel((unsigned)pairs, sm, s, c1, c2, N, N, N, tw, out, aligned, nullptr, nullptr, nullptr,
+                             nullptr);
 }
 
 cudaError_t launch_v2_align_norm(const double2* c1, const double2* c2, int64_t pairs, int N, const double2* tw,
                                  const double4* norm1, const double4* norm2, const int32_t* bad1,
                                  const int32_t* bad2, cva_alignment* out, double2* aligned, cudaStream_t s) {
   const size_t sm = v2_align_smem(N);
-  cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
-  if (e != cudaSuccess) return e;
-  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, N, N, tw, out, aligned, norm1, norm2, bad1,
-                                                        bad2);
-  return cudaGetLastError();
+  return launch_align_kernel((unsigned)pairs, sm, s, c1, c2, N, N, N, tw, out, aligned, norm1, norm2, bad1, bad2);
 }
 
 cudaError_t launch_v2_align_interleaved(const double2* rows, int64_t pairs, int N, const double2* tw,
                                         cva_alignment* out, double2* aligned, cudaStream_t s) {
   const size_t sm = v2_align_smem(N);
-  cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
-  if (e != cudaSuccess) return e;
-  v2::align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(rows, rows + N, N, 2 * (int64_t)N,
-                                                        2 * (int64_t)N, tw, out, aligned, nullptr, nullptr,
-                                                        nullptr, nullptr);
-  return cudaGetLastError();
+  return launch_align_kernel((unsigned)pairs, sm, s, rows, rows + N, N, 2 * (int64_t)N, 2 * (int64_t)N, tw, out,
+                             aligned, nullptr, nullptr, nullptr, nullptr);
 }
 
 // One row of an all-pairs matrix: pair j = (row, curves[j]) for j < count.
 cudaError_t launch_v2_align_row(const double2* row, const double2* curves, int64_t count, int N,
                                 const double2* tw, cva_alignment* out, cudaStream_t s) {
   const size_t sm = v2_align_smem(N);
-  cudaError_t e = set_smem((const void*)v2::align_kernel, sm);
-  if (e != cudaSuccess) return e;
-  v2::align_kernel<<<(unsigned)count, v2::kT, sm, s>>>(row, curves, N, 0, N, tw, out, nullptr, nullptr,
-                                                        nullptr, nullptr, nullptr);
-  return cudaGetLastError();
+  return launch_align_kernel((unsigned)count, sm, s, row, curves, N, 0, N, tw, out, nullptr, nullptr, nullptr,
+                             nullptr, nullptr);
 }
 
 namespace v2 {
@@ -349,9 +358,15 @@ cudaError_t launch_v2_srv_align(const double2* c1, const double2* c2, int64_t pa
                                 const double2* tw, cva_alignment* out, double2* aligned,
                                 double2* qbuf, cudaStream_t s) {
   const size_t sm = v2_align_smem(N);
-  cudaError_t e = set_smem((const void*)v2::srv_align_kernel, sm);
-  if (e != cudaSuccess) return e;
-  v2::srv_align_kernel<<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, tw, out, aligned, qbuf);
+  if (v2_inplace(N)) {
+    cudaError_t e = set_smem((const void*)v2::srv_align_kernel<true>, sm);
+    if (e != cudaSuccess) return e;
+    v2::srv_align_kernel<true><<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, tw, out, aligned, qbuf);
+  } else {
+    cudaError_t e = set_smem((const void*)v2::srv_align_kernel<false>, sm);
+    if (e != cudaSuccess) return e;
+    v2::srv_align_kernel<false><<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, tw, out, aligned, qbuf);
+  }
   return cudaGetLastError();
 }
 

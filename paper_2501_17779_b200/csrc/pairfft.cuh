@@ -92,6 +92,51 @@ __device__ inline double2* group_fft(Src src0, double2* b0, double2* b1, int N,
   return other;  // last written
 }
 
+// In-place variant (one buffer per transform; used where shared memory binds,
+// M = 2048): the pass sequence is fixed at compile time (8, 8, 8, 4) so every
+// register index is static. Each pass loads all of a thread's butterflies
+// (<= 16 values) into registers, syncs, then transforms and stores in place.
+template <int R, int NT, int M, int Ns, typename Src, typename Sync>
+__device__ __forceinline__ void pass_ip(Src src, double2* buf, const double2* __restrict__ tw, int g,
+                                        Sync sync) {
+  constexpr int nb = M / R;
+  constexpr int B = nb / NT;  // butterflies per thread
+  static_assert(B >= 1 && B * R <= 16, "in-place pass keeps <= 16 values per thread");
+  constexpr int tws = M / (Ns * R);
+  double2 v[B][R];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int j = g + b * NT;
+    const int jm = j & (Ns - 1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[b][r] = src(j + r * nb);
+    if (Ns > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], __ldg(&tw[r * jm * tws]));
+    }
+  }
+  sync();
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int j = g + b * NT;
+    const int jm = j & (Ns - 1);
+    dft_r<R>(v[b]);
+    const int base = (j - jm) * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[pad(base + r * Ns)] = v[b][dft_slot<R>(r)];
+  }
+  sync();
+}
+
+template <int NT, typename Src, typename Sync>
+__device__ inline void fft2048_ip(Src src0, double2* buf, const double2* __restrict__ tw, int g, Sync sync) {
+  auto src = [buf](int i) { return buf[pad(i)]; };
+  pass_ip<8, NT, 2048, 1>(src0, buf, tw, g, sync);
+  pass_ip<8, NT, 2048, 8>(src, buf, tw, g, sync);
+  pass_ip<8, NT, 2048, 64>(src, buf, tw, g, sync);
+  pass_ip<4, NT, 2048, 512>(src, buf, tw, g, sync);
+}
+
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
 
 struct PairIn {
@@ -120,6 +165,8 @@ __host__ __device__ inline int fft_len(int N) {
 // result (written by thread 0). aligned: this pair's aligned curve (may alias
 // in.z2: all reads happen before any write). red: >= 16 double2 shared.
 // Requires blockDim.x == 256, N >= 4, M <= 2048.
+// kInPlace: 2 * padded_len(M) buffers instead of 4; requires M == 2048.
+template <bool kInPlace = false>
 __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
                                   const double2* __restrict__ tw, cva_alignment* out,
                                   double2* aligned, double2* red) {
@@ -129,7 +176,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   const int NP = padded_len(M);
   double2* B0 = bufs;
   double2* B1 = bufs + NP;
-  double2* B2 = bufs + 2 * NP;
+  double2* B2 = bufs + (kInPlace ? 1 : 2) * NP;
   double2* B3 = bufs + 3 * NP;
 
   // ---- two forward transforms of the normalized curves (normalization fused into the load)
@@ -150,28 +197,41 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       return z;
     };
     auto sync = [grp]() { named_sync(1 + grp, kHalf); };
-    X = group_fft<kHalf>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, M, tw, g, sync);
+    if constexpr (kInPlace) {
+      fft2048_ip<kHalf>(load, grp == 0 ? B0 : B2, tw, g, sync);
+      X = grp == 0 ? B0 : B2;
+    } else {
+      X = group_fft<kHalf>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, M, tw, g, sync);
+    }
   }
   __syncthreads();
   CVA_MARK(20);
-  // group 0's result is B0 or B1, group 1's is B2 or B3 (same pass count)
-  const bool in0 = (X == B0 || X == B2);
-  const double2* X1 = in0 ? B0 : B1;
-  const double2* X2 = in0 ? B2 : B3;
-  double2* F0 = in0 ? B1 : B0;
-  double2* F1 = in0 ? B3 : B2;
-
   // ---- D_m = sum_l conj(z1_l) z2_{l+m} = IDFT(conj Z1 . Z2)_m = conj(FFT(Z1 conj Z2)_m) / N
-  auto prod = [X1, X2](int k) { return cmulconj(X1[pad(k)], X2[pad(k)]); };
   auto sync_all = []() { __syncthreads(); };
-  const double2* F = group_fft<kT>(prod, F0, F1, M, tw, t, sync_all);
+  const double2* F;
+  if constexpr (kInPlace) {
+    const double2* X1 = B0;
+    const double2* X2 = B2;
+    auto prod = [X1, X2](int k) { return cmulconj(X1[pad(k)], X2[pad(k)]); };
+    fft2048_ip<kT>(prod, B0, tw, t, sync_all);
+    F = B0;
+  } else {
+    // group 0's result is B0 or B1, group 1's is B2 or B3 (same pass count)
+    const bool in0 = (X == B0 || X == B2);
+    const double2* X1 = in0 ? B0 : B1;
+    const double2* X2 = in0 ? B2 : B3;
+    double2* F0 = in0 ? B1 : B0;
+    double2* F1 = in0 ? B3 : B2;
+    auto prod = [X1, X2](int k) { return cmulconj(X1[pad(k)], X2[pad(k)]); };
+    F = group_fft<kT>(prod, F0, F1, M, tw, t, sync_all);
+  }
 
   CVA_MARK(21);
   // ---- tie-broken argmax of |D_m| (rigid_align.cpp:31-47): max, then smallest index in band
   // |D_m| = |F_m| / M. The max and the band test run on squared magnitudes,
   // each thread's |F|^2 values read once into registers; the band threshold is
   // formed exactly as the reference does (on |D|).
-  constexpr int kMaxPer = 8;  // N <= 2048
+  constexpr int kMaxPer = kInPlace ? 8 : 4;  // N <= 2048 in-place, N <= 1024 otherwise
   const double invN = 1.0 / (double)N;  // h = 1/N (rigid_align.cpp:56)
   const double invM = 1.0 / (double)M;  // D_m = conj(F_m) / M
   double mag2[kMaxPer];
