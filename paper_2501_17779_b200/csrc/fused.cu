@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kT, 2)
   }
   __syncthreads();
   pf::PairIn in{Z1, al, A.centroid, B.centroid, A.inv_len, B.inv_len};
-  pf::pair_stage(in, bufs, N, tw, out + p, al, red);
+  pf::pair_stage<false, N>(in, bufs, N, tw, out + p, al, red);
 }
 
 // ------------------------------------------------------------- preprocess
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kT, 2)
 // batches; stride 2N with c2 = c1 + N: interleaved rows 2p, 2p+1).
 // Optional per-curve normalisation (centroid x, y, 1/length, -) and invalid
 // flags fuse preprocess(resample=false) into the load (cva_preprocess_align_uniform).
-template <bool kIP>
+template <bool kIP, int kN>
 __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
     align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
                  int64_t stride1, int64_t stride2, const double2* __restrict__ tw,
@@ -167,8 +167,8 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
     in.g2 = make_double2(b.x, b.y);
     in.sc2 = b.z;
   }
-  pf::pair_stage<kIP>(in, reinterpret_cast<double2*>(smem), N, tw, out + p,
-                      aligned ? aligned + p * N : nullptr, red);
+  pf::pair_stage<kIP, kN>(in, reinterpret_cast<double2*>(smem), N, tw, out + p,
+                          aligned ? aligned + p * N : nullptr, red);
 }
 
 // ------------------------------------------------------------------- SRV
@@ -187,7 +187,7 @@ __device__ __forceinline__ double2 srv_at(const double2* __restrict__ c, int l, 
 // SRV alignment (srv_transform -> srv_center -> align_fft, the (t0,R) step of
 // elastic.cpp:138-139). The centered SRVs are written to `qbuf` (this pair's
 // 2N scratch rows in global memory / L2) and aligned by the pair stage.
-template <bool kIP>
+template <bool kIP, int kN>
 __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
     srv_align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
                      const double2* __restrict__ tw, cva_alignment* __restrict__ out,
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
   const double invn = 1.0 / (double)N;  // srv_center (srv.cpp:90-98)
   pf::PairIn in{q1, q2, make_double2(invn * m1.x, invn * m1.y), make_double2(invn * m2.x, invn * m2y),
                 1.0, 1.0};
-  pf::pair_stage<kIP>(in, reinterpret_cast<double2*>(smem), N, tw, out + p, al, red);
+  pf::pair_stage<kIP, kN>(in, reinterpret_cast<double2*>(smem), N, tw, out + p, al, red);
 }
 
 }  // namespace v2
@@ -243,18 +243,39 @@ int v2_max_raw_nodes() { return rs::kNMax; }
 // so the pair kernels keep >= 2-3 CTAs per SM (N = 2048: 147 KB -> 74 KB).
 bool v2_inplace(int N) { return pf::fft_len(N) == 2048; }
 
+// Compile-time FFT plans for the common power-of-two lengths (no runtime
+// radix loop or index division); kN = 0 is the runtime-N kernel.
+template <int kN>
+static cudaError_t launch_align_n(unsigned grid, size_t sm, cudaStream_t s, const double2* c1,
+                                  const double2* c2, int N, int64_t st1, int64_t st2, const double2* tw,
+                                  cva_alignment* out, double2* aligned, const double4* n1, const double4* n2,
+                                  const int32_t* b1, const int32_t* b2) {
+  constexpr bool kIP = kN == 2048;
+  cudaError_t e = set_smem((const void*)v2::align_kernel<kIP, kN>, sm);
+  if (e != cudaSuccess) return e;
+  v2::align_kernel<kIP, kN><<<grid, v2::kT, sm, s>>>(c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
+  return cudaGetLastError();
+}
+
 static cudaError_t launch_align_kernel(unsigned grid, size_t sm, cudaStream_t s, const double2* c1,
                                        const double2* c2, int N, int64_t st1, int64_t st2, const double2* tw,
                                        cva_alignment* out, double2* aligned, const double4* n1, const double4* n2,
                                        const int32_t* b1, const int32_t* b2) {
+  switch (N) {
+    case 2048: return launch_align_n<2048>(grid, sm, s, c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
+    case 1024: return launch_align_n<1024>(grid, sm, s, c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
+    case 512: return launch_align_n<512>(grid, sm, s, c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
+    case 256: return launch_align_n<256>(grid, sm, s, c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
+    default: break;
+  }
   const bool ip = v2_inplace(N);
-  const void* fn = ip ? (const void*)v2::align_kernel<true> : (const void*)v2::align_kernel<false>;
+  const void* fn = ip ? (const void*)v2::align_kernel<true, 0> : (const void*)v2::align_kernel<false, 0>;
   cudaError_t e = set_smem(fn, sm);
   if (e != cudaSuccess) return e;
   if (ip)
-    v2::align_kernel<true><<<grid, v2::kT, sm, s>>>(c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
+    v2::align_kernel<true, 0><<<grid, v2::kT, sm, s>>>(c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
   else
-    v2::align_kernel<false><<<grid, v2::kT, sm, s>>>(c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
+    v2::align_kernel<false, 0><<<grid, v2::kT, sm, s>>>(c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
   return cudaGetLastError();
 }
 
@@ -276,7 +297,11 @@ bool v2_resample_align_supported(int N) { return N == 512 || N == 1024; }
 cudaError_t launch_v2_resample_align(const double2* pts, const int64_t* off, int64_t pairs, int N,
                                      const double2* tw, cva_alignment* out, double2* aligned,
                                      cudaStream_t s) {
-  const size_t sm = v2_resample_align_smem(N);
+  const size_t sm = v2_resample_align_smem(N)
+#ifdef CVA_PAD_SMEM
+      + CVA_PAD_SMEM
+#endif
+      ;
   const void* fn = N == 512 ? (const void*)v2::resample_align_kernel<512>
                             : (const void*)v2::resample_align_kernel<1024>;
   cudaError_t e = set_smem(fn, sm);
@@ -354,20 +379,28 @@ cudaError_t launch_unpack_row(const cva_alignment* in, int64_t count, double* en
   return cudaGetLastError();
 }
 
+template <bool kIP, int kN>
+static cudaError_t launch_srv_n(const double2* c1, const double2* c2, int64_t pairs, int N,
+                                const double2* tw, cva_alignment* out, double2* aligned,
+                                double2* qbuf, size_t sm, cudaStream_t s) {
+  cudaError_t e = set_smem((const void*)v2::srv_align_kernel<kIP, kN>, sm);
+  if (e != cudaSuccess) return e;
+  v2::srv_align_kernel<kIP, kN><<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, tw, out, aligned, qbuf);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_v2_srv_align(const double2* c1, const double2* c2, int64_t pairs, int N,
                                 const double2* tw, cva_alignment* out, double2* aligned,
                                 double2* qbuf, cudaStream_t s) {
   const size_t sm = v2_align_smem(N);
-  if (v2_inplace(N)) {
-    cudaError_t e = set_smem((const void*)v2::srv_align_kernel<true>, sm);
-    if (e != cudaSuccess) return e;
-    v2::srv_align_kernel<true><<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, tw, out, aligned, qbuf);
-  } else {
-    cudaError_t e = set_smem((const void*)v2::srv_align_kernel<false>, sm);
-    if (e != cudaSuccess) return e;
-    v2::srv_align_kernel<false><<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, tw, out, aligned, qbuf);
+  switch (N) {
+    case 2048: return launch_srv_n<true, 2048>(c1, c2, pairs, N, tw, out, aligned, qbuf, sm, s);
+    case 1024: return launch_srv_n<false, 1024>(c1, c2, pairs, N, tw, out, aligned, qbuf, sm, s);
+    case 512: return launch_srv_n<false, 512>(c1, c2, pairs, N, tw, out, aligned, qbuf, sm, s);
+    default: break;
   }
-  return cudaGetLastError();
+  if (v2_inplace(N)) return launch_srv_n<true, 0>(c1, c2, pairs, N, tw, out, aligned, qbuf, sm, s);
+  return launch_srv_n<false, 0>(c1, c2, pairs, N, tw, out, aligned, qbuf, sm, s);
 }
 
 }  // namespace cva

@@ -31,7 +31,7 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// One Stockham pass (see fft.cuh) reading through a functor.
+// One Stockham pass (see fft.cuh) reading through a functor (runtime N, Ns).
 template <int R, int NT, typename Src>
 __device__ __forceinline__ void pass(Src src, double2* dst, int N, int Ns,
                                      const double2* __restrict__ tw, int g) {
@@ -53,13 +53,59 @@ __device__ __forceinline__ void pass(Src src, double2* dst, int N, int Ns,
   }
 }
 
-// Forward FFT of length N (power of two) by NT threads (index g), first pass
-// reading through src0, then ping-ponging b0 -> b1 -> b0 ... Returns the
-// buffer holding the spectrum. sync() is the group barrier.
+// Compile-time pass: N, Ns, the butterfly count per thread and every index
+// stride are constants.
+template <int R, int NT, int N, int Ns, typename Src>
+__device__ __forceinline__ void pass_ct(Src src, double2* dst, const double2* __restrict__ tw, int g) {
+  constexpr int nb = N / R;
+  constexpr int tws = N / (Ns * R);
+#pragma unroll
+  for (int j0 = 0; j0 < nb; j0 += NT) {
+    const int j = j0 + g;
+    if (nb % NT == 0 || j < nb) {
+      double2 v[R];
+      const int jm = j & (Ns - 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = src(j + r * nb);
+      if (Ns > 1) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[r * jm * tws]));
+      }
+      dft_r<R>(v);
+      const int base = (j - jm) * R + jm;
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[pad(base + r * Ns)] = v[dft_slot<R>(r)];
+    }
+  }
+}
+
 // Radix plan: radix 8 while it keeps every thread of the group busy, then 4 / 2
 // (1024 points, 128 threads: 8 x 8 x 8 x 2). Radix 16 was measured slower here
 // (register spills at the 128-register cap, half the threads idle).
+template <int NT>
+__host__ __device__ constexpr int plan_radix(int N, int Ns) {
+  return ((N / Ns) % 8 == 0 && N / NT >= 8) ? 8 : ((N / Ns) % 4 == 0 ? 4 : 2);
+}
 
+// Forward FFT of compile-time length N by NT threads, first pass through src,
+// ping-ponging dst/other. Returns the buffer holding the spectrum.
+template <int NT, int N, int Ns = 1, typename Src, typename Sync>
+__device__ __forceinline__ double2* group_fft_ct(Src src, double2* dst, double2* other,
+                                                 const double2* __restrict__ tw, int g, Sync sync) {
+  constexpr int R = plan_radix<NT>(N, Ns);
+  pass_ct<R, NT, N, Ns>(src, dst, tw, g);
+  sync();
+  if constexpr (Ns * R < N) {
+    auto next = [dst](int i) { return dst[pad(i)]; };
+    return group_fft_ct<NT, N, Ns * R>(next, other, dst, tw, g, sync);
+  } else {
+    return dst;
+  }
+}
+
+// Forward FFT of length N (power of two) by NT threads (index g), first pass
+// reading through src0, then ping-ponging b0 -> b1 -> b0 ... Returns the
+// buffer holding the spectrum. sync() is the group barrier.
 template <int NT, typename Src, typename Sync>
 __device__ inline double2* group_fft(Src src0, double2* b0, double2* b1, int N,
                                      const double2* __restrict__ tw, int g, Sync sync) {
@@ -166,13 +212,15 @@ __host__ __device__ inline int fft_len(int N) {
 // in.z2: all reads happen before any write). red: >= 16 double2 shared.
 // Requires blockDim.x == 256, N >= 4, M <= 2048.
 // kInPlace: 2 * padded_len(M) buffers instead of 4; requires M == 2048.
-template <bool kInPlace = false>
+// kN: compile-time N (a power of two) or 0 for a runtime N.
+template <bool kInPlace = false, int kN = 0>
 __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
                                   const double2* __restrict__ tw, cva_alignment* out,
                                   double2* aligned, double2* red) {
   const int t = threadIdx.x;
   const int grp = t / kHalf, g = t % kHalf;
-  const int M = fft_len(N);
+  if constexpr (kN > 0) N = kN;
+  const int M = kN > 0 ? kN : fft_len(N);
   const int NP = padded_len(M);
   double2* B0 = bufs;
   double2* B1 = bufs + NP;
@@ -201,7 +249,10 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       fft2048_ip<kHalf>(load, grp == 0 ? B0 : B2, tw, g, sync);
       X = grp == 0 ? B0 : B2;
     } else {
-      X = group_fft<kHalf>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, M, tw, g, sync);
+      if constexpr (kN > 0)
+        X = group_fft_ct<kHalf, kN>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, tw, g, sync);
+      else
+        X = group_fft<kHalf>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, M, tw, g, sync);
     }
   }
   __syncthreads();
@@ -223,7 +274,10 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     double2* F0 = in0 ? B1 : B0;
     double2* F1 = in0 ? B3 : B2;
     auto prod = [X1, X2](int k) { return cmulconj(X1[pad(k)], X2[pad(k)]); };
-    F = group_fft<kT>(prod, F0, F1, M, tw, t, sync_all);
+    if constexpr (kN > 0)
+      F = group_fft_ct<kT, kN>(prod, F0, F1, tw, t, sync_all);
+    else
+      F = group_fft<kT>(prod, F0, F1, M, tw, t, sync_all);
   }
 
   CVA_MARK(21);
