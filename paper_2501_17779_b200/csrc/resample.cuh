@@ -54,10 +54,10 @@ constexpr int kScratchDoubles = 11 * kT + 2;  // PCR ping-pong (2 x 5 arrays; F 
 
 __device__ __forceinline__ void bar_sync() { __syncthreads(); }
 
-__device__ __forceinline__ int num_chunks(int n) {
-  int K = 2;
-  while (K * 2 <= kT && K * 2 <= n / 2) K *= 2;
-  return K;
+// log2 of the chunk count K: the largest power of two <= min(kT, n / 2), >= 2.
+__device__ __forceinline__ int log2_chunks(int n) {
+  const int c = min(kT, n >> 1);
+  return max(1, 31 - __clz(c));
 }
 
 // Fast reciprocal: MUFU seed + one cubic step (<= 1 ulp; the reference's
@@ -180,10 +180,11 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
                                             const int pb = 0 /* phase-stamp base */) {
   const int t = threadIdx.x;
   const int lane = t & 31, wid = t >> 5;
-  const int K = num_chunks(n);
+  const int lgK = log2_chunks(n);
+  const int K = 1 << lgK;
   const bool own = t < K;
-  const int a = own ? (t * n) / K : 0;
-  const int b = own ? ((t + 1) * n) / K : 0;
+  const int a = own ? (t * n) >> lgK : 0;
+  const int b = own ? ((t + 1) * n) >> lgK : 0;
   const int M = b - 1 - a;  // interior knots (>= 1); knot b-1 is the interface
   int bad = 0;
 
@@ -346,7 +347,6 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
     // (|a|,|c| / d ~ rho^(C 2^k) for a chunk of C knots, rho <= 1/2); once every
     // row's off-diagonals are below 2^-64 of its diagonal the remaining
     // steps cannot change w in fp64, and the closing 2x2 below reduces to r/d.
-    __shared__ int conv[kT / 32];
     for (int st = 1; st < K / 2; st *= 2) {
       bool done = true;
       if (own) {
@@ -370,15 +370,8 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
         P(nb, 4)[t] = rr.y;
         done = fabs(ra) + fabs(rc) <= 0x1p-64 * fabs(rd);
       }
-      done = __all_sync(0xffffffffu, done);
-      if (lane == 0) conv[wid] = done;
       buf ^= 1;
-      bar_sync();
-      bool all = true;
-#pragma unroll
-      for (int q = 0; q < kT / 32; ++q) all = all && conv[q];
-      if (all) break;
-      bar_sync();  // conv[] reads done before the next step overwrites it
+      if (__syncthreads_and(done)) break;  // the step's barrier doubles as the vote
     }
     double2 w = make_double2(0, 0);
     if (own) {

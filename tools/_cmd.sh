@@ -1,3 +1,3 @@
-timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-timeout 200 python tools/bench_parts.py 2>&1 | tail -4
-python bench.py --config c4 --no-cpu-baseline 2>&1 | tail -1 | cut -c1-200
+timeout 600 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 200 python tools/bench_parts.py 2>&1 | tail -4 | head -2
+timeout 120 python tools/dbg_resample.py 2>&1 | tail -3
