@@ -15,6 +15,10 @@
  * std::span<const Point2>::data(), so reference buffers pass through unchanged.
  * Batches are contiguous: pairs * n * 2 doubles. Ragged batches of raw curves
  * use an offsets array: curve c is points [offsets[c], offsets[c+1]).
+ * Device curve buffers are accessed as 16-byte (x, y) pairs and must be
+ * 16-byte aligned (cudaMalloc'd arrays at whole-point offsets are); an
+ * 8-byte-aligned pointer is rejected with CVA_INVALID_ARGUMENT. The *_host
+ * entry points copy into their own device buffers and accept any alignment.
  *
  * Conventions (identical to the reference):
  *  - shift m pairs c1[l] with c2[(l + m) mod N]            rigid_align.hpp:12-13

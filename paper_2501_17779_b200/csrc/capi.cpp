@@ -31,11 +31,18 @@ int fail(int status, const std::string& msg) {
   return status;
 }
 
+// Curve buffers are read and written as double2 (16 B): device pointers must
+// be 16-byte aligned (cudaMalloc'd arrays and whole-point offsets are).
+bool a16(const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+int misaligned(const char* what) {
+  return fail(CVA_INVALID_ARGUMENT, std::string(what) +
+                                        ": curve buffers must be 16-byte aligned (interleaved x, y doubles)");
+}
+
 int cuda_fail(cudaError_t e, const char* what) {
   return fail(CVA_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
 
 // Twiddle tables w_N^k, one per (device, N), built once and kept for the process.
 std::mutex g_tw_mu;
@@ -212,6 +219,7 @@ int cva_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n
   if (pairs < 0) return fail(CVA_INVALID_ARGUMENT, "align: negative pair count");
   if (pairs == 0) return CVA_OK;
   if (!c1 || !c2 || !out) return fail(CVA_INVALID_ARGUMENT, "align: null pointer");
+  if (!a16(c1) || !a16(c2) || !a16(aligned)) return misaligned("align");
   if (int rc = require_device()) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
@@ -228,6 +236,7 @@ int cva_preprocess_batch(const double* points, const int64_t* offsets, int64_t c
   if (curves < 0) return fail(CVA_INVALID_ARGUMENT, "preprocess: negative curve count");
   if (curves == 0) return CVA_OK;
   if (!points || !offsets || !out) return fail(CVA_INVALID_ARGUMENT, "preprocess: null pointer");
+  if (!a16(points) || !a16(out)) return misaligned("preprocess");
   if (resample && n_out < 8)
     return fail(CVA_INVALID_ARGUMENT, "resample: need at least 8 output nodes");
   if (int rc = require_device()) return rc;
@@ -247,6 +256,7 @@ int cva_resample_batch(const double* points, const int64_t* offsets, int64_t cur
   if (curves < 0) return fail(CVA_INVALID_ARGUMENT, "resample: negative curve count");
   if (curves == 0) return CVA_OK;
   if (!points || !offsets || !out) return fail(CVA_INVALID_ARGUMENT, "resample: null pointer");
+  if (!a16(points) || !a16(out)) return misaligned("resample");
   if (n_out < 8) return fail(CVA_INVALID_ARGUMENT, "resample: need at least 8 output nodes");
   if (int rc = require_device()) return rc;
   cudaStream_t s = (cudaStream_t)stream;
@@ -261,6 +271,7 @@ int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int
   if (pairs < 0) return fail(CVA_INVALID_ARGUMENT, "align: negative pair count");
   if (pairs == 0) return CVA_OK;
   if (!points || !offsets || !out) return fail(CVA_INVALID_ARGUMENT, "align: null pointer");
+  if (!a16(points) || !a16(aligned)) return misaligned("preprocess_align");
   if (!resample)
     return fail(CVA_UNSUPPORTED,
                 "preprocess_align: resample=0 takes equal-size pairs; use "
@@ -323,6 +334,7 @@ int cva_preprocess_align_uniform(const double* c1, const double* c2, int64_t pai
   if (pairs < 0) return fail(CVA_INVALID_ARGUMENT, "align: negative pair count");
   if (pairs == 0) return CVA_OK;
   if (!c1 || !c2 || !out) return fail(CVA_INVALID_ARGUMENT, "align: null pointer");
+  if (!a16(c1) || !a16(c2) || !a16(aligned)) return misaligned("preprocess_align_uniform");
   if (int rc = require_device()) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
@@ -352,6 +364,7 @@ int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64
   if (pairs < 0) return fail(CVA_INVALID_ARGUMENT, "srv: negative pair count");
   if (pairs == 0) return CVA_OK;
   if (!c1 || !c2 || !out) return fail(CVA_INVALID_ARGUMENT, "srv: null pointer");
+  if (!a16(c1) || !a16(c2) || !a16(aligned_q)) return misaligned("srv");
   if (int rc = require_device()) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
@@ -372,6 +385,7 @@ int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_beg
     return fail(CVA_INVALID_ARGUMENT, "allpairs: bad row range");
   if (row_end == row_begin || count == 0) return CVA_OK;
   if (!curves || !energy || !shift || !theta) return fail(CVA_INVALID_ARGUMENT, "allpairs: null pointer");
+  if (!a16(curves)) return misaligned("allpairs");
   if (int rc = require_device()) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const int M = cva::v2_fft_len((int)n);

@@ -25,13 +25,46 @@ constexpr size_t kScrBytes = sizeof(double) * rs::kScratchDoubles;
 
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
 
-// Stream a raw curve into shared memory (read-once data: evict-first loads).
-__device__ __forceinline__ void load_raw(const double2* __restrict__ g, double2* sm, int n) {
-  for (int i = threadIdx.x; i < n; i += kT) sm[i] = __ldcs(&g[i]);
+// One TMA bulk copy (cp.async.bulk, completion counted on an mbarrier) per raw
+// curve instead of n/256 dependent load->store rounds per thread. `bar` is a
+// CTA mbarrier initialised by bulk_init; `phase` alternates 0, 1, ... per use.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_init(uint64_t* bar) {
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+}
+// Loads g[0..n) into sm and returns once every thread can read it. Requires a
+// preceding __syncthreads() after the last generic access of sm's old data, and
+// g 16-byte aligned (checked at the C ABI).
+__device__ __forceinline__ void raw_to_smem(const double2* g, double2* sm, int n, uint64_t* bar,
+                                            uint32_t phase) {
+  if (threadIdx.x == 0) {
+    const uint32_t bytes = (uint32_t)n * 16u, b = smem_u32(bar);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(sm)),
+        "l"(g), "r"(bytes), "r"(b)
+        : "memory");
+  }
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
 }
 
 __device__ __forceinline__ void prefetch_l2(const void* p, int bytes) {
-  if (bytes >= 16)
+  if (bytes >= 16 && (reinterpret_cast<uintptr_t>(p) & 15) == 0)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes & ~15) : "memory");
 }
 
@@ -78,12 +111,13 @@ __global__ void __launch_bounds__(kT, 2)
     return;
   }
   CVA_MARK(0);
-  load_raw(pts + a0, xy, na);
-  __syncthreads();
+  __shared__ uint64_t mbar;
+  bulk_init(&mbar);
+  raw_to_smem(pts + a0, xy, na, &mbar, 0);
   CVA_MARK(1);
   const rs::CurveStats A = rs::resample_block<true>(xy, na, s, scr, red, Z1, N, 2);
-  load_raw(pts + a1, xy, nb);
-  __syncthreads();
+  __syncthreads();  // resample_block's last reads of xy are done
+  raw_to_smem(pts + a1, xy, nb, &mbar, 1);
   CVA_MARK(10);
   const rs::CurveStats B = rs::resample_block<true>(xy, nb, s, scr, red, al, N, 11);
   if (A.bad || B.bad) {
@@ -118,8 +152,9 @@ __global__ void __launch_bounds__(kT, 2)
   int bad = n < 4 || n > rs::kNMax;
   rs::CurveStats st{};
   if (!bad) {
-    load_raw(pts + b0, xy, n);
-    __syncthreads();
+    __shared__ uint64_t mbar;
+    bulk_init(&mbar);
+    raw_to_smem(pts + b0, xy, n, &mbar, 0);
     st = rs::resample_block<kPow2>(xy, n, s, scr, red, Z, n_out);
     bad = st.bad;
   }

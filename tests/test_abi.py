@@ -49,6 +49,14 @@ def test_argument_validation_without_device():
         == _native.CVA_INVALID_ARGUMENT
     # SRV needs >= 8 nodes (proj/src/srv.cpp:72)
     assert lib.cva_srv_align_batch_host(z.ctypes.data, z.ctypes.data, 1, 4, 0, 0) == _native.CVA_INVALID_ARGUMENT
+    # curve buffers are double2 arrays: 8-byte-aligned pointers are rejected before any launch
+    buf = np.zeros(8 * 64 + 2)
+    base = buf.ctypes.data + (8 if buf.ctypes.data % 16 == 0 else 0)  # an odd multiple of 8
+    out = np.zeros(1, dtype=_native.ALIGNMENT_DTYPE)
+    assert lib.cva_align_batch(base, base, 1, 64, out.ctypes.data, None, None) == _native.CVA_INVALID_ARGUMENT
+    assert b"16-byte aligned" in lib.cva_last_error()
+    assert lib.cva_preprocess_align_batch(base, offs.ctypes.data, 1, 3, 1024, 1, out.ctypes.data, None, None) \
+        == _native.CVA_INVALID_ARGUMENT
 
 
 @pytest.mark.skipif(_native.load().cva_device_count() > 0, reason="a CUDA device is present")

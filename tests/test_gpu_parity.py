@@ -432,3 +432,19 @@ def test_c2_full_size(cuda, oracle):
         g = np.zeros(1, dtype=_native.ALIGNMENT_DTYPE)[0]
         g["shift"], g["theta"], g["energy"], g["trace"], g["t0"] = k[i, j], th[i, j], e[i, j], want["trace"], k[i, j] / 512
         check_pair(g, want, p[i], p[j])
+
+
+def test_misaligned_curve_buffer_rejected(cuda):
+    """Curve buffers are double2 arrays: an 8-byte-aligned device pointer is an
+    invalid argument (checked before any launch), never a fault."""
+    import torch
+
+    pts, offs, _, _ = synth.ragged_pairs(77, 4, 1024)
+    do = torch.from_numpy(offs).cuda()
+    flat = torch.zeros(pts.size + 1, dtype=torch.float64, device="cuda")
+    out = torch.empty((4, 48), dtype=torch.uint8, device="cuda")
+    lib = _native.load()
+    rc = lib.cva_preprocess_align_batch(flat.data_ptr() + 8, do.data_ptr(), 4, int(np.diff(offs).max()), 1024, 1,
+                                        out.data_ptr(), None, torch.cuda.current_stream().cuda_stream)
+    assert rc == _native.CVA_INVALID_ARGUMENT and b"16-byte aligned" in lib.cva_last_error()
+    torch.cuda.synchronize()
