@@ -28,6 +28,30 @@ __device__ __forceinline__ double2 cmul_mi(double2 a) { return make_double2(a.y,
 // multiply by +i
 __device__ __forceinline__ double2 cmul_pi(double2 a) { return make_double2(-a.y, a.x); }
 
+// ------------------------------------------------------- fast fp64 rcp / sqrt
+// Fast reciprocal: MUFU seed + one cubic step (<= 1 ulp; the reference's
+// divisions are correctly rounded, the difference is far below the 1e-10 bar).
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  // one cubically convergent step: r (1 + e + e^2), e = 1 - x r (seed error
+  // <= 2^-19 -> <= 2^-57 before the final rounding)
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
+// Fast sqrt: MUFU rsqrt seed, one third-order step, one final correction (<= 1 ulp).
+__device__ __forceinline__ double fsqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  // one third-order step on the rsqrt seed: r (1 + e/2 + 3e^2/8), e = 1 - x r^2
+  const double e = fma(-x * r, r, 1.0);
+  r = fma(r * e, fma(0.375, e, 0.5), r);
+  double y = x * r;
+  y = fma(fma(-y, y, x), 0.5 * r, y);
+  return x > 0.0 ? y : (x == 0.0 ? 0.0 : __longlong_as_double(0x7ff8000000000000ULL));
+}
+
 // --------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

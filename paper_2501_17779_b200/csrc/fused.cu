@@ -115,11 +115,11 @@ __global__ void __launch_bounds__(kT, 2)
   bulk_init(&mbar);
   raw_to_smem(pts + a0, xy, na, &mbar, 0);
   CVA_MARK(1);
-  const rs::CurveStats A = rs::resample_block<true>(xy, na, s, scr, red, Z1, N, 2);
+  const rs::CurveStats A = rs::resample_block<true, false>(xy, na, s, scr, red, Z1, N, 2);
   __syncthreads();  // resample_block's last reads of xy are done
   raw_to_smem(pts + a1, xy, nb, &mbar, 1);
   CVA_MARK(10);
-  const rs::CurveStats B = rs::resample_block<true>(xy, nb, s, scr, red, al, N, 11);
+  const rs::CurveStats B = rs::resample_block<true, false>(xy, nb, s, scr, red, al, N, 11);
   if (A.bad || B.bad) {
     if (threadIdx.x == 0) write_bad(out + p, CVA_INVALID_ARGUMENT);
     for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kT, 2)
   }
   __syncthreads();
   pf::PairIn in{Z1, al, A.centroid, B.centroid, A.inv_len, B.inv_len};
-  pf::pair_stage<false, N>(in, bufs, N, tw, out + p, al, red);
+  pf::pair_stage<false, N, true>(in, bufs, N, tw, out + p, al, red);
 }
 
 // ------------------------------------------------------------- preprocess

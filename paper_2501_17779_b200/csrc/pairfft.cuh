@@ -192,6 +192,12 @@ struct PairIn {
   double sc1, sc2;    // scale applied after centering (1 for already-normalized input)
 };
 
+// 1 / polygon length (curve.cpp:17-25) of each curve, measured by the pair
+// stage while it loads the samples (kLenOnLoad); {NaN, NaN} flags a bad pair.
+struct PairScale {
+  double sc1, sc2;
+};
+
 // FFT length for N data points: N itself when N is a power of two, else the
 // smallest power of two M >= 2N. In the padded case the circular correlation
 // of length N is the first N lags of the length-M circular correlation of
@@ -213,7 +219,12 @@ __host__ __device__ inline int fft_len(int N) {
 // Requires blockDim.x == 256, N >= 4, M <= 2048.
 // kInPlace: 2 * padded_len(M) buffers instead of 4; requires M == 2048.
 // kN: compile-time N (a power of two) or 0 for a runtime N.
-template <bool kInPlace = false, int kN = 0>
+// kLenOnLoad: in.sc1 / in.sc2 are ignored; each curve's polygon length is
+// summed while its samples are loaded for the first FFT pass (the transforms
+// run on the centered, unscaled curves) and the scales 1/len are applied to
+// the correlation spectrum, the energies and the aligned curve. A length that
+// is not finite and > 0 marks the pair invalid (preprocess: curve.cpp:41-48).
+template <bool kInPlace = false, int kN = 0, bool kLenOnLoad = false>
 __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
                                   const double2* __restrict__ tw, cva_alignment* out,
                                   double2* aligned, double2* red) {
@@ -228,12 +239,13 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   double2* B3 = bufs + 3 * NP;
 
   // ---- two forward transforms of the normalized curves (normalization fused into the load)
-  double ss = 0.0;  // sum |z'|^2 of this group's curve (rigid_align.cpp:23-27)
+  double ss = 0.0;   // sum |z'|^2 of this group's curve (rigid_align.cpp:23-27)
+  double len = 0.0;  // kLenOnLoad: this thread's share of the polygon length
   double2* X;
   {
     const double2* src = grp == 0 ? in.z1 : in.z2;
     const double2 c = grp == 0 ? in.g1 : in.g2;
-    const double sc = grp == 0 ? in.sc1 : in.sc2;
+    const double sc = kLenOnLoad ? 1.0 : (grp == 0 ? in.sc1 : in.sc2);
     // group 0: a = [z1, 0...]; group 1: b = [z2, z2, 0...] (M == N: plain z)
     const int lim = (grp == 0 || M == N) ? N : 2 * N;
     auto load = [&](int i) {
@@ -241,7 +253,14 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       const int k = i < N ? i : i - N;
       const double2 q = src[k];
       const double2 z = make_double2((q.x - c.x) * sc, (q.y - c.y) * sc);
-      if (i < N) ss = fma(z.x, z.x, fma(z.y, z.y, ss));
+      if (i < N) {
+        ss = fma(z.x, z.x, fma(z.y, z.y, ss));
+        if constexpr (kLenOnLoad) {  // edge (k, k+1) of the closed polygon (curve.cpp:17-25)
+          const double2 o = src[k + 1 == N ? 0 : k + 1];
+          const double dx = o.x - q.x, dy = o.y - q.y;
+          len += fsqrt(fma(dx, dx, dy * dy));
+        }
+      }
       return z;
     };
     auto sync = [grp]() { named_sync(1 + grp, kHalf); };
@@ -255,7 +274,39 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
         X = group_fft<kHalf>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, M, tw, g, sync);
     }
   }
-  __syncthreads();
+  PairScale psc{in.sc1, in.sc2};
+  if constexpr (kLenOnLoad) {
+    __shared__ double s_len[kT / 32];
+    len = warp_sum(len);
+    if ((t & 31) == 0) s_len[t >> 5] = len;
+    __syncthreads();
+    double l1 = 0.0, l2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < kT / 64; ++w) {
+      l1 += s_len[w];
+      l2 += s_len[kT / 64 + w];
+    }
+    if (!(l1 > 0.0) || !isfinite(l1) || !(l2 > 0.0) || !isfinite(l2)) {  // curve.cpp:44-46
+      if (t == 0) {
+        cva_alignment r;
+        r.shift = 0;
+        r.t0 = 0.0;
+        r.theta = r.trace = r.energy = qnan();
+        r.degenerate = 0;
+        r.status = CVA_INVALID_ARGUMENT;
+        *out = r;
+      }
+      if (aligned != nullptr) {
+        __syncthreads();  // in.z2 may alias `aligned`
+        for (int l = t; l < N; l += kT) aligned[l] = make_double2(qnan(), qnan());
+      }
+      return;
+    }
+    psc.sc1 = 1.0 / l1;
+    psc.sc2 = 1.0 / l2;
+  } else {
+    __syncthreads();
+  }
   CVA_MARK(20);
   // ---- D_m = sum_l conj(z1_l) z2_{l+m} = IDFT(conj Z1 . Z2)_m = conj(FFT(Z1 conj Z2)_m) / N
   auto sync_all = []() { __syncthreads(); };
@@ -263,7 +314,11 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   if constexpr (kInPlace) {
     const double2* X1 = B0;
     const double2* X2 = B2;
-    auto prod = [X1, X2](int k) { return cmulconj(X1[pad(k)], X2[pad(k)]); };
+    const double s12 = kLenOnLoad ? psc.sc1 * psc.sc2 : 1.0;
+    auto prod = [X1, X2, s12](int k) {
+      const double2 v = cmulconj(X1[pad(k)], X2[pad(k)]);
+      return kLenOnLoad ? cscale(v, s12) : v;
+    };
     fft2048_ip<kT>(prod, B0, tw, t, sync_all);
     F = B0;
   } else {
@@ -273,7 +328,11 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     const double2* X2 = in0 ? B2 : B3;
     double2* F0 = in0 ? B1 : B0;
     double2* F1 = in0 ? B3 : B2;
-    auto prod = [X1, X2](int k) { return cmulconj(X1[pad(k)], X2[pad(k)]); };
+    const double s12 = kLenOnLoad ? psc.sc1 * psc.sc2 : 1.0;
+    auto prod = [X1, X2, s12](int k) {
+      const double2 v = cmulconj(X1[pad(k)], X2[pad(k)]);
+      return kLenOnLoad ? cscale(v, s12) : v;
+    };
     if constexpr (kN > 0)
       F = group_fft_ct<kT, kN>(prod, F0, F1, tw, t, sync_all);
     else
@@ -322,6 +381,10 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     s1 += red[w].y;
     s2 += red[8 + w].x;
   }
+  if constexpr (kLenOnLoad) {  // sums of |z - c|^2 -> of |(z - c) / len|^2
+    s1 *= psc.sc1 * psc.sc1;
+    s2 *= psc.sc2 * psc.sc2;
+  }
   const double best = sqrt(best2) * invM;  // NaN if the correlation is not finite
   const double thr = best - kTieRelTol * fmax(1.0, fabs(best));
   const double thrM = thr * (double)M;
@@ -359,7 +422,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   if (aligned != nullptr) {
     double2 v[kMaxPer];
     const double2 c = in.g2;
-    const double sc = in.sc2;
+    const double sc = psc.sc2;
 #pragma unroll
     for (int q = 0; q < kMaxPer; ++q) {
       const int j = t + q * kT;

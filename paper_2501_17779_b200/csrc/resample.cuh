@@ -60,28 +60,7 @@ __device__ __forceinline__ int log2_chunks(int n) {
   return max(1, 31 - __clz(c));
 }
 
-// Fast reciprocal: MUFU seed + one cubic step (<= 1 ulp; the reference's
-// divisions are correctly rounded, the difference is far below the 1e-10 bar).
-__device__ __forceinline__ double frcp(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  // one cubically convergent step: r (1 + e + e^2), e = 1 - x r (seed error
-  // <= 2^-19 -> <= 2^-57 before the final rounding)
-  const double e = fma(-x, r, 1.0);
-  return fma(r, fma(e, e, e), r);
-}
-
-// Fast sqrt: MUFU rsqrt seed, one third-order step, one final correction (<= 1 ulp).
-__device__ __forceinline__ double fsqrt(double x) {
-  double r;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  // one third-order step on the rsqrt seed: r (1 + e/2 + 3e^2/8), e = 1 - x r^2
-  const double e = fma(-x * r, r, 1.0);
-  r = fma(r * e, fma(0.375, e, 0.5), r);
-  double y = x * r;
-  y = fma(fma(-y, y, x), 0.5 * r, y);
-  return x > 0.0 ? y : (x == 0.0 ? 0.0 : __longlong_as_double(0x7ff8000000000000ULL));
-}
+// frcp / fsqrt: cva_common.cuh
 
 // Block exclusive scan of one double per thread (kT threads); also returns the
 // total. red: >= 16 double2 of shared scratch.
@@ -174,7 +153,9 @@ __device__ __forceinline__ double sample_t(int l, int N, double invN) {
 // N = 2^p), blockDim.x == kT. NOTE: no __restrict__ on these pointers: they
 // carry data between threads across __syncthreads(), and restrict lets the
 // compiler forward stale loads across the barrier.
-template <bool kPow2>
+// kLen = false skips the polygon length (inv_len is then not set, bad covers
+// the knots only): the fused pair kernel measures it while loading its FFT.
+template <bool kPow2, bool kLen = true>
 __device__ inline CurveStats resample_block(const double2* xy, int n, double* L, double* scr,
                                             double2* red, double2* out, const int N,
                                             const int pb = 0 /* phase-stamp base */) {
@@ -478,10 +459,12 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
 
     // ---- polygon length of the resampled curve and centroid (one reduction)
     double len = 0.0;
-    for (int q = t; q < N; q += kT) {
-      const double2 p = out[q], o = out[q + 1 == N ? 0 : q + 1];
-      const double dx = o.x - p.x, dy = o.y - p.y;
-      len += fsqrt(fma(dx, dx, dy * dy));
+    if constexpr (kLen) {
+      for (int q = t; q < N; q += kT) {
+        const double2 p = out[q], o = out[q + 1 == N ? 0 : q + 1];
+        const double dx = o.x - p.x, dy = o.y - p.y;
+        len += fsqrt(fma(dx, dx, dy * dy));
+      }
     }
     double sx = cacc.x, sy = cacc.y;
     double lb = len + (bad ? INFINITY : 0.0);
@@ -490,8 +473,13 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
     CurveStats cs;
     const double invn = 1.0 / (double)N;
     cs.centroid = make_double2(invn * sx, invn * sy);
-    cs.bad = !(lb > 0.0) || !isfinite(lb);
-    cs.inv_len = 1.0 / lb;
+    if constexpr (kLen) {
+      cs.bad = !(lb > 0.0) || !isfinite(lb);
+      cs.inv_len = 1.0 / lb;
+    } else {
+      cs.bad = lb != 0.0 || !isfinite(sx) || !isfinite(sy);
+      cs.inv_len = 0.0;
+    }
     return cs;
   }
 }

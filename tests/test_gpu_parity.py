@@ -297,10 +297,14 @@ def test_c1_live_vs_oracle(cuda, oracle):
     prep, _ = cva.preprocess_batch(pts, offs, 1024)
     kinds = [check_pair(res[p], ro[p], prep[2 * p], prep[2 * p + 1], al[p], ao[p]) for p in range(96)]
     assert kinds.count("ok") >= 95
-    # split path (preprocess then align) is the same computation, bitwise
+    # split path (preprocess then align): the fused kernel scales by 1/length
+    # after the transforms instead of before, so the two agree to rounding
     r2, a2 = cva.align_fft_batch(prep[0::2], prep[1::2], return_aligned=True)
-    np.testing.assert_array_equal(r2, res)
-    np.testing.assert_array_equal(a2, al)
+    np.testing.assert_array_equal(r2["shift"], res["shift"])
+    np.testing.assert_allclose(r2["theta"], res["theta"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(r2["trace"], res["trace"], rtol=1e-13)
+    np.testing.assert_allclose(r2["energy"], res["energy"], rtol=1e-10, atol=1e-14 * 2)
+    np.testing.assert_allclose(a2, al, rtol=0, atol=1e-13)
 
 
 def test_c1_full_size_properties(cuda, oracle):
