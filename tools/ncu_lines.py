@@ -75,6 +75,7 @@ def main():
     ap.add_argument("kernel")
     ap.add_argument("--lib", default="paper_2501_17779_b200/libcurvalign_cuda.so")
     ap.add_argument("--top", type=int, default=40)
+    ap.add_argument("--op", default=None, help="only SASS opcodes matching this regex (e.g. 'MOV')")
     a = ap.parse_args()
     recs = sass_page(a.report, a.kernel)
     lm = line_map(a.lib, a.kernel.split("::")[-1], recs)
@@ -83,6 +84,9 @@ def main():
     tot_s = tot_i = 0
     base = int(recs[0]["Address"], 16) if recs else 0
     for r in recs:
+        if a.op and not re.search(a.op, r["Source"].split(" ")[0] if not r["Source"].lstrip().startswith("@")
+                                  else r["Source"].split()[1]):
+            continue
         addr = int(r["Address"], 16) - base
         loc = lm.get(addr, "?")
         s = int(float(r.get("Warp Stall Sampling (All Samples)", "0") or 0))
