@@ -396,10 +396,6 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
             r.x = fma(-hm, wl.x, r.x);
             r.y = fma(-hm, wl.y, r.y);
           }
-          if (j == M - 1) {
-            r.x = fma(-h, w.x, r.x);
-            r.y = fma(-h, w.y, r.y);
-          }
           if (j == 0) {
             g = cscale(r, IB[0]);
           } else {
@@ -428,9 +424,11 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
           const double s0 = knot(i);
           const double h = s1 - s0;
           if (j < M) {
-            // mu_i = g_i - c'_i mu_{i+1}, c'_i = h_i / pivot_i
+            // mu_i = g_i - c'_i mu_{i+1}, c'_i = h_i / pivot_i (mu_{b-1} = w: the
+            // interface coupling of the last interior row is back-substituted,
+            // not moved to its right-hand side, so every row is the same update)
             const double cpr = h * IB[j];
-            mu0 = (j == M - 1) ? R[j] : make_double2(fma(-cpr, mu1.x, R[j].x), fma(-cpr, mu1.y, R[j].y));
+            mu0 = make_double2(fma(-cpr, mu1.x, R[j].x), fma(-cpr, mu1.y, R[j].y));
           }
           const double2 y0 = xy[i];
           if (l >= 0 && tl >= s0) {
