@@ -234,46 +234,52 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
     double gL = 0, Q = 1.0, ib = 0;
     double2 S = make_double2(0, 0);
     double SL = 0;
+    // interior rows a .. b-2 (j < M); the interface row b-1 follows the loop,
+    // so the unrolled rows carry no second data-dependent branch
 #pragma unroll
     for (int j = 0; j < kCMax; ++j) {
-      if (j <= M) {
+      if (j < M) {
         const int i = a + j;
         const double sn = knot(i + 1);
         const double h = sn - si;
         bad |= !(h > 0.0);  // strictly increasing knots (spline.cpp:66-68)
         const double ih = frcp(h);
-        const double2 y1 = xy[i + 1 == n ? 0 : i + 1];
+        const double2 y1 = xy[i + 1];  // i + 1 <= b - 1 < n
         const double2 sl = make_double2((y1.x - y0.x) * ih, (y1.y - y0.y) * ih);
         const double2 r = make_double2(sl.x - slp.x, sl.y - slp.y);
         R[j] = r;
-        if (j < M) {  // interior row i
-          if (j == 0) {
-            ib = frcp(2.0 * (hm + h));
-            g = cscale(r, ib);
-            gL = -hm * ib;
-            S = g;
-            SL = gL;
-          } else {
-            const double cpr = hm * ib;
-            ib = frcp(fma(-hm, cpr, 2.0 * (hm + h)));
-            g = make_double2(fma(-hm, g.x, r.x) * ib, fma(-hm, g.y, r.y) * ib);
-            gL = -hm * gL * ib;
-            Q *= -cpr;
-            S.x = fma(g.x, Q, S.x);
-            S.y = fma(g.y, Q, S.y);
-            SL = fma(gL, Q, SL);
-          }
-          IB[j] = ib;
-          hL = h;
+        if (j == 0) {
+          ib = frcp(2.0 * (hm + h));
+          g = cscale(r, ib);
+          gL = -hm * ib;
+          S = g;
+          SL = gL;
         } else {
-          hj = h;
-          rj = r;
+          const double cpr = hm * ib;
+          ib = frcp(fma(-hm, cpr, 2.0 * (hm + h)));
+          g = make_double2(fma(-hm, g.x, r.x) * ib, fma(-hm, g.y, r.y) * ib);
+          gL = -hm * gL * ib;
+          Q *= -cpr;
+          S.x = fma(g.x, Q, S.x);
+          S.y = fma(g.y, Q, S.y);
+          SL = fma(gL, Q, SL);
         }
+        IB[j] = ib;
         hm = h;
         slp = sl;
         y0 = y1;
         si = sn;
       }
+    }
+    {  // interface row b-1: its spacing and right-hand side
+      hL = hm;
+      const double sn = knot(b);
+      const double h = sn - si;
+      bad |= !(h > 0.0);
+      const double ih = frcp(h);
+      const double2 y1 = xy[b == n ? 0 : b];
+      rj = make_double2((y1.x - y0.x) * ih - slp.x, (y1.y - y0.y) * ih - slp.y);
+      hj = h;
     }
     v0l = g;
     vLl = gL;
