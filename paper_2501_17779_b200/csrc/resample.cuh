@@ -423,34 +423,44 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
       double2 y1 = xy[b == n ? 0 : b];
       double2 mu1 = mub;
       double2 mu0 = w;
+      // one interval [s_i, s_{i+1}): samples l, l-1, ... with t_l >= s_i
+      auto walk = [&](double s0, double2 y0) {
+        if (l >= 0 && tl >= s0) {
+          const double h = s1 - s0;
+          const double ih = frcp(h), h2 = h * h;
+          do {
+            const double A = (s1 - tl) * ih, B = (tl - s0) * ih;
+            const double ca = fma(A, A, -1.0) * A * h2, cb = fma(B, B, -1.0) * B * h2;
+            const double2 v = make_double2(fma(A, y0.x, fma(B, y1.x, fma(ca, mu0.x, cb * mu1.x))),
+                                           fma(A, y0.y, fma(B, y1.y, fma(ca, mu0.y, cb * mu1.y))));
+            out[l] = v;
+            cacc.x += v.x;
+            cacc.y += v.y;
+            --l;
+            tl = sample_t<kPow2>(l, N, invN);
+          } while (l >= 0 && tl >= s0);
+        }
+      };
+      {  // the interface interval [s_{b-1}, s_b): mu = (w, mu_b)
+        const double s0 = knot(b - 1);
+        const double2 y0 = xy[b - 1];
+        walk(s0, y0);
+        s1 = s0;
+        y1 = y0;
+        mu1 = mu0;
+      }
 #pragma unroll
       for (int j = kCMax - 1; j >= 0; --j) {
-        if (j <= M) {
+        if (j < M) {
           const int i = a + j;  // interval [s_i, s_{i+1})
           const double s0 = knot(i);
-          const double h = s1 - s0;
-          if (j < M) {
-            // mu_i = g_i - c'_i mu_{i+1}, c'_i = h_i / pivot_i (mu_{b-1} = w: the
-            // interface coupling of the last interior row is back-substituted,
-            // not moved to its right-hand side, so every row is the same update)
-            const double cpr = h * IB[j];
-            mu0 = make_double2(fma(-cpr, mu1.x, R[j].x), fma(-cpr, mu1.y, R[j].y));
-          }
+          // mu_i = g_i - c'_i mu_{i+1}, c'_i = h_i / pivot_i (mu_{b-1} = w: the
+          // interface coupling of the last interior row is back-substituted,
+          // not moved to its right-hand side, so every row is the same update)
+          const double cpr = (s1 - s0) * IB[j];
+          mu0 = make_double2(fma(-cpr, mu1.x, R[j].x), fma(-cpr, mu1.y, R[j].y));
           const double2 y0 = xy[i];
-          if (l >= 0 && tl >= s0) {
-            const double ih = frcp(h), h2 = h * h;
-            do {
-              const double A = (s1 - tl) * ih, B = (tl - s0) * ih;
-              const double ca = fma(A, A, -1.0) * A * h2, cb = fma(B, B, -1.0) * B * h2;
-              const double2 v = make_double2(fma(A, y0.x, fma(B, y1.x, fma(ca, mu0.x, cb * mu1.x))),
-                                             fma(A, y0.y, fma(B, y1.y, fma(ca, mu0.y, cb * mu1.y))));
-              out[l] = v;
-              cacc.x += v.x;
-              cacc.y += v.y;
-              --l;
-              tl = sample_t<kPow2>(l, N, invN);
-            } while (l >= 0 && tl >= s0);
-          }
+          walk(s0, y0);
           s1 = s0;
           y1 = y0;
           mu1 = mu0;
