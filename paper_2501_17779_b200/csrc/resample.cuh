@@ -387,29 +387,20 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
     double2 cacc = make_double2(0, 0);
     if (own) {
       const double2 mub = MB[t + 1 == K ? 0 : t + 1];
-      // forward with known boundary values (R[j] <- g_j)
-      const int ap = a == 0 ? n - 1 : a - 1;
-      double si = knot(a);
-      double hm = knot(a == 0 ? n : a) - knot(ap);
-      double2 g = make_double2(0, 0);
+      // forward with known boundary values, in place (R[j] <- g_j): each row
+      // reads its left spacing from the knots and g_{j-1} from R[j-1], so no
+      // value rotates through the data-dependent guard
+      {
+        const int ap = a == 0 ? n - 1 : a - 1;
+        const double hm0 = knot(a == 0 ? n : a) - knot(ap);
+        const double2 r0 = make_double2(fma(-hm0, wl.x, R[0].x), fma(-hm0, wl.y, R[0].y));
+        R[0] = cscale(r0, IB[0]);
+      }
 #pragma unroll
-      for (int j = 0; j < kCMax; ++j) {
+      for (int j = 1; j < kCMax; ++j) {
         if (j < M) {
-          const double sn = knot(a + j + 1);
-          const double h = sn - si;
-          double2 r = R[j];
-          if (j == 0) {
-            r.x = fma(-hm, wl.x, r.x);
-            r.y = fma(-hm, wl.y, r.y);
-          }
-          if (j == 0) {
-            g = cscale(r, IB[0]);
-          } else {
-            g = make_double2(fma(-hm, g.x, r.x) * IB[j], fma(-hm, g.y, r.y) * IB[j]);
-          }
-          R[j] = g;
-          hm = h;
-          si = sn;
+          const double hm = knot(a + j) - knot(a + j - 1);
+          R[j] = make_double2(fma(-hm, R[j - 1].x, R[j].x) * IB[j], fma(-hm, R[j - 1].y, R[j].y) * IB[j]);
         }
       }
       CVA_MARK(pb + 5);
