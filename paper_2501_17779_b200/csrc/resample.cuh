@@ -172,10 +172,12 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
   // ---- phase 0: chordal edges, chunk-local prefix sums, cross-chunk scan
   double tot = 0.0;
   if (own) {
+    double2 p = xy[a];
 #pragma unroll 4
     for (int i = a; i < b; ++i) {
-      const double2 p = xy[i], q = xy[i + 1 == n ? 0 : i + 1];
+      const double2 q = xy[i + 1 == n ? 0 : i + 1];
       const double dx = q.x - p.x, dy = q.y - p.y;
+      p = q;
       const double d = fsqrt(fma(dx, dx, dy * dy));  // curve.cpp:57
       bad |= !(d > 0.0);                             // coincident nodes (curve.cpp:58)
       tot += d;
