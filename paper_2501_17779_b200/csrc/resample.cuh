@@ -181,7 +181,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
       const double d = fsqrt(fma(dx, dx, dy * dy));  // curve.cpp:57
       bad |= !(d > 0.0);                             // coincident nodes (curve.cpp:58)
       tot += d;
-      if (i + 1 < b) L[i + 1] = tot;
+      if (i + 1 < b) L[(i + 1 - a) * K + t] = tot;
     }
   }
   double inc = tot;
@@ -202,18 +202,28 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
   }
   bad |= !isfinite(T);
   const double invT = 1.0 / T;
-  // normalise in place: L[i] <- s_i = (OFF_t + L_i) / T for this chunk's knots
-  // a..b-1 (s_a = OFF_t / T), and s_n = 1 (curve.cpp:63-64)
+  // normalise in place: s_i = (OFF_t + L_i) / T for this chunk's knots
+  // a..b-1 (s_a = OFF_t / T); s_n = 1 (curve.cpp:63-64) is not stored.
+  // Knot layout is chunk-major: s_{a_t + j} lives at sk[j K + t], so the
+  // per-chunk sweeps (thread t at offset j) hit consecutive words.
   double* sk = L;
   if (own) {
     const double off = pre + inc - tot;
-    sk[a] = off * invT;
+    sk[t] = off * invT;
 #pragma unroll 4
-    for (int i = a + 1; i < b; ++i) sk[i] = (off + sk[i]) * invT;
-    if (t == K - 1) sk[n] = 1.0;
+    for (int j = 1; j < b - a; ++j) sk[j * K + t] = (off + sk[j * K + t]) * invT;
   }
   bar_sync();
-  auto knot = [&](int i) -> double { return sk[i]; };
+  auto own_knot = [&](int j) -> double { return sk[j * K + t]; };  // s_{a+j}
+  // s_b: the next chunk's first knot (s_n = 1 after the last chunk)
+  auto next_knot = [&]() -> double { return t == K - 1 ? 1.0 : sk[t + 1]; };
+  // s_{a-1}: the previous chunk's last knot (s_{n-1} before the first chunk)
+  auto prev_knot = [&]() -> double {
+    const int tp = t == 0 ? K - 1 : t - 1;
+    const int ap = (tp * n) >> lgK;
+    const int cp = (t == 0 ? n : a) - ap;
+    return sk[(cp - 1) * K + tp];
+  };
   CVA_MARK(pb + 0);
 
   // ---- phase 1: rhs, forward sweep, chunk-end responses
@@ -226,8 +236,8 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
   if (own) {
     // h_{a-1} = s_a - s_{a-1} (h_{n-1} = s_n - s_{n-1} for the first chunk)
     const int ap = a == 0 ? n - 1 : a - 1;
-    double si = knot(a);
-    double hm = knot(a == 0 ? n : a) - knot(ap);
+    double si = own_knot(0);
+    double hm = (a == 0 ? 1.0 : si) - prev_knot();
     const double2 yp = xy[ap];
     double2 y0 = xy[a];
     const double ihm = frcp(hm);
@@ -242,7 +252,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
     for (int j = 0; j < kCMax; ++j) {
       if (j < M) {
         const int i = a + j;
-        const double sn = knot(i + 1);
+        const double sn = own_knot(j + 1);
         const double h = sn - si;
         bad |= !(h > 0.0);  // strictly increasing knots (spline.cpp:66-68)
         const double ih = frcp(h);
@@ -275,7 +285,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
     }
     {  // interface row b-1: its spacing and right-hand side
       hL = hm;
-      const double sn = knot(b);
+      const double sn = next_knot();
       const double h = sn - si;
       bad |= !(h > 0.0);
       const double ih = frcp(h);
@@ -311,7 +321,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
     const double nL = F[4 * tn + 2], nR = F[4 * tn + 3];
     double dj = 2.0 * (hL + hj), sj = hj;
     if (t == K - 1) {  // the reference's last row (see header, P11); h_0 = s_1 - s_0
-      const double h0 = knot(1) - knot(0);
+      const double h0 = sk[K] - sk[0];  // s_1 - s_0 (chunk 0, offsets 1 and 0)
       sj = hL;
       dj = 2.0 * (hL + hj) + hj * (hj - hL) / (2.0 * (hj + h0));
     }
@@ -393,15 +403,14 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
       // reads its left spacing from the knots and g_{j-1} from R[j-1], so no
       // value rotates through the data-dependent guard
       {
-        const int ap = a == 0 ? n - 1 : a - 1;
-        const double hm0 = knot(a == 0 ? n : a) - knot(ap);
+        const double hm0 = (a == 0 ? 1.0 : own_knot(0)) - prev_knot();
         const double2 r0 = make_double2(fma(-hm0, wl.x, R[0].x), fma(-hm0, wl.y, R[0].y));
         R[0] = cscale(r0, IB[0]);
       }
 #pragma unroll
       for (int j = 1; j < kCMax; ++j) {
         if (j < M) {
-          const double hm = knot(a + j) - knot(a + j - 1);
+          const double hm = own_knot(j) - own_knot(j - 1);
           R[j] = make_double2(fma(-hm, R[j - 1].x, R[j].x) * IB[j], fma(-hm, R[j - 1].y, R[j].y) * IB[j]);
         }
       }
@@ -410,7 +419,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
       // last one below s_b (sample l lies in interval i iff s_i <= t_l < s_{i+1},
       // the reference's upper_bound rule, spline.cpp:98-105)
       const double invN = 1.0 / (double)N;
-      double s1 = knot(b);
+      double s1 = next_knot();
       int l = ((t == K - 1) ? N : first_sample<kPow2>(s1, N)) - 1;
       double tl = sample_t<kPow2>(l, N, invN);
       double2 y1 = xy[b == n ? 0 : b];
@@ -435,7 +444,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
         }
       };
       {  // the interface interval [s_{b-1}, s_b): mu = (w, mu_b)
-        const double s0 = knot(b - 1);
+        const double s0 = own_knot(M);
         const double2 y0 = xy[b - 1];
         walk(s0, y0);
         s1 = s0;
@@ -446,7 +455,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
       for (int j = kCMax - 1; j >= 0; --j) {
         if (j < M) {
           const int i = a + j;  // interval [s_i, s_{i+1})
-          const double s0 = knot(i);
+          const double s0 = own_knot(j);
           // mu_i = g_i - c'_i mu_{i+1}, c'_i = h_i / pivot_i (mu_{b-1} = w: the
           // interface coupling of the last interior row is back-substituted,
           // not moved to its right-hand side, so every row is the same update)
