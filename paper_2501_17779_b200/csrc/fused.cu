@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(kT, 2)
   bulk_init(&mbar);
   raw_to_smem(pts + a0, xy, na, &mbar, 0);
   CVA_MARK(1);
-  const rs::CurveStats A = rs::resample_block<true, false>(xy, na, s, scr, red, Z1, N, 2);
+  const rs::CurveStats A = rs::resample_block<true, false, true>(xy, na, s, scr, red, Z1, N, 2);
   __syncthreads();  // resample_block's last reads of xy are done
   raw_to_smem(pts + a1, xy, nb, &mbar, 1);
   CVA_MARK(10);
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kT, 2)
   }
   __syncthreads();
   pf::PairIn in{Z1, al, A.centroid, B.centroid, A.inv_len, B.inv_len};
-  pf::pair_stage<false, N, true>(in, bufs, N, tw, out + p, al, red);
+  pf::pair_stage<false, N, true, true>(in, bufs, N, tw, out + p, al, red);
 }
 
 // ------------------------------------------------------------- preprocess
@@ -317,7 +317,7 @@ static cudaError_t launch_align_kernel(unsigned grid, size_t sm, cudaStream_t s,
 size_t v2_resample_align_smem(int N) {
   const size_t fft = 4 * sizeof(double2) * (size_t)pf::padded_len(N);
   const size_t raw = v2::kRawBytes > fft ? v2::kRawBytes : fft;
-  return raw + v2::kScrBytes + sizeof(double2) * (size_t)N;
+  return raw + v2::kScrBytes + sizeof(double2) * (size_t)(N + N / 8);  // Z1 padded
 }
 size_t v2_preprocess_smem(int n_out) {
   return v2::kRawBytes + v2::kScrBytes + sizeof(double2) * (size_t)n_out;

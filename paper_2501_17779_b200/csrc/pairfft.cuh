@@ -224,7 +224,9 @@ __host__ __device__ inline int fft_len(int N) {
 // run on the centered, unscaled curves) and the scales 1/len are applied to
 // the correlation spectrum, the energies and the aligned curve. A length that
 // is not finite and > 0 marks the pair invalid (preprocess: curve.cpp:41-48).
-template <bool kInPlace = false, int kN = 0, bool kLenOnLoad = false>
+// kPadZ1: in.z1 is shared memory in the resampler's padded layout
+// z1[l + (l >> 3)].
+template <bool kInPlace = false, int kN = 0, bool kLenOnLoad = false, bool kPadZ1 = false>
 __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
                                   const double2* __restrict__ tw, cva_alignment* out,
                                   double2* aligned, double2* red) {
@@ -251,12 +253,14 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     auto load = [&](int i) {
       if (i >= lim) return make_double2(0.0, 0.0);
       const int k = i < N ? i : i - N;
-      const double2 q = src[k];
+      const bool padded = kPadZ1 && grp == 0;
+      const double2 q = src[padded ? k + (k >> 3) : k];
       const double2 z = make_double2((q.x - c.x) * sc, (q.y - c.y) * sc);
       if (i < N) {
         ss = fma(z.x, z.x, fma(z.y, z.y, ss));
         if constexpr (kLenOnLoad) {  // edge (k, k+1) of the closed polygon (curve.cpp:17-25)
-          const double2 o = src[k + 1 == N ? 0 : k + 1];
+          const int k1 = k + 1 == N ? 0 : k + 1;
+          const double2 o = src[padded ? k1 + (k1 >> 3) : k1];
           const double dx = o.x - q.x, dy = o.y - q.y;
           len += fsqrt(fma(dx, dx, dy * dy));
         }

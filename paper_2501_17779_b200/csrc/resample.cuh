@@ -155,7 +155,9 @@ __device__ __forceinline__ double sample_t(int l, int N, double invN) {
 // compiler forward stale loads across the barrier.
 // kLen = false skips the polygon length (inv_len is then not set, bad covers
 // the knots only): the fused pair kernel measures it while loading its FFT.
-template <bool kPow2, bool kLen = true>
+// kPadOut: out is shared memory indexed out[l + (l >> 3)] (one pad slot per
+// 8 samples: the chunk-strided sample stores spread over all banks).
+template <bool kPow2, bool kLen = true, bool kPadOut = false>
 __device__ inline CurveStats resample_block(const double2* xy, int n, double* L, double* scr,
                                             double2* red, double2* out, const int N,
                                             const int pb = 0 /* phase-stamp base */) {
@@ -435,7 +437,7 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
             const double ca = fma(A, A, -1.0) * A * h2, cb = fma(B, B, -1.0) * B * h2;
             const double2 v = make_double2(fma(A, y0.x, fma(B, y1.x, fma(ca, mu0.x, cb * mu1.x))),
                                            fma(A, y0.y, fma(B, y1.y, fma(ca, mu0.y, cb * mu1.y))));
-            out[l] = v;
+            out[kPadOut ? l + (l >> 3) : l] = v;
             cacc.x += v.x;
             cacc.y += v.y;
             --l;
@@ -477,7 +479,8 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
     double len = 0.0;
     if constexpr (kLen) {
       for (int q = t; q < N; q += kT) {
-        const double2 p = out[q], o = out[q + 1 == N ? 0 : q + 1];
+        const int q1 = q + 1 == N ? 0 : q + 1;
+        const double2 p = out[kPadOut ? q + (q >> 3) : q], o = out[kPadOut ? q1 + (q1 >> 3) : q1];
         const double dx = o.x - p.x, dy = o.y - p.y;
         len += fsqrt(fma(dx, dx, dy * dy));
       }
