@@ -155,18 +155,18 @@ __global__ void __launch_bounds__(kT, 2)
     __shared__ uint64_t mbar;
     bulk_init(&mbar);
     raw_to_smem(pts + b0, xy, n, &mbar, 0);
-    st = rs::resample_block<kPow2>(xy, n, s, scr, red, Z, n_out);
+    st = rs::resample_block<kPow2, true, true>(xy, n, s, scr, red, Z, n_out);
     bad = st.bad;
   }
   if (bad) {
     for (int l = threadIdx.x; l < n_out; l += kT) o[l] = make_double2(qnan(), qnan());
   } else if (center_normalize) {
     for (int l = threadIdx.x; l < n_out; l += kT) {
-      const double2 z = Z[l];
+      const double2 z = Z[l + (l >> 3)];
       o[l] = make_double2((z.x - st.centroid.x) * st.inv_len, (z.y - st.centroid.y) * st.inv_len);
     }
   } else {
-    for (int l = threadIdx.x; l < n_out; l += kT) o[l] = Z[l];
+    for (int l = threadIdx.x; l < n_out; l += kT) o[l] = Z[l + (l >> 3)];
   }
   if (status && threadIdx.x == 0) status[c] = bad ? CVA_INVALID_ARGUMENT : CVA_OK;
 }
@@ -320,7 +320,7 @@ size_t v2_resample_align_smem(int N) {
   return raw + v2::kScrBytes + sizeof(double2) * (size_t)(N + N / 8);  // Z1 padded
 }
 size_t v2_preprocess_smem(int n_out) {
-  return v2::kRawBytes + v2::kScrBytes + sizeof(double2) * (size_t)n_out;
+  return v2::kRawBytes + v2::kScrBytes + sizeof(double2) * (size_t)(n_out + n_out / 8);  // Z padded
 }
 size_t v2_align_smem(int N) {
   return (v2_inplace(N) ? 2 : 4) * sizeof(double2) * (size_t)pf::padded_len(pf::fft_len(N));
