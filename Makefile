@@ -10,13 +10,13 @@ CSRC     := $(PKG)/csrc
 BUILD    := build
 REF      ?= /root/reference
 
-KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h $(CSRC)/fused.h $(CSRC)/largen.h include/curvalign_cuda.h
+KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h $(CSRC)/fused.h $(CSRC)/largen.h $(CSRC)/elastic.h include/curvalign_cuda.h
 
 .PHONY: all lib synth dropin dropin_test oracle ref clean prof
 
 # Phase-timing build (tools/phase_timing.py): separate .so, never shipped.
 prof: $(PKG)/libcurvalign_cuda_prof.so
-$(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kernels.cu $(CSRC)/allpairs.cu $(CSRC)/largen.cu $(CSRC)/dropin_kernels.cu $(KERNEL_HDRS) $(CSRC)/prof.cuh
+$(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kernels.cu $(CSRC)/allpairs.cu $(CSRC)/largen.cu $(CSRC)/dropin_kernels.cu $(CSRC)/elastic.cu $(KERNEL_HDRS) $(CSRC)/prof.cuh
 	@mkdir -p $(BUILD)/prof
 	$(NVCC) $(NVFLAGS) -DCVA_PHASE_TIMING -c $(CSRC)/fused.cu -o $(BUILD)/prof/fused.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/kernels.cu -o $(BUILD)/prof/kernels.o
@@ -25,6 +25,7 @@ $(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kern
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/allpairs.cu -o $(BUILD)/prof/allpairs.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/largen.cu -o $(BUILD)/prof/largen.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/dropin_kernels.cu -o $(BUILD)/prof/dropin_kernels.o
+	$(NVCC) $(NVFLAGS) -c $(CSRC)/elastic.cu -o $(BUILD)/prof/elastic.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(BUILD)/prof/*.o
 all: lib synth dropin dropin_test oracle ref
 
@@ -48,11 +49,15 @@ $(BUILD)/largen.o: $(CSRC)/largen.cu $(KERNEL_HDRS) $(CSRC)/largen.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_largen.log || (cat $(BUILD)/ptxas_largen.log; exit 1)
 
+$(BUILD)/elastic.o: $(CSRC)/elastic.cu $(KERNEL_HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_elastic.log || (cat $(BUILD)/ptxas_elastic.log; exit 1)
+
 $(BUILD)/dropin_kernels.o: $(CSRC)/dropin_kernels.cu $(KERNEL_HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(BUILD)/capi.o: $(CSRC)/capi.cpp $(CSRC)/kernels.h $(CSRC)/fused.h include/curvalign_cuda.h
+$(BUILD)/capi.o: $(CSRC)/capi.cpp $(CSRC)/kernels.h $(CSRC)/fused.h $(CSRC)/elastic.h include/curvalign_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
 
@@ -60,7 +65,7 @@ $(BUILD)/probe.o: $(CSRC)/probe.cu include/curvalign_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/fused.o $(BUILD)/allpairs.o $(BUILD)/largen.o $(BUILD)/dropin_kernels.o $(BUILD)/capi.o $(BUILD)/probe.o
+$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/fused.o $(BUILD)/allpairs.o $(BUILD)/largen.o $(BUILD)/elastic.o $(BUILD)/dropin_kernels.o $(BUILD)/capi.o $(BUILD)/probe.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
 
 # Synthetic workload generators (bench harness; host only).

@@ -188,6 +188,45 @@ int cva_dft_host(const double* x_complex, int64_t n, int64_t kcount, int sign, d
                  double* out_complex);
 
 /* ---------------------------------------------------------------------------
+ * Elastic (SRV) matching: the rigid path's callers in the reference's elastic
+ * distance (proj/src/srv.cpp:100-257, proj/src/elastic.cpp:102-236).
+ * Device entry points are asynchronous on `stream`; *_host are synchronous.
+ * Failures are per pair in `status` (NaN outputs), like distance_matrix's NaN
+ * cells (elastic.cpp:210-217).
+ * ------------------------------------------------------------------------- */
+
+/* dp_reparam(q1[p], q2[p], max_slope) (srv.cpp:180-257) for pairs x n SRV samples:
+ * gamma pairs x (n+1), energy pairs. Bitwise the reference's result.
+ * status (nullable): CVA_RUNTIME_ERROR where no admissible path exists. */
+int cva_dp_reparam_batch(const double* q1, const double* q2, int64_t pairs, int64_t n, int max_slope,
+                         double* gamma, double* energy, int32_t* status, void* stream);
+int cva_dp_reparam_batch_host(const double* q1, const double* q2, int64_t pairs, int64_t n,
+                              int max_slope, double* gamma, double* energy, int32_t* status);
+
+/* elastic_distance_approach2(c1[p], c2[p], opts) (elastic.cpp:102-174) on
+ * preprocessed curves (pairs x n points each). Outputs per pair: distance,
+ * energy, t0, theta (Rotation2 angle), gamma (nullable, pairs x (n+1)),
+ * iterations, converged, status. The GPU always uses the FFT correlation
+ * (use_fft = true); ElasticOptions defaults: max_iters 30, energy_tol 1e-6,
+ * max_slope 4. Supports 8 <= n <= 1024 (non-powers of two <= 512). */
+int cva_elastic_approach2_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                int max_iters, double energy_tol, int max_slope, double* distance,
+                                double* energy, double* t0, double* theta, double* gamma,
+                                int32_t* iterations, int32_t* converged, int32_t* status, void* stream);
+int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                     int max_iters, double energy_tol, int max_slope, double* distance,
+                                     double* energy, double* t0, double* theta, double* gamma,
+                                     int32_t* iterations, int32_t* converged, int32_t* status);
+
+/* distance_matrix(curves, approach2, n) cells (elastic.cpp:176-236) for `count`
+ * preprocessed curves of n nodes: d[i * count + j] = distance of matching curve j
+ * onto curve i; NaN for a failed pair. */
+int cva_elastic_distance_matrix(const double* curves, int64_t count, int64_t n, int max_iters,
+                                double energy_tol, int max_slope, double* d, void* stream);
+int cva_elastic_distance_matrix_host(const double* curves, int64_t count, int64_t n, int max_iters,
+                                     double energy_tol, int max_slope, double* d);
+
+/* ---------------------------------------------------------------------------
  * Diagnostics (not on the hot path).
  * ------------------------------------------------------------------------- */
 

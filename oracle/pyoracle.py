@@ -288,5 +288,68 @@ class Reference(_Base):
         return e, k, th
 
 
+    # ---- elastic (SRV) matching: proj/src/srv.cpp, proj/src/elastic.cpp ----
+    def apply_srv_action(self, q, t0, theta, gamma):
+        a, g = _f64(q), _f64(gamma)
+        out = np.zeros_like(a)
+        f = self._fn("apply_srv_action", [c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p])
+        _raise(f(_p(a), a.shape[0], t0, theta, _p(g), _p(out)), "apply_srv_action")
+        return out
+
+    def elastic_energy(self, q1, q2, t0, theta, gamma):
+        a, b, g = _f64(q1), _f64(q2), _f64(gamma)
+        out = np.zeros(1)
+        f = self._fn("elastic_energy", [c_void_p, c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p])
+        _raise(f(_p(a), _p(b), a.shape[0], t0, theta, _p(g), _p(out)), "elastic_energy")
+        return float(out[0])
+
+    def dp_step_cost(self, q1, q2, i0, j0, di, dj):
+        a, b = _f64(q1), _f64(q2)
+        out = np.zeros(1)
+        f = self._fn("dp_step_cost", [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int, c_void_p])
+        _raise(f(_p(a), _p(b), a.shape[0], i0, j0, di, dj, _p(out)), "dp_step_cost")
+        return float(out[0])
+
+    def dp_reparam_batch(self, q1, q2, max_slope=4, threads=1):
+        a, b = _f64(q1), _f64(q2)
+        pairs, n = a.shape[0], a.shape[1]
+        g = np.zeros((pairs, n + 1))
+        e = np.zeros(pairs)
+        st = np.zeros(pairs, dtype=np.int32)
+        f = self._fn("dp_reparam_batch", [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int, c_void_p, c_void_p,
+                                          c_void_p])
+        f(_p(a), _p(b), pairs, n, max_slope, threads, _p(g), _p(e), _p(st))
+        return g, e, st
+
+    def elastic_approach2_batch(self, c1, c2, max_iters=30, energy_tol=1e-6, use_fft=True, max_slope=4,
+                                threads=1, gamma=False):
+        a, b = _f64(c1), _f64(c2)
+        pairs, n = a.shape[0], a.shape[1]
+        out = {k: np.zeros(pairs) for k in ("distance", "energy", "t0", "theta")}
+        g = np.zeros((pairs, n + 1)) if gamma else None
+        it = np.zeros(pairs, dtype=np.int32)
+        cv = np.zeros(pairs, dtype=np.int32)
+        st = np.zeros(pairs, dtype=np.int32)
+        f = self._fn("elastic_approach2_batch", [c_void_p, c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_int,
+                                                 c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                                 c_void_p, c_void_p])
+        f(_p(a), _p(b), pairs, n, max_iters, energy_tol, 1 if use_fft else 0, max_slope, threads,
+          _p(out["distance"]), _p(out["energy"]), _p(out["t0"]), _p(out["theta"]), _p(g) if gamma else None,
+          _p(it), _p(cv), _p(st))
+        out.update(iterations=it, converged=cv, status=st)
+        if gamma:
+            out["gamma"] = g
+        return out
+
+    def distance_matrix_approach2(self, curves, n, max_iters=30, energy_tol=1e-6, max_slope=4, threads=1):
+        c = _f64(curves)
+        k, n_in = c.shape[0], c.shape[1]
+        out = np.zeros((k, k))
+        f = self._fn("distance_matrix_approach2", [c_void_p, c_int64, c_int64, c_int64, c_int, c_double, c_int,
+                                                   c_int, c_void_p])
+        _raise(f(_p(c), k, n_in, n, max_iters, energy_tol, max_slope, threads, _p(out)), "distance_matrix")
+        return out
+
+
 def reference_available() -> bool:
     return os.path.exists(REF_PATH)

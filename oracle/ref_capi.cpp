@@ -1,7 +1,7 @@
 // TEST INFRASTRUCTURE ONLY — C-ABI over the reference's OWN implementation.
 //
 // oracle/Makefile compiles the reference sources in place
-// (/root/reference/proj/src/{fft,rigid_align,curve,spline,srv,synthetic}.cpp,
+// (/root/reference/proj/src/{fft,rigid_align,curve,spline,srv,synthetic,elastic}.cpp,
 // unmodified, never copied) together with this file and the FFTW/Eigen shims
 // into oracle/_ref/libcurvalign_ref.so. Tests use it to pin the C restatement
 // (oracle/curvalign_oracle.c) and to generate golden vectors; bench.py uses it
@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "curvalign/curve.hpp"
+#include "curvalign/elastic.hpp"
 #include "curvalign/fft.hpp"
 #include "curvalign/rigid_align.hpp"
 #include "curvalign/spline.hpp"
@@ -364,6 +365,109 @@ int ref_allpairs(const double* curves, int64_t m, int64_t n, int64_t row_begin, 
     }
   });
   return first_err.load();
+}
+
+// ---- elastic (SRV) matching: the path's callers --
+
+SrvCurve to_srv(const double* q, int64_t n) {
+  SrvCurve s;
+  s.q = to_points(q, n);
+  s.h = n ? 1.0 / static_cast<double>(n) : 0.0;
+  return s;
+}
+
+Reparameterization to_reparam(const double* g, int64_t n) {
+  Reparameterization r;
+  r.gamma.assign(g, g + n + 1);
+  return r;
+}
+
+int ref_apply_srv_action(const double* q, int64_t n, double t0, double theta, const double* gamma,
+                         double* out) {
+  return guard([&] { from_points(apply_srv_action(to_srv(q, n), t0, Rotation2(theta), to_reparam(gamma, n)).q, out); });
+}
+
+int ref_elastic_energy(const double* q1, const double* q2, int64_t n, double t0, double theta,
+                       const double* gamma, double* out) {
+  return guard([&] { *out = elastic_energy(to_srv(q1, n), to_srv(q2, n), t0, Rotation2(theta), to_reparam(gamma, n)); });
+}
+
+int ref_dp_step_cost(const double* q1, const double* q2, int64_t n, int i0, int j0, int di, int dj,
+                     double* out) {
+  return guard([&] { *out = dp_step_cost(to_srv(q1, n), to_srv(q2, n), i0, j0, di, dj); });
+}
+
+// pairs x n SRV samples each; gamma_out pairs x (n+1).
+int ref_dp_reparam_batch(const double* q1, const double* q2, int64_t pairs, int64_t n, int max_slope,
+                         int threads, double* gamma_out, double* energy_out, int32_t* status) {
+  std::atomic<int> first_err{0};
+  parallel_for(pairs, threads, [&](int64_t p) {
+    const int rc = guard([&] {
+      const DpResult r = dp_reparam(to_srv(q1 + 2 * p * n, n), to_srv(q2 + 2 * p * n, n), max_slope);
+      std::memcpy(gamma_out + p * (n + 1), r.gamma.gamma.data(), sizeof(double) * (n + 1));
+      energy_out[p] = r.energy;
+    });
+    status[p] = rc;
+    if (rc != kOk) {
+      energy_out[p] = std::nan("");
+      int expected = 0;
+      first_err.compare_exchange_strong(expected, rc);
+    }
+  });
+  return first_err.load();
+}
+
+// elastic_distance_approach2 (proj/src/elastic.cpp:102-174) on pairs of
+// preprocessed curves (pairs x n points each). gamma_out (nullable) pairs x (n+1).
+int ref_elastic_approach2_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                int max_iters, double energy_tol, int use_fft, int max_slope,
+                                int threads, double* distance, double* energy, double* t0,
+                                double* theta, double* gamma_out, int32_t* iterations,
+                                int32_t* converged, int32_t* status) {
+  ElasticOptions o;
+  o.max_iters = max_iters;
+  o.energy_tol = energy_tol;
+  o.use_fft = use_fft != 0;
+  o.max_slope = max_slope;
+  std::atomic<int> first_err{0};
+  parallel_for(pairs, threads, [&](int64_t p) {
+    const int rc = guard([&] {
+      const ElasticMatch m = elastic_distance_approach2(to_curve(c1 + 2 * p * n, n), to_curve(c2 + 2 * p * n, n), o);
+      distance[p] = m.distance;
+      energy[p] = m.energy;
+      t0[p] = m.t0;
+      theta[p] = m.rotation.theta();
+      if (gamma_out) std::memcpy(gamma_out + p * (n + 1), m.gamma.gamma.data(), sizeof(double) * (n + 1));
+      iterations[p] = m.iterations;
+      converged[p] = m.converged ? 1 : 0;
+    });
+    status[p] = rc;
+    if (rc != kOk) {
+      distance[p] = energy[p] = std::nan("");
+      int expected = 0;
+      first_err.compare_exchange_strong(expected, rc);
+    }
+  });
+  return first_err.load();
+}
+
+// distance_matrix(curves, approach2, n) (proj/src/elastic.cpp:176-236): count
+// raw curves of n_in nodes each (uniform size), preprocessed to n inside.
+int ref_distance_matrix_approach2(const double* curves, int64_t count, int64_t n_in, int64_t n,
+                                  int max_iters, double energy_tol, int max_slope, int threads,
+                                  double* out) {
+  return guard([&] {
+    std::vector<Curve> cs;
+    for (int64_t i = 0; i < count; ++i) cs.push_back(to_curve(curves + 2 * i * n_in, n_in));
+    ElasticOptions o;
+    o.max_iters = max_iters;
+    o.energy_tol = energy_tol;
+    o.max_slope = max_slope;
+    const auto d = distance_matrix(cs, DistanceMethod::approach2, static_cast<std::size_t>(n), o,
+                                   static_cast<unsigned>(threads));
+    for (int64_t i = 0; i < count; ++i)
+      for (int64_t j = 0; j < count; ++j) out[i * count + j] = d[i][j];
+  });
 }
 
 }  // extern "C"

@@ -9,7 +9,14 @@ the C ABI in include/curvalign_cuda.h); this package is the Python host mirror
 of the reference's API (proj/include/curvalign/*.hpp).
 """
 from .api import (  # noqa: F401
+    ElasticMatch,
     RigidAlignment,
+    distance_matrix,
+    dp_reparam,
+    dp_reparam_batch,
+    elastic_approach2_batch,
+    elastic_distance_approach2,
+    elastic_distance_matrix,
     align_fft,
     allpairs,
     align_fft_batch,
@@ -26,7 +33,14 @@ from .api import (  # noqa: F401
 )
 
 __all__ = [
+    "ElasticMatch",
     "RigidAlignment",
+    "distance_matrix",
+    "dp_reparam",
+    "dp_reparam_batch",
+    "elastic_approach2_batch",
+    "elastic_distance_approach2",
+    "elastic_distance_matrix",
     "align_fft",
     "allpairs",
     "align_fft_batch",

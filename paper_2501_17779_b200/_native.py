@@ -94,6 +94,23 @@ SIGNATURES = {
         [c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_void_p],
     ),
     "cva_allpairs_host": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
+    "cva_dp_reparam_batch": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int, c_void_p, c_void_p, c_void_p,
+                                     c_void_p]),
+    "cva_dp_reparam_batch_host": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_int, c_void_p, c_void_p,
+                                          c_void_p]),
+    "cva_elastic_approach2_batch": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
+    "cva_elastic_approach2_batch_host": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+         c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
+    "cva_elastic_distance_matrix": (c_int, [c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_void_p,
+                                            c_void_p]),
+    "cva_elastic_distance_matrix_host": (c_int, [c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_void_p]),
 }
 
 _lib = None

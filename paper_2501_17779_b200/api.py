@@ -345,3 +345,146 @@ def preprocess_align_uniform(c1, c2, return_aligned: bool = False):
     check(lib.cva_preprocess_align_uniform_host(_ptr(a), _ptr(b), pairs, n, res.ctypes.data,
                                                 al.ctypes.data if al is not None else 0))
     return res, al
+
+
+# --------------------------------------------------------------- elastic (SRV) matching
+
+
+@dataclass
+class ElasticMatch:
+    """Mirror of ``curvalign::ElasticMatch`` (proj/include/curvalign/elastic.hpp:23-32)
+    without the energy trace."""
+
+    t0: float
+    theta: float
+    gamma: np.ndarray
+    energy: float
+    distance: float
+    iterations: int
+    converged: bool
+
+
+def dp_reparam_batch(q1, q2, max_slope: int = 4):
+    """dp_reparam (srv.cpp:180-257) per pair of SRV sample arrays ``(pairs, n, 2)``.
+
+    Returns ``(gamma (pairs, n+1), energy (pairs,), status (pairs,))``; numpy in ->
+    numpy out, CUDA tensors in -> CUDA tensors out. Bitwise the reference's DP."""
+    lib = _native.load()
+    if _is_cuda_tensor(q1):
+        a, b = q1.contiguous(), q2.contiguous()
+        pairs, n = a.shape[0], a.shape[1]
+        g = torch.empty((pairs, n + 1), dtype=torch.float64, device=a.device)
+        e = torch.empty(pairs, dtype=torch.float64, device=a.device)
+        st = torch.empty(pairs, dtype=torch.int32, device=a.device)
+        check(lib.cva_dp_reparam_batch(a.data_ptr(), b.data_ptr(), pairs, n, max_slope, g.data_ptr(),
+                                       e.data_ptr(), st.data_ptr(), _stream_of(a)))
+        return g, e, st
+    a, b = _f64c(q1), _f64c(q2)
+    if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 2:
+        raise ValueError("dp: size mismatch")
+    pairs, n = a.shape[0], a.shape[1]
+    g = np.empty((pairs, n + 1))
+    e = np.empty(pairs)
+    st = np.empty(pairs, dtype=np.int32)
+    check(lib.cva_dp_reparam_batch_host(_ptr(a), _ptr(b), pairs, n, max_slope, g.ctypes.data, e.ctypes.data,
+                                        st.ctypes.data))
+    return g, e, st
+
+
+def dp_reparam(q1, q2, max_slope: int = 4):
+    """Single-pair dp_reparam: returns ``(gamma, energy)``; RuntimeError if no
+    admissible path (srv.cpp:233)."""
+    g, e, st = dp_reparam_batch(np.asarray(q1)[None], np.asarray(q2)[None], max_slope)
+    if st[0] != 0:
+        raise RuntimeError("dp: no admissible path")
+    return g[0], float(e[0])
+
+
+def elastic_approach2_batch(c1, c2, max_iters: int = 30, energy_tol: float = 1e-6, max_slope: int = 4,
+                            return_gamma: bool = False):
+    """elastic_distance_approach2 (elastic.cpp:102-174) per pair of preprocessed
+    curves ``(pairs, n, 2)``. Returns a dict of per-pair arrays: distance,
+    energy, t0, theta, iterations, converged, status (+ gamma). numpy in -> numpy
+    out; CUDA tensors in -> CUDA tensors out (stream-ordered)."""
+    lib = _native.load()
+    if _is_cuda_tensor(c1):
+        a, b = c1.contiguous(), c2.contiguous()
+        pairs, n = a.shape[0], a.shape[1]
+        dev = a.device
+        out = {k: torch.empty(pairs, dtype=torch.float64, device=dev) for k in ("distance", "energy", "t0", "theta")}
+        for k in ("iterations", "converged", "status"):
+            out[k] = torch.empty(pairs, dtype=torch.int32, device=dev)
+        g = torch.empty((pairs, n + 1), dtype=torch.float64, device=dev) if return_gamma else None
+        check(lib.cva_elastic_approach2_batch(
+            a.data_ptr(), b.data_ptr(), pairs, n, max_iters, energy_tol, max_slope, out["distance"].data_ptr(),
+            out["energy"].data_ptr(), out["t0"].data_ptr(), out["theta"].data_ptr(), _tptr(g),
+            out["iterations"].data_ptr(), out["converged"].data_ptr(), out["status"].data_ptr(), _stream_of(a)))
+        if return_gamma:
+            out["gamma"] = g
+        return out
+    a, b = _f64c(c1), _f64c(c2)
+    if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 2:
+        raise ValueError("elastic: node count mismatch")
+    pairs, n = a.shape[0], a.shape[1]
+    out = {k: np.empty(pairs) for k in ("distance", "energy", "t0", "theta")}
+    for k in ("iterations", "converged", "status"):
+        out[k] = np.empty(pairs, dtype=np.int32)
+    g = np.empty((pairs, n + 1)) if return_gamma else None
+    check(lib.cva_elastic_approach2_batch_host(
+        _ptr(a), _ptr(b), pairs, n, max_iters, energy_tol, max_slope, out["distance"].ctypes.data,
+        out["energy"].ctypes.data, out["t0"].ctypes.data, out["theta"].ctypes.data,
+        g.ctypes.data if g is not None else 0, out["iterations"].ctypes.data, out["converged"].ctypes.data,
+        out["status"].ctypes.data))
+    if return_gamma:
+        out["gamma"] = g
+    return out
+
+
+def elastic_distance_approach2(c1, c2, max_iters: int = 30, energy_tol: float = 1e-6,
+                               max_slope: int = 4) -> ElasticMatch:
+    """Single pair (reference name and exceptions: ValueError for invalid input,
+    RuntimeError for a DP without admissible path)."""
+    a, b = np.asarray(c1, dtype=np.float64), np.asarray(c2, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValueError("elastic: node count mismatch")
+    r = elastic_approach2_batch(a[None], b[None], max_iters, energy_tol, max_slope, return_gamma=True)
+    st = int(r["status"][0])
+    if st == _native.CVA_INVALID_ARGUMENT:
+        raise ValueError("elastic: invalid input")
+    if st == _native.CVA_RUNTIME_ERROR:
+        raise RuntimeError("dp: no admissible path")
+    return ElasticMatch(t0=float(r["t0"][0]), theta=float(r["theta"][0]), gamma=r["gamma"][0],
+                        energy=float(r["energy"][0]), distance=float(r["distance"][0]),
+                        iterations=int(r["iterations"][0]), converged=bool(r["converged"][0]))
+
+
+def elastic_distance_matrix(curves, max_iters: int = 30, energy_tol: float = 1e-6, max_slope: int = 4):
+    """distance_matrix cells for approach 2 (elastic.cpp:176-236) on already
+    preprocessed curves ``(count, n, 2)``: d[i, j] = distance matching curve j
+    onto curve i, NaN for a failed pair."""
+    lib = _native.load()
+    if _is_cuda_tensor(curves):
+        c = curves.contiguous()
+        count, n = c.shape[0], c.shape[1]
+        d = torch.empty((count, count), dtype=torch.float64, device=c.device)
+        check(lib.cva_elastic_distance_matrix(c.data_ptr(), count, n, max_iters, energy_tol, max_slope,
+                                              d.data_ptr(), _stream_of(c)))
+        return d
+    c = _f64c(curves)
+    count, n = c.shape[0], c.shape[1]
+    d = np.empty((count, count))
+    check(lib.cva_elastic_distance_matrix_host(_ptr(c), count, n, max_iters, energy_tol, max_slope, d.ctypes.data))
+    return d
+
+
+def distance_matrix(curves, n: int, max_iters: int = 30, energy_tol: float = 1e-6, max_slope: int = 4):
+    """distance_matrix(curves, approach2, n) (elastic.cpp:176-236): raw curves
+    (a list of ``(n_i, 2)`` arrays) are preprocessed to n nodes on the GPU, then
+    every ordered pair is matched."""
+    if len(curves) < 2:
+        raise ValueError("distance_matrix: need at least 2 curves")
+    pts, offs = ragged(curves)
+    prep, st = preprocess_batch(pts, offs, n)
+    if (st != 0).any():
+        raise ValueError("distance_matrix: invalid curve")
+    return elastic_distance_matrix(prep, max_iters, energy_tol, max_slope)

@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/curvalign_cuda.h"
+#include "elastic.h"
 #include "fused.h"
 #include "kernels.h"
 #include "largen.h"
@@ -656,6 +657,175 @@ int cva_srv_align_batch_host(const double* c1, const double* c2, int64_t pairs, 
     e = cudaMemcpyAsync(aligned_q, dal.p, cb, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   return finish(e, "srv_align_batch_host");
+}
+
+// ------------------------------------------------------------- elastic (SRV) matching
+
+namespace {
+int check_elastic(int64_t pairs, int64_t n, int max_slope, const char* what) {
+  if (pairs < 0) return fail(CVA_INVALID_ARGUMENT, std::string(what) + ": negative pair count");
+  if (n < 8) return fail(CVA_INVALID_ARGUMENT, std::string(what) + ": need at least 8 nodes");  // elastic.cpp:57, srv.cpp:183
+  if (max_slope < 1) return fail(CVA_INVALID_ARGUMENT, "dp: max_slope must be >= 1");  // srv.cpp:131
+  if (n > 1 << 20 || !cva::elastic_supported((int)n, max_slope))
+    return fail(CVA_UNSUPPORTED, std::string(what) +
+                                     ": supported sizes are 8 <= n <= 1024 (powers of two; other n <= 512), "
+                                     "max_slope <= 8");
+  return CVA_OK;
+}
+
+struct Slab {
+  void* p = nullptr;
+  cudaStream_t s = nullptr;
+  ~Slab() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+}  // namespace
+
+int cva_dp_reparam_batch(const double* q1, const double* q2, int64_t pairs, int64_t n, int max_slope,
+                         double* gamma, double* energy, int32_t* status, void* stream) {
+  if (int rc = check_elastic(pairs, n, max_slope, "dp")) return rc;
+  if (pairs == 0) return CVA_OK;
+  if (!q1 || !q2 || !gamma || !energy) return fail(CVA_INVALID_ARGUMENT, "dp: null pointer");
+  if (!a16(q1) || !a16(q2)) return misaligned("dp");
+  if (int rc = require_device()) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int grid = cva::elastic_grid(pairs, (int)n, max_slope);
+  Slab slab;
+  slab.s = s;
+  const size_t per = cva::elastic_parent_slab(pairs, (int)n, max_slope);
+  if (per && scratch_alloc(&slab.p, per * (size_t)grid, s) != cudaSuccess)
+    return fail(CVA_BAD_ALLOC, "dp: parent scratch allocation failed");
+  return finish(cva::launch_dp_reparam((const double2*)q1, (const double2*)q2, pairs, (int)n, max_slope,
+                                       (uint8_t*)slab.p, grid, gamma, energy, status, s),
+                "dp launch");
+}
+
+static int elastic_launch(const double* A, const double* B, int64_t pairs, int64_t k, int64_t n, int max_iters,
+                          double energy_tol, int max_slope, const cva::ElasticOut& o, cudaStream_t s) {
+  const double2* tw = nullptr;
+  if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
+  const int grid = cva::elastic_grid(pairs, (int)n, max_slope);
+  Slab slab;
+  slab.s = s;
+  const size_t per = cva::elastic_parent_slab(pairs, (int)n, max_slope);
+  if (per && scratch_alloc(&slab.p, per * (size_t)grid, s) != cudaSuccess)
+    return fail(CVA_BAD_ALLOC, "elastic: parent scratch allocation failed");
+  const cva::ElasticParams prm{max_iters, energy_tol, max_slope};
+  return finish(cva::launch_elastic_approach2((const double2*)A, (const double2*)B, pairs, k, (int)n, prm,
+                                              (uint8_t*)slab.p, grid, tw, o, s),
+                "elastic launch");
+}
+
+int cva_elastic_approach2_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                int max_iters, double energy_tol, int max_slope, double* distance,
+                                double* energy, double* t0, double* theta, double* gamma,
+                                int32_t* iterations, int32_t* converged, int32_t* status, void* stream) {
+  if (int rc = check_elastic(pairs, n, max_slope, "elastic")) return rc;
+  if (pairs == 0) return CVA_OK;
+  if (!c1 || !c2 || !distance || !energy || !t0 || !theta || !iterations || !converged || !status)
+    return fail(CVA_INVALID_ARGUMENT, "elastic: null pointer");
+  if (!a16(c1) || !a16(c2)) return misaligned("elastic");
+  if (int rc = require_device()) return rc;
+  const cva::ElasticOut o{distance, energy, t0, theta, gamma, iterations, converged, status};
+  return elastic_launch(c1, c2, pairs, 0, n, max_iters, energy_tol, max_slope, o, (cudaStream_t)stream);
+}
+
+int cva_elastic_distance_matrix(const double* curves, int64_t count, int64_t n, int max_iters,
+                                double energy_tol, int max_slope, double* d, void* stream) {
+  if (count < 2) return fail(CVA_INVALID_ARGUMENT, "distance_matrix: need at least 2 curves");  // elastic.cpp:181
+  if (int rc = check_elastic(count * count, n, max_slope, "distance_matrix")) return rc;
+  if (!curves || !d) return fail(CVA_INVALID_ARGUMENT, "distance_matrix: null pointer");
+  if (!a16(curves)) return misaligned("distance_matrix");
+  if (int rc = require_device()) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t pairs = count * count;
+  void* ws = nullptr;
+  const size_t per = 3 * sizeof(double) + 3 * sizeof(int32_t);
+  if (scratch_alloc(&ws, per * (size_t)pairs + 256, s) != cudaSuccess)
+    return fail(CVA_BAD_ALLOC, "scratch allocation failed");
+  double* e = (double*)ws;
+  cva::ElasticOut o{d, e, e + pairs, e + 2 * pairs, nullptr, (int32_t*)(e + 3 * pairs),
+                    (int32_t*)(e + 3 * pairs) + pairs, (int32_t*)(e + 3 * pairs) + 2 * pairs};
+  const int rc = elastic_launch(curves, nullptr, pairs, count, n, max_iters, energy_tol, max_slope, o, s);
+  cudaFreeAsync(ws, s);
+  return rc;
+}
+
+int cva_dp_reparam_batch_host(const double* q1, const double* q2, int64_t pairs, int64_t n,
+                              int max_slope, double* gamma, double* energy, int32_t* status) {
+  if (int rc = check_elastic(pairs, n, max_slope, "dp")) return rc;
+  if (pairs == 0) return CVA_OK;
+  if (int rc = require_device()) return rc;
+  const size_t cb = sizeof(double2) * (size_t)(pairs * n), gb = sizeof(double) * (size_t)(pairs * (n + 1));
+  DevBuf d1, d2, dg, de, ds;
+  if (d1.alloc(cb) || d2.alloc(cb) || dg.alloc(gb) || de.alloc(sizeof(double) * pairs) ||
+      ds.alloc(sizeof(int32_t) * pairs))
+    return fail(CVA_BAD_ALLOC, "device allocation failed");
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaMemcpyAsync(d1.p, q1, cb, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, q2, cb, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  if (int rc = cva_dp_reparam_batch((const double*)d1.p, (const double*)d2.p, pairs, n, max_slope, (double*)dg.p,
+                                    (double*)de.p, (int32_t*)ds.p, s))
+    return rc;
+  e = cudaMemcpyAsync(gamma, dg.p, gb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(energy, de.p, sizeof(double) * pairs, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && status) e = cudaMemcpyAsync(status, ds.p, sizeof(int32_t) * pairs, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return finish(e, "dp_reparam_batch_host");
+}
+
+int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                     int max_iters, double energy_tol, int max_slope, double* distance,
+                                     double* energy, double* t0, double* theta, double* gamma,
+                                     int32_t* iterations, int32_t* converged, int32_t* status) {
+  if (int rc = check_elastic(pairs, n, max_slope, "elastic")) return rc;
+  if (pairs == 0) return CVA_OK;
+  if (int rc = require_device()) return rc;
+  const size_t cb = sizeof(double2) * (size_t)(pairs * n), gb = sizeof(double) * (size_t)(pairs * (n + 1));
+  const size_t vb = sizeof(double) * pairs, ib = sizeof(int32_t) * pairs;
+  DevBuf d1, d2, dv, dg, di;
+  if (d1.alloc(cb) || d2.alloc(cb) || dv.alloc(4 * vb) || (gamma && dg.alloc(gb)) || di.alloc(3 * ib))
+    return fail(CVA_BAD_ALLOC, "device allocation failed");
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  double* v = (double*)dv.p;
+  int32_t* iv = (int32_t*)di.p;
+  if (int rc = cva_elastic_approach2_batch((const double*)d1.p, (const double*)d2.p, pairs, n, max_iters,
+                                           energy_tol, max_slope, v, v + pairs, v + 2 * pairs, v + 3 * pairs,
+                                           gamma ? (double*)dg.p : nullptr, iv, iv + pairs, iv + 2 * pairs, s))
+    return rc;
+  double* hv[4] = {distance, energy, t0, theta};
+  for (int k = 0; k < 4 && e == cudaSuccess; ++k)
+    if (hv[k]) e = cudaMemcpyAsync(hv[k], v + k * pairs, vb, cudaMemcpyDeviceToHost, s);
+  int32_t* hi[3] = {iterations, converged, status};
+  for (int k = 0; k < 3 && e == cudaSuccess; ++k)
+    if (hi[k]) e = cudaMemcpyAsync(hi[k], iv + k * pairs, ib, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && gamma) e = cudaMemcpyAsync(gamma, dg.p, gb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return finish(e, "elastic_approach2_batch_host");
+}
+
+int cva_elastic_distance_matrix_host(const double* curves, int64_t count, int64_t n, int max_iters,
+                                     double energy_tol, int max_slope, double* d) {
+  if (count < 2) return fail(CVA_INVALID_ARGUMENT, "distance_matrix: need at least 2 curves");
+  if (int rc = check_elastic(count * count, n, max_slope, "distance_matrix")) return rc;
+  if (int rc = require_device()) return rc;
+  const size_t cb = sizeof(double2) * (size_t)(count * n), db = sizeof(double) * (size_t)(count * count);
+  DevBuf dc, dd;
+  if (dc.alloc(cb) || dd.alloc(db)) return fail(CVA_BAD_ALLOC, "device allocation failed");
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaMemcpyAsync(dc.p, curves, cb, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  if (int rc = cva_elastic_distance_matrix((const double*)dc.p, count, n, max_iters, energy_tol, max_slope,
+                                           (double*)dd.p, s))
+    return rc;
+  e = cudaMemcpyAsync(d, dd.p, db, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return finish(e, "elastic_distance_matrix_host");
 }
 
 }  // extern "C"

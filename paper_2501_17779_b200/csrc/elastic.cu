@@ -1,0 +1,652 @@
+// Elastic (SRV) matching on the GPU — the rigid path's caller in the
+// reference's elastic distance:
+//
+//   * dp_kernel        batched dp_reparam (proj/src/srv.cpp:180-257): the
+//                      monotone lattice path of least discretised SRV mismatch;
+//   * elastic_kernel   batched elastic_distance_approach2
+//                      (proj/src/elastic.cpp:102-174): rigid pre-alignment,
+//                      then alternating DP gamma-steps and FFT (t0, R)-steps
+//                      with the raw-pair SVD refit, each accepted only if the
+//                      realised energy does not increase.
+//
+// One 256-thread CTA per pair (a grid-stride loop over pairs). The DP walks
+// its rows in order (row i depends on rows i-1 .. i-W) with the cells of a row
+// spread over the threads; dp values live in a (W+1)-row ring in shared
+// memory, parent steps in shared memory (N <= 256) or a per-CTA global slab.
+//
+// Exactness. dp_step_cost, apply_srv_action, compose/rebase and the DP
+// recurrence are restated operation for operation with __dadd_rn/__dmul_rn
+// (no FMA contraction) and the reference's summation order, so dp_reparam is
+// bitwise the reference's for the same inputs. Inside approach 2 the rigid
+// alignments run on the FFT pair stage (rotation within ulps of the
+// reference's SVD) and cos/sin come from CUDA's libm (<= 2 ulp), so the
+// alternating search agrees with the reference to rounding, not bitwise.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "../../include/curvalign_cuda.h"
+#include "cva_common.cuh"
+#include "elastic.h"
+#include "pairfft.cuh"
+
+namespace cva {
+namespace el {
+
+constexpr int kT = 256;
+constexpr double kGridSnap = 1e-9;  // srv.cpp:14
+constexpr int kMaxSteps = 64;
+
+// ------------------------------------------------------------ exact arithmetic
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dvd(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double norm2(double2 p) { return add(mul(p.x, p.x), mul(p.y, p.y)); }
+
+// geometry.hpp:90-94
+__device__ __forceinline__ double wrap_unit(double t) {
+  double r = sub(t, floor(t));
+  if (r >= 1.0) r = sub(r, 1.0);
+  return r;
+}
+
+// srv.cpp:19-37 (periodic linear interpolation with grid snapping)
+__device__ __forceinline__ double2 interp_periodic(const double2* q, int n, double u) {
+  const double x = mul(u, (double)n);
+  double i0f = floor(x);
+  double frac = sub(x, i0f);
+  if (frac > 1.0 - kGridSnap) {
+    i0f = add(i0f, 1.0);
+    frac = 0.0;
+  } else if (frac < kGridSnap) {
+    frac = 0.0;
+  }
+  long long i0 = (long long)i0f % (long long)n;
+  if (i0 < 0) i0 += n;
+  if (frac == 0.0) return q[i0];
+  const long long i1 = (i0 + 1) % n;
+  const double2 a = q[i0], b = q[i1];
+  return make_double2(add(a.x, mul(frac, sub(b.x, a.x))), add(a.y, mul(frac, sub(b.y, a.y))));
+}
+
+// Rotation2::apply (geometry.hpp:70-73) with (c, s) = (cos, sin)(theta)
+__device__ __forceinline__ double2 rot_apply(double c, double s, double2 p) {
+  return make_double2(add(mul(c, p.x), mul(s, p.y)), add(mul(-s, p.x), mul(c, p.y)));
+}
+
+// apply_srv_action element l (srv.cpp:100-118)
+__device__ __forceinline__ double2 action_at(const double2* q, int n, double t0, double c, double s,
+                                             const double* g, int l) {
+  const double gdot = mul(sub(g[l + 1], g[l]), (double)n);
+  const double u = wrap_unit(add(t0, g[l]));
+  const double2 v = interp_periodic(q, n, u);
+  const double k = sqrt(fmax(gdot, 0.0));
+  const double2 r = rot_apply(c, s, v);
+  return make_double2(mul(r.x, k), mul(r.y, k));
+}
+
+// Sequential sum of x[0..n) by thread 0 (the reference's loop order), returned
+// to every thread. `cell`: one shared double.
+__device__ __forceinline__ double seq_sum(const double* x, int n, double* cell) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double e = 0.0;
+    for (int l = 0; l < n; ++l) e = add(e, x[l]);
+    *cell = e;
+  }
+  __syncthreads();
+  return *cell;
+}
+
+// elastic_energy (srv.cpp:120-128): terms computed in parallel into T, summed
+// in order, / n.
+__device__ double energy(const double2* q1, const double2* q2, int n, double t0, double theta,
+                         const double* g, double* T, double* cell) {
+  double s, c;
+  sincos(theta, &s, &c);
+  for (int l = threadIdx.x; l < n; l += kT) {
+    const double2 w = action_at(q2, n, t0, c, s, g, l);
+    T[l] = norm2(make_double2(sub(q1[l].x, w.x), sub(q1[l].y, w.y)));
+  }
+  return dvd(seq_sum(T, n, cell), (double)n);
+}
+
+// srv_transform (srv.cpp:71-88)
+__device__ void srv_transform(const double2* c, int n, double2* q) {
+  const double nn = (double)n;
+  const double eps = mul(1e-8, nn);
+  for (int l = threadIdx.x; l < n; l += kT) {
+    const double2 nx = c[l + 1 == n ? 0 : l + 1], pv = c[l == 0 ? n - 1 : l - 1];
+    const double h = dvd(nn, 2.0);
+    const double2 d = make_double2(mul(sub(nx.x, pv.x), h), mul(sub(nx.y, pv.y), h));
+    const double mag = sqrt(norm2(d));
+    if (mag < eps) {
+      q[l] = make_double2(0.0, 0.0);
+    } else {
+      const double r = dvd(1.0, sqrt(mag));
+      q[l] = make_double2(mul(d.x, r), mul(d.y, r));
+    }
+  }
+}
+
+// srv_center (srv.cpp:90-98): mean by the reference's sequential sum.
+__device__ void srv_center(const double2* q, int n, double2* out, double* cell2) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mx = 0.0, my = 0.0;
+    for (int l = 0; l < n; ++l) {
+      mx = add(mx, q[l].x);
+      my = add(my, q[l].y);
+    }
+    const double r = dvd(1.0, (double)n);
+    cell2[0] = mul(mx, r);
+    cell2[1] = mul(my, r);
+  }
+  __syncthreads();
+  const double mx = cell2[0], my = cell2[1];
+  for (int l = threadIdx.x; l < n; l += kT) out[l] = make_double2(sub(q[l].x, mx), sub(q[l].y, my));
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------- DP
+
+// Admissible steps (srv.cpp:130-139): (a, b) in 1..W, gcd 1, a-major order.
+struct Steps {
+  int count;
+  int a[kMaxSteps], b[kMaxSteps];
+};
+__host__ __device__ constexpr int gcd_i(int x, int y) { return y == 0 ? x : gcd_i(y, x % y); }
+__host__ __device__ constexpr Steps make_steps(int W) {
+  Steps s{};
+  s.count = 0;
+  for (int a = 1; a <= W; ++a)
+    for (int b = 1; b <= W; ++b)
+      if (gcd_i(a, b) == 1 && s.count < kMaxSteps) {
+        s.a[s.count] = a;
+        s.b[s.count] = b;
+        ++s.count;
+      }
+  return s;
+}
+
+// dp_step_cost (srv.cpp:145-176) with q1, q2 in shared memory.
+__device__ __forceinline__ double step_cost(const double2* q1, const double2* q2, int n, int i0, int j0,
+                                            int a, int b) {
+  const double slope = dvd((double)b, (double)a);
+  const double sq = sqrt(slope);
+  double cost = 0.0;
+  for (int k = 0; k <= a; ++k) {
+    int i = i0 + k;
+    if (i >= n) i -= n;
+    const int num = k * b;
+    double2 s;
+    if (num % a == 0) {
+      int jj = j0 + num / a;
+      jj %= n;
+      s = q2[jj];
+    } else {
+      const double pos = add((double)j0, dvd((double)num, (double)a));
+      const int base = (int)pos;
+      const double frac = sub(pos, (double)base);
+      const double2 u = q2[base % n];
+      const double2 v = q2[(base + 1) % n];
+      s = make_double2(add(u.x, mul(frac, sub(v.x, u.x))), add(u.y, mul(frac, sub(v.y, u.y))));
+    }
+    const double2 d = make_double2(sub(q1[i].x, mul(s.x, sq)), sub(q1[i].y, mul(s.y, sq)));
+    const double w = (k == 0 || k == a) ? 0.5 : 1.0;
+    cost = add(cost, mul(w, norm2(d)));
+  }
+  return dvd(cost, (double)n);
+}
+
+__device__ __forceinline__ int jmin_of(int i, int n, int W) {
+  const int lo1 = (i + W - 1) / W;
+  const int lo2 = n - W * (n - i);
+  return max(max(lo1, lo2), 0);
+}
+__device__ __forceinline__ int jmax_of(int i, int n, int W) {
+  const int hi1 = W * i;
+  const int hi2 = n - (n - i + W - 1) / W;
+  return min(min(hi1, hi2), n);
+}
+
+// dp_reparam (srv.cpp:180-257) on shared q1, q2 (n samples). ring: (W+1) x
+// (n+1) doubles; parent: (n+1)^2 bytes (shared or global); gamma: n+1.
+// Returns the path energy (thread-uniform); +inf if no admissible path.
+template <int kW>
+__device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wrt, double* ring,
+                             uint8_t* parent, double* gamma, double* cell) {
+  const int W = kW > 0 ? kW : Wrt;
+  const int stride = n + 1;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  auto row = [&](int i) { return ring + (size_t)(i % (W + 1)) * stride; };
+  for (int j = threadIdx.x; j <= n; j += kT) row(0)[j] = j == 0 ? 0.0 : inf;
+  __syncthreads();
+  for (int i = 1; i <= n; ++i) {
+    const int lo = jmin_of(i, n, W), hi = jmax_of(i, n, W);
+    double* cur = row(i);
+    for (int j = threadIdx.x; j <= n; j += kT) {
+      double best = inf;
+      uint8_t best_s = 0xff;
+      if (j >= lo && j <= hi) {
+        auto try_step = [&](int s, int a, int b) {
+          const int pi = i - a, pj = j - b;
+          if (pi < 0 || pj < 0) return;
+          const double base = row(pi)[pj];
+          if (base == inf) return;
+          const double cand = add(base, step_cost(q1, q2, n, pi, pj, a, b));
+          if (cand < best) {
+            best = cand;
+            best_s = (uint8_t)s;
+          }
+        };
+        if constexpr (kW > 0) {
+          constexpr Steps kS = make_steps(kW);
+#pragma unroll
+          for (int s = 0; s < kS.count; ++s) try_step(s, kS.a[s], kS.b[s]);
+        } else {
+          int s = 0;
+          for (int a = 1; a <= W; ++a)
+            for (int b = 1; b <= W; ++b)
+              if (gcd_i(a, b) == 1) try_step(s++, a, b);
+        }
+      }
+      cur[j] = best;
+      parent[(size_t)i * stride + j] = best_s;
+    }
+    __syncthreads();
+  }
+  const double e = row(n)[n];
+  // backtrack (thread 0): gamma on the lattice path (srv.cpp:235-255)
+  if (threadIdx.x == 0) {
+    const Steps st = make_steps(W);
+    int ok = e != inf;
+    if (ok) {
+      int i = n, j = n;
+      gamma[n] = 1.0;
+      while (i > 0) {
+        const uint8_t s = parent[(size_t)i * stride + j];
+        if (s == 0xff || s >= st.count) {
+          ok = 0;
+          break;
+        }
+        const int a = st.a[s], b = st.b[s];
+        const int pi = i - a, pj = j - b;
+        for (int k = 0; k < a; ++k) {
+          const double jj = add((double)pj, dvd((double)(k * b), (double)a));
+          gamma[pi + k] = dvd(jj, (double)n);
+        }
+        i = pi;
+        j = pj;
+      }
+      gamma[0] = 0.0;
+    }
+    *cell = ok ? e : inf;
+  }
+  __syncthreads();
+  const double r = *cell;
+  __syncthreads();
+  return r;
+}
+
+// Reparameterization::eval (srv.cpp:39-50)
+__device__ __forceinline__ double reparam_eval(const double* g, int n, double t) {
+  if (t <= 0.0) return g[0];
+  if (t >= 1.0) return g[n];
+  const double x = mul(t, (double)n);
+  const int i = min((int)x, n - 1);
+  const double frac = sub(x, (double)i);
+  return add(g[i], mul(frac, sub(g[i + 1], g[i])));
+}
+
+// compose_reparam(outer, inner) (elastic.cpp:21-33) -> out (n+1)
+__device__ void compose(const double* outer, const double* inner, int n, double* out) {
+  for (int l = threadIdx.x; l <= n; l += kT) out[l] = reparam_eval(outer, n, inner[l]);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out[0] = 0.0;
+    out[n] = 1.0;
+    for (int l = 1; l <= n; ++l) out[l] = fmax(out[l], out[l - 1]);
+  }
+  __syncthreads();
+}
+
+// rebase_reparam(gamma, m) (elastic.cpp:37-50) -> out (n+1)
+__device__ void rebase(const double* g, int n, int m, double* out) {
+  const double gm = g[m];
+  for (int l = threadIdx.x; l <= n; l += kT) {
+    const int lm = l + m;
+    out[l] = lm <= n ? sub(g[lm], gm) : sub(add(g[lm - n], 1.0), gm);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out[0] = 0.0;
+    out[n] = 1.0;
+  }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------- kernels
+
+struct Smem {
+  double2 *c1, *c2, *q1, *q2, *q1c, *w, *wc, *fft;
+  double *g, *gc, *gd, *T, *ring, *cell;
+  uint8_t* parent;
+  cva_alignment* rec;
+};
+
+__host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+// Layout shared by the host size query and the kernel.
+__host__ __device__ inline size_t smem_layout(int n, int W, bool parent_in_smem, char* base, Smem* S) {
+  const int M = pf::fft_len(n);
+  const size_t fft = 4 * sizeof(double2) * (size_t)pf::padded_len(M);
+  const size_t dp = align_up(sizeof(double) * (size_t)(W + 1) * (n + 1)) +
+                    (parent_in_smem ? align_up((size_t)(n + 1) * (n + 1)) : 0);
+  const size_t scratch = fft > dp ? fft : dp;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += align_up(bytes);
+    return base ? base + o : nullptr;
+  };
+  char* X = take(scratch);
+  char* q1 = take(sizeof(double2) * n);
+  char* q2 = take(sizeof(double2) * n);
+  char* q1c = take(sizeof(double2) * n);
+  char* w = take(sizeof(double2) * n);
+  char* wc = take(sizeof(double2) * n);
+  char* g = take(sizeof(double) * (n + 1));
+  char* gc = take(sizeof(double) * (n + 1));
+  char* gd = take(sizeof(double) * (n + 1));
+  char* T = take(sizeof(double) * n);
+  char* cell = take(sizeof(double) * 4);
+  char* rec = take(sizeof(cva_alignment));
+  if (S) {
+    S->c1 = (double2*)w;  // raw curves: only before the first iteration
+    S->c2 = (double2*)wc;
+    S->fft = (double2*)X;
+    S->ring = (double*)X;
+    S->parent = parent_in_smem ? (uint8_t*)(X + align_up(sizeof(double) * (size_t)(W + 1) * (n + 1))) : nullptr;
+    S->q1 = (double2*)q1;
+    S->q2 = (double2*)q2;
+    S->q1c = (double2*)q1c;
+    S->w = (double2*)w;
+    S->wc = (double2*)wc;
+    S->g = (double*)g;
+    S->gc = (double*)gc;
+    S->gd = (double*)gd;
+    S->T = (double*)T;
+    S->cell = (double*)cell;
+    S->rec = (cva_alignment*)rec;
+  }
+  return off;
+}
+
+__device__ __forceinline__ void load_curve(const double2* src, double2* dst, int n) {
+  for (int l = threadIdx.x; l < n; l += kT) dst[l] = src[l];
+}
+
+// Batched dp_reparam on SRV pairs (q1, q2: pairs x n).
+template <int kW>
+__global__ void __launch_bounds__(kT, 1)
+    dp_kernel(const double2* __restrict__ q1, const double2* __restrict__ q2, int64_t pairs, int n, int W,
+              int parent_in_smem, uint8_t* parent_slab, double* gamma, double* energy, int32_t* status) {
+  extern __shared__ __align__(16) char smem[];
+  Smem S;
+  smem_layout(n, W, parent_in_smem != 0, smem, &S);
+  uint8_t* parent = parent_in_smem ? S.parent : parent_slab + (size_t)blockIdx.x * (n + 1) * (n + 1);
+  for (int64_t p = blockIdx.x; p < pairs; p += gridDim.x) {
+    load_curve(q1 + p * n, S.q1, n);
+    load_curve(q2 + p * n, S.q2, n);
+    __syncthreads();
+    const double e = dp_reparam<kW>(S.q1, S.q2, n, W, S.ring, parent, S.gd, S.cell);
+    const bool ok = isfinite(e);
+    for (int l = threadIdx.x; l <= n; l += kT)
+      gamma[p * (n + 1) + l] = ok ? S.gd[l] : __longlong_as_double(0x7ff8000000000000LL);
+    if (threadIdx.x == 0) {
+      energy[p] = ok ? e : __longlong_as_double(0x7ff8000000000000LL);
+      if (status) status[p] = ok ? CVA_OK : CVA_RUNTIME_ERROR;  // srv.cpp:233
+    }
+    __syncthreads();
+  }
+}
+
+// align_fft(a, b) on shared curves via the pair stage; result in S.rec.
+template <int kN>
+__device__ __forceinline__ cva_alignment align(const double2* a, const double2* b, int n, const Smem& S,
+                                              const double2* tw, double2* red) {
+  pf::PairIn in{a, b, make_double2(0, 0), make_double2(0, 0), 1.0, 1.0};
+  __syncthreads();
+  pf::pair_stage<false, kN>(in, S.fft, n, tw, S.rec, nullptr, red);
+  __syncthreads();
+  const cva_alignment r = *S.rec;
+  __syncthreads();
+  return r;
+}
+
+// elastic_distance_approach2 per pair. Pair p matches c2 onto c1 where
+// matrix_k == 0: c1 = A + p n, c2 = B + p n; else (distance matrix of
+// matrix_k curves A): c1 = A + (p / k) n, c2 = A + (p % k) n.
+template <int kN, int kW>
+__global__ void __launch_bounds__(kT, 1)
+    elastic_kernel(const double2* __restrict__ A, const double2* __restrict__ B, int64_t pairs, int64_t matrix_k,
+                   int n_rt, ElasticParams prm, int parent_in_smem, uint8_t* parent_slab, const double2* tw,
+                   ElasticOut out) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double2 red[16];
+  const int n = kN > 0 ? kN : n_rt;
+  const int W = kW > 0 ? kW : prm.max_slope;
+  Smem S;
+  smem_layout(n, W, parent_in_smem != 0, smem, &S);
+  uint8_t* parent = parent_in_smem ? S.parent : parent_slab + (size_t)blockIdx.x * (n + 1) * (n + 1);
+  const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+  for (int64_t p = blockIdx.x; p < pairs; p += gridDim.x) {
+    const double2* c1 = matrix_k ? A + (p / matrix_k) * n : A + p * n;
+    const double2* c2 = matrix_k ? A + (p % matrix_k) * n : B + p * n;
+    load_curve(c1, S.c1, n);
+    load_curve(c2, S.c2, n);
+    __syncthreads();
+    // finite input (validate_curve, curve.cpp:11-14)
+    int bad = 0;
+    for (int l = threadIdx.x; l < n; l += kT)
+      bad |= !(isfinite(S.c1[l].x) && isfinite(S.c1[l].y) && isfinite(S.c2[l].x) && isfinite(S.c2[l].y));
+    bad = __syncthreads_or(bad);
+    int status = CVA_OK;
+    double t0 = 0.0, theta = 0.0, en = qnan;
+    int iters = 0, conv = 0;
+    if (bad) {
+      status = CVA_INVALID_ARGUMENT;
+    } else {
+      srv_transform(S.c1, n, S.q1);
+      srv_transform(S.c2, n, S.q2);
+      __syncthreads();
+      srv_center(S.q1, n, S.q1c, S.cell);
+      // rigid pre-alignment of the curves themselves (elastic.cpp:114-117)
+      const cva_alignment pre = align<kN>(S.c1, S.c2, n, S, tw, red);
+      if (pre.status != CVA_OK) {
+        status = CVA_INVALID_ARGUMENT;
+      } else {
+        t0 = pre.t0;
+        theta = pre.theta;
+        for (int l = threadIdx.x; l <= n; l += kT) S.g[l] = l == n ? 1.0 : dvd((double)l, (double)n);
+        __syncthreads();
+        en = energy(S.q1, S.q2, n, t0, theta, S.g, S.T, S.cell);
+        for (int iter = 1; iter <= prm.max_iters; ++iter) {
+          const double prev = en;
+          {  // gamma-step (elastic.cpp:124-133)
+            double s, c;
+            sincos(theta, &s, &c);
+            for (int l = threadIdx.x; l < n; l += kT) S.w[l] = action_at(S.q2, n, t0, c, s, S.g, l);
+            __syncthreads();
+            const double de = dp_reparam<kW>(S.q1, S.w, n, W, S.ring, parent, S.gd, S.cell);
+            if (!isfinite(de)) {
+              status = CVA_RUNTIME_ERROR;  // srv.cpp:233
+              break;
+            }
+            compose(S.g, S.gd, n, S.gc);
+            const double e = energy(S.q1, S.q2, n, t0, theta, S.gc, S.T, S.cell);
+            if (e <= en) {
+              for (int l = threadIdx.x; l <= n; l += kT) S.g[l] = S.gc[l];
+              en = e;
+            }
+            __syncthreads();
+          }
+          {  // (t0, R)-step (elastic.cpp:135-158)
+            for (int l = threadIdx.x; l < n; l += kT) S.w[l] = action_at(S.q2, n, t0, 1.0, 0.0, S.g, l);
+            __syncthreads();
+            srv_center(S.w, n, S.wc, S.cell);
+            const cva_alignment ra = align<kN>(S.q1c, S.wc, n, S, tw, red);
+            if (ra.status != CVA_OK) {
+              status = CVA_INVALID_ARGUMENT;
+              break;
+            }
+            const int m = (int)ra.shift;
+            const double t0c = wrap_unit(add(t0, S.g[m]));
+            rebase(S.g, n, m, S.gc);
+            // raw-pair refit: optimal_rotation_svd(cross_correlation_matrix(q1, w, m))
+            if (threadIdx.x == 0) {
+              double a11 = 0.0, a12 = 0.0, a21 = 0.0, a22 = 0.0;
+              for (int l = 0; l < n; ++l) {
+                const double2 pq = S.q1[l];
+                int lm = l + m;
+                if (lm >= n) lm -= n;
+                const double2 qq = S.w[lm];
+                a11 = add(a11, mul(pq.x, qq.x));
+                a12 = add(a12, mul(pq.x, qq.y));
+                a21 = add(a21, mul(pq.y, qq.x));
+                a22 = add(a22, mul(pq.y, qq.y));
+              }
+              const bool finite = isfinite(a11) && isfinite(a12) && isfinite(a21) && isfinite(a22);
+              const bool zero = a11 == 0.0 && a12 == 0.0 && a21 == 0.0 && a22 == 0.0;
+              S.cell[2] = !finite ? qnan : (zero ? 0.0 : atan2(sub(a12, a21), add(a11, a22)));
+            }
+            __syncthreads();
+            const double th_raw = S.cell[2];
+            __syncthreads();
+            if (!isfinite(th_raw)) {
+              status = CVA_INVALID_ARGUMENT;  // rigid_align.cpp:83
+              break;
+            }
+            const double e_c = energy(S.q1, S.q2, n, t0c, ra.theta, S.gc, S.T, S.cell);
+            const double e_r = energy(S.q1, S.q2, n, t0c, th_raw, S.gc, S.T, S.cell);
+            const double r_cand = e_r <= e_c ? th_raw : ra.theta;
+            const double e = fmin(e_r, e_c);
+            if (e <= en) {
+              t0 = t0c;
+              theta = r_cand;
+              for (int l = threadIdx.x; l <= n; l += kT) S.g[l] = S.gc[l];
+              en = e;
+            }
+            __syncthreads();
+          }
+          iters = iter;
+          if (prev - en < prm.energy_tol) {
+            conv = 1;
+            break;
+          }
+        }
+      }
+    }
+    const bool ok = status == CVA_OK;
+    if (out.gamma)
+      for (int l = threadIdx.x; l <= n; l += kT) out.gamma[p * (n + 1) + l] = ok ? S.g[l] : qnan;
+    if (threadIdx.x == 0) {
+      out.distance[p] = ok ? sqrt(fmax(en, 0.0)) : qnan;  // elastic.cpp:19
+      out.energy[p] = ok ? en : qnan;
+      out.t0[p] = ok ? t0 : qnan;
+      out.theta[p] = ok ? theta : qnan;
+      out.iterations[p] = iters;
+      out.converged[p] = conv;
+      out.status[p] = status;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace el
+
+// ------------------------------------------------------------- launchers
+
+namespace {
+constexpr size_t kMaxSmem = 227 * 1024;
+
+bool parent_fits(int n, int W) {
+  return el::smem_layout(n, W, true, nullptr, nullptr) <= 110 * 1024;  // keep 2 CTAs/SM
+}
+
+int resident(const void* fn, size_t smem) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, el::kT, smem) != cudaSuccess || per < 1) per = 1;
+  return sms * per;
+}
+}  // namespace
+
+size_t elastic_smem(int n, int W) { return el::smem_layout(n, W, parent_fits(n, W), nullptr, nullptr); }
+bool elastic_supported(int n, int W) {
+  return n >= 8 && W >= 1 && W <= 8 && pf::fft_len(n) <= 1024 &&
+         el::smem_layout(n, W, false, nullptr, nullptr) <= kMaxSmem;
+}
+
+size_t elastic_parent_slab(int64_t pairs, int n, int W) {
+  if (parent_fits(n, W)) return 0;
+  return (size_t)(n + 1) * (n + 1);  // per CTA; the launcher multiplies by the grid
+}
+
+template <int kW>
+static cudaError_t launch_dp_w(const double2* q1, const double2* q2, int64_t pairs, int n, int W, uint8_t* slab,
+                               int grid, double* gamma, double* energy, int32_t* status, cudaStream_t s) {
+  const bool ps = parent_fits(n, W);
+  const size_t sm = el::smem_layout(n, W, ps, nullptr, nullptr);
+  const void* fn = (const void*)el::dp_kernel<kW>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  el::dp_kernel<kW><<<grid, el::kT, sm, s>>>(q1, q2, pairs, n, W, ps ? 1 : 0, slab, gamma, energy, status);
+  return cudaGetLastError();
+}
+
+int elastic_grid(int64_t pairs, int n, int W) {
+  const bool ps = parent_fits(n, W);
+  const size_t sm = el::smem_layout(n, W, ps, nullptr, nullptr);
+  const int r = resident((const void*)el::dp_kernel<4>, sm);
+  return (int)(pairs < r ? pairs : r);
+}
+
+cudaError_t launch_dp_reparam(const double2* q1, const double2* q2, int64_t pairs, int n, int W, uint8_t* slab,
+                              int grid, double* gamma, double* energy, int32_t* status, cudaStream_t s) {
+  if (W == 4) return launch_dp_w<4>(q1, q2, pairs, n, W, slab, grid, gamma, energy, status, s);
+  return launch_dp_w<0>(q1, q2, pairs, n, W, slab, grid, gamma, energy, status, s);
+}
+
+template <int kN, int kW>
+static cudaError_t launch_el(const double2* A, const double2* B, int64_t pairs, int64_t k, int n,
+                             const ElasticParams& prm, uint8_t* slab, int grid, const double2* tw,
+                             const ElasticOut& out, cudaStream_t s) {
+  const bool ps = parent_fits(n, prm.max_slope);
+  const size_t sm = el::smem_layout(n, prm.max_slope, ps, nullptr, nullptr);
+  const void* fn = (const void*)el::elastic_kernel<kN, kW>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  el::elastic_kernel<kN, kW><<<grid, el::kT, sm, s>>>(A, B, pairs, k, n, prm, ps ? 1 : 0, slab, tw, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_elastic_approach2(const double2* A, const double2* B, int64_t pairs, int64_t matrix_k, int n,
+                                     const ElasticParams& prm, uint8_t* slab, int grid, const double2* tw,
+                                     const ElasticOut& out, cudaStream_t s) {
+  if (prm.max_slope == 4) {
+    switch (n) {
+      case 64: return launch_el<64, 4>(A, B, pairs, matrix_k, n, prm, slab, grid, tw, out, s);
+      case 128: return launch_el<128, 4>(A, B, pairs, matrix_k, n, prm, slab, grid, tw, out, s);
+      case 256: return launch_el<256, 4>(A, B, pairs, matrix_k, n, prm, slab, grid, tw, out, s);
+      case 512: return launch_el<512, 4>(A, B, pairs, matrix_k, n, prm, slab, grid, tw, out, s);
+      default: return launch_el<0, 4>(A, B, pairs, matrix_k, n, prm, slab, grid, tw, out, s);
+    }
+  }
+  return launch_el<0, 0>(A, B, pairs, matrix_k, n, prm, slab, grid, tw, out, s);
+}
+
+}  // namespace cva

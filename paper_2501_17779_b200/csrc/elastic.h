@@ -1,0 +1,40 @@
+// Host-side declarations of the elastic (SRV) matching launchers (elastic.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace cva {
+
+struct ElasticParams {
+  int max_iters;      // ElasticOptions::max_iters (proj/include/curvalign/elastic.hpp:14)
+  double energy_tol;  // ElasticOptions::energy_tol
+  int max_slope;      // ElasticOptions::max_slope (DP step bound W)
+};
+
+struct ElasticOut {
+  double* distance;
+  double* energy;
+  double* t0;
+  double* theta;
+  double* gamma;  // nullable: pairs x (n + 1)
+  int32_t* iterations;
+  int32_t* converged;
+  int32_t* status;
+};
+
+bool elastic_supported(int n, int W);
+size_t elastic_smem(int n, int W);
+// Bytes of per-CTA parent scratch in global memory (0: parents fit in shared memory).
+size_t elastic_parent_slab(int64_t pairs, int n, int W);
+int elastic_grid(int64_t pairs, int n, int W);
+
+cudaError_t launch_dp_reparam(const double2* q1, const double2* q2, int64_t pairs, int n, int W,
+                              uint8_t* slab, int grid, double* gamma, double* energy, int32_t* status,
+                              cudaStream_t s);
+cudaError_t launch_elastic_approach2(const double2* A, const double2* B, int64_t pairs, int64_t matrix_k, int n,
+                                     const ElasticParams& prm, uint8_t* slab, int grid, const double2* tw,
+                                     const ElasticOut& out, cudaStream_t s);
+
+}  // namespace cva
