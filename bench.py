@@ -38,6 +38,9 @@ sys.path.insert(0, ROOT)
 METRIC = "aligned curve pairs/sec (fp64, N=1024)"
 UNIT = "pairs/s"
 WORKLOAD = "C1: 4096 pairs/GPU, raw n_in~U{300..3000} jittered arc length, noise 1e-3 -> N=1024, fp64"
+E1_METRIC = "elastic distance pairs/sec (approach 2, fp64, N=256)"
+E1_WORKLOAD = ("E1: distance_matrix(approach2) of 64 curves (raw n_in~U{300..3000}) preprocessed to N=256: "
+               "4096 ordered pairs, max_iters 30, energy_tol 1e-6, max_slope 4")
 
 
 def parse():
@@ -46,8 +49,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c4"],
-                    help="c1 is the headline (BASELINE metric); c2/c4 are secondary workloads")
+    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c4", "e1"],
+                    help="c1 is the headline (BASELINE metric); c2/c3/c4 are secondary workloads; "
+                         "e1 is the elastic distance matrix (SURVEY.md 8(f))")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -153,9 +157,54 @@ def algorithmic_bytes(offs, pairs, N):
     return raw + 8 * (2 * pairs + 1) + 16 * N * pairs + 48 * pairs
 
 
+def run_reference_arm_e1(args):
+    """The reference's elastic_distance_approach2 (oracle/_ref) on all host
+    threads over a bounded sample of E1's ordered pairs per step."""
+    import paper_2501_17779_b200 as cva
+    from paper_2501_17779_b200 import synth
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Reference
+
+    cfg = synth.CONFIGS["e1"]
+    M, N = cfg["curves"], cfg["N"]
+    pts, offs = synth.ragged_curves(args.seed, M)
+    R = Reference()
+    prep = np.stack([R.preprocess(pts[offs[c]:offs[c + 1]], N, True) for c in range(M)])
+    threads = os.cpu_count() or 1
+    sample = max(32, threads * 2)
+    times, done = [], 0
+    for it in range(args.warmup + args.steps):
+        cells = (np.arange(sample) + it * sample) % (M * M)
+        c1, c2 = prep[cells // M], prep[cells % M]
+        t0 = time.perf_counter()
+        R.elastic_approach2_batch(c1, c2, threads=threads)
+        dt = time.perf_counter() - t0
+        if it >= args.warmup:
+            times.append(dt)
+            done += sample
+    total = sum(times)
+    value = done / total
+    line = {
+        "impl": "reference", "metric": E1_METRIC, "value": value, "unit": UNIT, "n_gpus": dist_env()[1],
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded C2 generator)",
+        "config": {"workload": E1_WORKLOAD, "pairs_per_step": sample, "N": N},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{sample} E1 ordered pairs per step, reference elastic.cpp/srv.cpp sources"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    del cva
+    print(json.dumps(line), flush=True)
+
+
 def run_reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
+        return
+    if args.config == "e1":
+        run_reference_arm_e1(args)
         return
     from paper_2501_17779_b200 import synth
 
@@ -250,6 +299,23 @@ def run_secondary(args):
         workload = f"C3: {P} pairs/GPU, N={N}, center+normalize+align_fft+aligned curve (L2-chunked multi-pass FFT)"
         bytes_unit = 16 * 2 * N + 16 * N + 48
         bound = "hbm"
+    elif args.config == "e1":
+        cfg = synth.CONFIGS["e1"]
+        M, N = cfg["curves"], cfg["N"]
+        pts, offs = synth.ragged_curves(args.seed, M)
+        dp, do = torch.from_numpy(pts).to(dev), torch.from_numpy(offs).to(dev)
+        mx = int(np.diff(offs).max())
+        prep = torch.empty((M, N, 2), dtype=torch.float64, device=dev)
+        d = torch.empty((M, M), dtype=torch.float64, device=dev)
+
+        def step():
+            _native.check(lib.cva_preprocess_batch(dp.data_ptr(), do.data_ptr(), M, mx, N, 1, prep.data_ptr(), 0,
+                                                   stream.cuda_stream))
+            _native.check(lib.cva_elastic_distance_matrix(prep.data_ptr(), M, N, 30, 1e-6, 4, d.data_ptr(),
+                                                          stream.cuda_stream))
+        units = M * M  # every rank computes the whole matrix (weak scaling: replicas)
+        workload = E1_WORKLOAD
+        bound = "none"
     else:
         cfg = synth.CONFIGS["c4"]
         P, N = cfg["pairs"], cfg["N"]
@@ -285,7 +351,9 @@ def run_secondary(args):
     total_units = units * world
     value = total_units / (ms_step * 1e-3)
     launch_s = (ms / args.steps) * 1e-3
-    if bound == "fp64":
+    if bound == "none":
+        roof = None
+    elif bound == "fp64":
         ach = units * flops_unit / launch_s / 1e12
         roof = {"bound": "fp64", "achieved": ach, "peak": fp64, "unit": "TFLOP/s", "frac": ach / fp64 if fp64 else None,
                 "traffic": None, "peak_source": "measured here (cva_probe_fp64_tflops)",
@@ -297,12 +365,14 @@ def run_secondary(args):
                 "traffic": None, "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"}
     if rank == 0:
         print(json.dumps({
-            "metric": f"aligned curve pairs/sec (fp64, {args.config})", "value": value, "unit": UNIT,
+            "metric": E1_METRIC if args.config == "e1" else f"aligned curve pairs/sec (fp64, {args.config})",
+            "value": value, "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong" if args.config == "c2" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, csrc/synth.cpp)",
             "config": {"workload": workload}, "roofline": roof, "cpu_baseline": None, "e2e": None,
-            "gpu_launches": args.steps * (2 if args.config == "c2" else 1), "clocks": clk.summary()}), flush=True)
+            "gpu_launches": args.steps * (2 if args.config in ("c2", "e1") else 1), "clocks": clk.summary()}),
+              flush=True)
     if world > 1:
         dist.destroy_process_group()
 

@@ -19,6 +19,9 @@ CONFIGS = {
     "c2": dict(curves=2048, N=512, modes=16, amp=0.3, amp_exp=1.0, n_min=300, n_max=3000),
     "c3": dict(pairs=256, N=65536, modes=64, amp=0.3, amp_exp=1.5, sigma=1e-4),
     "c4": dict(pairs=8192, N=2048, modes=16, amp=0.3, amp_exp=1.0),
+    # elastic distance matrix (approach 2): all ordered pairs of
+    # `curves` C2-generator curves preprocessed to N (distance_matrix(curves, approach2, N))
+    "e1": dict(curves=64, N=256, modes=16, amp=0.3, amp_exp=1.0, n_min=300, n_max=3000),
 }
 
 
