@@ -76,6 +76,25 @@ int or_circular_cross_correlation(const double* a, const double* b, int64_t n, d
 int or_srv_transform(const double* xy, int64_t n, double* q);
 int or_srv_center(const double* q, int64_t n, double* out);
 
+/* elastic (SRV) matching (oracle/elastic_oracle.c; proj/src/srv.cpp:100-257,
+ * proj/src/elastic.cpp:21-174). gamma arrays hold n+1 values. */
+typedef struct or_elastic_match {
+  double t0, theta, energy, distance;
+  int32_t iterations, converged;
+  double* gamma; /* nullable: n+1 values */
+} or_elastic_match;
+double or_wrap_unit(double t);
+int or_apply_srv_action(const double* q, int64_t n, double t0, double theta, const double* gamma,
+                        double* out);
+int or_elastic_energy(const double* q1, const double* q2, int64_t n, double t0, double theta,
+                      const double* gamma, double* out);
+int or_dp_step_cost(const double* q1, const double* q2, int64_t n, int i0, int j0, int di, int dj,
+                    double* out);
+int or_dp_reparam(const double* q1, const double* q2, int64_t n, int max_slope, double* gamma,
+                  double* energy);
+int or_elastic_approach2(const double* c1, const double* c2, int64_t n, int max_iters, double energy_tol,
+                         int use_fft, int max_slope, or_elastic_match* out);
+
 /* Batched drivers over a ragged point array: pair p aligns curve 2p against
  * curve 2p+1, curve c = points [offsets[c], offsets[c+1]).
  *   mode 0: preprocess(raw, n_out, resample) both curves, then align_fft

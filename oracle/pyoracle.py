@@ -182,13 +182,79 @@ class _Base:
         return res, al
 
 
-class Oracle(_Base):
-    """The plain-C restatement (oracle/curvalign_oracle.c)."""
+class _ElasticShared:
+    """apply_srv_action / elastic_energy / dp_step_cost: same C signature in both libraries."""
+
+    def apply_srv_action(self, q, t0, theta, gamma):
+        a, g = _f64(q), _f64(gamma)
+        out = np.zeros_like(a)
+        f = self._fn("apply_srv_action", [c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p])
+        _raise(f(_p(a), a.shape[0], t0, theta, _p(g), _p(out)), "apply_srv_action")
+        return out
+
+    def elastic_energy(self, q1, q2, t0, theta, gamma):
+        a, b, g = _f64(q1), _f64(q2), _f64(gamma)
+        out = np.zeros(1)
+        f = self._fn("elastic_energy", [c_void_p, c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p])
+        _raise(f(_p(a), _p(b), a.shape[0], t0, theta, _p(g), _p(out)), "elastic_energy")
+        return float(out[0])
+
+    def dp_step_cost(self, q1, q2, i0, j0, di, dj):
+        a, b = _f64(q1), _f64(q2)
+        out = np.zeros(1)
+        f = self._fn("dp_step_cost", [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int, c_void_p])
+        _raise(f(_p(a), _p(b), a.shape[0], i0, j0, di, dj, _p(out)), "dp_step_cost")
+        return float(out[0])
+
+
+
+class _OrElasticMatch(ctypes.Structure):
+    _fields_ = [("t0", c_double), ("theta", c_double), ("energy", c_double), ("distance", c_double),
+                ("iterations", c_int32), ("converged", c_int32), ("gamma", c_void_p)]
+
+
+class Oracle(_ElasticShared, _Base):
+    """The plain-C restatement (oracle/curvalign_oracle.c, oracle/elastic_oracle.c)."""
 
     prefix = "or_"
 
     def __init__(self, path=ORACLE_PATH):
         super().__init__(path)
+
+    def dp_reparam_batch(self, q1, q2, max_slope=4, threads=1):
+        a, b = _f64(q1), _f64(q2)
+        pairs, n = a.shape[0], a.shape[1]
+        g = np.zeros((pairs, n + 1))
+        e = np.zeros(pairs)
+        st = np.zeros(pairs, dtype=np.int32)
+        f = self._fn("dp_reparam", [c_void_p, c_void_p, c_int64, c_int, c_void_p, c_void_p])
+        for p in range(pairs):
+            ep = np.zeros(1)
+            st[p] = f(_p(a[p]), _p(b[p]), n, max_slope, _p(g[p]), _p(ep))
+            e[p] = ep[0] if st[p] == 0 else np.nan
+        return g, e, st
+
+    def elastic_approach2_batch(self, c1, c2, max_iters=30, energy_tol=1e-6, use_fft=True, max_slope=4,
+                                threads=1, gamma=False):
+        a, b = _f64(c1), _f64(c2)
+        pairs, n = a.shape[0], a.shape[1]
+        out = {k: np.full(pairs, np.nan) for k in ("distance", "energy", "t0", "theta")}
+        out.update(iterations=np.zeros(pairs, dtype=np.int32), converged=np.zeros(pairs, dtype=np.int32),
+                   status=np.zeros(pairs, dtype=np.int32))
+        g = np.zeros((pairs, n + 1))
+        f = self._fn("elastic_approach2", [c_void_p, c_void_p, c_int64, c_int, c_double, c_int, c_int,
+                                           ctypes.POINTER(_OrElasticMatch)])
+        for p in range(pairs):
+            m = _OrElasticMatch(gamma=g[p].ctypes.data)
+            rc = f(_p(a[p]), _p(b[p]), n, max_iters, energy_tol, 1 if use_fft else 0, max_slope, ctypes.byref(m))
+            out["status"][p] = rc
+            if rc == 0:
+                for k in ("distance", "energy", "t0", "theta"):
+                    out[k][p] = getattr(m, k)
+                out["iterations"][p], out["converged"][p] = m.iterations, m.converged
+        if gamma:
+            out["gamma"] = g
+        return out
 
     def spline(self, x, y, xq):
         """Second derivatives + evaluation of the periodic spline at xq."""
@@ -225,7 +291,7 @@ class Oracle(_Base):
         return out
 
 
-class Reference(_Base):
+class Reference(_ElasticShared, _Base):
     """The reference's own code compiled in place (oracle/_ref)."""
 
     prefix = "ref_"
@@ -287,28 +353,6 @@ class Reference(_Base):
         _raise(f(_p(c), m, n, row_begin, row_end, threads, _p(e), _p(k), _p(th)), "allpairs")
         return e, k, th
 
-
-    # ---- elastic (SRV) matching: proj/src/srv.cpp, proj/src/elastic.cpp ----
-    def apply_srv_action(self, q, t0, theta, gamma):
-        a, g = _f64(q), _f64(gamma)
-        out = np.zeros_like(a)
-        f = self._fn("apply_srv_action", [c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p])
-        _raise(f(_p(a), a.shape[0], t0, theta, _p(g), _p(out)), "apply_srv_action")
-        return out
-
-    def elastic_energy(self, q1, q2, t0, theta, gamma):
-        a, b, g = _f64(q1), _f64(q2), _f64(gamma)
-        out = np.zeros(1)
-        f = self._fn("elastic_energy", [c_void_p, c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p])
-        _raise(f(_p(a), _p(b), a.shape[0], t0, theta, _p(g), _p(out)), "elastic_energy")
-        return float(out[0])
-
-    def dp_step_cost(self, q1, q2, i0, j0, di, dj):
-        a, b = _f64(q1), _f64(q2)
-        out = np.zeros(1)
-        f = self._fn("dp_step_cost", [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int, c_void_p])
-        _raise(f(_p(a), _p(b), a.shape[0], i0, j0, di, dj, _p(out)), "dp_step_cost")
-        return float(out[0])
 
     def dp_reparam_batch(self, q1, q2, max_slope=4, threads=1):
         a, b = _f64(q1), _f64(q2)

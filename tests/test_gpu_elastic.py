@@ -188,3 +188,20 @@ def test_elastic_errors(cuda, reference):  # test_elastic.cpp:103-111
     bad[3, 0] = np.nan
     r = cva.elastic_approach2_batch(np.stack([a, bad]), np.stack([a, a]))
     assert r["status"][0] == 0 and r["status"][1] != 0 and np.isnan(r["distance"][1])
+
+
+def test_golden_fixtures(cuda):
+    """The committed reference outputs (tests/golden/elastic_kat.npz) on the GPU:
+    DP bitwise, approach 2 and distance_matrix within the rule above."""
+    import os
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "elastic_kat.npz"))
+    for n in (16, 48):
+        gam, e, st = cva.dp_reparam_batch(g[f"dp{n}_q1"], g[f"dp{n}_q2"])
+        np.testing.assert_array_equal(gam, g[f"dp{n}_gamma"])
+        np.testing.assert_array_equal(e, g[f"dp{n}_energy"])
+    r = cva.elastic_approach2_batch(g["a2_c1"], g["a2_c2"], return_gamma=True)
+    np.testing.assert_allclose(r["distance"], g["a2_distance"], rtol=DIST_RTOL, atol=1e-12)
+    np.testing.assert_array_equal(r["iterations"], g["a2_iterations"])
+    d = cva.distance_matrix(list(g["dm_raw"]), 64)
+    np.testing.assert_allclose(d, g["dm_d"], rtol=DIST_RTOL, atol=1e-12)

@@ -162,5 +162,57 @@ def main():
         print(f, os.path.getsize(os.path.join(OUT, f)))
 
 
+FAMILIES = ["circle", "superellipse", "hippopede", "bumps", "limacon", "clover", "fourier_random"]
+
+
+def elastic():
+    """tests/golden/elastic_kat.npz: the reference's dp_reparam, apply_srv_action,
+    elastic_energy, elastic_distance_approach2 and distance_matrix on seeded
+    inputs (restating proj/tests/test_srv.cpp:130-230, test_elastic.cpp:35-150 and
+    acceptance.cpp:296-330, :455-530 cases at small sizes)."""
+    R = Reference()
+
+    def prep(fam, n, seed):
+        return R.preprocess(R.gen_curve(fam, 512, seed=seed), n, True)
+
+    el = {}
+    # dp_reparam on SRV pairs (n = 16 as in acceptance.cpp:296-330, 48 as in :483-497)
+    for n in (16, 48):
+        q1 = np.stack([R.srv_transform(prep("fourier_random", n, s)) for s in range(1, 6)])
+        q2 = np.stack([R.srv_transform(prep("fourier_random", n, s + 100)) for s in range(1, 6)])
+        g, e, st = R.dp_reparam_batch(q1, q2)
+        el[f"dp{n}_q1"], el[f"dp{n}_q2"], el[f"dp{n}_gamma"], el[f"dp{n}_energy"] = q1, q2, g, e
+    q1, q2 = el["dp48_q1"][0], el["dp48_q2"][0]
+    for w in (1, 2, 3, 5):
+        g, e, st = R.dp_reparam_batch(q1[None], q2[None], max_slope=w)
+        el[f"dp48_w{w}_gamma"], el[f"dp48_w{w}_energy"] = g[0], e[0]
+    # apply_srv_action / elastic_energy with a warp (acceptance.cpp:499-512, test_srv.cpp:150-170)
+    q = R.srv_transform(prep("bumps", 64, 3))
+    gam = el["dp48_gamma"][0]
+    g64 = np.interp(np.arange(65) / 64, np.arange(49) / 48, gam)
+    g64[0], g64[-1] = 0.0, 1.0
+    el["act_q"], el["act_gamma"] = q, g64
+    el["act_out"] = R.apply_srv_action(q, 0.37, 1.1, g64)
+    el["act_out_identity"] = R.apply_srv_action(q, 0.0, 0.0, np.arange(65) / 64)
+    q2b = R.srv_transform(prep("limacon", 64, 4))
+    el["act_q2"], el["act_energy"] = q2b, np.array([R.elastic_energy(q, q2b, 0.37, 1.1, g64)])
+    # approach 2 on preprocessed pairs
+    c1 = np.stack([prep(FAMILIES[k % 7], 64, k + 1) for k in range(7)])
+    c2 = np.stack([prep(FAMILIES[(k + 3) % 7], 64, k + 51) for k in range(7)])
+    r = R.elastic_approach2_batch(c1, c2, gamma=True)
+    el["a2_c1"], el["a2_c2"] = c1, c2
+    for k in ("distance", "energy", "t0", "theta", "iterations", "converged", "gamma"):
+        el[f"a2_{k}"] = r[k]
+    # distance_matrix(approach2) of 4 raw curves at n = 64 (test_elastic.cpp:113-135)
+    raw = np.stack([R.gen_curve(FAMILIES[k], 400, seed=k + 1) for k in range(4)])
+    el["dm_raw"], el["dm_d"] = raw, R.distance_matrix_approach2(raw, 64, threads=4)
+    np.savez_compressed(os.path.join(OUT, "elastic_kat.npz"), **el)
+    print("elastic_kat.npz", os.path.getsize(os.path.join(OUT, "elastic_kat.npz")))
+
+
 if __name__ == "__main__":
-    main()
+    if "--only" in sys.argv and sys.argv[sys.argv.index("--only") + 1] == "elastic":
+        elastic()
+    else:
+        main()
+        elastic()
