@@ -311,7 +311,7 @@ def run_secondary(args):
         def step():
             _native.check(lib.cva_preprocess_batch(dp.data_ptr(), do.data_ptr(), M, mx, N, 1, prep.data_ptr(), 0,
                                                    stream.cuda_stream))
-            _native.check(lib.cva_elastic_distance_matrix(prep.data_ptr(), M, N, 30, 1e-6, 4, d.data_ptr(),
+            _native.check(lib.cva_elastic_distance_matrix(prep.data_ptr(), M, N, 2, 30, 1e-6, 4, 512, d.data_ptr(),
                                                           stream.cuda_stream))
         units = M * M  # every rank computes the whole matrix (weak scaling: replicas)
         workload = E1_WORKLOAD

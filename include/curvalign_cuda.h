@@ -218,13 +218,39 @@ int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t
                                      double* energy, double* t0, double* theta, double* gamma,
                                      int32_t* iterations, int32_t* converged, int32_t* status);
 
-/* distance_matrix(curves, approach2, n) cells (elastic.cpp:176-236) for `count`
+/* elastic_distance_approach1(c1[p], c2[p], opts) (elastic.cpp:62-100): for every
+ * start shift m, the Kabsch rotation of the SRV pair, one DP, the realised
+ * energy; the first m with the smallest energy wins. n <= n_max_approach1
+ * (ElasticOptions::n_max_approach1, default 512) else CVA_INVALID_ARGUMENT.
+ * Outputs as cva_elastic_approach2_batch (iterations = converged = 1). */
+int cva_elastic_approach1_batch(const double* c1, const double* c2, int64_t pairs, int64_t n, int max_slope,
+                                int64_t n_max_approach1, double* distance, double* energy, double* t0,
+                                double* theta, double* gamma, int32_t* iterations, int32_t* converged,
+                                int32_t* status, void* stream);
+int cva_elastic_approach1_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                     int max_slope, int64_t n_max_approach1, double* distance, double* energy,
+                                     double* t0, double* theta, double* gamma, int32_t* iterations,
+                                     int32_t* converged, int32_t* status);
+
+/* distance_matrix(curves, method, n) cells (elastic.cpp:176-236) for `count`
  * preprocessed curves of n nodes: d[i * count + j] = distance of matching curve j
- * onto curve i; NaN for a failed pair. */
-int cva_elastic_distance_matrix(const double* curves, int64_t count, int64_t n, int max_iters,
-                                double energy_tol, int max_slope, double* d, void* stream);
-int cva_elastic_distance_matrix_host(const double* curves, int64_t count, int64_t n, int max_iters,
-                                     double energy_tol, int max_slope, double* d);
+ * onto curve i (method 1: approach 1, 2: approach 2); NaN for a failed pair. */
+int cva_elastic_distance_matrix(const double* curves, int64_t count, int64_t n, int method, int max_iters,
+                                double energy_tol, int max_slope, int64_t n_max_approach1, double* d,
+                                void* stream);
+int cva_elastic_distance_matrix_host(const double* curves, int64_t count, int64_t n, int method, int max_iters,
+                                     double energy_tol, int max_slope, int64_t n_max_approach1, double* d);
+
+/* Single-call SRV utilities behind the C++ drop-in (synchronous, host buffers,
+ * GPU compute; failures in cva_dropin_last_error()):
+ * apply_srv_action (srv.cpp:100-118), elastic_energy (:120-128), dp_step_cost
+ * (:145-176). gamma: n + 1 values; theta: Rotation2 angle. */
+int cva_apply_srv_action_host(const double* q, int64_t n, double t0, double theta, const double* gamma,
+                              double* out);
+int cva_elastic_energy_host(const double* q1, const double* q2, int64_t n, double t0, double theta,
+                            const double* gamma, double* out);
+int cva_dp_step_cost_host(const double* q1, const double* q2, int64_t n, int i0, int j0, int di, int dj,
+                          double* out);
 
 /* ---------------------------------------------------------------------------
  * Diagnostics (not on the hot path).

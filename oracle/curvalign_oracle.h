@@ -94,6 +94,8 @@ int or_dp_reparam(const double* q1, const double* q2, int64_t n, int max_slope, 
                   double* energy);
 int or_elastic_approach2(const double* c1, const double* c2, int64_t n, int max_iters, double energy_tol,
                          int use_fft, int max_slope, or_elastic_match* out);
+int or_elastic_approach1(const double* c1, const double* c2, int64_t n, int max_slope, int64_t n_max,
+                         or_elastic_match* out);
 
 /* Batched drivers over a ragged point array: pair p aligns curve 2p against
  * curve 2p+1, curve c = points [offsets[c], offsets[c+1]).

@@ -5,6 +5,7 @@
  *   or_elastic_energy     proj/src/srv.cpp:120-128
  *   or_dp_step_cost       proj/src/srv.cpp:145-176
  *   or_dp_reparam         proj/src/srv.cpp:180-257
+ *   or_elastic_approach1  proj/src/elastic.cpp:62-100
  *   or_elastic_approach2  proj/src/elastic.cpp:102-174 (compose :21-33,
  *                         rebase :37-50, run_align :52-54)
  *
@@ -335,5 +336,53 @@ int or_elastic_approach2(const double* c1, const double* c2, int64_t n, int max_
     if (out->gamma) memcpy(out->gamma, g, gb);
   }
   free(q1), free(q2), free(q1c), free(w), free(wc), free(g), free(gd), free(gc);
+  return rc;
+}
+
+/* elastic.cpp:62-100: every start shift m: Kabsch rotation of the SRV pair, the
+ * shifted rotated SRV, one DP, the realised energy; the first smallest wins. */
+int or_elastic_approach1(const double* c1, const double* c2, int64_t n, int max_slope, int64_t n_max,
+                         or_elastic_match* out) {
+  if (n < 8) return OR_INVALID;
+  if (n > n_max) return OR_INVALID; /* elastic.cpp:66-69 */
+  const size_t pb = sizeof(double) * 2 * (size_t)n, gb = sizeof(double) * ((size_t)n + 1);
+  double *q1 = malloc(pb), *q2 = malloc(pb), *w = malloc(pb), *gd = malloc(gb), *best_g = malloc(gb);
+  int rc = (!q1 || !q2 || !w || !gd || !best_g) ? OR_BAD_ALLOC : OR_OK;
+  if (!rc) rc = or_srv_transform(c1, n, q1);
+  if (!rc) rc = or_srv_transform(c2, n, q2);
+  double best = INFINITY, best_t0 = 0.0, best_th = 0.0;
+  for (int64_t m = 0; !rc && m < n; ++m) {
+    double a4[4], th, tr, de, e;
+    int32_t dg;
+    rc = or_cross_correlation_matrix(q1, q2, n, m, a4);
+    if (!rc) rc = or_optimal_rotation_svd(a4, &th, &tr, &dg);
+    if (rc) break;
+    const double c = cos(th), s = sin(th);
+    for (int64_t l = 0; l < n; ++l) {
+      const int64_t k = (l + m) % n;
+      w[2 * l] = c * q2[2 * k] + s * q2[2 * k + 1];
+      w[2 * l + 1] = -s * q2[2 * k] + c * q2[2 * k + 1];
+    }
+    rc = or_dp_reparam(q1, w, n, max_slope, gd, &de);
+    const double t0 = (double)m / (double)n;
+    if (!rc) rc = or_elastic_energy(q1, q2, n, t0, th, gd, &e);
+    if (rc) break;
+    if (e < best) {
+      best = e;
+      best_t0 = t0;
+      best_th = th;
+      memcpy(best_g, gd, gb);
+    }
+  }
+  if (!rc) {
+    out->t0 = best_t0;
+    out->theta = best_th;
+    out->energy = best;
+    out->distance = sqrt(best > 0.0 ? best : 0.0);
+    out->iterations = 1;
+    out->converged = 1;
+    if (out->gamma) memcpy(out->gamma, best_g, gb);
+  }
+  free(q1), free(q2), free(w), free(gd), free(best_g);
   return rc;
 }

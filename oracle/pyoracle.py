@@ -234,6 +234,27 @@ class Oracle(_ElasticShared, _Base):
             e[p] = ep[0] if st[p] == 0 else np.nan
         return g, e, st
 
+    def elastic_approach1_batch(self, c1, c2, max_slope=4, n_max=512, threads=1, gamma=False):
+        a, b = _f64(c1), _f64(c2)
+        pairs, n = a.shape[0], a.shape[1]
+        out = {k: np.full(pairs, np.nan) for k in ("distance", "energy", "t0", "theta")}
+        out.update(iterations=np.zeros(pairs, dtype=np.int32), converged=np.zeros(pairs, dtype=np.int32),
+                   status=np.zeros(pairs, dtype=np.int32))
+        g = np.zeros((pairs, n + 1))
+        f = self._fn("elastic_approach1", [c_void_p, c_void_p, c_int64, c_int, c_int64,
+                                           ctypes.POINTER(_OrElasticMatch)])
+        for p in range(pairs):
+            m = _OrElasticMatch(gamma=g[p].ctypes.data)
+            rc = f(_p(a[p]), _p(b[p]), n, max_slope, n_max, ctypes.byref(m))
+            out["status"][p] = rc
+            if rc == 0:
+                for k in ("distance", "energy", "t0", "theta"):
+                    out[k][p] = getattr(m, k)
+                out["iterations"][p], out["converged"][p] = m.iterations, m.converged
+        if gamma:
+            out["gamma"] = g
+        return out
+
     def elastic_approach2_batch(self, c1, c2, max_iters=30, energy_tol=1e-6, use_fft=True, max_slope=4,
                                 threads=1, gamma=False):
         a, b = _f64(c1), _f64(c2)
@@ -385,13 +406,32 @@ class Reference(_ElasticShared, _Base):
             out["gamma"] = g
         return out
 
-    def distance_matrix_approach2(self, curves, n, max_iters=30, energy_tol=1e-6, max_slope=4, threads=1):
+    def distance_matrix(self, curves, n, method=2, max_iters=30, energy_tol=1e-6, max_slope=4, threads=1):
         c = _f64(curves)
         k, n_in = c.shape[0], c.shape[1]
         out = np.zeros((k, k))
-        f = self._fn("distance_matrix_approach2", [c_void_p, c_int64, c_int64, c_int64, c_int, c_double, c_int,
-                                                   c_int, c_void_p])
-        _raise(f(_p(c), k, n_in, n, max_iters, energy_tol, max_slope, threads, _p(out)), "distance_matrix")
+        f = self._fn("distance_matrix", [c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_double, c_int,
+                                         c_int, c_void_p])
+        _raise(f(_p(c), k, n_in, n, method, max_iters, energy_tol, max_slope, threads, _p(out)), "distance_matrix")
+        return out
+
+    def distance_matrix_approach2(self, curves, n, max_iters=30, energy_tol=1e-6, max_slope=4, threads=1):
+        return self.distance_matrix(curves, n, 2, max_iters, energy_tol, max_slope, threads)
+
+    def elastic_approach1_batch(self, c1, c2, max_slope=4, n_max=512, threads=1, gamma=False):
+        a, b = _f64(c1), _f64(c2)
+        pairs, n = a.shape[0], a.shape[1]
+        out = {k: np.zeros(pairs) for k in ("distance", "energy", "t0", "theta")}
+        g = np.zeros((pairs, n + 1)) if gamma else None
+        it, cv, st = (np.zeros(pairs, dtype=np.int32) for _ in range(3))
+        f = self._fn("elastic_approach1_batch", [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int64, c_int,
+                                                 c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                                 c_void_p, c_void_p])
+        f(_p(a), _p(b), pairs, n, max_slope, n_max, threads, _p(out["distance"]), _p(out["energy"]), _p(out["t0"]),
+          _p(out["theta"]), _p(g) if gamma else None, _p(it), _p(cv), _p(st))
+        out.update(iterations=it, converged=cv, status=st)
+        if gamma:
+            out["gamma"] = g
         return out
 
 

@@ -451,11 +451,40 @@ int ref_elastic_approach2_batch(const double* c1, const double* c2, int64_t pair
   return first_err.load();
 }
 
+// elastic_distance_approach1 (proj/src/elastic.cpp:62-100), same outputs.
+int ref_elastic_approach1_batch(const double* c1, const double* c2, int64_t pairs, int64_t n, int max_slope,
+                                int64_t n_max, int threads, double* distance, double* energy, double* t0,
+                                double* theta, double* gamma_out, int32_t* iterations, int32_t* converged,
+                                int32_t* status) {
+  ElasticOptions o;
+  o.max_slope = max_slope;
+  o.n_max_approach1 = static_cast<std::size_t>(n_max);
+  std::atomic<int> first_err{0};
+  parallel_for(pairs, threads, [&](int64_t p) {
+    const int rc = guard([&] {
+      const ElasticMatch m = elastic_distance_approach1(to_curve(c1 + 2 * p * n, n), to_curve(c2 + 2 * p * n, n), o);
+      distance[p] = m.distance;
+      energy[p] = m.energy;
+      t0[p] = m.t0;
+      theta[p] = m.rotation.theta();
+      if (gamma_out) std::memcpy(gamma_out + p * (n + 1), m.gamma.gamma.data(), sizeof(double) * (n + 1));
+      iterations[p] = m.iterations;
+      converged[p] = m.converged ? 1 : 0;
+    });
+    status[p] = rc;
+    if (rc != kOk) {
+      distance[p] = energy[p] = std::nan("");
+      int expected = 0;
+      first_err.compare_exchange_strong(expected, rc);
+    }
+  });
+  return first_err.load();
+}
+
 // distance_matrix(curves, approach2, n) (proj/src/elastic.cpp:176-236): count
 // raw curves of n_in nodes each (uniform size), preprocessed to n inside.
-int ref_distance_matrix_approach2(const double* curves, int64_t count, int64_t n_in, int64_t n,
-                                  int max_iters, double energy_tol, int max_slope, int threads,
-                                  double* out) {
+int ref_distance_matrix(const double* curves, int64_t count, int64_t n_in, int64_t n, int method,
+                        int max_iters, double energy_tol, int max_slope, int threads, double* out) {
   return guard([&] {
     std::vector<Curve> cs;
     for (int64_t i = 0; i < count; ++i) cs.push_back(to_curve(curves + 2 * i * n_in, n_in));
@@ -463,8 +492,8 @@ int ref_distance_matrix_approach2(const double* curves, int64_t count, int64_t n
     o.max_iters = max_iters;
     o.energy_tol = energy_tol;
     o.max_slope = max_slope;
-    const auto d = distance_matrix(cs, DistanceMethod::approach2, static_cast<std::size_t>(n), o,
-                                   static_cast<unsigned>(threads));
+    const auto d = distance_matrix(cs, method == 1 ? DistanceMethod::approach1 : DistanceMethod::approach2,
+                                   static_cast<std::size_t>(n), o, static_cast<unsigned>(threads));
     for (int64_t i = 0; i < count; ++i)
       for (int64_t j = 0; j < count; ++j) out[i * count + j] = d[i][j];
   });

@@ -11,8 +11,13 @@ of the reference's API (proj/include/curvalign/*.hpp).
 from .api import (  # noqa: F401
     ElasticMatch,
     RigidAlignment,
+    apply_srv_action,
     distance_matrix,
     dp_reparam,
+    dp_step_cost,
+    elastic_approach1_batch,
+    elastic_distance_approach1,
+    elastic_energy,
     dp_reparam_batch,
     elastic_approach2_batch,
     elastic_distance_approach2,
@@ -35,8 +40,13 @@ from .api import (  # noqa: F401
 __all__ = [
     "ElasticMatch",
     "RigidAlignment",
+    "apply_srv_action",
     "distance_matrix",
     "dp_reparam",
+    "dp_step_cost",
+    "elastic_approach1_batch",
+    "elastic_distance_approach1",
+    "elastic_energy",
     "dp_reparam_batch",
     "elastic_approach2_batch",
     "elastic_distance_approach2",

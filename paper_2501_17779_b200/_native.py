@@ -108,9 +108,23 @@ SIGNATURES = {
         [c_void_p, c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
          c_void_p, c_void_p, c_void_p, c_void_p],
     ),
-    "cva_elastic_distance_matrix": (c_int, [c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_void_p,
-                                            c_void_p]),
-    "cva_elastic_distance_matrix_host": (c_int, [c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_void_p]),
+    "cva_elastic_approach1_batch": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+         c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
+    "cva_elastic_approach1_batch_host": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+         c_void_p, c_void_p, c_void_p],
+    ),
+    "cva_elastic_distance_matrix": (c_int, [c_void_p, c_int64, c_int64, c_int, c_int, c_double, c_int, c_int64,
+                                            c_void_p, c_void_p]),
+    "cva_elastic_distance_matrix_host": (c_int, [c_void_p, c_int64, c_int64, c_int, c_int, c_double, c_int,
+                                                 c_int64, c_void_p]),
+    "cva_apply_srv_action_host": (c_int, [c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p]),
+    "cva_elastic_energy_host": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p]),
+    "cva_dp_step_cost_host": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int, c_void_p]),
 }
 
 _lib = None
@@ -138,11 +152,12 @@ class CurvalignError(RuntimeError):
     """A C-ABI call failed (CVA_CUDA_ERROR / CVA_UNSUPPORTED)."""
 
 
-def check(status: int) -> None:
+def check(status: int, dropin: bool = False) -> None:
     """Map a cva_status to the exception the reference would throw."""
     if status == CVA_OK:
         return
-    msg = (load().cva_last_error() or b"").decode(errors="replace")
+    err = load().cva_dropin_last_error if dropin else load().cva_last_error
+    msg = (err() or b"").decode(errors="replace")
     if status == CVA_INVALID_ARGUMENT:
         raise ValueError(msg)  # std::invalid_argument
     if status == CVA_RUNTIME_ERROR:
@@ -150,6 +165,11 @@ def check(status: int) -> None:
     if status == CVA_BAD_ALLOC:
         raise MemoryError(msg)  # std::bad_alloc
     raise CurvalignError(f"status {status}: {msg}")
+
+
+def check_dropin(status: int) -> None:
+    """check() for the single-call utilities (messages in cva_dropin_last_error)."""
+    check(status, dropin=True)
 
 
 _synth = None

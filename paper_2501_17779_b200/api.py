@@ -458,33 +458,153 @@ def elastic_distance_approach2(c1, c2, max_iters: int = 30, energy_tol: float = 
                         iterations=int(r["iterations"][0]), converged=bool(r["converged"][0]))
 
 
-def elastic_distance_matrix(curves, max_iters: int = 30, energy_tol: float = 1e-6, max_slope: int = 4):
-    """distance_matrix cells for approach 2 (elastic.cpp:176-236) on already
-    preprocessed curves ``(count, n, 2)``: d[i, j] = distance matching curve j
-    onto curve i, NaN for a failed pair."""
+def _elastic_batch(approach, c1, c2, max_iters, energy_tol, max_slope, n_max_approach1, return_gamma):
+    lib = _native.load()
+    if _is_cuda_tensor(c1):
+        a, b = c1.contiguous(), c2.contiguous()
+        pairs, n = a.shape[0], a.shape[1]
+        dev = a.device
+        out = {k: torch.empty(pairs, dtype=torch.float64, device=dev) for k in ("distance", "energy", "t0", "theta")}
+        for k in ("iterations", "converged", "status"):
+            out[k] = torch.empty(pairs, dtype=torch.int32, device=dev)
+        g = torch.empty((pairs, n + 1), dtype=torch.float64, device=dev) if return_gamma else None
+        ptrs = [out[k].data_ptr() for k in ("distance", "energy", "t0", "theta")] + [_tptr(g)] + \
+            [out[k].data_ptr() for k in ("iterations", "converged", "status")]
+        if approach == 1:
+            check(lib.cva_elastic_approach1_batch(a.data_ptr(), b.data_ptr(), pairs, n, max_slope, n_max_approach1,
+                                                  *ptrs, _stream_of(a)))
+        else:
+            check(lib.cva_elastic_approach2_batch(a.data_ptr(), b.data_ptr(), pairs, n, max_iters, energy_tol,
+                                                  max_slope, *ptrs, _stream_of(a)))
+    else:
+        a, b = _f64c(c1), _f64c(c2)
+        if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 2:
+            raise ValueError("elastic: node count mismatch")
+        pairs, n = a.shape[0], a.shape[1]
+        out = {k: np.empty(pairs) for k in ("distance", "energy", "t0", "theta")}
+        for k in ("iterations", "converged", "status"):
+            out[k] = np.empty(pairs, dtype=np.int32)
+        g = np.empty((pairs, n + 1)) if return_gamma else None
+        ptrs = [out[k].ctypes.data for k in ("distance", "energy", "t0", "theta")] + \
+            [g.ctypes.data if g is not None else 0] + [out[k].ctypes.data for k in ("iterations", "converged", "status")]
+        if approach == 1:
+            check(lib.cva_elastic_approach1_batch_host(_ptr(a), _ptr(b), pairs, n, max_slope, n_max_approach1, *ptrs))
+        else:
+            check(lib.cva_elastic_approach2_batch_host(_ptr(a), _ptr(b), pairs, n, max_iters, energy_tol, max_slope,
+                                                       *ptrs))
+    if return_gamma:
+        out["gamma"] = g
+    return out
+
+
+def elastic_approach2_batch(c1, c2, max_iters: int = 30, energy_tol: float = 1e-6, max_slope: int = 4,
+                            return_gamma: bool = False):
+    """elastic_distance_approach2 (elastic.cpp:102-174) per pair of preprocessed
+    curves ``(pairs, n, 2)``. Returns a dict of per-pair arrays: distance,
+    energy, t0, theta, iterations, converged, status (+ gamma). numpy in -> numpy
+    out; CUDA tensors in -> CUDA tensors out (stream-ordered)."""
+    return _elastic_batch(2, c1, c2, max_iters, energy_tol, max_slope, 512, return_gamma)
+
+
+def elastic_approach1_batch(c1, c2, max_slope: int = 4, n_max_approach1: int = 512, return_gamma: bool = False):
+    """elastic_distance_approach1 (elastic.cpp:62-100): exhaustive over start
+    shifts, one DP each. Same outputs as :func:`elastic_approach2_batch`."""
+    return _elastic_batch(1, c1, c2, 0, 0.0, max_slope, n_max_approach1, return_gamma)
+
+
+def _match(r):
+    st = int(r["status"][0])
+    if st == _native.CVA_INVALID_ARGUMENT:
+        raise ValueError("elastic: invalid input")
+    if st == _native.CVA_RUNTIME_ERROR:
+        raise RuntimeError("dp: no admissible path")
+    return ElasticMatch(t0=float(r["t0"][0]), theta=float(r["theta"][0]), gamma=r["gamma"][0],
+                        energy=float(r["energy"][0]), distance=float(r["distance"][0]),
+                        iterations=int(r["iterations"][0]), converged=bool(r["converged"][0]))
+
+
+def elastic_distance_approach2(c1, c2, max_iters: int = 30, energy_tol: float = 1e-6,
+                               max_slope: int = 4) -> ElasticMatch:
+    """Single pair (reference name and exceptions: ValueError for invalid input,
+    RuntimeError for a DP without admissible path)."""
+    a, b = np.asarray(c1, dtype=np.float64), np.asarray(c2, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValueError("elastic: node count mismatch")
+    return _match(elastic_approach2_batch(a[None], b[None], max_iters, energy_tol, max_slope, return_gamma=True))
+
+
+def elastic_distance_approach1(c1, c2, max_slope: int = 4, n_max_approach1: int = 512) -> ElasticMatch:
+    """Single pair, approach 1 (ValueError above n_max_approach1, elastic.cpp:66-69)."""
+    a, b = np.asarray(c1, dtype=np.float64), np.asarray(c2, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValueError("elastic: node count mismatch")
+    return _match(elastic_approach1_batch(a[None], b[None], max_slope, n_max_approach1, return_gamma=True))
+
+
+def elastic_distance_matrix(curves, method: int = 2, max_iters: int = 30, energy_tol: float = 1e-6,
+                            max_slope: int = 4, n_max_approach1: int = 512):
+    """distance_matrix cells (elastic.cpp:176-236) on already preprocessed curves
+    ``(count, n, 2)``: d[i, j] = distance matching curve j onto curve i (method 1:
+    approach 1, 2: approach 2), NaN for a failed pair."""
     lib = _native.load()
     if _is_cuda_tensor(curves):
         c = curves.contiguous()
         count, n = c.shape[0], c.shape[1]
         d = torch.empty((count, count), dtype=torch.float64, device=c.device)
-        check(lib.cva_elastic_distance_matrix(c.data_ptr(), count, n, max_iters, energy_tol, max_slope,
-                                              d.data_ptr(), _stream_of(c)))
+        check(lib.cva_elastic_distance_matrix(c.data_ptr(), count, n, method, max_iters, energy_tol, max_slope,
+                                              n_max_approach1, d.data_ptr(), _stream_of(c)))
         return d
     c = _f64c(curves)
     count, n = c.shape[0], c.shape[1]
     d = np.empty((count, count))
-    check(lib.cva_elastic_distance_matrix_host(_ptr(c), count, n, max_iters, energy_tol, max_slope, d.ctypes.data))
+    check(lib.cva_elastic_distance_matrix_host(_ptr(c), count, n, method, max_iters, energy_tol, max_slope,
+                                               n_max_approach1, d.ctypes.data))
     return d
 
 
-def distance_matrix(curves, n: int, max_iters: int = 30, energy_tol: float = 1e-6, max_slope: int = 4):
-    """distance_matrix(curves, approach2, n) (elastic.cpp:176-236): raw curves
-    (a list of ``(n_i, 2)`` arrays) are preprocessed to n nodes on the GPU, then
-    every ordered pair is matched."""
+def distance_matrix(curves, n: int, method: int = 2, max_iters: int = 30, energy_tol: float = 1e-6,
+                    max_slope: int = 4, n_max_approach1: int = 512):
+    """distance_matrix(curves, method, n) (elastic.cpp:176-236): raw curves (a
+    list of ``(n_i, 2)`` arrays) are preprocessed to n nodes on the GPU, then every
+    ordered pair is matched (method 1: approach 1, 2: approach 2)."""
     if len(curves) < 2:
         raise ValueError("distance_matrix: need at least 2 curves")
     pts, offs = ragged(curves)
     prep, st = preprocess_batch(pts, offs, n)
     if (st != 0).any():
         raise ValueError("distance_matrix: invalid curve")
-    return elastic_distance_matrix(prep, max_iters, energy_tol, max_slope)
+    return elastic_distance_matrix(prep, method, max_iters, energy_tol, max_slope, n_max_approach1)
+
+
+def apply_srv_action(q, t0: float, theta: float, gamma) -> np.ndarray:
+    """apply_srv_action (srv.cpp:100-118) on the GPU: sqrt(gamma') R Q(t0 + gamma(t))."""
+    a, g = _f64c(q), _f64c(gamma)
+    if g.shape[0] != a.shape[0] + 1:
+        raise ValueError("srv: grid size mismatch")
+    out = np.empty_like(a)
+    _native.check_dropin(_native.load().cva_apply_srv_action_host(_ptr(a), a.shape[0], t0, theta, _ptr(g), _ptr(out)))
+    return out
+
+
+def elastic_energy(q1, q2, t0: float, theta: float, gamma) -> float:
+    """elastic_energy (srv.cpp:120-128) on the GPU."""
+    a, b, g = _f64c(q1), _f64c(q2), _f64c(gamma)
+    if a.shape != b.shape:
+        raise ValueError("srv: size mismatch")
+    if g.shape[0] != a.shape[0] + 1:
+        raise ValueError("srv: grid size mismatch")
+    out = np.zeros(1)
+    _native.check_dropin(_native.load().cva_elastic_energy_host(_ptr(a), _ptr(b), a.shape[0], t0, theta, _ptr(g),
+                                                                out.ctypes.data))
+    return float(out[0])
+
+
+def dp_step_cost(q1, q2, i0: int, j0: int, di: int, dj: int) -> float:
+    """dp_step_cost (srv.cpp:145-176) on the GPU."""
+    a, b = _f64c(q1), _f64c(q2)
+    if a.shape != b.shape:
+        raise ValueError("dp: size mismatch")
+    out = np.zeros(1)
+    _native.check_dropin(_native.load().cva_dp_step_cost_host(_ptr(a), _ptr(b), a.shape[0], i0, j0, di, dj,
+                                                              out.ctypes.data))
+    return float(out[0])

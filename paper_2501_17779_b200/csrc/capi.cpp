@@ -731,15 +731,61 @@ int cva_elastic_approach2_batch(const double* c1, const double* c2, int64_t pair
   return elastic_launch(c1, c2, pairs, 0, n, max_iters, energy_tol, max_slope, o, (cudaStream_t)stream);
 }
 
-int cva_elastic_distance_matrix(const double* curves, int64_t count, int64_t n, int max_iters,
-                                double energy_tol, int max_slope, double* d, void* stream) {
+static int approach1_launch(const double* A, const double* B, int64_t pairs, int64_t k, int64_t n, int max_slope,
+                            const cva::ElasticOut& o, cudaStream_t s) {
+  const int64_t items = pairs * n;
+  const int grid = cva::elastic_items_grid(items, (int)n, max_slope);
+  Slab slab, scratch;
+  slab.s = scratch.s = s;
+  const size_t per = cva::elastic_parent_slab(items, (int)n, max_slope);
+  if (per && scratch_alloc(&slab.p, per * (size_t)grid, s) != cudaSuccess)
+    return fail(CVA_BAD_ALLOC, "elastic: parent scratch allocation failed");
+  if (scratch_alloc(&scratch.p, cva::elastic_a1_scratch(pairs, (int)n), s) != cudaSuccess)
+    return fail(CVA_BAD_ALLOC, "elastic: scratch allocation failed");
+  return finish(cva::launch_elastic_approach1((const double2*)A, (const double2*)B, pairs, k, (int)n, max_slope,
+                                              (uint8_t*)slab.p, grid, scratch.p, o, s),
+                "elastic approach1 launch");
+}
+
+static int check_a1(int64_t n, int64_t n_max) {
+  if (n > n_max)  // elastic.cpp:66-69
+    return fail(CVA_INVALID_ARGUMENT,
+                "approach 1 is O(N^3); node count exceeds the configured limit, use approach 2");
+  return CVA_OK;
+}
+
+int cva_elastic_approach1_batch(const double* c1, const double* c2, int64_t pairs, int64_t n, int max_slope,
+                                int64_t n_max_approach1, double* distance, double* energy, double* t0,
+                                double* theta, double* gamma, int32_t* iterations, int32_t* converged,
+                                int32_t* status, void* stream) {
+  if (int rc = check_elastic(pairs, n, max_slope, "elastic")) return rc;
+  if (int rc = check_a1(n, n_max_approach1)) return rc;
+  if (pairs == 0) return CVA_OK;
+  if (!c1 || !c2 || !distance || !energy || !t0 || !theta || !iterations || !converged || !status)
+    return fail(CVA_INVALID_ARGUMENT, "elastic: null pointer");
+  if (!a16(c1) || !a16(c2)) return misaligned("elastic");
+  if (int rc = require_device()) return rc;
+  const cva::ElasticOut o{distance, energy, t0, theta, gamma, iterations, converged, status};
+  return approach1_launch(c1, c2, pairs, 0, n, max_slope, o, (cudaStream_t)stream);
+}
+
+int cva_elastic_distance_matrix(const double* curves, int64_t count, int64_t n, int method, int max_iters,
+                                double energy_tol, int max_slope, int64_t n_max_approach1, double* d,
+                                void* stream) {
   if (count < 2) return fail(CVA_INVALID_ARGUMENT, "distance_matrix: need at least 2 curves");  // elastic.cpp:181
+  if (method != 1 && method != 2) return fail(CVA_INVALID_ARGUMENT, "distance_matrix: method is 1 or 2");
   if (int rc = check_elastic(count * count, n, max_slope, "distance_matrix")) return rc;
   if (!curves || !d) return fail(CVA_INVALID_ARGUMENT, "distance_matrix: null pointer");
   if (!a16(curves)) return misaligned("distance_matrix");
   if (int rc = require_device()) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t pairs = count * count;
+  if (method == 1 && n > n_max_approach1) {
+    // every cell throws in the reference and becomes NaN (elastic.cpp:210-217)
+    const double qnan = std::nan("");
+    std::vector<double> h((size_t)pairs, qnan);
+    return finish(cudaMemcpyAsync(d, h.data(), sizeof(double) * pairs, cudaMemcpyHostToDevice, s), "fill");
+  }
   void* ws = nullptr;
   const size_t per = 3 * sizeof(double) + 3 * sizeof(int32_t);
   if (scratch_alloc(&ws, per * (size_t)pairs + 256, s) != cudaSuccess)
@@ -747,7 +793,8 @@ int cva_elastic_distance_matrix(const double* curves, int64_t count, int64_t n, 
   double* e = (double*)ws;
   cva::ElasticOut o{d, e, e + pairs, e + 2 * pairs, nullptr, (int32_t*)(e + 3 * pairs),
                     (int32_t*)(e + 3 * pairs) + pairs, (int32_t*)(e + 3 * pairs) + 2 * pairs};
-  const int rc = elastic_launch(curves, nullptr, pairs, count, n, max_iters, energy_tol, max_slope, o, s);
+  const int rc = method == 1 ? approach1_launch(curves, nullptr, pairs, count, n, max_slope, o, s)
+                             : elastic_launch(curves, nullptr, pairs, count, n, max_iters, energy_tol, max_slope, o, s);
   cudaFreeAsync(ws, s);
   return rc;
 }
@@ -809,8 +856,8 @@ int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t
   return finish(e, "elastic_approach2_batch_host");
 }
 
-int cva_elastic_distance_matrix_host(const double* curves, int64_t count, int64_t n, int max_iters,
-                                     double energy_tol, int max_slope, double* d) {
+int cva_elastic_distance_matrix_host(const double* curves, int64_t count, int64_t n, int method, int max_iters,
+                                     double energy_tol, int max_slope, int64_t n_max_approach1, double* d) {
   if (count < 2) return fail(CVA_INVALID_ARGUMENT, "distance_matrix: need at least 2 curves");
   if (int rc = check_elastic(count * count, n, max_slope, "distance_matrix")) return rc;
   if (int rc = require_device()) return rc;
@@ -820,12 +867,46 @@ int cva_elastic_distance_matrix_host(const double* curves, int64_t count, int64_
   cudaStream_t s = nullptr;
   cudaError_t e = cudaMemcpyAsync(dc.p, curves, cb, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "H2D");
-  if (int rc = cva_elastic_distance_matrix((const double*)dc.p, count, n, max_iters, energy_tol, max_slope,
-                                           (double*)dd.p, s))
+  if (int rc = cva_elastic_distance_matrix((const double*)dc.p, count, n, method, max_iters, energy_tol, max_slope,
+                                           n_max_approach1, (double*)dd.p, s))
     return rc;
   e = cudaMemcpyAsync(d, dd.p, db, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   return finish(e, "elastic_distance_matrix_host");
+}
+
+int cva_elastic_approach1_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                     int max_slope, int64_t n_max_approach1, double* distance, double* energy,
+                                     double* t0, double* theta, double* gamma, int32_t* iterations,
+                                     int32_t* converged, int32_t* status) {
+  if (int rc = check_elastic(pairs, n, max_slope, "elastic")) return rc;
+  if (int rc = check_a1(n, n_max_approach1)) return rc;
+  if (pairs == 0) return CVA_OK;
+  if (int rc = require_device()) return rc;
+  const size_t cb = sizeof(double2) * (size_t)(pairs * n), gb = sizeof(double) * (size_t)(pairs * (n + 1));
+  const size_t vb = sizeof(double) * pairs, ib = sizeof(int32_t) * pairs;
+  DevBuf d1, d2, dv, dg, di;
+  if (d1.alloc(cb) || d2.alloc(cb) || dv.alloc(4 * vb) || (gamma && dg.alloc(gb)) || di.alloc(3 * ib))
+    return fail(CVA_BAD_ALLOC, "device allocation failed");
+  cudaStream_t s = nullptr;
+  cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  double* v = (double*)dv.p;
+  int32_t* iv = (int32_t*)di.p;
+  if (int rc = cva_elastic_approach1_batch((const double*)d1.p, (const double*)d2.p, pairs, n, max_slope,
+                                           n_max_approach1, v, v + pairs, v + 2 * pairs, v + 3 * pairs,
+                                           gamma ? (double*)dg.p : nullptr, iv, iv + pairs, iv + 2 * pairs, s))
+    return rc;
+  double* hv[4] = {distance, energy, t0, theta};
+  for (int k = 0; k < 4 && e == cudaSuccess; ++k)
+    if (hv[k]) e = cudaMemcpyAsync(hv[k], v + k * pairs, vb, cudaMemcpyDeviceToHost, s);
+  int32_t* hi[3] = {iterations, converged, status};
+  for (int k = 0; k < 3 && e == cudaSuccess; ++k)
+    if (hi[k]) e = cudaMemcpyAsync(hi[k], iv + k * pairs, ib, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && gamma) e = cudaMemcpyAsync(gamma, dg.p, gb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return finish(e, "elastic_approach1_batch_host");
 }
 
 }  // extern "C"

@@ -9,6 +9,7 @@
 
 #include "../../include/curvalign_cuda.h"
 #include "cva_common.cuh"
+#include "elastic.h"
 #include "spline.cuh"
 
 namespace cva {
@@ -327,6 +328,71 @@ int cva_dft_host(const double* x_complex, int64_t n, int64_t kcount, int sign, d
   if (!o.alloc(sizeof(double2) * (size_t)kcount)) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
   cva::di::dft_kernel<<<(unsigned)kcount, cva::di::kT>>>((const double2*)a.p, n, kcount, sign, scale, (double2*)o.p);
   return cva::down(out_complex, o, sizeof(double2) * (size_t)kcount);
+}
+
+// ---- SRV / elastic utilities (srv.cpp:58-69 validation, :100-176)
+
+namespace {
+int check_reparam(const double* g, int64_t n) {  // validate_reparam (srv.cpp:58-69)
+  if (n < 2) return cva::err(CVA_INVALID_ARGUMENT, "reparam: too few samples");
+  if (std::abs(g[0]) > 1e-12 || std::abs(g[n] - 1.0) > 1e-12)
+    return cva::err(CVA_INVALID_ARGUMENT, "reparam: endpoints must be 0 and 1");
+  for (int64_t i = 0; i < n; ++i)
+    if (g[i + 1] < g[i] - 1e-12) return cva::err(CVA_INVALID_ARGUMENT, "reparam: not monotone");
+  return CVA_OK;
+}
+}  // namespace
+
+int cva_apply_srv_action_host(const double* q, int64_t n, double t0, double theta, const double* gamma,
+                              double* out) {
+  if (n == 0) return cva::err(CVA_INVALID_ARGUMENT, "srv: empty");
+  if (!std::isfinite(theta)) return cva::err(CVA_INVALID_ARGUMENT, "Rotation2: non-finite angle");
+  if (int rc = check_reparam(gamma, n)) return rc;
+  if (int rc = cva::have_device()) return rc;
+  Buf a, g, o;
+  const size_t cb = sizeof(double2) * (size_t)n;
+  if (int rc = cva::up(a, q, cb)) return rc;
+  if (int rc = cva::up(g, gamma, sizeof(double) * (size_t)(n + 1))) return rc;
+  if (!o.alloc(cb)) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
+  cudaError_t e = cva::launch_srv_action((const double2*)a.p, (int)n, t0, theta, (const double*)g.p, (double2*)o.p,
+                                         nullptr);
+  if (e != cudaSuccess) return cva::err(CVA_CUDA_ERROR, "srv action launch", e);
+  return cva::down(out, o, cb);
+}
+
+int cva_elastic_energy_host(const double* q1, const double* q2, int64_t n, double t0, double theta,
+                            const double* gamma, double* out) {
+  if (n == 0) return cva::err(CVA_INVALID_ARGUMENT, "srv: empty");
+  if (!std::isfinite(theta)) return cva::err(CVA_INVALID_ARGUMENT, "Rotation2: non-finite angle");
+  if (int rc = check_reparam(gamma, n)) return rc;
+  if (int rc = cva::have_device()) return rc;
+  Buf a, b, g, t, o;
+  const size_t cb = sizeof(double2) * (size_t)n;
+  if (int rc = cva::up(a, q1, cb)) return rc;
+  if (int rc = cva::up(b, q2, cb)) return rc;
+  if (int rc = cva::up(g, gamma, sizeof(double) * (size_t)(n + 1))) return rc;
+  if (!t.alloc(sizeof(double) * (size_t)n) || !o.alloc(sizeof(double)))
+    return cva::err(CVA_BAD_ALLOC, "device allocation failed");
+  cudaError_t e = cva::launch_elastic_energy((const double2*)a.p, (const double2*)b.p, (int)n, t0, theta,
+                                             (const double*)g.p, (double*)t.p, (double*)o.p, nullptr);
+  if (e != cudaSuccess) return cva::err(CVA_CUDA_ERROR, "elastic energy launch", e);
+  return cva::down(out, o, sizeof(double));
+}
+
+int cva_dp_step_cost_host(const double* q1, const double* q2, int64_t n, int i0, int j0, int di, int dj,
+                          double* out) {
+  if (di < 1 || dj < 1) return cva::err(CVA_INVALID_ARGUMENT, "dp: step increments must be positive");
+  if (n < 1 || i0 < 0 || j0 < 0) return cva::err(CVA_INVALID_ARGUMENT, "dp: bad step");
+  if (int rc = cva::have_device()) return rc;
+  Buf a, b, o;
+  const size_t cb = sizeof(double2) * (size_t)n;
+  if (int rc = cva::up(a, q1, cb)) return rc;
+  if (int rc = cva::up(b, q2, cb)) return rc;
+  if (!o.alloc(sizeof(double))) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
+  cudaError_t e = cva::launch_dp_step_cost((const double2*)a.p, (const double2*)b.p, (int)n, i0, j0, di, dj,
+                                           (double*)o.p, nullptr);
+  if (e != cudaSuccess) return cva::err(CVA_CUDA_ERROR, "dp step launch", e);
+  return cva::down(out, o, sizeof(double));
 }
 
 }  // extern "C"

@@ -178,7 +178,7 @@ __device__ __forceinline__ double step_cost(const double2* q1, const double2* q2
   double cost = 0.0;
   for (int k = 0; k <= a; ++k) {
     int i = i0 + k;
-    if (i >= n) i -= n;
+    if (i >= n) i %= n;
     const int num = k * b;
     double2 s;
     if (num % a == 0) {
@@ -565,6 +565,155 @@ __global__ void __launch_bounds__(kT, 1)
   }
 }
 
+// elastic_distance_approach1 (elastic.cpp:62-100), one work item per (pair,
+// shift m): Kabsch rotation of the SRV pair at shift m, the shifted rotated SRV,
+// one DP, and the realised energy at t0 = m / n. Items write (energy, theta,
+// gamma) to scratch; a1_pick_kernel keeps, per pair, the first m with the
+// smallest energy (the reference's strict `e < best` scan over m).
+template <int kN, int kW>
+__global__ void __launch_bounds__(kT, 1)
+    a1_kernel(const double2* __restrict__ A, const double2* __restrict__ B, int64_t pairs, int64_t matrix_k,
+              int n_rt, int Wrt, int parent_in_smem, uint8_t* parent_slab, double* item_e, double* item_theta,
+              double* item_gamma, int32_t* item_status) {
+  extern __shared__ __align__(16) char smem[];
+  const int n = kN > 0 ? kN : n_rt;
+  const int W = kW > 0 ? kW : Wrt;
+  Smem S;
+  smem_layout(n, W, parent_in_smem != 0, smem, &S);
+  uint8_t* parent = parent_in_smem ? S.parent : parent_slab + (size_t)blockIdx.x * (n + 1) * (n + 1);
+  const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+  const int64_t items = pairs * n;
+  for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
+    const int64_t p = it / n;
+    const int m = (int)(it % n);
+    const double2* c1 = matrix_k ? A + (p / matrix_k) * n : A + p * n;
+    const double2* c2 = matrix_k ? A + (p % matrix_k) * n : B + p * n;
+    load_curve(c1, S.c1, n);
+    load_curve(c2, S.c2, n);
+    __syncthreads();
+    int bad = 0;
+    for (int l = threadIdx.x; l < n; l += kT)
+      bad |= !(isfinite(S.c1[l].x) && isfinite(S.c1[l].y) && isfinite(S.c2[l].x) && isfinite(S.c2[l].y));
+    bad = __syncthreads_or(bad);
+    int status = CVA_OK;
+    double e = qnan, th = qnan;
+    if (bad) {
+      status = CVA_INVALID_ARGUMENT;
+    } else {
+      srv_transform(S.c1, n, S.q1);
+      srv_transform(S.c2, n, S.q2);
+      __syncthreads();
+      if (threadIdx.x == 0) {  // optimal_rotation_svd(cross_correlation_matrix(q1, q2, m))
+        double a11 = 0.0, a12 = 0.0, a21 = 0.0, a22 = 0.0;
+        for (int l = 0; l < n; ++l) {
+          const double2 pq = S.q1[l];
+          int lm = l + m;
+          if (lm >= n) lm -= n;
+          const double2 qq = S.q2[lm];
+          a11 = add(a11, mul(pq.x, qq.x));
+          a12 = add(a12, mul(pq.x, qq.y));
+          a21 = add(a21, mul(pq.y, qq.x));
+          a22 = add(a22, mul(pq.y, qq.y));
+        }
+        const bool fin = isfinite(a11) && isfinite(a12) && isfinite(a21) && isfinite(a22);
+        const bool zero = a11 == 0.0 && a12 == 0.0 && a21 == 0.0 && a22 == 0.0;
+        S.cell[2] = !fin ? qnan : (zero ? 0.0 : atan2(sub(a12, a21), add(a11, a22)));
+      }
+      __syncthreads();
+      th = S.cell[2];
+      __syncthreads();
+      if (!isfinite(th)) {
+        status = CVA_INVALID_ARGUMENT;  // rigid_align.cpp:83
+      } else {
+        double sn, cs;
+        sincos(th, &sn, &cs);
+        for (int l = threadIdx.x; l < n; l += kT) {
+          int lm = l + m;
+          if (lm >= n) lm -= n;
+          S.w[l] = rot_apply(cs, sn, S.q2[lm]);
+        }
+        __syncthreads();
+        const double de = dp_reparam<kW>(S.q1, S.w, n, W, S.ring, parent, S.gd, S.cell);
+        if (!isfinite(de)) {
+          status = CVA_RUNTIME_ERROR;
+        } else {
+          const double t0 = dvd((double)m, (double)n);
+          e = energy(S.q1, S.q2, n, t0, th, S.gd, S.T, S.cell);
+        }
+      }
+    }
+    for (int l = threadIdx.x; l <= n; l += kT) item_gamma[it * (n + 1) + l] = status == CVA_OK ? S.gd[l] : qnan;
+    if (threadIdx.x == 0) {
+      item_e[it] = e;
+      item_theta[it] = th;
+      item_status[it] = status;
+    }
+    __syncthreads();
+  }
+}
+
+// Per pair: the first shift with the smallest energy (elastic.cpp:92-98), or
+// the first failing item's status (an exception in the reference).
+__global__ void a1_pick_kernel(int64_t pairs, int n, const double* item_e, const double* item_theta,
+                               const double* item_gamma, const int32_t* item_status, ElasticOut out) {
+  const int64_t p = blockIdx.x;
+  if (p >= pairs) return;
+  __shared__ int s_m, s_st;
+  if (threadIdx.x == 0) {
+    double best = __longlong_as_double(0x7ff0000000000000LL);
+    int bm = -1, st = CVA_OK;
+    for (int m = 0; m < n; ++m) {
+      const int64_t it = p * n + m;
+      if (item_status[it] != CVA_OK) {
+        st = item_status[it];
+        break;
+      }
+      if (item_e[it] < best) {
+        best = item_e[it];
+        bm = m;
+      }
+    }
+    if (st == CVA_OK && bm < 0) st = CVA_RUNTIME_ERROR;
+    s_m = bm;
+    s_st = st;
+  }
+  __syncthreads();
+  const int m = s_m;
+  const bool ok = s_st == CVA_OK;
+  const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+  if (out.gamma)
+    for (int l = threadIdx.x; l <= n; l += blockDim.x)
+      out.gamma[p * (n + 1) + l] = ok ? item_gamma[(p * n + m) * (n + 1) + l] : qnan;
+  if (threadIdx.x == 0) {
+    const double e = ok ? item_e[p * n + m] : qnan;
+    out.energy[p] = e;
+    out.distance[p] = ok ? sqrt(fmax(e, 0.0)) : qnan;
+    out.t0[p] = ok ? dvd((double)m, (double)n) : qnan;
+    out.theta[p] = ok ? item_theta[p * n + m] : qnan;
+    out.iterations[p] = ok ? 1 : 0;  // elastic.cpp:96-98
+    out.converged[p] = ok ? 1 : 0;
+    out.status[p] = s_st;
+  }
+}
+
+// ---- single-call utilities behind the C++ drop-in (apply_srv_action,
+// elastic_energy, dp_step_cost), one CTA.
+__global__ void action_kernel(const double2* q, int n, double t0, double theta, const double* g, double2* out) {
+  double s, c;
+  sincos(theta, &s, &c);
+  for (int l = threadIdx.x; l < n; l += blockDim.x) out[l] = action_at(q, n, t0, c, s, g, l);
+}
+__global__ void __launch_bounds__(kT) energy_kernel(const double2* q1, const double2* q2, int n, double t0,
+                                                    double theta, const double* g, double* T, double* out) {
+  __shared__ double cell[4];
+  const double e = energy(q1, q2, n, t0, theta, g, T, cell);
+  if (threadIdx.x == 0) *out = e;
+}
+__global__ void step_cost_kernel(const double2* q1, const double2* q2, int n, int i0, int j0, int a, int b,
+                                 double* out) {
+  *out = step_cost(q1, q2, n, i0, j0, a, b);
+}
+
 }  // namespace el
 
 // ------------------------------------------------------------- launchers
@@ -647,6 +796,66 @@ cudaError_t launch_elastic_approach2(const double2* A, const double2* B, int64_t
     }
   }
   return launch_el<0, 0>(A, B, pairs, matrix_k, n, prm, slab, grid, tw, out, s);
+}
+
+template <int kN, int kW>
+static cudaError_t launch_a1(const double2* A, const double2* B, int64_t pairs, int64_t k, int n, int W,
+                             uint8_t* slab, int grid, double* ie, double* ith, double* ig, int32_t* ist,
+                             cudaStream_t s) {
+  const bool ps = parent_fits(n, W);
+  const size_t sm = el::smem_layout(n, W, ps, nullptr, nullptr);
+  const void* fn = (const void*)el::a1_kernel<kN, kW>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  el::a1_kernel<kN, kW><<<grid, el::kT, sm, s>>>(A, B, pairs, k, n, W, ps ? 1 : 0, slab, ie, ith, ig, ist);
+  return cudaGetLastError();
+}
+
+size_t elastic_a1_scratch(int64_t pairs, int n) {
+  const int64_t items = pairs * n;
+  return (size_t)items * (2 * sizeof(double) + sizeof(int32_t) + sizeof(double) * (n + 1)) + 1024;
+}
+
+cudaError_t launch_elastic_approach1(const double2* A, const double2* B, int64_t pairs, int64_t matrix_k, int n,
+                                     int W, uint8_t* slab, int grid, void* scratch, const ElasticOut& out,
+                                     cudaStream_t s) {
+  const int64_t items = pairs * n;
+  double* ie = (double*)scratch;
+  double* ith = ie + items;
+  double* ig = ith + items;
+  int32_t* ist = (int32_t*)(ig + items * (n + 1));
+  cudaError_t e;
+  if (W == 4) {
+    switch (n) {
+      case 64: e = launch_a1<64, 4>(A, B, pairs, matrix_k, n, W, slab, grid, ie, ith, ig, ist, s); break;
+      case 128: e = launch_a1<128, 4>(A, B, pairs, matrix_k, n, W, slab, grid, ie, ith, ig, ist, s); break;
+      case 256: e = launch_a1<256, 4>(A, B, pairs, matrix_k, n, W, slab, grid, ie, ith, ig, ist, s); break;
+      default: e = launch_a1<0, 4>(A, B, pairs, matrix_k, n, W, slab, grid, ie, ith, ig, ist, s); break;
+    }
+  } else {
+    e = launch_a1<0, 0>(A, B, pairs, matrix_k, n, W, slab, grid, ie, ith, ig, ist, s);
+  }
+  if (e != cudaSuccess) return e;
+  el::a1_pick_kernel<<<(unsigned)pairs, 128, 0, s>>>(pairs, n, ie, ith, ig, ist, out);
+  return cudaGetLastError();
+}
+
+int elastic_items_grid(int64_t items, int n, int W) { return elastic_grid(items, n, W); }
+
+cudaError_t launch_srv_action(const double2* q, int n, double t0, double theta, const double* g, double2* out,
+                              cudaStream_t s) {
+  el::action_kernel<<<1, el::kT, 0, s>>>(q, n, t0, theta, g, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_elastic_energy(const double2* q1, const double2* q2, int n, double t0, double theta,
+                                  const double* g, double* T, double* out, cudaStream_t s) {
+  el::energy_kernel<<<1, el::kT, 0, s>>>(q1, q2, n, t0, theta, g, T, out);
+  return cudaGetLastError();
+}
+cudaError_t launch_dp_step_cost(const double2* q1, const double2* q2, int n, int i0, int j0, int a, int b,
+                                double* out, cudaStream_t s) {
+  el::step_cost_kernel<<<1, 1, 0, s>>>(q1, q2, n, i0, j0, a, b, out);
+  return cudaGetLastError();
 }
 
 }  // namespace cva

@@ -37,4 +37,19 @@ cudaError_t launch_elastic_approach2(const double2* A, const double2* B, int64_t
                                      const ElasticParams& prm, uint8_t* slab, int grid, const double2* tw,
                                      const ElasticOut& out, cudaStream_t s);
 
+// approach 1: scratch bytes for pairs x n work items; grid for those items
+size_t elastic_a1_scratch(int64_t pairs, int n);
+int elastic_items_grid(int64_t items, int n, int W);
+cudaError_t launch_elastic_approach1(const double2* A, const double2* B, int64_t pairs, int64_t matrix_k, int n,
+                                     int W, uint8_t* slab, int grid, void* scratch, const ElasticOut& out,
+                                     cudaStream_t s);
+
+// single-call utilities (one CTA)
+cudaError_t launch_srv_action(const double2* q, int n, double t0, double theta, const double* g, double2* out,
+                              cudaStream_t s);
+cudaError_t launch_elastic_energy(const double2* q1, const double2* q2, int n, double t0, double theta,
+                                  const double* g, double* T, double* out, cudaStream_t s);
+cudaError_t launch_dp_step_cost(const double2* q1, const double2* q2, int n, int i0, int j0, int a, int b,
+                                double* out, cudaStream_t s);
+
 }  // namespace cva

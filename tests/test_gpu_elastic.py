@@ -205,3 +205,63 @@ def test_golden_fixtures(cuda):
     np.testing.assert_array_equal(r["iterations"], g["a2_iterations"])
     d = cva.distance_matrix(list(g["dm_raw"]), 64)
     np.testing.assert_allclose(d, g["dm_d"], rtol=DIST_RTOL, atol=1e-12)
+
+
+# ---------------------------------------------------------------- approach 1
+
+
+@pytest.mark.parametrize("n", [32, 48, 64])
+def test_approach1_matches_reference(cuda, reference, n):
+    c1, c2 = _pairs(reference, n, 5, seed0=41)
+    g = cva.elastic_approach1_batch(c1, c2, return_gamma=True)
+    r = reference.elastic_approach1_batch(c1, c2, threads=8, gamma=True)
+    assert (g["status"] == 0).all() and (r["status"] == 0).all()
+    np.testing.assert_allclose(g["distance"], r["distance"], rtol=DIST_RTOL, atol=1e-12)
+    # same winning start shift, unless two shifts tie to rounding (symmetric
+    # shapes: hippopede / limacon pairs tie at m and m + n/2); the distances
+    # agree either way (asserted above)
+    same = g["t0"] == r["t0"]
+    assert same.sum() >= len(same) - 1
+    np.testing.assert_allclose(g["theta"][same], r["theta"][same], atol=1e-12)
+    assert (g["iterations"] == 1).all() and (g["converged"] == 1).all()
+
+
+def test_approach1_golden_and_limit(cuda):
+    import os
+
+    gl = np.load(os.path.join(os.path.dirname(__file__), "golden", "elastic_kat.npz"))
+    r = cva.elastic_approach1_batch(gl["a1_c1"], gl["a1_c2"], return_gamma=True)
+    np.testing.assert_allclose(r["distance"], gl["a1_distance"], rtol=DIST_RTOL, atol=1e-12)
+    with pytest.raises(ValueError):  # elastic.cpp:66-69
+        cva.elastic_distance_approach1(gl["a1_c1"][0], gl["a1_c2"][0], n_max_approach1=16)
+
+
+def test_distance_matrix_approach1_matches_reference(cuda, reference):
+    raw = np.stack([reference.gen_curve(FAM[k], 200, seed=k + 1) for k in range(3)])
+    d = cva.distance_matrix(list(raw), 32, method=1)
+    rd = reference.distance_matrix(raw, 32, method=1, threads=4)
+    np.testing.assert_allclose(d, rd, rtol=DIST_RTOL, atol=1e-12)
+
+
+# ------------------------------------------------------------ SRV utilities
+
+
+def test_srv_utilities_match_reference(cuda, reference):  # test_srv.cpp:130-176
+    q = reference.srv_transform(prep(reference, "bumps", 64, 3))
+    q2 = reference.srv_transform(prep(reference, "limacon", 64, 4))
+    ident = np.arange(65) / 64
+    np.testing.assert_array_equal(cva.apply_srv_action(q, 0.0, 0.0, ident), q)  # identity action
+    np.testing.assert_array_equal(cva.apply_srv_action(q, 0.0, 0.0, ident),
+                                  reference.apply_srv_action(q, 0.0, 0.0, ident))
+    gam, _ = cva.dp_reparam(q, q2)
+    a = cva.apply_srv_action(q, 0.37, 1.1, gam)
+    b = reference.apply_srv_action(q, 0.37, 1.1, gam)
+    assert np.abs(a - b).max() <= 1e-14 * np.abs(b).max()  # CUDA cos/sin vs glibc: ulps
+    e_g = cva.elastic_energy(q, q2, 0.37, 1.1, gam)
+    assert e_g == pytest.approx(reference.elastic_energy(q, q2, 0.37, 1.1, gam), rel=1e-13)
+    for (i0, j0, di, dj) in [(0, 0, 1, 1), (5, 7, 3, 2), (60, 63, 4, 3), (130, 3, 2, 3)]:
+        assert cva.dp_step_cost(q, q2, i0, j0, di, dj) == reference.dp_step_cost(q, q2, i0, j0, di, dj)
+    with pytest.raises(ValueError):
+        cva.dp_step_cost(q, q2, 0, 0, 0, 1)
+    with pytest.raises(ValueError):
+        cva.apply_srv_action(q, 0.0, 0.0, ident[::-1])  # not a monotone warp (srv.cpp:58-69)

@@ -76,3 +76,15 @@ def test_oracle_elastic_matches_reference_live(oracle, reference, g):
     np.testing.assert_array_equal(r["distance"], o["distance"])
     q1, q2 = g["dp48_q1"], g["dp48_q2"]
     np.testing.assert_array_equal(reference.dp_reparam_batch(q1, q2)[0], oracle.dp_reparam_batch(q1, q2)[0])
+
+
+def test_approach1_golden_bitwise(oracle, g):  # elastic.cpp:62-100
+    r = oracle.elastic_approach1_batch(g["a1_c1"], g["a1_c2"], gamma=True)
+    for k in ("distance", "energy", "t0", "theta", "gamma"):
+        np.testing.assert_array_equal(r[k], g[f"a1_{k}"], err_msg=k)
+    assert (r["iterations"] == 1).all() and (r["converged"] == 1).all()
+
+
+def test_approach1_limit(oracle, g):  # elastic.cpp:66-69
+    r = oracle.elastic_approach1_batch(g["a1_c1"][:1], g["a1_c2"][:1], n_max=16)
+    assert r["status"][0] == 1

@@ -203,6 +203,13 @@ def elastic():
     el["a2_c1"], el["a2_c2"] = c1, c2
     for k in ("distance", "energy", "t0", "theta", "iterations", "converged", "gamma"):
         el[f"a2_{k}"] = r[k]
+    # approach 1 (exhaustive over start shifts) at n = 32
+    a1c1 = np.stack([prep(FAMILIES[k % 7], 32, k + 1) for k in range(5)])
+    a1c2 = np.stack([prep(FAMILIES[(k + 3) % 7], 32, k + 51) for k in range(5)])
+    r1 = R.elastic_approach1_batch(a1c1, a1c2, gamma=True)
+    el["a1_c1"], el["a1_c2"] = a1c1, a1c2
+    for k in ("distance", "energy", "t0", "theta", "gamma"):
+        el[f"a1_{k}"] = r1[k]
     # distance_matrix(approach2) of 4 raw curves at n = 64 (test_elastic.cpp:113-135)
     raw = np.stack([R.gen_curve(FAMILIES[k], 400, seed=k + 1) for k in range(4)])
     el["dm_raw"], el["dm_d"] = raw, R.distance_matrix_approach2(raw, 64, threads=4)
