@@ -206,17 +206,20 @@ int cva_dp_reparam_batch_host(const double* q1, const double* q2, int64_t pairs,
 /* elastic_distance_approach2(c1[p], c2[p], opts) (elastic.cpp:102-174) on
  * preprocessed curves (pairs x n points each). Outputs per pair: distance,
  * energy, t0, theta (Rotation2 angle), gamma (nullable, pairs x (n+1)),
- * iterations, converged, status. The GPU always uses the FFT correlation
+ * iterations, converged, status, energy_trace (nullable, pairs x (max_iters+1):
+ * ElasticMatch::energy_trace, NaN after the last iteration). The GPU always uses the FFT correlation
  * (use_fft = true); ElasticOptions defaults: max_iters 30, energy_tol 1e-6,
  * max_slope 4. Supports 8 <= n <= 1024 (non-powers of two <= 512). */
 int cva_elastic_approach2_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
                                 int max_iters, double energy_tol, int max_slope, double* distance,
                                 double* energy, double* t0, double* theta, double* gamma,
-                                int32_t* iterations, int32_t* converged, int32_t* status, void* stream);
+                                int32_t* iterations, int32_t* converged, int32_t* status,
+                                double* energy_trace, void* stream);
 int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
                                      int max_iters, double energy_tol, int max_slope, double* distance,
                                      double* energy, double* t0, double* theta, double* gamma,
-                                     int32_t* iterations, int32_t* converged, int32_t* status);
+                                     int32_t* iterations, int32_t* converged, int32_t* status,
+                                     double* energy_trace);
 
 /* elastic_distance_approach1(c1[p], c2[p], opts) (elastic.cpp:62-100): for every
  * start shift m, the Kabsch rotation of the SRV pair, one DP, the realised

@@ -395,13 +395,14 @@ class Reference(_ElasticShared, _Base):
         it = np.zeros(pairs, dtype=np.int32)
         cv = np.zeros(pairs, dtype=np.int32)
         st = np.zeros(pairs, dtype=np.int32)
+        tr = np.zeros((pairs, max_iters + 1))
         f = self._fn("elastic_approach2_batch", [c_void_p, c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_int,
                                                  c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                                 c_void_p, c_void_p])
+                                                 c_void_p, c_void_p, c_void_p])
         f(_p(a), _p(b), pairs, n, max_iters, energy_tol, 1 if use_fft else 0, max_slope, threads,
           _p(out["distance"]), _p(out["energy"]), _p(out["t0"]), _p(out["theta"]), _p(g) if gamma else None,
-          _p(it), _p(cv), _p(st))
-        out.update(iterations=it, converged=cv, status=st)
+          _p(it), _p(cv), _p(st), _p(tr))
+        out.update(iterations=it, converged=cv, status=st, energy_trace=tr)
         if gamma:
             out["gamma"] = g
         return out

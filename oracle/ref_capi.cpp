@@ -423,7 +423,7 @@ int ref_elastic_approach2_batch(const double* c1, const double* c2, int64_t pair
                                 int max_iters, double energy_tol, int use_fft, int max_slope,
                                 int threads, double* distance, double* energy, double* t0,
                                 double* theta, double* gamma_out, int32_t* iterations,
-                                int32_t* converged, int32_t* status) {
+                                int32_t* converged, int32_t* status, double* trace) {
   ElasticOptions o;
   o.max_iters = max_iters;
   o.energy_tol = energy_tol;
@@ -440,6 +440,10 @@ int ref_elastic_approach2_batch(const double* c1, const double* c2, int64_t pair
       if (gamma_out) std::memcpy(gamma_out + p * (n + 1), m.gamma.gamma.data(), sizeof(double) * (n + 1));
       iterations[p] = m.iterations;
       converged[p] = m.converged ? 1 : 0;
+      if (trace)
+        for (int k = 0; k <= max_iters; ++k)
+          trace[p * (max_iters + 1) + k] =
+              k < (int)m.energy_trace.size() ? m.energy_trace[(std::size_t)k] : std::nan("");
     });
     status[p] = rc;
     if (rc != kOk) {

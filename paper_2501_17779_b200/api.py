@@ -474,8 +474,10 @@ def _elastic_batch(approach, c1, c2, max_iters, energy_tol, max_slope, n_max_app
             check(lib.cva_elastic_approach1_batch(a.data_ptr(), b.data_ptr(), pairs, n, max_slope, n_max_approach1,
                                                   *ptrs, _stream_of(a)))
         else:
+            tr = torch.empty((pairs, max_iters + 1), dtype=torch.float64, device=dev)
             check(lib.cva_elastic_approach2_batch(a.data_ptr(), b.data_ptr(), pairs, n, max_iters, energy_tol,
-                                                  max_slope, *ptrs, _stream_of(a)))
+                                                  max_slope, *ptrs, tr.data_ptr(), _stream_of(a)))
+            out["energy_trace"] = tr
     else:
         a, b = _f64c(c1), _f64c(c2)
         if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 2:
@@ -490,8 +492,10 @@ def _elastic_batch(approach, c1, c2, max_iters, energy_tol, max_slope, n_max_app
         if approach == 1:
             check(lib.cva_elastic_approach1_batch_host(_ptr(a), _ptr(b), pairs, n, max_slope, n_max_approach1, *ptrs))
         else:
+            tr = np.empty((pairs, max_iters + 1))
             check(lib.cva_elastic_approach2_batch_host(_ptr(a), _ptr(b), pairs, n, max_iters, energy_tol, max_slope,
-                                                       *ptrs))
+                                                       *ptrs, tr.ctypes.data))
+            out["energy_trace"] = tr
     if return_gamma:
         out["gamma"] = g
     return out
@@ -501,8 +505,9 @@ def elastic_approach2_batch(c1, c2, max_iters: int = 30, energy_tol: float = 1e-
                             return_gamma: bool = False):
     """elastic_distance_approach2 (elastic.cpp:102-174) per pair of preprocessed
     curves ``(pairs, n, 2)``. Returns a dict of per-pair arrays: distance,
-    energy, t0, theta, iterations, converged, status (+ gamma). numpy in -> numpy
-    out; CUDA tensors in -> CUDA tensors out (stream-ordered)."""
+    energy, t0, theta, iterations, converged, status, energy_trace (pairs x
+    (max_iters+1), NaN-padded) (+ gamma). numpy in -> numpy out; CUDA tensors in ->
+    CUDA tensors out (stream-ordered)."""
     return _elastic_batch(2, c1, c2, max_iters, energy_tol, max_slope, 512, return_gamma)
 
 

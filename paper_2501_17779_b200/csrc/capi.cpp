@@ -720,14 +720,16 @@ static int elastic_launch(const double* A, const double* B, int64_t pairs, int64
 int cva_elastic_approach2_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
                                 int max_iters, double energy_tol, int max_slope, double* distance,
                                 double* energy, double* t0, double* theta, double* gamma,
-                                int32_t* iterations, int32_t* converged, int32_t* status, void* stream) {
+                                int32_t* iterations, int32_t* converged, int32_t* status,
+                                double* energy_trace, void* stream) {
   if (int rc = check_elastic(pairs, n, max_slope, "elastic")) return rc;
   if (pairs == 0) return CVA_OK;
   if (!c1 || !c2 || !distance || !energy || !t0 || !theta || !iterations || !converged || !status)
     return fail(CVA_INVALID_ARGUMENT, "elastic: null pointer");
   if (!a16(c1) || !a16(c2)) return misaligned("elastic");
   if (int rc = require_device()) return rc;
-  const cva::ElasticOut o{distance, energy, t0, theta, gamma, iterations, converged, status};
+  if (max_iters < 0) return fail(CVA_INVALID_ARGUMENT, "elastic: negative max_iters");
+  const cva::ElasticOut o{distance, energy, t0, theta, gamma, iterations, converged, status, energy_trace};
   return elastic_launch(c1, c2, pairs, 0, n, max_iters, energy_tol, max_slope, o, (cudaStream_t)stream);
 }
 
@@ -765,7 +767,7 @@ int cva_elastic_approach1_batch(const double* c1, const double* c2, int64_t pair
     return fail(CVA_INVALID_ARGUMENT, "elastic: null pointer");
   if (!a16(c1) || !a16(c2)) return misaligned("elastic");
   if (int rc = require_device()) return rc;
-  const cva::ElasticOut o{distance, energy, t0, theta, gamma, iterations, converged, status};
+  const cva::ElasticOut o{distance, energy, t0, theta, gamma, iterations, converged, status, nullptr};
   return approach1_launch(c1, c2, pairs, 0, n, max_slope, o, (cudaStream_t)stream);
 }
 
@@ -792,7 +794,7 @@ int cva_elastic_distance_matrix(const double* curves, int64_t count, int64_t n, 
     return fail(CVA_BAD_ALLOC, "scratch allocation failed");
   double* e = (double*)ws;
   cva::ElasticOut o{d, e, e + pairs, e + 2 * pairs, nullptr, (int32_t*)(e + 3 * pairs),
-                    (int32_t*)(e + 3 * pairs) + pairs, (int32_t*)(e + 3 * pairs) + 2 * pairs};
+                    (int32_t*)(e + 3 * pairs) + pairs, (int32_t*)(e + 3 * pairs) + 2 * pairs, nullptr};
   const int rc = method == 1 ? approach1_launch(curves, nullptr, pairs, count, n, max_slope, o, s)
                              : elastic_launch(curves, nullptr, pairs, count, n, max_iters, energy_tol, max_slope, o, s);
   cudaFreeAsync(ws, s);
@@ -826,14 +828,18 @@ int cva_dp_reparam_batch_host(const double* q1, const double* q2, int64_t pairs,
 int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
                                      int max_iters, double energy_tol, int max_slope, double* distance,
                                      double* energy, double* t0, double* theta, double* gamma,
-                                     int32_t* iterations, int32_t* converged, int32_t* status) {
+                                     int32_t* iterations, int32_t* converged, int32_t* status,
+                                     double* energy_trace) {
   if (int rc = check_elastic(pairs, n, max_slope, "elastic")) return rc;
+  if (max_iters < 0) return fail(CVA_INVALID_ARGUMENT, "elastic: negative max_iters");
   if (pairs == 0) return CVA_OK;
   if (int rc = require_device()) return rc;
   const size_t cb = sizeof(double2) * (size_t)(pairs * n), gb = sizeof(double) * (size_t)(pairs * (n + 1));
   const size_t vb = sizeof(double) * pairs, ib = sizeof(int32_t) * pairs;
-  DevBuf d1, d2, dv, dg, di;
-  if (d1.alloc(cb) || d2.alloc(cb) || dv.alloc(4 * vb) || (gamma && dg.alloc(gb)) || di.alloc(3 * ib))
+  const size_t tb = sizeof(double) * (size_t)(pairs * (max_iters + 1));
+  DevBuf d1, d2, dv, dg, di, dt;
+  if (d1.alloc(cb) || d2.alloc(cb) || dv.alloc(4 * vb) || (gamma && dg.alloc(gb)) || di.alloc(3 * ib) ||
+      (energy_trace && dt.alloc(tb)))
     return fail(CVA_BAD_ALLOC, "device allocation failed");
   cudaStream_t s = nullptr;
   cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
@@ -843,7 +849,8 @@ int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t
   int32_t* iv = (int32_t*)di.p;
   if (int rc = cva_elastic_approach2_batch((const double*)d1.p, (const double*)d2.p, pairs, n, max_iters,
                                            energy_tol, max_slope, v, v + pairs, v + 2 * pairs, v + 3 * pairs,
-                                           gamma ? (double*)dg.p : nullptr, iv, iv + pairs, iv + 2 * pairs, s))
+                                           gamma ? (double*)dg.p : nullptr, iv, iv + pairs, iv + 2 * pairs,
+                                           energy_trace ? (double*)dt.p : nullptr, s))
     return rc;
   double* hv[4] = {distance, energy, t0, theta};
   for (int k = 0; k < 4 && e == cudaSuccess; ++k)
@@ -852,6 +859,7 @@ int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t
   for (int k = 0; k < 3 && e == cudaSuccess; ++k)
     if (hi[k]) e = cudaMemcpyAsync(hi[k], iv + k * pairs, ib, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && gamma) e = cudaMemcpyAsync(gamma, dg.p, gb, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && energy_trace) e = cudaMemcpyAsync(energy_trace, dt.p, tb, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   return finish(e, "elastic_approach2_batch_host");
 }

@@ -473,6 +473,7 @@ __global__ void __launch_bounds__(kT, 1)
         for (int l = threadIdx.x; l <= n; l += kT) S.g[l] = l == n ? 1.0 : dvd((double)l, (double)n);
         __syncthreads();
         en = energy(S.q1, S.q2, n, t0, theta, S.g, S.T, S.cell);
+        if (out.trace && threadIdx.x == 0) out.trace[p * (prm.max_iters + 1)] = en;
         for (int iter = 1; iter <= prm.max_iters; ++iter) {
           const double prev = en;
           {  // gamma-step (elastic.cpp:124-133)
@@ -542,6 +543,7 @@ __global__ void __launch_bounds__(kT, 1)
             __syncthreads();
           }
           iters = iter;
+          if (out.trace && threadIdx.x == 0) out.trace[p * (prm.max_iters + 1) + iter] = en;  // elastic.cpp:160
           if (prev - en < prm.energy_tol) {
             conv = 1;
             break;
@@ -552,6 +554,9 @@ __global__ void __launch_bounds__(kT, 1)
     const bool ok = status == CVA_OK;
     if (out.gamma)
       for (int l = threadIdx.x; l <= n; l += kT) out.gamma[p * (n + 1) + l] = ok ? S.g[l] : qnan;
+    if (out.trace)  // NaN past the last recorded iteration (and everywhere for a failed pair)
+      for (int k = threadIdx.x; k <= prm.max_iters; k += kT)
+        if (!ok || k > iters) out.trace[p * (prm.max_iters + 1) + k] = qnan;
     if (threadIdx.x == 0) {
       out.distance[p] = ok ? sqrt(fmax(en, 0.0)) : qnan;  // elastic.cpp:19
       out.energy[p] = ok ? en : qnan;

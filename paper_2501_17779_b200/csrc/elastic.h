@@ -22,6 +22,7 @@ struct ElasticOut {
   int32_t* iterations;
   int32_t* converged;
   int32_t* status;
+  double* trace;  // nullable: pairs x (max_iters + 1) energies per accepted iteration, NaN-padded
 };
 
 bool elastic_supported(int n, int W);

@@ -1,7 +1,7 @@
 // C++ tests of the drop-in API (include/curvalign/*.hpp over libcurvalign_cuda.so).
 // Each case restates a hot-path test of the reference's own suite
 // (/root/reference/proj/tests/test_rigid_align.cpp, test_curve_core.cpp,
-// test_srv.cpp; file:line cited per case), written against the same API so a
+// test_srv.cpp, test_elastic.cpp; file:line cited per case), written against the same API so a
 // reference user's code compiles unchanged. Fixture curves are generated here
 // (the reference's synthetic.cpp generators are outside this library).
 // Exit status = number of failed checks.
@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "curvalign/curve.hpp"
+#include "curvalign/elastic.hpp"
 #include "curvalign/fft.hpp"
 #include "curvalign/rigid_align.hpp"
 #include "curvalign/spline.hpp"
@@ -370,6 +371,150 @@ int main() {
     }
     const auto pr = preprocess_align_batch(a, b, 256);
     CHECK(pr.size() == 5);
+  });
+
+  // --------------------------------------------------------- srv / DP / elastic
+  // a monotone warp of [0, 1] (fixed endpoints) for the action cases
+  auto warp = [](std::size_t n) {
+    Reparameterization g;
+    g.gamma.resize(n + 1);
+    for (std::size_t l = 0; l <= n; ++l) {
+      const double t = (double)l / (double)n;
+      g.gamma[l] = t + 0.05 * std::sin(2.0 * kPi * t);
+    }
+    g.gamma[0] = 0.0;
+    g.gamma[n] = 1.0;
+    return g;
+  };
+  auto srv_norm2 = [](const SrvCurve& q) {
+    double s = 0.0;
+    for (const auto& p : q.q) s += p.norm2();
+    return s * q.h;
+  };
+  run("identity action", [] {  // test_srv.cpp:130-137
+    const SrvCurve q = srv_transform(preprocess(bumps(256), 128));
+    const SrvCurve out = apply_srv_action(q, 0.0, Rotation2(0.0), identity_reparam(q.size()));
+    for (std::size_t l = 0; l < q.size(); ++l) CHECK((out.q[l] - q.q[l]).norm() < 1e-12);
+  });
+  run("shift action relabels", [] {  // test_srv.cpp:139-147
+    const std::size_t n = 128, m = 48;
+    const SrvCurve q = srv_transform(preprocess(bumps(256), n));
+    const SrvCurve out = apply_srv_action(q, double(m) / double(n), Rotation2(0.0), identity_reparam(n));
+    for (std::size_t l = 0; l < n; ++l) CHECK(out.q[l].x == q.q[(l + m) % n].x && out.q[l].y == q.q[(l + m) % n].y);
+  });
+  run("action norm", [&] {  // test_srv.cpp:149-155
+    const SrvCurve q = srv_transform(preprocess(bumps(512), 256));
+    const SrvCurve out = apply_srv_action(q, 0.37, Rotation2(1.1), warp(256));
+    CHECK(std::fabs(srv_norm2(out) - srv_norm2(q)) <= 0.02 * srv_norm2(q));
+  });
+  run("energy resummation", [&] {  // test_srv.cpp:157-170
+    const std::size_t n = 128;
+    const SrvCurve q1 = srv_transform(preprocess(bumps(256), n));
+    const SrvCurve q2 = srv_transform(preprocess(limacon(256), n));
+    const Reparameterization g = warp(n);
+    const double e = elastic_energy(q1, q2, 0.21, Rotation2(0.8), g);
+    const SrvCurve act = apply_srv_action(q2, 0.21, Rotation2(0.8), g);
+    double direct = 0.0;
+    for (std::size_t l = 0; l < n; ++l) direct += (q1.q[l] - act.q[l]).norm2();
+    direct *= q1.h;
+    CHECK(std::fabs(e - direct) <= 1e-12 * direct);
+    CHECK(elastic_energy(q1, q1, 0.0, Rotation2(0.0), identity_reparam(n)) < 1e-15);
+  });
+  run("admissible steps", [] {  // test_srv.cpp:179-187
+    const auto st = dp_admissible_steps(4);
+    CHECK(st.size() == 11);
+    CHECK(dp_admissible_steps(1).size() == 1);
+    CHECK(throws<std::invalid_argument>([] { dp_admissible_steps(0); }));
+  });
+  run("dp identity / bound / valid", [] {  // test_srv.cpp:189-229
+    const std::size_t n = 64;
+    const SrvCurve q = srv_transform(preprocess(bumps(256), n));
+    const DpResult r = dp_reparam(q, q);
+    CHECK(r.gamma.gamma.size() == n + 1 && r.energy < 1e-12);
+    for (std::size_t l = 0; l <= n; ++l) CHECK(std::fabs(r.gamma.gamma[l] - double(l) / double(n)) < 1e-10);
+    const SrvCurve q2 = srv_transform(preprocess(hippopede(256), n));
+    const DpResult s = dp_reparam(q, q2);
+    CHECK(s.energy <= elastic_energy(q, q2, 0.0, Rotation2(0.0), identity_reparam(n)) + 1e-12);
+    validate_reparam(s.gamma);
+    std::mt19937_64 rng(5);
+    for (int k = 0; k < 2; ++k) {
+      const SrvCurve a = srv_transform(preprocess(random_curve(rng, 48), 48, false));
+      const SrvCurve b = srv_transform(preprocess(random_curve(rng, 48), 48, false));
+      const DpResult t = dp_reparam(a, b);
+      CHECK(t.gamma.gamma.front() == 0.0 && t.gamma.gamma.back() == 1.0 && std::isfinite(t.energy) && t.energy >= 0);
+      for (std::size_t l = 0; l < 48; ++l) CHECK(t.gamma.gamma[l + 1] >= t.gamma.gamma[l]);
+    }
+    CHECK(throws<std::invalid_argument>([&] { dp_step_cost(q, q2, 0, 0, 0, 1); }));
+  });
+  run("elastic self distance", [] {  // test_elastic.cpp:35-44
+    const Curve c = preprocess(bumps(256), 64);
+    const ElasticMatch m1 = elastic_distance_approach1(c, c);
+    CHECK(m1.distance <= 1e-6 && m1.converged);
+    const ElasticMatch m2 = elastic_distance_approach2(c, c);
+    CHECK(m2.distance <= 1e-6 && m2.converged && m2.iterations >= 1);
+  });
+  run("energy traces", [] {  // test_elastic.cpp:46-61
+    const Curve c1 = preprocess(limacon(256), 64), c2 = preprocess(bumps(256), 64);
+    const ElasticMatch m2 = elastic_distance_approach2(c1, c2);
+    CHECK(!m2.energy_trace.empty() && m2.energy_trace.size() == (std::size_t)m2.iterations + 1);
+    for (std::size_t i = 1; i < m2.energy_trace.size(); ++i) CHECK(m2.energy_trace[i] <= m2.energy_trace[i - 1] + 1e-12);
+    CHECK(std::fabs(m2.energy - m2.energy_trace.back()) <= 1e-12 * m2.energy);
+    CHECK(std::fabs(m2.distance - std::sqrt(m2.energy)) <= 1e-12 * m2.distance);
+    const ElasticMatch m1 = elastic_distance_approach1(c1, c2);
+    CHECK(m1.energy >= 0.0 && m1.energy <= 4.0 + 1e-9);
+    CHECK(std::fabs(m1.distance - std::sqrt(m1.energy)) <= 1e-12 * m1.distance);
+  });
+  run("elastic invariance", [] {  // test_elastic.cpp:63-73
+    const std::size_t n = 128;
+    const Curve c1 = preprocess(hippopede(256), n);
+    Curve c2;
+    c2.nodes.resize(n);
+    for (std::size_t l = 0; l < n; ++l) c2.nodes[l] = rotate_ccw(c1[(l + n / 3) % n], 0.9);
+    CHECK(elastic_distance_approach2(c1, c2).distance <= 0.005);
+    CHECK(elastic_distance_approach1(c1, c2).distance <= 0.005);
+  });
+  run("approach 1 limit", [] {  // test_elastic.cpp:91-101
+    const Curve c = preprocess(circle(1024), 600);
+    bool threw = false;
+    try {
+      elastic_distance_approach1(c, c);
+    } catch (const std::invalid_argument& e) {
+      threw = std::string(e.what()).find("approach 2") != std::string::npos;
+    }
+    CHECK(threw);
+  });
+  run("elastic validation", [] {  // test_elastic.cpp:103-111
+    const Curve a = preprocess(circle(64), 32), b = preprocess(circle(64), 16);
+    CHECK(throws<std::invalid_argument>([&] { elastic_distance_approach2(a, b); }));
+    Curve tiny;
+    tiny.nodes = {{0, 0}, {1, 0}, {1, 1}, {0, 1}};
+    CHECK(throws<std::invalid_argument>([&] { elastic_distance_approach2(tiny, tiny); }));
+  });
+  run("distance matrix", [] {  // test_elastic.cpp:113-160
+    const std::vector<Curve> dup = {bumps(200), bumps(200)};
+    const auto d = distance_matrix(dup, DistanceMethod::approach2, 64);
+    CHECK(d.size() == 2 && d[0].size() == 2);
+    for (const auto& row : d)
+      for (double v : row) CHECK(v <= 1e-6);
+    const std::vector<Curve> three = {bumps(128), limacon(128), hippopede(128)};
+    const auto d1 = distance_matrix(three, DistanceMethod::approach2, 64, {}, 1);
+    const auto d4 = distance_matrix(three, DistanceMethod::approach2, 64, {}, 4);
+    for (std::size_t i = 0; i < 3; ++i)
+      for (std::size_t j = 0; j < 3; ++j) CHECK(d1[i][j] == d4[i][j]);
+    CHECK(d1[0][1] > 0.01 && d1[0][2] > 0.01);
+    ElasticOptions o;
+    o.n_max_approach1 = 16;
+    for (const auto& row : distance_matrix(three, DistanceMethod::approach1, 64, o, 1))
+      for (double v : row) CHECK(std::isnan(v));
+    int calls = 0;
+    distance_matrix(dup, DistanceMethod::approach2, 64, {}, 1, [&](std::size_t, std::size_t, double, double) { ++calls; });
+    CHECK(calls == 4);
+  });
+  run("elastic batch == single", [] {
+    const std::vector<Curve> a = {preprocess(bumps(200), 64), preprocess(limacon(200), 64)};
+    const std::vector<Curve> b = {preprocess(hippopede(200), 64), preprocess(bumps(200), 64)};
+    const auto r = elastic_distance_batch(a, b, DistanceMethod::approach2);
+    for (int p = 0; p < 2; ++p) CHECK(r[p].distance == elastic_distance_approach2(a[p], b[p]).distance);
   });
 
   std::printf("%d checks, %d failed\n", g_checks, g_fail);

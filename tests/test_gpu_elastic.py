@@ -114,6 +114,12 @@ def test_approach2_matches_reference(cuda, reference, n):
     g = cva.elastic_approach2_batch(c1, c2, return_gamma=True)
     r = reference.elastic_approach2_batch(c1, c2, threads=8, gamma=True)
     _check_vs_reference(g, r)
+    # energy trace (ElasticMatch::energy_trace, elastic.cpp:119, :160): same length, same values
+    # to rounding, never increasing (acceptance.cpp:463-470)
+    np.testing.assert_array_equal(np.isnan(g["energy_trace"]), np.isnan(r["energy_trace"]))
+    np.testing.assert_allclose(g["energy_trace"], r["energy_trace"], rtol=2 * DIST_RTOL, atol=1e-12)
+    t = g["energy_trace"]
+    assert np.all(np.nan_to_num(np.diff(t, axis=1), nan=-1.0) <= 1e-12)
     np.testing.assert_allclose(g["t0"], r["t0"], atol=1e-9)
     # gamma: a valid warp in every pair (srv.cpp:58-69)
     assert (g["gamma"][:, 0] == 0).all() and (g["gamma"][:, -1] == 1).all()
