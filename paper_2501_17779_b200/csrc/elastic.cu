@@ -23,6 +23,8 @@
 // alternating search agrees with the reference to rounding, not bitwise.
 #include <cuda_runtime.h>
 #include <math.h>
+
+#include <algorithm>
 #include <stdint.h>
 
 #include "../../include/curvalign_cuda.h"
@@ -36,6 +38,9 @@ namespace el {
 constexpr int kT = 256;
 constexpr double kGridSnap = 1e-9;  // srv.cpp:14
 constexpr int kMaxSteps = 64;
+#ifndef CVA_EL_MINB
+#define CVA_EL_MINB 2
+#endif
 
 // ------------------------------------------------------------ exact arithmetic
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
@@ -170,11 +175,20 @@ __host__ __device__ constexpr Steps make_steps(int W) {
   return s;
 }
 
-// dp_step_cost (srv.cpp:145-176) with q1, q2 in shared memory.
-__device__ __forceinline__ double step_cost(const double2* q1, const double2* q2, int n, int i0, int j0,
-                                            int a, int b) {
-  const double slope = dvd((double)b, (double)a);
-  const double sq = sqrt(slope);
+// Per-step constants of dp_step_cost, formed once per CTA with the reference's
+// operations: sq = sqrt((double)b / a) and the interpolation offsets
+// (double)(k b) / a, so the per-cell work has no division or square root.
+struct StepTab {
+  double sq[kMaxSteps];
+  double fr[kMaxSteps][9];
+  int a[kMaxSteps], b[kMaxSteps];
+};
+
+// dp_step_cost (srv.cpp:145-176) with q1, q2 in shared memory. sq, fr: the
+// step's StepTab row; inv_n: 1/n when n is a power of two (then cost * inv_n
+// == cost / n exactly), else 0 (divide).
+__device__ __forceinline__ double step_cost_t(const double2* q1, const double2* q2, int n, int i0, int j0, int a,
+                                              int b, double sq, const double* fr, double inv_n) {
   double cost = 0.0;
   for (int k = 0; k <= a; ++k) {
     int i = i0 + k;
@@ -183,21 +197,37 @@ __device__ __forceinline__ double step_cost(const double2* q1, const double2* q2
     double2 s;
     if (num % a == 0) {
       int jj = j0 + num / a;
-      jj %= n;
+      if (jj >= n) jj %= n;
       s = q2[jj];
     } else {
-      const double pos = add((double)j0, dvd((double)num, (double)a));
+      const double pos = add((double)j0, fr[k]);
       const int base = (int)pos;
       const double frac = sub(pos, (double)base);
-      const double2 u = q2[base % n];
-      const double2 v = q2[(base + 1) % n];
+      int b0 = base, b1 = base + 1;
+      if (b0 >= n) b0 %= n;
+      if (b1 >= n) b1 %= n;
+      const double2 u = q2[b0];
+      const double2 v = q2[b1];
       s = make_double2(add(u.x, mul(frac, sub(v.x, u.x))), add(u.y, mul(frac, sub(v.y, u.y))));
     }
     const double2 d = make_double2(sub(q1[i].x, mul(s.x, sq)), sub(q1[i].y, mul(s.y, sq)));
-    const double w = (k == 0 || k == a) ? 0.5 : 1.0;
-    cost = add(cost, mul(w, norm2(d)));
+    const double nd = norm2(d);
+    cost = add(cost, (k == 0 || k == a) ? mul(0.5, nd) : nd);  // w = 1 multiplies exactly
   }
-  return dvd(cost, (double)n);
+  return inv_n != 0.0 ? mul(cost, inv_n) : dvd(cost, (double)n);
+}
+
+// Reference-order constants for one step (used by the table and the single-call utility).
+__device__ __forceinline__ void step_consts(int a, int b, double* sq, double* fr) {
+  *sq = sqrt(dvd((double)b, (double)a));
+  for (int k = 0; k <= a; ++k) fr[k] = dvd((double)(k * b), (double)a);
+}
+
+__device__ __forceinline__ double step_cost(const double2* q1, const double2* q2, int n, int i0, int j0, int a,
+                                            int b) {
+  double sq, fr[9];
+  step_consts(a, b, &sq, fr);
+  return step_cost_t(q1, q2, n, i0, j0, a, b, sq, fr, 0.0);
 }
 
 __device__ __forceinline__ int jmin_of(int i, int n, int W) {
@@ -220,6 +250,21 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
   const int W = kW > 0 ? kW : Wrt;
   const int stride = n + 1;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  const double inv_n = (n & (n - 1)) == 0 ? dvd(1.0, (double)n) : 0.0;
+  __shared__ StepTab tab;
+  {
+    int s = 0;
+    for (int a = 1; a <= W; ++a)
+      for (int b = 1; b <= W; ++b)
+        if (gcd_i(a, b) == 1) {
+          if (threadIdx.x == s) {
+            step_consts(a, b, &tab.sq[s], tab.fr[s]);
+            tab.a[s] = a;
+            tab.b[s] = b;
+          }
+          ++s;
+        }
+  }
   auto row = [&](int i) { return ring + (size_t)(i % (W + 1)) * stride; };
   for (int j = threadIdx.x; j <= n; j += kT) row(0)[j] = j == 0 ? 0.0 : inf;
   __syncthreads();
@@ -235,7 +280,7 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
           if (pi < 0 || pj < 0) return;
           const double base = row(pi)[pj];
           if (base == inf) return;
-          const double cand = add(base, step_cost(q1, q2, n, pi, pj, a, b));
+          const double cand = add(base, step_cost_t(q1, q2, n, pi, pj, a, b, tab.sq[s], tab.fr[s], inv_n));
           if (cand < best) {
             best = cand;
             best_s = (uint8_t)s;
@@ -260,18 +305,20 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
   const double e = row(n)[n];
   // backtrack (thread 0): gamma on the lattice path (srv.cpp:235-255)
   if (threadIdx.x == 0) {
-    const Steps st = make_steps(W);
+    int count = 0;
+    for (int a = 1; a <= W; ++a)
+      for (int b = 1; b <= W; ++b) count += gcd_i(a, b) == 1;
     int ok = e != inf;
     if (ok) {
       int i = n, j = n;
       gamma[n] = 1.0;
       while (i > 0) {
         const uint8_t s = parent[(size_t)i * stride + j];
-        if (s == 0xff || s >= st.count) {
+        if (s == 0xff || s >= count) {
           ok = 0;
           break;
         }
-        const int a = st.a[s], b = st.b[s];
+        const int a = tab.a[s], b = tab.b[s];
         const int pi = i - a, pj = j - b;
         for (int k = 0; k < a; ++k) {
           const double jj = add((double)pj, dvd((double)(k * b), (double)a));
@@ -390,7 +437,7 @@ __device__ __forceinline__ void load_curve(const double2* src, double2* dst, int
 
 // Batched dp_reparam on SRV pairs (q1, q2: pairs x n).
 template <int kW>
-__global__ void __launch_bounds__(kT, 1)
+__global__ void __launch_bounds__(kT, CVA_EL_MINB)
     dp_kernel(const double2* __restrict__ q1, const double2* __restrict__ q2, int64_t pairs, int n, int W,
               int parent_in_smem, uint8_t* parent_slab, double* gamma, double* energy, int32_t* status) {
   extern __shared__ __align__(16) char smem[];
@@ -430,7 +477,7 @@ __device__ __forceinline__ cva_alignment align(const double2* a, const double2* 
 // matrix_k == 0: c1 = A + p n, c2 = B + p n; else (distance matrix of
 // matrix_k curves A): c1 = A + (p / k) n, c2 = A + (p % k) n.
 template <int kN, int kW>
-__global__ void __launch_bounds__(kT, 1)
+__global__ void __launch_bounds__(kT, CVA_EL_MINB)
     elastic_kernel(const double2* __restrict__ A, const double2* __restrict__ B, int64_t pairs, int64_t matrix_k,
                    int n_rt, ElasticParams prm, int parent_in_smem, uint8_t* parent_slab, const double2* tw,
                    ElasticOut out) {
@@ -576,7 +623,7 @@ __global__ void __launch_bounds__(kT, 1)
 // gamma) to scratch; a1_pick_kernel keeps, per pair, the first m with the
 // smallest energy (the reference's strict `e < best` scan over m).
 template <int kN, int kW>
-__global__ void __launch_bounds__(kT, 1)
+__global__ void __launch_bounds__(kT, CVA_EL_MINB)
     a1_kernel(const double2* __restrict__ A, const double2* __restrict__ B, int64_t pairs, int64_t matrix_k,
               int n_rt, int Wrt, int parent_in_smem, uint8_t* parent_slab, double* item_e, double* item_theta,
               double* item_gamma, int32_t* item_status) {
@@ -730,10 +777,14 @@ bool parent_fits(int n, int W) {
   return el::smem_layout(n, W, true, nullptr, nullptr) <= 110 * 1024;  // keep 2 CTAs/SM
 }
 
+// Resident CTAs of fn on the device. The dynamic shared-memory attribute must
+// be raised first: without it the occupancy query sees the 48 KB default and
+// reports 0 (which silently halved the grid before).
 int resident(const void* fn, size_t smem) {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, el::kT, smem) != cudaSuccess || per < 1) per = 1;
   return sms * per;
 }
@@ -765,7 +816,10 @@ static cudaError_t launch_dp_w(const double2* q1, const double2* q2, int64_t pai
 int elastic_grid(int64_t pairs, int n, int W) {
   const bool ps = parent_fits(n, W);
   const size_t sm = el::smem_layout(n, W, ps, nullptr, nullptr);
-  const int r = resident((const void*)el::dp_kernel<4>, sm);
+  // the largest-footprint instance (most static shared memory) bounds all three kernels
+  int r = resident((const void*)el::elastic_kernel<0, 0>, sm);
+  r = std::min(r, resident((const void*)el::dp_kernel<0>, sm));
+  r = std::min(r, resident((const void*)el::a1_kernel<0, 0>, sm));
   return (int)(pairs < r ? pairs : r);
 }
 
