@@ -185,12 +185,13 @@ __global__ void __launch_bounds__(kT)
 //   global max (fixed order), forms the band threshold and reports its smallest
 //   index in the band (INT_MAX if none).
 __global__ void __launch_bounds__(kT)
-    lcand_kernel(const double2* __restrict__ F, int M, int N, const double* __restrict__ bmax, int* bcand) {
+    lcand_kernel(const double2* __restrict__ F, int M, int N, const double* __restrict__ bmax, int nbmax,
+                 int* bcand) {
   __shared__ double2 red[64];
   const int64_t p = blockIdx.y;
   const int nblk = gridDim.x;
   double best2 = -1.0;
-  for (int b = threadIdx.x; b < nblk; b += kT) best2 = fmax(best2, bmax[p * nblk + b]);
+  for (int b = threadIdx.x; b < nbmax; b += kT) best2 = fmax(best2, bmax[p * nbmax + b]);
   best2 = block_max(best2, red);
   const double best = sqrt(best2) / (double)M;
   const double thr = best - pf::kTieRelTol * fmax(1.0, fabs(best));
@@ -280,6 +281,193 @@ __global__ void __launch_bounds__(kT)
   }
 }
 
+// ----------------------------------------------------------- four-step path
+//
+// For 4096 <= M <= 65536 the three transforms run as M = M1 x M2 four-step
+// FFTs (M1, M2 in {64, 128, 256}) with every length-M1 / M2 sub-transform done
+// by one warp on a shared-memory vector, so a correlation costs three passes
+// over the data instead of twelve radix-16 passes:
+//   f1_kernel  per curve, column FFTs (length M1, stride M2) of the normalised
+//              curve + twiddle W_M^{n2 k1}  -> U[k1][n2]
+//   fp_kernel  per pair and row k1: row FFTs of U1 and U2 (the spectra
+//              Z[k1 + M1 k2]), the product Z1 conj(Z2), its row FFT and twiddle
+//              W_M^{k1 m2}                   -> G[k1][m2]
+//   p2_kernel  column FFTs of G: F[m2 + M2 m1] in natural order, + block max
+// The product's transform is a forward FFT over the spectral index
+// k = k1 + M1 k2 (D = conj(FFT(Z1 conj Z2)) / M, as in pairfft.cuh), which is
+// why the second step of the forward transforms and the first of the third
+// share one pass and the spectra are never stored.
+namespace fs {
+constexpr int kT = 256;  // 8 warps, one sub-FFT each
+constexpr int kCT = 8;   // columns per column tile (128-byte row segments)
+constexpr int kRT = 8;   // rows per row tile
+
+__device__ __forceinline__ int padL(int i) { return i + (i >> 3); }
+// shared vector stride: padded length + 1 so the 8 vectors of a tile start in
+// different banks
+template <int L>
+__host__ __device__ constexpr int vstride() {
+  return L + L / 8 + 1;
+}
+
+template <int L, int Ns>
+__host__ __device__ constexpr int radix_at() {
+  return ((L / Ns) % 8 == 0 && L / 8 >= 32) ? 8 : ((L / Ns) % 4 == 0 ? 4 : 2);
+}
+
+// One in-place Stockham pass of radix R on a length-L shared vector by one warp.
+// Twiddles of the sub-transform: W_L^k = tw[k * twstride] (tw: length-M table).
+template <int L, int R, int Ns>
+__device__ __forceinline__ void wpass(double2* x, const double2* __restrict__ tw, int twstride, int lane) {
+  constexpr int nb = L / R;
+  constexpr int B = (nb + 31) / 32;
+  constexpr int tws = L / (Ns * R);
+  double2 v[B][R];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int j = lane + 32 * b;
+    if (nb % 32 == 0 || j < nb) {
+      const int jm = j & (Ns - 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[b][r] = x[padL(j + r * nb)];
+      if (Ns > 1) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], __ldg(&tw[(r * jm * tws) * twstride]));
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int j = lane + 32 * b;
+    if (nb % 32 == 0 || j < nb) {
+      const int jm = j & (Ns - 1);
+      dft_r<R>(v[b]);
+      const int base = (j - jm) * R + jm;
+#pragma unroll
+      for (int r = 0; r < R; ++r) x[padL(base + r * Ns)] = v[b][dft_slot<R>(r)];
+    }
+  }
+  __syncwarp();
+}
+
+template <int L, int Ns = 1>
+__device__ __forceinline__ void wfft(double2* x, const double2* __restrict__ tw, int twstride, int lane) {
+  constexpr int R = radix_at<L, Ns>();
+  wpass<L, R, Ns>(x, tw, twstride, lane);
+  if constexpr (Ns * R < L) wfft<L, Ns * R>(x, tw, twstride, lane);
+}
+
+// Column pass of the forward transforms. grid (M2 / kCT, 2 P): sequence s < P is
+// curve 1 of pair s (the a = [z1', 0...] form), s >= P curve 2 of pair s - P
+// (b = [z2', z2', 0...]). Writes U[s][k1 M2 + n2] and sum |z'|^2 partials.
+template <int M1>
+__global__ void __launch_bounds__(kT)
+    f1_kernel(const double2* __restrict__ z1, const double2* __restrict__ z2, int64_t P, int N, int M2,
+              const double2* __restrict__ tw, const CurveNorm* __restrict__ n1, const CurveNorm* __restrict__ n2,
+              double2* U, double* sq1, double* sq2) {
+  constexpr int VS = vstride<M1>();
+  __shared__ __align__(16) double2 sm[kCT * VS];
+  __shared__ double2 red[64];
+  const int M = M1 * M2;
+  const int64_t sidx = blockIdx.y;
+  const bool second = sidx >= P;
+  const int64_t p = second ? sidx - P : sidx;
+  const double2* z = (second ? z2 : z1) + p * N;
+  const CurveNorm cn = (second ? n2 : n1)[p];
+  const int lim = (!second || M == N) ? N : 2 * N;
+  const int c0 = blockIdx.x * kCT;
+  double sq = 0.0;
+  for (int idx = threadIdx.x; idx < M1 * kCT; idx += kT) {
+    const int n1i = idx / kCT, c = idx % kCT;
+    const int n = M2 * n1i + c0 + c;
+    double2 v = make_double2(0.0, 0.0);
+    if (n < lim) {
+      const double2 q = __ldg(&z[n < N ? n : n - N]);
+      v = make_double2((q.x - cn.g.x) * cn.sc, (q.y - cn.g.y) * cn.sc);
+      if (n < N) sq = fma(v.x, v.x, fma(v.y, v.y, sq));
+    }
+    sm[c * VS + padL(n1i)] = v;
+  }
+  sq = block_sum(sq, red);  // syncs the tile too
+  if (threadIdx.x == 0) (second ? sq2 : sq1)[p * gridDim.x + blockIdx.x] = sq;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  wfft<M1>(sm + w * VS, tw, M / M1, lane);
+  __syncthreads();
+  double2* u = U + sidx * (int64_t)M;
+  for (int idx = threadIdx.x; idx < M1 * kCT; idx += kT) {
+    const int k1 = idx / kCT, c = idx % kCT;
+    const int n2 = c0 + c;
+    u[(int64_t)k1 * M2 + n2] = cmul(sm[c * VS + padL(k1)], __ldg(&tw[n2 * k1]));
+  }
+}
+
+// Row pass: per pair p and rows k1 in [r0, r0 + kRT): spectra rows of both
+// curves, product, its row FFT and twiddle. grid (M1 / kRT, P).
+template <int M2>
+__global__ void __launch_bounds__(kT, 2)
+    fp_kernel(const double2* __restrict__ U, int64_t P, int M1, const double2* __restrict__ tw, double2* G) {
+  constexpr int VS = vstride<M2>();
+  extern __shared__ __align__(16) double2 smv[];  // 2 kRT vectors
+  const int M = M1 * M2;
+  const int64_t p = blockIdx.y;
+  const int r0 = blockIdx.x * kRT;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp w: spectra rows r0 + w of curve 1 (vector w) and of curve 2 (vector kRT + w)
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const double2* u = U + (h ? P + p : p) * (int64_t)M + (int64_t)(r0 + w) * M2;
+    double2* x = smv + (h * kRT + w) * VS;
+    for (int i = lane; i < M2; i += 32) x[padL(i)] = __ldg(&u[i]);
+    __syncwarp();
+    wfft<M2>(x, tw, M / M2, lane);
+  }
+  // product Z1 conj(Z2) (same warp owns both rows), its row FFT, twiddle W_M^{k1 m2}
+  double2* x = smv + w * VS;
+  const double2* y = smv + (kRT + w) * VS;
+  for (int i = lane; i < M2; i += 32) x[padL(i)] = cmulconj(x[padL(i)], y[padL(i)]);
+  __syncwarp();
+  wfft<M2>(x, tw, M / M2, lane);
+  const int k1 = r0 + w;
+  double2* g = G + p * (int64_t)M + (int64_t)k1 * M2;
+  for (int m2 = lane; m2 < M2; m2 += 32) g[m2] = cmul(x[padL(m2)], __ldg(&tw[k1 * m2]));
+}
+
+// Column pass of the correlation transform: F[m2 + M2 m1] (natural order) and
+// the per-block max of |F|^2 over m < N. grid (M2 / kCT, P).
+template <int M1>
+__global__ void __launch_bounds__(kT)
+    p2_kernel(const double2* __restrict__ G, int64_t P, int N, int M2, const double2* __restrict__ tw, double2* F,
+              double* bmax) {
+  constexpr int VS = vstride<M1>();
+  __shared__ __align__(16) double2 sm[kCT * VS];
+  __shared__ double2 red[64];
+  const int M = M1 * M2;
+  const int64_t p = blockIdx.y;
+  const int c0 = blockIdx.x * kCT;
+  const double2* g = G + p * (int64_t)M;
+  for (int idx = threadIdx.x; idx < M1 * kCT; idx += kT) {
+    const int k1 = idx / kCT, c = idx % kCT;
+    sm[c * VS + padL(k1)] = __ldg(&g[(int64_t)k1 * M2 + c0 + c]);
+  }
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  wfft<M1>(sm + w * VS, tw, M / M1, lane);
+  __syncthreads();
+  double2* f = F + p * (int64_t)M;
+  double mx = -1.0;
+  for (int idx = threadIdx.x; idx < M1 * kCT; idx += kT) {
+    const int m1 = idx / kCT, c = idx % kCT;
+    const int m = (c0 + c) + M2 * m1;
+    const double2 v = sm[c * VS + padL(m1)];
+    f[m] = v;
+    if (m < N) mx = fmax(mx, fma(v.x, v.x, v.y * v.y));
+  }
+  mx = block_max(mx, red);
+  if (threadIdx.x == 0) bmax[p * gridDim.x + blockIdx.x] = mx;
+}
+}  // namespace fs
+
 }  // namespace ln
 
 // ------------------------------------------------------------------ host
@@ -346,6 +534,64 @@ Layout layout(int N) {
   return L;
 }
 
+// Four-step split M = M1 x M2 with M1, M2 in {64, 128, 256} (M1 <= M2); 0 if none.
+int four_step_m1(int M) {
+  if (M < 4096 || M > 65536) return 0;
+  int p = 0;
+  while ((1 << p) < M) ++p;
+  return 1 << (p / 2);
+}
+
+template <int M1>
+cudaError_t f1_launch(const double2* z1, const double2* z2, int64_t P, int N, int M2, const double2* tw,
+                      const ln::CurveNorm* n1, const ln::CurveNorm* n2, double2* U, double* q1, double* q2,
+                      cudaStream_t s) {
+  ln::fs::f1_kernel<M1><<<dim3((unsigned)(M2 / ln::fs::kCT), (unsigned)(2 * P)), ln::fs::kT, 0, s>>>(
+      z1, z2, P, N, M2, tw, n1, n2, U, q1, q2);
+  return cudaGetLastError();
+}
+template <int M1>
+cudaError_t p2_launch(const double2* G, int64_t P, int N, int M2, const double2* tw, double2* F, double* bmax,
+                      cudaStream_t s) {
+  ln::fs::p2_kernel<M1><<<dim3((unsigned)(M2 / ln::fs::kCT), (unsigned)P), ln::fs::kT, 0, s>>>(G, P, N, M2, tw, F,
+                                                                                               bmax);
+  return cudaGetLastError();
+}
+template <int M2>
+cudaError_t fp_launch(const double2* U, int64_t P, int M1, const double2* tw, double2* G, cudaStream_t s) {
+  const size_t sm = sizeof(double2) * 2 * ln::fs::kRT * ln::fs::vstride<M2>();
+  cudaError_t e = cudaFuncSetAttribute((const void*)ln::fs::fp_kernel<M2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  ln::fs::fp_kernel<M2><<<dim3((unsigned)(M1 / ln::fs::kRT), (unsigned)P), ln::fs::kT, sm, s>>>(U, P, M1, tw, G);
+  return cudaGetLastError();
+}
+
+// The three passes of one chunk; F in natural order, bmax / sq partials per tile.
+cudaError_t four_step(int M1, const double2* z1, const double2* z2, int64_t P, int N, const double2* tw,
+                      const ln::CurveNorm* n1, const ln::CurveNorm* n2, double2* U, double2* G, double2* F,
+                      double* q1, double* q2, double* bmax, cudaStream_t s) {
+  const int M = pf::fft_len(N), M2 = M / M1;
+  cudaError_t e;
+  switch (M1) {
+    case 64: e = f1_launch<64>(z1, z2, P, N, M2, tw, n1, n2, U, q1, q2, s); break;
+    case 128: e = f1_launch<128>(z1, z2, P, N, M2, tw, n1, n2, U, q1, q2, s); break;
+    default: e = f1_launch<256>(z1, z2, P, N, M2, tw, n1, n2, U, q1, q2, s); break;
+  }
+  if (e != cudaSuccess) return e;
+  switch (M2) {
+    case 64: e = fp_launch<64>(U, P, M1, tw, G, s); break;
+    case 128: e = fp_launch<128>(U, P, M1, tw, G, s); break;
+    default: e = fp_launch<256>(U, P, M1, tw, G, s); break;
+  }
+  if (e != cudaSuccess) return e;
+  switch (M1) {
+    case 64: return p2_launch<64>(G, P, N, M2, tw, F, bmax, s);
+    case 128: return p2_launch<128>(G, P, N, M2, tw, F, bmax, s);
+    default: return p2_launch<256>(G, P, N, M2, tw, F, bmax, s);
+  }
+}
+
 }  // namespace
 
 size_t large_workspace_bytes(int64_t chunk, int N) {
@@ -354,10 +600,10 @@ size_t large_workspace_bytes(int64_t chunk, int N) {
   return 4 * seq * (size_t)chunk + 4096                                        // spectra ping-pong
          + 2 * sizeof(ln::CurveNorm) * (size_t)chunk                           // norms
          + 2 * sizeof(double4) * (size_t)(chunk * ln::kStatBlocks)             // stat partials
-         + 2 * sizeof(double) * (size_t)(chunk * L.sqn)                        // |z'|^2 partials
+         + 2 * sizeof(double) * (size_t)(chunk * (L.sqn > L.M / 8 ? L.sqn : L.M / 8))  // |z'|^2 partials
          + 2 * sizeof(int32_t) * (size_t)chunk                                 // bad flags
          + sizeof(double2) * (size_t)chunk                                     // rotations
-         + (sizeof(double) + sizeof(int)) * (size_t)(chunk * L.nblk) + 4096;   // argmax partials
+         + (sizeof(double) + sizeof(int)) * (size_t)(chunk * (L.nblk + L.M / 8)) + 4096;  // argmax partials
 }
 
 int64_t large_chunk_pairs(int N) {
@@ -387,13 +633,15 @@ cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pai
   ln::CurveNorm* n2 = (ln::CurveNorm*)take(sizeof(ln::CurveNorm) * chunk);
   double4* sp1 = (double4*)take(sizeof(double4) * chunk * ln::kStatBlocks);
   double4* sp2 = (double4*)take(sizeof(double4) * chunk * ln::kStatBlocks);
-  double* q1 = (double*)take(sizeof(double) * chunk * sqn);
-  double* q2 = (double*)take(sizeof(double) * chunk * sqn);
+  const int sqcap = sqn > M / 8 ? sqn : M / 8;
+  double* q1 = (double*)take(sizeof(double) * chunk * sqcap);
+  double* q2 = (double*)take(sizeof(double) * chunk * sqcap);
   int32_t* b1 = (int32_t*)take(sizeof(int32_t) * chunk);
   int32_t* b2 = (int32_t*)take(sizeof(int32_t) * chunk);
   double2* rot = (double2*)take(sizeof(double2) * chunk);
-  double* bmax = (double*)take(sizeof(double) * chunk * nblk);
+  double* bmax = (double*)take(sizeof(double) * chunk * (nblk + M / 8));
   int* bcand = (int*)take(sizeof(int) * chunk * nblk);
+  const int fm1 = four_step_m1(M);
   cudaError_t e = cudaSuccess;
   for (int64_t p0 = 0; p0 < pairs && e == cudaSuccess; p0 += chunk) {
     const int64_t P = pairs - p0 < chunk ? pairs - p0 : chunk;
@@ -403,17 +651,26 @@ cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pai
     ln::stats_partial<<<dim3(ln::kStatBlocks, (unsigned)P), ln::kT, 0, s>>>(z2, N, sp2);
     ln::stats_final<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(sp1, P, N, normalize, n1, b1);
     ln::stats_final<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(sp2, P, N, normalize, n2, b2);
-    double2 *Z1 = nullptr, *Z2 = nullptr, *F = nullptr;
-    e = fft_many<ln::kLoadA>(z1, nullptr, A, B, M, N, tw, n1, P, q1, s, &Z1);
-    if (e == cudaSuccess) e = fft_many<ln::kLoadB>(z2, nullptr, C, D, M, N, tw, n2, P, q2, s, &Z2);
-    if (e != cudaSuccess) break;
-    double2* fa = (Z1 == A) ? B : A;  // free buffers for the correlation transform
-    double2* fb = (Z2 == C) ? D : C;
-    e = fft_many<ln::kProduct>(Z1, Z2, fa, fb, M, N, tw, nullptr, P, nullptr, s, &F);
-    if (e != cudaSuccess) break;
-    ln::lmax_kernel<<<dim3((unsigned)nblk, (unsigned)P), ln::kT, 0, s>>>(F, M, N, bmax);
-    ln::lcand_kernel<<<dim3((unsigned)nblk, (unsigned)P), ln::kT, 0, s>>>(F, M, N, bmax, bcand);
-    ln::lpick_kernel<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(F, M, N, bcand, nblk, q1, q2, sqn, b1, b2, P, out + p0,
+    double2* F = nullptr;
+    int nbmax = nblk, nsq = sqn;
+    if (fm1) {  // four-step: U = A|B (2P sequences, adjacent), G = C, F = D
+      e = four_step(fm1, z1, z2, P, N, tw, n1, n2, A, C, D, q1, q2, bmax, s);
+      if (e != cudaSuccess) break;
+      F = D;
+      nbmax = nsq = (M / fm1) / ln::fs::kCT;
+    } else {
+      double2 *Z1 = nullptr, *Z2 = nullptr;
+      e = fft_many<ln::kLoadA>(z1, nullptr, A, B, M, N, tw, n1, P, q1, s, &Z1);
+      if (e == cudaSuccess) e = fft_many<ln::kLoadB>(z2, nullptr, C, D, M, N, tw, n2, P, q2, s, &Z2);
+      if (e != cudaSuccess) break;
+      double2* fa = (Z1 == A) ? B : A;  // free buffers for the correlation transform
+      double2* fb = (Z2 == C) ? D : C;
+      e = fft_many<ln::kProduct>(Z1, Z2, fa, fb, M, N, tw, nullptr, P, nullptr, s, &F);
+      if (e != cudaSuccess) break;
+      ln::lmax_kernel<<<dim3((unsigned)nblk, (unsigned)P), ln::kT, 0, s>>>(F, M, N, bmax);
+    }
+    ln::lcand_kernel<<<dim3((unsigned)nblk, (unsigned)P), ln::kT, 0, s>>>(F, M, N, bmax, nbmax, bcand);
+    ln::lpick_kernel<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(F, M, N, bcand, nblk, q1, q2, nsq, b1, b2, P, out + p0,
                                                              rot);
     if (aligned)
       ln::aligned_kernel<<<dim3((unsigned)((N + 4 * ln::kT - 1) / (4 * ln::kT)), (unsigned)P), ln::kT, 0, s>>>(
