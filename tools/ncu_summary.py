@@ -64,9 +64,10 @@ def main():
             v = num(d[k])
             unit = u.get(k, "")
             if name.endswith("_MB") and isinstance(v, float):
-                v = v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit, 1.0)
+                v = v * {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "B": 1e-6, "KB": 1e-3, "MB": 1.0,
+                         "GB": 1e3}.get(unit, 1.0)
             if name == "gpu__time_duration_us" and isinstance(v, float):
-                v = v * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
+                v = v * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
             if name == "dynamic_smem_per_block_KB" and isinstance(v, float):
                 v = v * {"byte": 1e-3, "Kbyte": 1.0}.get(unit, 1.0)
             out[name] = v
