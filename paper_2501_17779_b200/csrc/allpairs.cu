@@ -178,33 +178,32 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       const double thr = best - pf::kTieRelTol * fmax(1.0, fabs(best));
       const double thrN = thr * (double)kM;
       const double thr2 = thr > 0.0 ? thrN * thrN : -1.0;
+      // each lane's smallest qualifying index (m = lane + 32 b + 64 r grows with
+      // (r, b)) and its value; the warp minimum's owner lane reports
       int cand = INT_MAX;
+      double2 fc = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int b = 0; b < kB; ++b)
+      for (int r = 0; r < kR; ++r)
 #pragma unroll
-        for (int r = 0; r < kR; ++r) {
-          const int m = lane + 32 * b + r * 64;
-          if (fma(v[b][r].x, v[b][r].x, v[b][r].y * v[b][r].y) >= thr2) cand = min(cand, m);
+        for (int b = 0; b < kB; ++b) {
+          const bool hit = fma(v[b][r].x, v[b][r].x, v[b][r].y * v[b][r].y) >= thr2;
+          if (cand == INT_MAX && hit) {
+            cand = lane + 32 * b + r * 64;
+            fc = v[b][r];
+          }
         }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
-      // the owner of m reports
       const int m = cand;
       const int64_t cell = (i0 + rr - row_begin) * count + j;
-#pragma unroll
-      for (int b = 0; b < kB; ++b)
-#pragma unroll
-        for (int r = 0; r < kR; ++r) {
-          if (lane + 32 * b + r * 64 == m) {
-            const double2 f = v[b][r];
-            const double tr = sqrt(fma(f.x, f.x, f.y * f.y)) * invN;
-            double e = invN * (__ldg(&ss[i0 + rr]) + sj) - 2.0 * invN * tr;
-            if (e < 0.0) e = 0.0;
-            energy[cell] = e;
-            shift[cell] = m;
-            theta[cell] = tr == 0.0 ? 0.0 : atan2(-f.y, f.x);
-          }
-        }
+      if (m != INT_MAX && lane == (m & 31)) {
+        const double tr = sqrt(fma(fc.x, fc.x, fc.y * fc.y)) * invN;
+        double e = invN * (__ldg(&ss[i0 + rr]) + sj) - 2.0 * invN * tr;
+        if (e < 0.0) e = 0.0;
+        energy[cell] = e;
+        shift[cell] = m;
+        theta[cell] = tr == 0.0 ? 0.0 : atan2(-fc.y, fc.x);
+      }
       if (m == INT_MAX && lane == 0) {  // non-finite correlation
         energy[cell] = __longlong_as_double(0x7ff8000000000000ULL);
         shift[cell] = 0;
