@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
     allpairs_kernel(const double2* __restrict__ za, const double2* __restrict__ zb,
                     const double* __restrict__ ss, int64_t count, int64_t row_begin, int64_t row_end,
                     int64_t col_chunk, const double2* __restrict__ tw, double* energy,
-                    int32_t* shift, double* theta) {
+                    int32_t* shift, double2* dm) {
   extern __shared__ __align__(16) char smem[];
   double2* rows = reinterpret_cast<double2*>(smem);  // kRowTile x kM spectra
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -202,16 +202,26 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
         if (e < 0.0) e = 0.0;
         energy[cell] = e;
         shift[cell] = m;
-        theta[cell] = tr == 0.0 ? 0.0 : atan2(-fc.y, fc.x);
+        dm[cell] = fc;  // theta = arg conj(F_m) in a coalesced pass (theta_kernel)
       }
       if (m == INT_MAX && lane == 0) {  // non-finite correlation
         energy[cell] = __longlong_as_double(0x7ff8000000000000ULL);
         shift[cell] = 0;
-        theta[cell] = __longlong_as_double(0x7ff8000000000000ULL);
+        dm[cell] = make_double2(__longlong_as_double(0x7ff8000000000000ULL), 0.0);
       }
       __syncwarp();
     }
   }
+}
+
+// theta per cell from the winning correlation value (one full warp of cells at
+// a time instead of one lane per cell inside allpairs_kernel): degenerate
+// (F_m = 0) -> 0, non-finite -> NaN (rigid_align.cpp:86-88, :83).
+__global__ void theta_kernel(const double2* __restrict__ dm, int64_t cells, double* theta) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cells) return;
+  const double2 f = dm[c];
+  theta[c] = (f.x == 0.0 && f.y == 0.0) ? 0.0 : atan2(-f.y, f.x);
 }
 
 }  // namespace ap
@@ -230,9 +240,11 @@ cudaError_t launch_spectra(const double2* curves, int64_t count, int N, const do
 
 bool allpairs_fast_supported(int N) { return N == ap::kM; }
 
+size_t allpairs_scratch_cells(int64_t rows, int64_t count) { return sizeof(double2) * (size_t)(rows * count); }
+
 cudaError_t launch_allpairs(const double2* za, const double2* zb, const double* ss, int64_t count,
                             int64_t row_begin, int64_t row_end, const double2* tw, double* energy,
-                            int32_t* shift, double* theta, cudaStream_t s) {
+                            int32_t* shift, double* theta, double2* dm, cudaStream_t s) {
   const size_t sm = sizeof(double2) * (size_t)(ap::kRowTile * ap::kM + ap::kWarps * pf::padded_len(ap::kM));
   cudaError_t e = cudaFuncSetAttribute((const void*)ap::allpairs_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -245,7 +257,9 @@ cudaError_t launch_allpairs(const double2* za, const double2* zb, const double* 
   const int64_t chunk = (count + splits - 1) / splits;
   dim3 grid(gx, (unsigned)splits);
   ap::allpairs_kernel<<<grid, ap::kWarps * 32, sm, s>>>(za, zb, ss, count, row_begin, row_end, chunk, tw,
-                                                         energy, shift, theta);
+                                                         energy, shift, dm);
+  const int64_t cells = rows * count;
+  ap::theta_kernel<<<(unsigned)((cells + 255) / 256), 256, 0, s>>>(dm, cells, theta);
   return cudaGetLastError();
 }
 

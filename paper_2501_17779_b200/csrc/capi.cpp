@@ -396,13 +396,16 @@ int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_beg
     // spectra once per curve (kept L2-resident), then one warp per cell
     void* ws = nullptr;
     const size_t zbytes = sizeof(double2) * (size_t)(count * M);
-    if (scratch_alloc(&ws, zbytes + sizeof(double) * (size_t)count, s) != cudaSuccess)
+    const size_t sbytes = (sizeof(double) * (size_t)count + 255) & ~size_t(255);
+    const size_t dbytes = cva::allpairs_scratch_cells(row_end - row_begin, count);
+    if (scratch_alloc(&ws, zbytes + sbytes + dbytes, s) != cudaSuccess)
       return fail(CVA_BAD_ALLOC, "scratch allocation failed");
     double2* za = (double2*)ws;
     double* ss = (double*)((char*)ws + zbytes);
+    double2* dm = (double2*)((char*)ws + zbytes + sbytes);
     cudaError_t e = cva::launch_spectra((const double2*)curves, count, (int)n, tw, za, za, ss, s);
     if (e == cudaSuccess)
-      e = cva::launch_allpairs(za, za, ss, count, row_begin, row_end, tw, energy, shift, theta, s);
+      e = cva::launch_allpairs(za, za, ss, count, row_begin, row_end, tw, energy, shift, theta, dm, s);
     cudaFreeAsync(ws, s);
     return finish(e, "allpairs launch");
   }

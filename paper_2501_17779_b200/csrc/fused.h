@@ -40,9 +40,10 @@ size_t allpairs_spectra_smem(int N);
 cudaError_t launch_spectra(const double2* curves, int64_t count, int N, const double2* tw, double2* za,
                            double2* zb, double* ss, cudaStream_t s);
 bool allpairs_fast_supported(int N);
+size_t allpairs_scratch_cells(int64_t rows, int64_t count);  // bytes of the per-cell scratch `dm`
 cudaError_t launch_allpairs(const double2* za, const double2* zb, const double* ss, int64_t count,
                             int64_t row_begin, int64_t row_end, const double2* tw, double* energy,
-                            int32_t* shift, double* theta, cudaStream_t s);
+                            int32_t* shift, double* theta, double2* dm, cudaStream_t s);
 
 cudaError_t launch_v2_srv_align(const double2* c1, const double2* c2, int64_t pairs, int N,
                                 const double2* tw, cva_alignment* out, double2* aligned,
