@@ -162,12 +162,21 @@ int finish(cudaError_t e, const char* what) {
 
 int large_align(const double* c1, const double* c2, int64_t pairs, int64_t n, int normalize,
                 cva_alignment* out, double* aligned, const double2* tw, cudaStream_t s) {
+  // four-step twiddle tables (sub-transform lengths and the two-level W_M)
+  cva::FourStepTw fst{};
+  const int M = cva::v2_fft_len((int)n), m1 = cva::four_step_m1(M);
+  if (m1) {
+    fst.lo = tw;
+    if (int rc = get_twiddles(m1, s, &fst.s1)) return rc;
+    if (int rc = get_twiddles(M / m1, s, &fst.s2)) return rc;
+    if (int rc = get_twiddles(M / 256, s, &fst.hi)) return rc;
+  }
   const int64_t chunk = std::min<int64_t>(pairs, cva::large_chunk_pairs((int)n));
   void* ws = nullptr;
   if (scratch_alloc(&ws, cva::large_workspace_bytes(chunk, (int)n), s) != cudaSuccess)
     return fail(CVA_BAD_ALLOC, "large-N workspace allocation failed");
   cudaError_t e = cva::launch_large_align((const double2*)c1, (const double2*)c2, pairs, (int)n, normalize, tw,
-                                          out, (double2*)aligned, ws, chunk, s);
+                                          m1 ? &fst : nullptr, out, (double2*)aligned, ws, chunk, s);
   cudaFreeAsync(ws, s);
   return finish(e, "large-N align launch");
 }

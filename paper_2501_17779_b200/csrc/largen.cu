@@ -351,6 +351,13 @@ __device__ __forceinline__ void wpass(double2* x, const double2* __restrict__ tw
   __syncwarp();
 }
 
+// W_M^e for e < M from two short tables (L1-resident): W_M^(256 h + l) =
+// hi[h] * lo[l], hi = W_{M/256}, lo = W_M^l (l < 256). One extra rounding
+// against the direct table entry.
+__device__ __forceinline__ double2 tw_m(const double2* __restrict__ lo, const double2* __restrict__ hi, int e) {
+  return cmul(__ldg(&hi[e >> 8]), __ldg(&lo[e & 255]));
+}
+
 template <int L, int Ns = 1>
 __device__ __forceinline__ void wfft(double2* x, const double2* __restrict__ tw, int twstride, int lane) {
   constexpr int R = radix_at<L, Ns>();
@@ -364,8 +371,9 @@ __device__ __forceinline__ void wfft(double2* x, const double2* __restrict__ tw,
 template <int M1>
 __global__ void __launch_bounds__(kT)
     f1_kernel(const double2* __restrict__ z1, const double2* __restrict__ z2, int64_t P, int N, int M2,
-              const double2* __restrict__ tw, const CurveNorm* __restrict__ n1, const CurveNorm* __restrict__ n2,
-              double2* U, double* sq1, double* sq2) {
+              const double2* __restrict__ twS, const double2* __restrict__ lo, const double2* __restrict__ hi,
+              const CurveNorm* __restrict__ n1, const CurveNorm* __restrict__ n2, double2* U, double* sq1,
+              double* sq2) {
   constexpr int VS = vstride<M1>();
   __shared__ __align__(16) double2 sm[kCT * VS];
   __shared__ double2 red[64];
@@ -392,13 +400,13 @@ __global__ void __launch_bounds__(kT)
   sq = block_sum(sq, red);  // syncs the tile too
   if (threadIdx.x == 0) (second ? sq2 : sq1)[p * gridDim.x + blockIdx.x] = sq;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  wfft<M1>(sm + w * VS, tw, M / M1, lane);
+  wfft<M1>(sm + w * VS, twS, 1, lane);
   __syncthreads();
   double2* u = U + sidx * (int64_t)M;
   for (int idx = threadIdx.x; idx < M1 * kCT; idx += kT) {
     const int k1 = idx / kCT, c = idx % kCT;
     const int n2 = c0 + c;
-    u[(int64_t)k1 * M2 + n2] = cmul(sm[c * VS + padL(k1)], __ldg(&tw[n2 * k1]));
+    u[(int64_t)k1 * M2 + n2] = cmul(sm[c * VS + padL(k1)], tw_m(lo, hi, n2 * k1));
   }
 }
 
@@ -406,7 +414,8 @@ __global__ void __launch_bounds__(kT)
 // curves, product, its row FFT and twiddle. grid (M1 / kRT, P).
 template <int M2>
 __global__ void __launch_bounds__(kT, 2)
-    fp_kernel(const double2* __restrict__ U, int64_t P, int M1, const double2* __restrict__ tw, double2* G) {
+    fp_kernel(const double2* __restrict__ U, int64_t P, int M1, const double2* __restrict__ twS,
+              const double2* __restrict__ lo, const double2* __restrict__ hi, double2* G) {
   constexpr int VS = vstride<M2>();
   extern __shared__ __align__(16) double2 smv[];  // 2 kRT vectors
   const int M = M1 * M2;
@@ -420,24 +429,24 @@ __global__ void __launch_bounds__(kT, 2)
     double2* x = smv + (h * kRT + w) * VS;
     for (int i = lane; i < M2; i += 32) x[padL(i)] = __ldg(&u[i]);
     __syncwarp();
-    wfft<M2>(x, tw, M / M2, lane);
+    wfft<M2>(x, twS, 1, lane);
   }
   // product Z1 conj(Z2) (same warp owns both rows), its row FFT, twiddle W_M^{k1 m2}
   double2* x = smv + w * VS;
   const double2* y = smv + (kRT + w) * VS;
   for (int i = lane; i < M2; i += 32) x[padL(i)] = cmulconj(x[padL(i)], y[padL(i)]);
   __syncwarp();
-  wfft<M2>(x, tw, M / M2, lane);
+  wfft<M2>(x, twS, 1, lane);
   const int k1 = r0 + w;
   double2* g = G + p * (int64_t)M + (int64_t)k1 * M2;
-  for (int m2 = lane; m2 < M2; m2 += 32) g[m2] = cmul(x[padL(m2)], __ldg(&tw[k1 * m2]));
+  for (int m2 = lane; m2 < M2; m2 += 32) g[m2] = cmul(x[padL(m2)], tw_m(lo, hi, k1 * m2));
 }
 
 // Column pass of the correlation transform: F[m2 + M2 m1] (natural order) and
 // the per-block max of |F|^2 over m < N. grid (M2 / kCT, P).
 template <int M1>
 __global__ void __launch_bounds__(kT)
-    p2_kernel(const double2* __restrict__ G, int64_t P, int N, int M2, const double2* __restrict__ tw, double2* F,
+    p2_kernel(const double2* __restrict__ G, int64_t P, int N, int M2, const double2* __restrict__ twS, double2* F,
               double* bmax) {
   constexpr int VS = vstride<M1>();
   __shared__ __align__(16) double2 sm[kCT * VS];
@@ -452,7 +461,7 @@ __global__ void __launch_bounds__(kT)
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  wfft<M1>(sm + w * VS, tw, M / M1, lane);
+  wfft<M1>(sm + w * VS, twS, 1, lane);
   __syncthreads();
   double2* f = F + p * (int64_t)M;
   double mx = -1.0;
@@ -535,7 +544,7 @@ Layout layout(int N) {
 }
 
 // Four-step split M = M1 x M2 with M1, M2 in {64, 128, 256} (M1 <= M2); 0 if none.
-int four_step_m1(int M) {
+int four_step_m1_impl(int M) {
   if (M < 4096 || M > 65536) return 0;
   int p = 0;
   while ((1 << p) < M) ++p;
@@ -543,52 +552,53 @@ int four_step_m1(int M) {
 }
 
 template <int M1>
-cudaError_t f1_launch(const double2* z1, const double2* z2, int64_t P, int N, int M2, const double2* tw,
+cudaError_t f1_launch(const double2* z1, const double2* z2, int64_t P, int N, int M2, const FourStepTw& t,
                       const ln::CurveNorm* n1, const ln::CurveNorm* n2, double2* U, double* q1, double* q2,
                       cudaStream_t s) {
   ln::fs::f1_kernel<M1><<<dim3((unsigned)(M2 / ln::fs::kCT), (unsigned)(2 * P)), ln::fs::kT, 0, s>>>(
-      z1, z2, P, N, M2, tw, n1, n2, U, q1, q2);
+      z1, z2, P, N, M2, t.s1, t.lo, t.hi, n1, n2, U, q1, q2);
   return cudaGetLastError();
 }
 template <int M1>
-cudaError_t p2_launch(const double2* G, int64_t P, int N, int M2, const double2* tw, double2* F, double* bmax,
+cudaError_t p2_launch(const double2* G, int64_t P, int N, int M2, const FourStepTw& t, double2* F, double* bmax,
                       cudaStream_t s) {
-  ln::fs::p2_kernel<M1><<<dim3((unsigned)(M2 / ln::fs::kCT), (unsigned)P), ln::fs::kT, 0, s>>>(G, P, N, M2, tw, F,
+  ln::fs::p2_kernel<M1><<<dim3((unsigned)(M2 / ln::fs::kCT), (unsigned)P), ln::fs::kT, 0, s>>>(G, P, N, M2, t.s1, F,
                                                                                                bmax);
   return cudaGetLastError();
 }
 template <int M2>
-cudaError_t fp_launch(const double2* U, int64_t P, int M1, const double2* tw, double2* G, cudaStream_t s) {
+cudaError_t fp_launch(const double2* U, int64_t P, int M1, const FourStepTw& t, double2* G, cudaStream_t s) {
   const size_t sm = sizeof(double2) * 2 * ln::fs::kRT * ln::fs::vstride<M2>();
   cudaError_t e = cudaFuncSetAttribute((const void*)ln::fs::fp_kernel<M2>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  ln::fs::fp_kernel<M2><<<dim3((unsigned)(M1 / ln::fs::kRT), (unsigned)P), ln::fs::kT, sm, s>>>(U, P, M1, tw, G);
+  ln::fs::fp_kernel<M2><<<dim3((unsigned)(M1 / ln::fs::kRT), (unsigned)P), ln::fs::kT, sm, s>>>(U, P, M1, t.s2, t.lo,
+                                                                                                 t.hi, G);
   return cudaGetLastError();
 }
 
 // The three passes of one chunk; F in natural order, bmax / sq partials per tile.
-cudaError_t four_step(int M1, const double2* z1, const double2* z2, int64_t P, int N, const double2* tw,
+cudaError_t four_step(int M1, const double2* z1, const double2* z2, int64_t P, int N, const FourStepTw& t,
                       const ln::CurveNorm* n1, const ln::CurveNorm* n2, double2* U, double2* G, double2* F,
                       double* q1, double* q2, double* bmax, cudaStream_t s) {
   const int M = pf::fft_len(N), M2 = M / M1;
   cudaError_t e;
   switch (M1) {
-    case 64: e = f1_launch<64>(z1, z2, P, N, M2, tw, n1, n2, U, q1, q2, s); break;
-    case 128: e = f1_launch<128>(z1, z2, P, N, M2, tw, n1, n2, U, q1, q2, s); break;
-    default: e = f1_launch<256>(z1, z2, P, N, M2, tw, n1, n2, U, q1, q2, s); break;
+    case 64: e = f1_launch<64>(z1, z2, P, N, M2, t, n1, n2, U, q1, q2, s); break;
+    case 128: e = f1_launch<128>(z1, z2, P, N, M2, t, n1, n2, U, q1, q2, s); break;
+    default: e = f1_launch<256>(z1, z2, P, N, M2, t, n1, n2, U, q1, q2, s); break;
   }
   if (e != cudaSuccess) return e;
   switch (M2) {
-    case 64: e = fp_launch<64>(U, P, M1, tw, G, s); break;
-    case 128: e = fp_launch<128>(U, P, M1, tw, G, s); break;
-    default: e = fp_launch<256>(U, P, M1, tw, G, s); break;
+    case 64: e = fp_launch<64>(U, P, M1, t, G, s); break;
+    case 128: e = fp_launch<128>(U, P, M1, t, G, s); break;
+    default: e = fp_launch<256>(U, P, M1, t, G, s); break;
   }
   if (e != cudaSuccess) return e;
   switch (M1) {
-    case 64: return p2_launch<64>(G, P, N, M2, tw, F, bmax, s);
-    case 128: return p2_launch<128>(G, P, N, M2, tw, F, bmax, s);
-    default: return p2_launch<256>(G, P, N, M2, tw, F, bmax, s);
+    case 64: return p2_launch<64>(G, P, N, M2, t, F, bmax, s);
+    case 128: return p2_launch<128>(G, P, N, M2, t, F, bmax, s);
+    default: return p2_launch<256>(G, P, N, M2, t, F, bmax, s);
   }
 }
 
@@ -614,9 +624,11 @@ int64_t large_chunk_pairs(int N) {
   return c < 1 ? 1 : c;
 }
 
+int four_step_m1(int M) { return four_step_m1_impl(M); }
+
 cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pairs, int N, int normalize,
-                               const double2* tw, cva_alignment* out, double2* aligned, void* ws,
-                               int64_t chunk, cudaStream_t s) {
+                               const double2* tw, const FourStepTw* fst, cva_alignment* out, double2* aligned,
+                               void* ws, int64_t chunk, cudaStream_t s) {
   const Layout Ly = layout(N);
   const int M = Ly.M, nblk = Ly.nblk, sqn = Ly.sqn;
   char* w = (char*)ws;
@@ -641,7 +653,7 @@ cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pai
   double2* rot = (double2*)take(sizeof(double2) * chunk);
   double* bmax = (double*)take(sizeof(double) * chunk * (nblk + M / 8));
   int* bcand = (int*)take(sizeof(int) * chunk * nblk);
-  const int fm1 = four_step_m1(M);
+  const int fm1 = fst ? four_step_m1_impl(M) : 0;
   cudaError_t e = cudaSuccess;
   for (int64_t p0 = 0; p0 < pairs && e == cudaSuccess; p0 += chunk) {
     const int64_t P = pairs - p0 < chunk ? pairs - p0 : chunk;
@@ -654,7 +666,7 @@ cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pai
     double2* F = nullptr;
     int nbmax = nblk, nsq = sqn;
     if (fm1) {  // four-step: U = A|B (2P sequences, adjacent), G = C, F = D
-      e = four_step(fm1, z1, z2, P, N, tw, n1, n2, A, C, D, q1, q2, bmax, s);
+      e = four_step(fm1, z1, z2, P, N, *fst, n1, n2, A, C, D, q1, q2, bmax, s);
       if (e != cudaSuccess) break;
       F = D;
       nbmax = nsq = (M / fm1) / ln::fs::kCT;
