@@ -116,10 +116,14 @@ __global__ void __launch_bounds__(kT)
 //   invariant; the reference centres first, a rounding-level difference).
 constexpr int kStatBlocks = 32;
 
+// curves y < P2 come from `curves`, the rest from `curves2` (one launch for
+// both curves of a chunk of pairs); P2 = gridDim.y when curves2 is null.
 __global__ void __launch_bounds__(kT)
-    stats_partial(const double2* __restrict__ curves, int N, double4* part) {
+    stats_partial(const double2* __restrict__ curves, int N, double4* part,
+                  const double2* __restrict__ curves2 = nullptr, int64_t P2 = 0) {
   __shared__ double2 red[64];
-  const double2* z = curves + (int64_t)blockIdx.y * N;
+  const int64_t y = blockIdx.y;
+  const double2* z = (curves2 && y >= P2) ? curves2 + (y - P2) * N : curves + y * N;
   double2 acc = make_double2(0, 0);
   double len = 0.0;
   int nf = 0;
@@ -475,6 +479,37 @@ __global__ void __launch_bounds__(kT)
   mx = block_max(mx, red);
   if (threadIdx.x == 0) bmax[p * gridDim.x + blockIdx.x] = mx;
 }
+// Tie-band candidate of the four-step layout (one CTA per pair): global max
+// from the column-tile maxima, then only tiles whose maximum reaches the band
+// are scanned (usually one) for the smallest m with |F_m|^2 >= thr^2.
+template <int M1>
+__global__ void __launch_bounds__(kT)
+    cand_kernel(const double2* __restrict__ F, int N, int M2, const double* __restrict__ bmax, int* cand_out) {
+  __shared__ double2 red[64];
+  const int64_t p = blockIdx.x;
+  const int nt = M2 / kCT, M = M1 * M2;
+  double best2 = -1.0;
+  for (int b = threadIdx.x; b < nt; b += kT) best2 = fmax(best2, bmax[p * nt + b]);
+  best2 = block_max(best2, red);
+  const double best = sqrt(best2) / (double)M;
+  const double thr = best - pf::kTieRelTol * fmax(1.0, fabs(best));
+  const double thrM = thr * (double)M;
+  const double thr2 = thr > 0.0 ? thrM * thrM : -1.0;
+  const double2* f = F + p * (int64_t)M;
+  int cand = INT_MAX;
+  for (int b = 0; b < nt; ++b) {
+    if (!(bmax[p * nt + b] >= thr2)) continue;  // uniform over the block
+    for (int idx = threadIdx.x; idx < M1 * kCT; idx += kT) {
+      const int m = (b * kCT + idx % kCT) + M2 * (idx / kCT);
+      if (m < N && m < cand) {
+        const double2 v = __ldg(&f[m]);
+        if (fma(v.x, v.x, v.y * v.y) >= thr2) cand = m;
+      }
+    }
+  }
+  cand = block_min_int(cand, red);
+  if (threadIdx.x == 0) cand_out[p] = isfinite(best) && best2 >= 0.0 ? cand : INT_MAX;
+}
 }  // namespace fs
 
 }  // namespace ln
@@ -641,15 +676,12 @@ cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pai
   double2* B = (double2*)take(sizeof(double2) * (size_t)M * chunk);
   double2* C = (double2*)take(sizeof(double2) * (size_t)M * chunk);
   double2* D = (double2*)take(sizeof(double2) * (size_t)M * chunk);
-  ln::CurveNorm* n1 = (ln::CurveNorm*)take(sizeof(ln::CurveNorm) * chunk);
-  ln::CurveNorm* n2 = (ln::CurveNorm*)take(sizeof(ln::CurveNorm) * chunk);
-  double4* sp1 = (double4*)take(sizeof(double4) * chunk * ln::kStatBlocks);
-  double4* sp2 = (double4*)take(sizeof(double4) * chunk * ln::kStatBlocks);
+  ln::CurveNorm* nn = (ln::CurveNorm*)take(sizeof(ln::CurveNorm) * 2 * chunk);   // curve 1s then curve 2s
+  double4* spp = (double4*)take(sizeof(double4) * 2 * chunk * ln::kStatBlocks);
   const int sqcap = sqn > M / 8 ? sqn : M / 8;
   double* q1 = (double*)take(sizeof(double) * chunk * sqcap);
   double* q2 = (double*)take(sizeof(double) * chunk * sqcap);
-  int32_t* b1 = (int32_t*)take(sizeof(int32_t) * chunk);
-  int32_t* b2 = (int32_t*)take(sizeof(int32_t) * chunk);
+  int32_t* bb = (int32_t*)take(sizeof(int32_t) * 2 * chunk);
   double2* rot = (double2*)take(sizeof(double2) * chunk);
   double* bmax = (double*)take(sizeof(double) * chunk * (nblk + M / 8));
   int* bcand = (int*)take(sizeof(int) * chunk * nblk);
@@ -659,10 +691,10 @@ cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pai
     const int64_t P = pairs - p0 < chunk ? pairs - p0 : chunk;
     const double2* z1 = c1 + p0 * N;
     const double2* z2 = c2 + p0 * N;
-    ln::stats_partial<<<dim3(ln::kStatBlocks, (unsigned)P), ln::kT, 0, s>>>(z1, N, sp1);
-    ln::stats_partial<<<dim3(ln::kStatBlocks, (unsigned)P), ln::kT, 0, s>>>(z2, N, sp2);
-    ln::stats_final<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(sp1, P, N, normalize, n1, b1);
-    ln::stats_final<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(sp2, P, N, normalize, n2, b2);
+    ln::CurveNorm *n1 = nn, *n2 = nn + P;
+    int32_t *b1 = bb, *b2 = bb + P;
+    ln::stats_partial<<<dim3(ln::kStatBlocks, (unsigned)(2 * P)), ln::kT, 0, s>>>(z1, N, spp, z2, P);
+    ln::stats_final<<<(unsigned)((2 * P + 7) / 8), 256, 0, s>>>(spp, 2 * P, N, normalize, nn, bb);
     double2* F = nullptr;
     int nbmax = nblk, nsq = sqn;
     if (fm1) {  // four-step: U = A|B (2P sequences, adjacent), G = C, F = D
@@ -681,8 +713,19 @@ cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pai
       if (e != cudaSuccess) break;
       ln::lmax_kernel<<<dim3((unsigned)nblk, (unsigned)P), ln::kT, 0, s>>>(F, M, N, bmax);
     }
-    ln::lcand_kernel<<<dim3((unsigned)nblk, (unsigned)P), ln::kT, 0, s>>>(F, M, N, bmax, nbmax, bcand);
-    ln::lpick_kernel<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(F, M, N, bcand, nblk, q1, q2, nsq, b1, b2, P, out + p0,
+    int ncand = nblk;
+    if (fm1) {
+      const int M2 = M / fm1;
+      switch (fm1) {
+        case 64: ln::fs::cand_kernel<64><<<(unsigned)P, ln::kT, 0, s>>>(F, N, M2, bmax, bcand); break;
+        case 128: ln::fs::cand_kernel<128><<<(unsigned)P, ln::kT, 0, s>>>(F, N, M2, bmax, bcand); break;
+        default: ln::fs::cand_kernel<256><<<(unsigned)P, ln::kT, 0, s>>>(F, N, M2, bmax, bcand); break;
+      }
+      ncand = 1;
+    } else {
+      ln::lcand_kernel<<<dim3((unsigned)nblk, (unsigned)P), ln::kT, 0, s>>>(F, M, N, bmax, nbmax, bcand);
+    }
+    ln::lpick_kernel<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(F, M, N, bcand, ncand, q1, q2, nsq, b1, b2, P, out + p0,
                                                              rot);
     if (aligned)
       ln::aligned_kernel<<<dim3((unsigned)((N + 4 * ln::kT - 1) / (4 * ln::kT)), (unsigned)P), ln::kT, 0, s>>>(
