@@ -390,7 +390,9 @@ __global__ void __launch_bounds__(kT)
   const int lim = (!second || M == N) ? N : 2 * N;
   const int c0 = blockIdx.x * kCT;
   double sq = 0.0;
-  for (int idx = threadIdx.x; idx < M1 * kCT; idx += kT) {
+#pragma unroll
+  for (int it = 0; it < M1 * kCT / kT; ++it) {  // all loads of the tile in flight
+    const int idx = threadIdx.x + it * kT;
     const int n1i = idx / kCT, c = idx % kCT;
     const int n = M2 * n1i + c0 + c;
     double2 v = make_double2(0.0, 0.0);
@@ -407,7 +409,9 @@ __global__ void __launch_bounds__(kT)
   wfft<M1>(sm + w * VS, twS, 1, lane);
   __syncthreads();
   double2* u = U + sidx * (int64_t)M;
-  for (int idx = threadIdx.x; idx < M1 * kCT; idx += kT) {
+#pragma unroll
+  for (int it = 0; it < M1 * kCT / kT; ++it) {
+    const int idx = threadIdx.x + it * kT;
     const int k1 = idx / kCT, c = idx % kCT;
     const int n2 = c0 + c;
     u[(int64_t)k1 * M2 + n2] = cmul(sm[c * VS + padL(k1)], tw_m(lo, hi, n2 * k1));
@@ -431,19 +435,22 @@ __global__ void __launch_bounds__(kT, 2)
   for (int h = 0; h < 2; ++h) {
     const double2* u = U + (h ? P + p : p) * (int64_t)M + (int64_t)(r0 + w) * M2;
     double2* x = smv + (h * kRT + w) * VS;
-    for (int i = lane; i < M2; i += 32) x[padL(i)] = __ldg(&u[i]);
+#pragma unroll
+    for (int i0 = 0; i0 < M2; i0 += 32) x[padL(i0 + lane)] = __ldg(&u[i0 + lane]);
     __syncwarp();
     wfft<M2>(x, twS, 1, lane);
   }
   // product Z1 conj(Z2) (same warp owns both rows), its row FFT, twiddle W_M^{k1 m2}
   double2* x = smv + w * VS;
   const double2* y = smv + (kRT + w) * VS;
-  for (int i = lane; i < M2; i += 32) x[padL(i)] = cmulconj(x[padL(i)], y[padL(i)]);
+#pragma unroll
+  for (int i0 = 0; i0 < M2; i0 += 32) x[padL(i0 + lane)] = cmulconj(x[padL(i0 + lane)], y[padL(i0 + lane)]);
   __syncwarp();
   wfft<M2>(x, twS, 1, lane);
   const int k1 = r0 + w;
   double2* g = G + p * (int64_t)M + (int64_t)k1 * M2;
-  for (int m2 = lane; m2 < M2; m2 += 32) g[m2] = cmul(x[padL(m2)], tw_m(lo, hi, k1 * m2));
+#pragma unroll
+  for (int i0 = 0; i0 < M2; i0 += 32) g[i0 + lane] = cmul(x[padL(i0 + lane)], tw_m(lo, hi, k1 * (i0 + lane)));
 }
 
 // Column pass of the correlation transform: F[m2 + M2 m1] (natural order) and
@@ -459,7 +466,9 @@ __global__ void __launch_bounds__(kT)
   const int64_t p = blockIdx.y;
   const int c0 = blockIdx.x * kCT;
   const double2* g = G + p * (int64_t)M;
-  for (int idx = threadIdx.x; idx < M1 * kCT; idx += kT) {
+#pragma unroll
+  for (int it = 0; it < M1 * kCT / kT; ++it) {
+    const int idx = threadIdx.x + it * kT;
     const int k1 = idx / kCT, c = idx % kCT;
     sm[c * VS + padL(k1)] = __ldg(&g[(int64_t)k1 * M2 + c0 + c]);
   }
@@ -469,7 +478,9 @@ __global__ void __launch_bounds__(kT)
   __syncthreads();
   double2* f = F + p * (int64_t)M;
   double mx = -1.0;
-  for (int idx = threadIdx.x; idx < M1 * kCT; idx += kT) {
+#pragma unroll
+  for (int it = 0; it < M1 * kCT / kT; ++it) {
+    const int idx = threadIdx.x + it * kT;
     const int m1 = idx / kCT, c = idx % kCT;
     const int m = (c0 + c) + M2 * m1;
     const double2 v = sm[c * VS + padL(m1)];
