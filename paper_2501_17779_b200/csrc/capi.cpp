@@ -379,13 +379,9 @@ int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
   if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
-  void* ws = nullptr;
-  if (scratch_alloc(&ws, 2 * sizeof(double2) * (size_t)(pairs * n), s) != cudaSuccess)
-    return fail(CVA_BAD_ALLOC, "scratch allocation failed");
-  cudaError_t e = cva::launch_v2_srv_align((const double2*)c1, (const double2*)c2, pairs, (int)n,
-                                           tw, out, (double2*)aligned_q, (double2*)ws, s);
-  cudaFreeAsync(ws, s);
-  return finish(e, "srv_align launch");
+  return finish(cva::launch_v2_srv_align((const double2*)c1, (const double2*)c2, pairs, (int)n, tw, out,
+                                         (double2*)aligned_q, s),
+                "srv_align launch");
 }
 
 int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_begin, int64_t row_end,

@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kT, 2)
   }
   __syncthreads();
   pf::PairIn in{Z1, al, A.centroid, B.centroid, A.inv_len, B.inv_len};
-  pf::pair_stage<false, N, true, true>(in, bufs, N, tw, out + p, al, red);
+  pf::pair_stage<false, N, true, 1>(in, bufs, N, tw, out + p, al, red);
 }
 
 // ------------------------------------------------------------- preprocess
@@ -208,58 +208,93 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
 
 // ------------------------------------------------------------------- SRV
 
-// q_l = d_l / sqrt(|d_l|), d_l = (N/2)(c[l+1] - c[l-1]); 0 if |d_l| < 1e-8 N (srv.cpp:71-88)
-__device__ __forceinline__ double2 srv_at(const double2* __restrict__ c, int l, int N) {
-  const double nn = (double)N;
-  const double2 nx = c[l + 1 == N ? 0 : l + 1], pv = c[l == 0 ? N - 1 : l - 1];
-  const double2 d = make_double2((nn / 2.0) * (nx.x - pv.x), (nn / 2.0) * (nx.y - pv.y));
-  const double mag = sqrt(fma(d.x, d.x, d.y * d.y));
-  if (mag < 1e-8 * nn) return make_double2(0.0, 0.0);
-  const double r = 1.0 / sqrt(mag);
-  return make_double2(r * d.x, r * d.y);
-}
-
 // SRV alignment (srv_transform -> srv_center -> align_fft, the (t0,R) step of
-// elastic.cpp:138-139). The centered SRVs are written to `qbuf` (this pair's
-// 2N scratch rows in global memory / L2) and aligned by the pair stage.
+// elastic.cpp:138-139). Both raw curves arrive by TMA bulk copy in the
+// transform buffers they will be read from; the SRVs are formed from shared
+// memory into the padded layout the first transform pass reads (the input
+// buffers of that pass: in place at M = 2048, the ping-pong partner
+// otherwise), and the aligned output recomputes q2 from the raw curve (L2).
 template <bool kIP, int kN>
 __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
     srv_align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
-                     const double2* __restrict__ tw, cva_alignment* __restrict__ out,
-                     double2* aligned, double2* qbuf) {
+                     const double2* __restrict__ tw, cva_alignment* __restrict__ out, double2* aligned) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double2 red[16];
+  __shared__ uint64_t mbar;
+  constexpr int kMaxPer = 8;  // N / kT values per thread (N <= 2048)
+  if constexpr (kN > 0) N = kN;
   const int64_t p = blockIdx.x;
   const double2* a = c1 + p * N;
   const double2* b = c2 + p * N;
-  double2* q1 = qbuf + 2 * p * N;
-  double2* q2 = q1 + N;
-  int bad = 0;
-  double2 m1 = make_double2(0, 0), m2 = make_double2(0, 0);
-  for (int l = threadIdx.x; l < N; l += kT) {
-    const double2 u = a[l], v = b[l];
-    bad |= !(isfinite(u.x) && isfinite(u.y) && isfinite(v.x) && isfinite(v.y));
-    const double2 x = srv_at(a, l, N), y = srv_at(b, l, N);
-    q1[l] = x;
-    q2[l] = y;
-    m1 = cadd(m1, x);
-    m2 = cadd(m2, y);
+  const int NP = pf::padded_len(pf::fft_len(N));
+  double2* bufs = reinterpret_cast<double2*>(smem);
+  double2* qa = kIP ? bufs : bufs + NP;           // B0 (in place) or B1
+  double2* qb = kIP ? bufs + NP : bufs + 3 * NP;  // B2 (in place: bufs + NP) or B3
+  bulk_init(&mbar);
+  if (threadIdx.x == 0) {  // both raw curves on one mbarrier phase
+    const uint32_t bytes = (uint32_t)N * 16u, bar = smem_u32(&mbar);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(qa)),
+                 "l"(a), "r"(bytes), "r"(bar)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(qb)),
+                 "l"(b), "r"(bytes), "r"(bar)
+                 : "memory");
   }
-  double bs = bad ? 1.0 : 0.0;
-  rs::block_sum3(m1.x, m1.y, bs, red);
-  double m2y = m2.y, dummy = 0.0;
-  rs::block_sum3(m2.x, m2y, dummy, red);
+  {
+    uint32_t done = 0;
+    do {
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}"
+          : "=r"(done)
+          : "r"(smem_u32(&mbar))
+          : "memory");
+    } while (!done);
+  }
+  // one curve at a time (half the live registers): SRV of the raw samples into
+  // registers, a barrier (every raw read done), then the padded write in place
+  int bad = 0;
+  double2 mean[2];
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    double2* qc = h ? qb : qa;
+    double2 x[kMaxPer];
+    double2 m = make_double2(0, 0);
+#pragma unroll
+    for (int q = 0; q < kMaxPer; ++q) {
+      const int l = threadIdx.x + q * kT;
+      if (l < N) {
+        const double2 u = qc[l];
+        bad |= !(isfinite(u.x) && isfinite(u.y));
+        x[q] = pf::srv_at(qc, l, N);
+        m = cadd(m, x[q]);
+      }
+    }
+    double mz = 0.0;
+    rs::block_sum3(m.x, m.y, mz, red);  // its barriers order every raw read before the writes
+    mean[h] = m;
+#pragma unroll
+    for (int q = 0; q < kMaxPer; ++q) {
+      const int l = threadIdx.x + q * kT;
+      if (l < N) qc[pf::pad(l)] = x[q];
+    }
+  }
+  bad = __syncthreads_or(bad);
   double2* al = aligned ? aligned + p * N : nullptr;
-  if (bs != 0.0) {
+  if (bad) {
     if (threadIdx.x == 0) write_bad(out + p, CVA_INVALID_ARGUMENT);
     if (al)
       for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
     return;
   }
+  const double2 m1 = mean[0];
+  const double m2x = mean[1].x, m2y = mean[1].y;
   const double invn = 1.0 / (double)N;  // srv_center (srv.cpp:90-98)
-  pf::PairIn in{q1, q2, make_double2(invn * m1.x, invn * m1.y), make_double2(invn * m2.x, invn * m2y),
-                1.0, 1.0};
-  pf::pair_stage<kIP, kN>(in, reinterpret_cast<double2*>(smem), N, tw, out + p, al, red);
+  pf::PairIn in{qa, qb, make_double2(invn * m1.x, invn * m1.y), make_double2(invn * m2x, invn * m2y), 1.0, 1.0, b};
+  pf::pair_stage<kIP, kN, false, 2>(in, bufs, N, tw, out + p, al, red);
 }
 
 }  // namespace v2
@@ -416,26 +451,24 @@ cudaError_t launch_unpack_row(const cva_alignment* in, int64_t count, double* en
 
 template <bool kIP, int kN>
 static cudaError_t launch_srv_n(const double2* c1, const double2* c2, int64_t pairs, int N,
-                                const double2* tw, cva_alignment* out, double2* aligned,
-                                double2* qbuf, size_t sm, cudaStream_t s) {
+                                const double2* tw, cva_alignment* out, double2* aligned, size_t sm, cudaStream_t s) {
   cudaError_t e = set_smem((const void*)v2::srv_align_kernel<kIP, kN>, sm);
   if (e != cudaSuccess) return e;
-  v2::srv_align_kernel<kIP, kN><<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, tw, out, aligned, qbuf);
+  v2::srv_align_kernel<kIP, kN><<<(unsigned)pairs, v2::kT, sm, s>>>(c1, c2, N, tw, out, aligned);
   return cudaGetLastError();
 }
 
 cudaError_t launch_v2_srv_align(const double2* c1, const double2* c2, int64_t pairs, int N,
-                                const double2* tw, cva_alignment* out, double2* aligned,
-                                double2* qbuf, cudaStream_t s) {
+                                const double2* tw, cva_alignment* out, double2* aligned, cudaStream_t s) {
   const size_t sm = v2_align_smem(N);
   switch (N) {
-    case 2048: return launch_srv_n<true, 2048>(c1, c2, pairs, N, tw, out, aligned, qbuf, sm, s);
-    case 1024: return launch_srv_n<false, 1024>(c1, c2, pairs, N, tw, out, aligned, qbuf, sm, s);
-    case 512: return launch_srv_n<false, 512>(c1, c2, pairs, N, tw, out, aligned, qbuf, sm, s);
+    case 2048: return launch_srv_n<true, 2048>(c1, c2, pairs, N, tw, out, aligned, sm, s);
+    case 1024: return launch_srv_n<false, 1024>(c1, c2, pairs, N, tw, out, aligned, sm, s);
+    case 512: return launch_srv_n<false, 512>(c1, c2, pairs, N, tw, out, aligned, sm, s);
     default: break;
   }
-  if (v2_inplace(N)) return launch_srv_n<true, 0>(c1, c2, pairs, N, tw, out, aligned, qbuf, sm, s);
-  return launch_srv_n<false, 0>(c1, c2, pairs, N, tw, out, aligned, qbuf, sm, s);
+  if (v2_inplace(N)) return launch_srv_n<true, 0>(c1, c2, pairs, N, tw, out, aligned, sm, s);
+  return launch_srv_n<false, 0>(c1, c2, pairs, N, tw, out, aligned, sm, s);
 }
 
 }  // namespace cva

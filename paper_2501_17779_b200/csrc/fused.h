@@ -46,7 +46,6 @@ cudaError_t launch_allpairs(const double2* za, const double2* zb, const double* 
                             int32_t* shift, double* theta, double2* dm, cudaStream_t s);
 
 cudaError_t launch_v2_srv_align(const double2* c1, const double2* c2, int64_t pairs, int N,
-                                const double2* tw, cva_alignment* out, double2* aligned,
-                                double2* qbuf, cudaStream_t s);
+                                const double2* tw, cva_alignment* out, double2* aligned, cudaStream_t s);
 
 }  // namespace cva

@@ -197,7 +197,21 @@ struct PairIn {
   const double2* z2;  // curve 2 samples (global or shared), uncentered
   double2 g1, g2;     // centroids subtracted on load
   double sc1, sc2;    // scale applied after centering (1 for already-normalized input)
+  // optional: the raw curve whose SRV z2 holds (global memory); the aligned
+  // output then recomputes z2[j] = srv_at(srv2, j) because z2 was overwritten
+  const double2* srv2 = nullptr;
 };
+
+// q_l = d_l / sqrt(|d_l|), d_l = (N/2)(c[l+1] - c[l-1]); 0 if |d_l| < 1e-8 N (srv.cpp:71-88)
+__device__ __forceinline__ double2 srv_at(const double2* c, int l, int N) {
+  const double nn = (double)N;
+  const double2 nx = c[l + 1 == N ? 0 : l + 1], pv = c[l == 0 ? N - 1 : l - 1];
+  const double2 d = make_double2((nn / 2.0) * (nx.x - pv.x), (nn / 2.0) * (nx.y - pv.y));
+  const double mag = sqrt(fma(d.x, d.x, d.y * d.y));
+  if (mag < 1e-8 * nn) return make_double2(0.0, 0.0);
+  const double r = 1.0 / sqrt(mag);
+  return make_double2(r * d.x, r * d.y);
+}
 
 // 1 / polygon length (curve.cpp:17-25) of each curve, measured by the pair
 // stage while it loads the samples (kLenOnLoad); {NaN, NaN} flags a bad pair.
@@ -231,9 +245,9 @@ __host__ __device__ inline int fft_len(int N) {
 // run on the centered, unscaled curves) and the scales 1/len are applied to
 // the correlation spectrum, the energies and the aligned curve. A length that
 // is not finite and > 0 marks the pair invalid (preprocess: curve.cpp:41-48).
-// kPadZ1: in.z1 is shared memory in the resampler's padded layout
-// z1[l + (l >> 3)].
-template <bool kInPlace = false, int kN = 0, bool kLenOnLoad = false, bool kPadZ1 = false>
+// kPad: 1 = in.z1 is shared memory in the padded layout z1[l + (l >> 3)]
+// (the resampler's and the transform buffers' layout); 2 = in.z1 and in.z2 both.
+template <bool kInPlace = false, int kN = 0, bool kLenOnLoad = false, int kPad = 0>
 __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
                                   const double2* __restrict__ tw, cva_alignment* out,
                                   double2* aligned, double2* red) {
@@ -260,7 +274,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     auto load = [&](int i) {
       if (i >= lim) return make_double2(0.0, 0.0);
       const int k = i < N ? i : i - N;
-      const bool padded = kPadZ1 && grp == 0;
+      const bool padded = kPad == 2 || (kPad == 1 && grp == 0);
       const double2 q = src[padded ? k + (k >> 3) : k];
       const double2 z = make_double2((q.x - c.x) * sc, (q.y - c.y) * sc);
       if (i < N) {
@@ -438,7 +452,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     for (int q = 0; q < kMaxPer; ++q) {
       const int j = t + q * kT;
       if (j < N) {
-        const double2 z = in.z2[j];
+        const double2 z = in.srv2 ? srv_at(in.srv2, j, N) : in.z2[j];
         const double2 p = make_double2((z.x - c.x) * sc, (z.y - c.y) * sc);
         v[q] = make_double2(fma(rot.x, p.x, rot.y * p.y), fma(-rot.y, p.x, rot.x * p.y));
       }
