@@ -160,7 +160,6 @@ def algorithmic_bytes(offs, pairs, N):
 def run_reference_arm_e1(args):
     """The reference's elastic_distance_approach2 (oracle/_ref) on all host
     threads over a bounded sample of E1's ordered pairs per step."""
-    import paper_2501_17779_b200 as cva
     from paper_2501_17779_b200 import synth
 
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -195,7 +194,6 @@ def run_reference_arm_e1(args):
                          "sample": f"{sample} E1 ordered pairs per step, reference elastic.cpp/srv.cpp sources"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    del cva
     print(json.dumps(line), flush=True)
 
 

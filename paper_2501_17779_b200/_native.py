@@ -11,6 +11,8 @@ import os
 from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
+# CVA_LIB_PATH: developer override to A/B an alternative build of the same
+# library (tools/variant.sh); unset in normal use.
 LIB_PATH = os.environ.get("CVA_LIB_PATH") or os.path.join(_HERE, "libcurvalign_cuda.so")
 SYNTH_PATH = os.path.join(_HERE, "libcurvalign_synth.so")
 
