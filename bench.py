@@ -145,10 +145,30 @@ def cpu_reference_run(pts, offs, pairs, N, seconds=12.0, threads=None, max_pairs
         lib.batch(pts[offs[2 * done]:offs[2 * p1]], sub, N, mode=0, threads=threads)
         done = p1
     dt = time.perf_counter() - t0
+    # single-thread figure on a short sample (T = 1 and T = all cores)
+    t1_pairs, t1 = 0, time.perf_counter()
+    while t1_pairs < limit and (time.perf_counter() - t1) < 2.0:
+        p1 = min(limit, t1_pairs + 16)
+        sub = offs[2 * t1_pairs:2 * p1 + 1] - offs[2 * t1_pairs]
+        lib.batch(pts[offs[2 * t1_pairs]:offs[2 * p1]], sub, N, mode=0, threads=1)
+        t1_pairs = p1
+    dt1 = time.perf_counter() - t1
     return {"value": done / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "value_1_thread": t1_pairs / dt1, "cpu_model": cpu_model(),
             "sample": f"{done} C1 pairs (of {pairs}) in {dt:.1f}s, {threads} threads, "
                       "reference sources + FFTW/Eigen shims" if kind == "reference" else
                       f"{done} C1 pairs in {dt:.1f}s, C oracle port, {threads} threads"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical CPUs)"
+    except OSError:
+        pass
+    return f"{os.cpu_count()} logical CPUs"
 
 
 def algorithmic_bytes(offs, pairs, N):
