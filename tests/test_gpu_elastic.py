@@ -271,3 +271,38 @@ def test_srv_utilities_match_reference(cuda, reference):  # test_srv.cpp:130-176
         cva.dp_step_cost(q, q2, 0, 0, 0, 1)
     with pytest.raises(ValueError):
         cva.apply_srv_action(q, 0.0, 0.0, ident[::-1])  # not a monotone warp (srv.cpp:58-69)
+
+
+# ------------------------------------------------- other shapes of the kernels
+
+
+def test_dp_n512_global_parent_slab(cuda, reference):
+    """n = 512: the DP parents no longer fit in shared memory and go to a
+    per-CTA global slab; still bitwise the reference."""
+    q1, q2 = srv_pair(reference, 512, 3)
+    g, e, st = cva.dp_reparam_batch(q1[None], q2[None])
+    rg, re_, rst = reference.dp_reparam_batch(q1[None], q2[None])
+    assert st[0] == rst[0] == 0
+    np.testing.assert_array_equal(g, rg)
+    np.testing.assert_array_equal(e, re_)
+
+
+def test_approach2_n512_matches_reference(cuda, reference):
+    c1, c2 = _pairs(reference, 512, 2, seed0=61)
+    _check_vs_reference(cva.elastic_approach2_batch(c1, c2), reference.elastic_approach2_batch(c1, c2, threads=2))
+
+
+@pytest.mark.parametrize("w", [2, 3])
+def test_approach2_other_slopes_match_reference(cuda, reference, w):
+    c1, c2 = _pairs(reference, 64, 4, seed0=71)
+    g = cva.elastic_approach2_batch(c1, c2, max_slope=w)
+    r = reference.elastic_approach2_batch(c1, c2, max_slope=w, threads=4)
+    _check_vs_reference(g, r)
+
+
+def test_approach2_iteration_cap_and_tolerance(cuda, reference):
+    c1, c2 = _pairs(reference, 64, 4, seed0=81)
+    for it, tol in ((1, 1e-6), (3, 0.0), (0, 1e-6)):
+        g = cva.elastic_approach2_batch(c1, c2, max_iters=it, energy_tol=tol)
+        r = reference.elastic_approach2_batch(c1, c2, max_iters=it, energy_tol=tol, threads=4)
+        _check_vs_reference(g, r)
