@@ -2,7 +2,11 @@
 #   make            -> product library + harness + oracle (+ reference oracle if /root/reference exists)
 #   make lib        -> paper_2501_17779_b200/libcurvalign_cuda.so
 NVCC     ?= /usr/local/cuda/bin/nvcc
-CXX      ?= g++
+# Host C++ libraries are loaded into processes (Python, user binaries) that map
+# the system libstdc++.so.6: link it dynamically (the image's default $CXX,
+# /opt/gcc/bin/g++, would link libstdc++.a, whose separate iostream/locale
+# state is unsafe next to the shared one).
+CXX      := $(if $(wildcard /usr/bin/g++),/usr/bin/g++,$(CXX))
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS  := $(ARCH) $(EXTRA) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 PKG      := paper_2501_17779_b200

@@ -436,5 +436,53 @@ class Reference(_ElasticShared, _Base):
         return out
 
 
+class _RefFormats:
+    """proj/src/io.cpp through oracle/_ref (strings returned via a buffer)."""
+
+    def _str(self, name, argtypes, *args):
+        buf = ctypes.create_string_buffer(1 << 22)
+        ln = np.zeros(1, dtype=np.int64)
+        f = self._fn(name, argtypes + [c_void_p, c_int64, c_void_p])
+        _raise(f(*args, ctypes.addressof(buf), len(buf), _p(ln)), name)
+        return buf.raw[: int(ln[0])].decode()
+
+    def load_curve(self, path):
+        out = np.zeros((1 << 20, 2))
+        n = np.zeros(1, dtype=np.int64)
+        f = self._fn("load_curve", [ctypes.c_char_p, c_void_p, c_int64, c_void_p])
+        _raise(f(path.encode(), _p(out), out.shape[0], _p(n)), "load_curve")
+        return out[: int(n[0])].copy()
+
+    def write_curve(self, path, c, json=False):
+        a = _f64(c)
+        f = self._fn("write_curve", [ctypes.c_char_p, c_void_p, c_int64, c_int])
+        _raise(f(path.encode(), _p(a), a.shape[0], 1 if json else 0), "write_curve")
+
+    def curve_to_csv(self, c):
+        a = _f64(c)
+        return self._str("curve_to_csv", [c_void_p, c_int64], _p(a), a.shape[0])
+
+    def curve_to_json(self, c):
+        a = _f64(c)
+        return self._str("curve_to_json", [c_void_p, c_int64], _p(a), a.shape[0])
+
+    def alignment_to_json(self, rec):
+        r = np.ascontiguousarray(np.asarray(rec, dtype=ALIGNMENT_DTYPE).reshape(1))
+        return self._str("alignment_to_json", [c_void_p], r.ctypes.data)
+
+    def elastic_to_json(self, t0, theta, gamma, distance, iterations, converged):
+        g = _f64(gamma)
+        return self._str("elastic_to_json", [c_double, c_double, c_void_p, c_int64, c_double, c_int, c_int],
+                         t0, theta, _p(g), g.shape[0], distance, int(iterations), int(converged))
+
+    def matrix_to_csv(self, names, d):
+        m = _f64(d)
+        return self._str("matrix_to_csv", [ctypes.c_char_p, c_int64, c_void_p], "\n".join(names).encode(),
+                         m.shape[0], _p(m))
+
+
+Reference.__bases__ = (_RefFormats,) + Reference.__bases__
+
+
 def reference_available() -> bool:
     return os.path.exists(REF_PATH)

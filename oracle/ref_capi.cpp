@@ -21,6 +21,7 @@
 #include "curvalign/curve.hpp"
 #include "curvalign/elastic.hpp"
 #include "curvalign/fft.hpp"
+#include "curvalign/io.hpp"
 #include "curvalign/rigid_align.hpp"
 #include "curvalign/spline.hpp"
 #include "curvalign/srv.hpp"
@@ -501,6 +502,94 @@ int ref_distance_matrix(const double* curves, int64_t count, int64_t n_in, int64
     for (int64_t i = 0; i < count; ++i)
       for (int64_t j = 0; j < count; ++j) out[i * count + j] = d[i][j];
   });
+}
+
+// ---- file formats (proj/src/io.cpp): strings returned through (buf, cap) ----
+
+static int put(const std::string& v, char* buf, int64_t cap, int64_t* len) {
+  *len = (int64_t)v.size();
+  if ((int64_t)v.size() + 1 > cap) return kOther;
+  std::memcpy(buf, v.c_str(), v.size() + 1);
+  return kOk;
+}
+
+int ref_load_curve(const char* path, double* out, int64_t cap_nodes, int64_t* n) {
+  return guard([&] {
+    const Curve c = load_curve(path);
+    *n = (int64_t)c.size();
+    if ((int64_t)c.size() > cap_nodes) throw std::runtime_error("capacity");
+    from_points(c.nodes, out);
+  });
+}
+
+int ref_curve_to_csv(const double* xy, int64_t n, char* buf, int64_t cap, int64_t* len) {
+  int rc = kOk;
+  const int g = guard([&] { rc = put(curve_to_csv(to_curve(xy, n)), buf, cap, len); });
+  return g ? g : rc;
+}
+
+int ref_curve_to_json(const double* xy, int64_t n, char* buf, int64_t cap, int64_t* len) {
+  int rc = kOk;
+  const int g = guard([&] { rc = put(curve_to_json(to_curve(xy, n)), buf, cap, len); });
+  return g ? g : rc;
+}
+
+int ref_write_curve(const char* path, const double* xy, int64_t n, int json) {
+  return guard([&] { json ? write_curve_json(path, to_curve(xy, n)) : write_curve_csv(path, to_curve(xy, n)); });
+}
+
+int ref_alignment_to_json(const ref_alignment* a, char* buf, int64_t cap, int64_t* len) {
+  int rc = kOk;
+  const int g = guard([&] {
+    RigidAlignment r;
+    r.shift = (std::size_t)a->shift;
+    r.t0 = a->t0;
+    r.rotation = Rotation2(a->theta);
+    r.trace = a->trace;
+    r.energy = a->energy;
+    r.degenerate = a->degenerate != 0;
+    rc = put(alignment_to_json(r), buf, cap, len);
+  });
+  return g ? g : rc;
+}
+
+int ref_elastic_to_json(double t0, double theta, const double* gamma, int64_t n_gamma, double distance,
+                        int iterations, int converged, char* buf, int64_t cap, int64_t* len) {
+  int rc = kOk;
+  const int g = guard([&] {
+    ElasticMatch m;
+    m.t0 = t0;
+    m.rotation = Rotation2(theta);
+    m.gamma.gamma.assign(gamma, gamma + n_gamma);
+    m.distance = distance;
+    m.iterations = iterations;
+    m.converged = converged != 0;
+    rc = put(elastic_to_json(m), buf, cap, len);
+  });
+  return g ? g : rc;
+}
+
+// names: k labels separated by '\n'; d: k x k row-major
+int ref_matrix_to_csv(const char* names, int64_t k, const double* d, char* buf, int64_t cap, int64_t* len) {
+  int rc = kOk;
+  const int g = guard([&] {
+    std::vector<std::string> nm;
+    std::string cur;
+    for (const char* p = names; *p; ++p) {
+      if (*p == '\n') {
+        nm.push_back(cur);
+        cur.clear();
+      } else {
+        cur += *p;
+      }
+    }
+    nm.push_back(cur);
+    std::vector<std::vector<double>> m((std::size_t)k, std::vector<double>((std::size_t)k));
+    for (int64_t i = 0; i < k; ++i)
+      for (int64_t j = 0; j < k; ++j) m[(std::size_t)i][(std::size_t)j] = d[i * k + j];
+    rc = put(matrix_to_csv(nm, m), buf, cap, len);
+  });
+  return g ? g : rc;
 }
 
 }  // extern "C"

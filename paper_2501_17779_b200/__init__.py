@@ -37,7 +37,30 @@ from .api import (  # noqa: F401
     srv_align_batch,
 )
 
+from .formats import (  # noqa: F401
+    alignment_to_json,
+    curve_to_csv,
+    curve_to_json,
+    elastic_to_json,
+    load_curve,
+    matrix_to_csv,
+    read_curve_csv,
+    read_curve_json,
+    write_curve_csv,
+    write_curve_json,
+)
+
 __all__ = [
+    "alignment_to_json",
+    "curve_to_csv",
+    "curve_to_json",
+    "elastic_to_json",
+    "load_curve",
+    "matrix_to_csv",
+    "read_curve_csv",
+    "read_curve_json",
+    "write_curve_csv",
+    "write_curve_json",
     "ElasticMatch",
     "RigidAlignment",
     "apply_srv_action",

@@ -6,7 +6,11 @@
 // (the reference's synthetic.cpp generators are outside this library).
 // Exit status = number of failed checks.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
+#include <fstream>
+#include <sstream>
+#include <unistd.h>
 #include <functional>
 #include <random>
 #include <stdexcept>
@@ -16,6 +20,7 @@
 #include "curvalign/curve.hpp"
 #include "curvalign/elastic.hpp"
 #include "curvalign/fft.hpp"
+#include "curvalign/io.hpp"
 #include "curvalign/rigid_align.hpp"
 #include "curvalign/spline.hpp"
 #include "curvalign/srv.hpp"
@@ -516,6 +521,57 @@ int main() {
     const auto r = elastic_distance_batch(a, b, DistanceMethod::approach2);
     for (int p = 0; p < 2; ++p) CHECK(r[p].distance == elastic_distance_approach2(a[p], b[p]).distance);
   });
+
+  // --------------------------------------------------------------- file formats
+  const std::string tmpdir = "/tmp/cva_dropin_io_" + std::to_string((long)getpid());
+  std::system(("mkdir -p " + tmpdir).c_str());
+  auto tpath = [&](const char* n) { return tmpdir + "/" + n; };
+  auto write_text = [](const std::string& p, const std::string& t) { std::ofstream(p, std::ios::binary) << t; };
+  run("io round trips", [&] {  // test_io_cli.cpp:50-72, :110-118
+    const Curve c = limacon(32);
+    write_curve_csv(tpath("r.csv"), c);
+    write_curve_json(tpath("r.json"), c);
+    for (const char* f : {"r.csv", "r.json"}) {
+      const Curve b = load_curve(tpath(f));
+      CHECK(b.size() == c.size());
+      for (std::size_t i = 0; i < c.size(); ++i) CHECK(b[i].x == c[i].x && b[i].y == c[i].y);
+    }
+  });
+  run("io csv header / duplicate / malformed", [&] {  // test_io_cli.cpp:74-98
+    write_text(tpath("h.csv"), "x,y\n1,0\n0,1\n-1,0\n0,-1\n1,0\n");
+    const Curve c = read_curve_csv(tpath("h.csv"));
+    CHECK(c.size() == 4 && c[0].x == 1.0 && c[3].y == -1.0);
+    write_text(tpath("b1.csv"), "1,2\nthree\n4,5\n6,7\n");
+    write_text(tpath("b2.csv"), "x,y\n1,2\nalpha,beta\n3,4\n5,6\n");
+    write_text(tpath("few.csv"), "1,2\n3,4\n");
+    CHECK(throws<std::runtime_error>([&] { read_curve_csv(tpath("b1.csv")); }));
+    CHECK(throws<std::runtime_error>([&] { read_curve_csv(tpath("b2.csv")); }));
+    CHECK(throws<std::invalid_argument>([&] { read_curve_csv(tpath("few.csv")); }));
+    CHECK(throws<std::runtime_error>([&] { read_curve_csv(tpath("none.csv")); }));
+  });
+  run("io json schema", [&] {  // test_io_cli.cpp:100-108
+    write_text(tpath("bad.json"), "{\"points\": [[0, 0]]}");
+    write_text(tpath("rag.json"), "{\"nodes\": [[0, 0, 0], [1, 1]]}");
+    CHECK(throws<std::runtime_error>([&] { read_curve_json(tpath("bad.json")); }));
+    CHECK(throws<std::runtime_error>([&] { read_curve_json(tpath("rag.json")); }));
+    write_text(tpath("ok.json"), " { \"closed\" : true , \"nodes\": [ [1,0], [0, 1.5e0], [-1,0],[0,-1],[1,0] ] } ");
+    const Curve c = read_curve_json(tpath("ok.json"));
+    CHECK(c.size() == 4 && c[1].y == 1.5);
+  });
+  run("io results", [] {  // test_io_cli.cpp:120-135
+    const std::string csv = matrix_to_csv({"a", "b"}, {{0.0, 0.5}, {std::nan(""), 0.0}});
+    CHECK(csv == "id,a,b\na,0,0.5\nb,nan,0\n");
+    CHECK(throws<std::invalid_argument>([] { matrix_to_csv({"a"}, {{0.0, 0.5}, {0.0, 0.0}}); }));
+    RigidAlignment r;
+    r.shift = 29;
+    r.t0 = 0.25;
+    r.rotation = Rotation2(0.5);
+    r.trace = 21.5;
+    r.energy = 1e-07;
+    CHECK(alignment_to_json(r) == "{\"energy\":1e-07,\"shift\":29,\"t0\":0.25,\"theta\":0.5,\"trace\":21.5}");
+    CHECK(curve_to_json(Curve{{{1.0, 0.0}, {0.25, 2.0}}}) == "{\"closed\":true,\"nodes\":[[1.0,0.0],[0.25,2.0]]}");
+  });
+  std::system(("rm -rf " + tmpdir).c_str());
 
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail;
