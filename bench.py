@@ -299,6 +299,7 @@ def run_secondary(args):
                                            stream.cuda_stream))
         units = (r1 - r0) * M
         workload = f"C2: all ordered pairs of {M} curves (raw n_in~U{{300..3000}}), N={N}, rows sharded"
+        l2 = "spectra (16.8 MB) L2-resident by design (reused by every cell); 4.2 M cells of output per step"
         flops_unit = 5 * N * math.log2(N)
         bound = "fp64"
     elif args.config == "c3":
@@ -314,7 +315,8 @@ def run_secondary(args):
             _native.check(lib.cva_preprocess_align_uniform(d1.data_ptr(), d2.data_ptr(), P, N, out.data_ptr(),
                                                            al.data_ptr(), stream.cuda_stream))
         units = P
-        workload = f"C3: {P} pairs/GPU, N={N}, center+normalize+align_fft+aligned curve (L2-chunked multi-pass FFT)"
+        workload = f"C3: {P} pairs/GPU, N={N}, center+normalize+align_fft+aligned curve (L2-chunked four-step FFT)"
+        l2 = "inputs larger than L2 (2 x 268 MB curves + 268 MB aligned vs 126 MB)"
         bytes_unit = 16 * 2 * N + 16 * N + 48
         bound = "hbm"
     elif args.config == "e1":
@@ -333,6 +335,7 @@ def run_secondary(args):
                                                           stream.cuda_stream))
         units = M * M  # every rank computes the whole matrix (weak scaling: replicas)
         workload = E1_WORKLOAD
+        l2 = "inputs L2-resident (64 curves); the DP is compute-bound"
         bound = "none"
     else:
         cfg = synth.CONFIGS["c4"]
@@ -347,6 +350,7 @@ def run_secondary(args):
                                                   stream.cuda_stream))
         units = P
         workload = f"C4: {P} SRV pairs/GPU, N={N}, srv_transform+srv_center+align_fft+aligned q"
+        l2 = "inputs larger than L2 (2 x 268 MB curves + 268 MB aligned vs 126 MB)"
         bytes_unit = 16 * 2 * N + 16 * N + 48
         bound = "hbm"
     for _ in range(max(3, args.warmup)):
@@ -388,7 +392,7 @@ def run_secondary(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong" if args.config == "c2" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generators, csrc/synth.cpp)",
-            "config": {"workload": workload}, "roofline": roof, "cpu_baseline": None, "e2e": None,
+            "config": {"workload": workload, "l2": l2}, "roofline": roof, "cpu_baseline": None, "e2e": None,
             "gpu_launches": args.steps * (2 if args.config in ("c2", "e1") else 1), "clocks": clk.summary()}),
               flush=True)
     if world > 1:
