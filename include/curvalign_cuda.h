@@ -109,8 +109,10 @@ int cva_resample_batch(const double* points, const int64_t* offsets, int64_t cur
                        int64_t max_n_in, int64_t n_out, double* out, int32_t* status,
                        void* stream);
 
-/* Fused C1 path: pair p = (curve 2p, curve 2p+1) of the ragged raw batch;
- * preprocess both to n_out nodes (resample != 0) then align_fft. aligned
+/* Fused C1 path (the BASELINE headline): pair p = (curve 2p, curve 2p+1) of
+ * the ragged raw batch; preprocess both to n_out nodes (resample != 0;
+ * proj/src/curve.cpp:93-97) then align_fft (proj/src/rigid_align.cpp:204-208),
+ * the sequence of cmd_align / run_align (proj/src/cli.cpp:41-44, :99). aligned
  * (nullable): pairs x n_out points. */
 int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int64_t pairs,
                                int64_t max_n_in, int64_t n_out, int resample,
@@ -141,7 +143,8 @@ int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_beg
 
 /* ---------------------------------------------------------------------------
  * Host-buffer entry points (synchronous; host <-> device copies included).
- * These are what the C++ drop-in API (include/curvalign/ headers) calls.
+ * These are what the C++ drop-in API (include/curvalign/ headers) calls; each
+ * replaces the reference function its device twin above cites.
  * ------------------------------------------------------------------------- */
 
 int cva_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
@@ -183,7 +186,8 @@ int cva_arc_length_params_host(const double* xy, int64_t n, double* s, double* t
 int cva_spline_solve_host(const double* x, const double* y, int64_t n_knots, double* m);
 /* srv_transform (srv.cpp:71-88); center != 0 also applies srv_center (srv.cpp:90-98) */
 int cva_srv_transform_host(const double* xy, int64_t n, int center, double* q);
-/* X_k = scale * sum_j x_j exp(sign 2 pi i j k / n), k < kcount (any n; real_dft / real_idft) */
+/* X_k = scale * sum_j x_j exp(sign 2 pi i j k / n), k < kcount (any n; real_dft /
+ * real_idft / circular_cross_correlation, proj/src/fft.cpp:81-125) */
 int cva_dft_host(const double* x_complex, int64_t n, int64_t kcount, int sign, double scale,
                  double* out_complex);
 
