@@ -141,6 +141,17 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
     rows[k] = za[(i0 + k / kM) * kM + (k % kM)];
   __syncthreads();
   const double invN = 1.0 / (double)kM;
+  // twiddles of passes 2 and 3 in shared memory, laid out [r - 1][jm] so a
+  // warp's reads are consecutive (pass 2: jm = lane & 7; pass 3: jm = lane + 32 b)
+  __shared__ double2 s_t2[kR - 1][8], s_t3[kR - 1][64];
+  for (int k = threadIdx.x; k < (kR - 1) * 72; k += blockDim.x) {
+    const int r = k / 72 + 1, q = k % 72;
+    if (q < 8)
+      s_t2[r - 1][q] = __ldg(&tw[r * q * (kM / (8 * kR))]);
+    else
+      s_t3[r - 1][q - 8] = __ldg(&tw[r * (q - 8) * (kM / (64 * kR))]);
+  }
+  __syncthreads();
   const int64_t j_begin = (int64_t)blockIdx.y * col_chunk;
   const int64_t j_end = min(count, j_begin + col_chunk);
   for (int64_t j = j_begin + warp; j < j_end; j += kWarps) {
@@ -160,11 +171,21 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       __syncwarp();
       warp_load<kM, kR>(v, buf, lane);
       __syncwarp();
-      warp_compute<kM, kR>(v, 8, lane, tw);
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+#pragma unroll
+        for (int r = 1; r < kR; ++r) v[b][r] = cmul(v[b][r], s_t2[r - 1][lane & 7]);
+        dft_r<kR>(v[b]);
+      }
       warp_store<kM, kR>(v, buf, 8, lane);
       __syncwarp();
       warp_load<kM, kR>(v, buf, lane);
-      warp_compute<kM, kR>(v, 64, lane, tw);
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+#pragma unroll
+        for (int r = 1; r < kR; ++r) v[b][r] = cmul(v[b][r], s_t3[r - 1][lane + 32 * b]);
+        dft_r<kR>(v[b]);
+      }
       // last pass output index of v[b][r]: base + r * 64 with base = j (Ns = 64 = nb)
       // |D_m| = |F_m| / N; band test on squared magnitudes (see pairfft.cuh)
       double best2 = -1.0;
