@@ -469,18 +469,25 @@ def main():
     achieved_gbs = bytes_launch / launch_s / 1e9
     fp64 = ctypes_probe(lib)
     flops_launch = pairs * 3 * 5 * N * math.log2(N)
-    traffic = None
+    traffic, ncu = None, {}
     prof = os.path.join(ROOT, "profiles", "ncu_c1_summary.json")
     if os.path.exists(prof):
         with open(prof) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            ncu = json.load(f)
+            traffic = ncu.get("dram_bytes_per_launch")
     roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved_gbs / hbm_peak, "traffic": traffic,
             "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
             "algorithmic_bytes_per_launch": bytes_launch,
             "fp64": {"achieved_tflops": flops_launch / launch_s / 1e12, "peak_tflops_measured": fp64,
                      "frac": (flops_launch / launch_s / 1e12) / fp64 if fp64 else None,
-                     "flops_per_launch": flops_launch, "note": "15 N log2 N per pair (3 complex FFTs)"}}
+                     "flops_per_launch": flops_launch, "note": "15 N log2 N per pair (3 complex FFTs)"},
+            # what actually binds (ncu capture of the same kernel, profiles/ncu_c1_summary.json)
+            "binding": {"resource": "fp64 dependency latency / issue at 25 % occupancy (128 regs, 115 KB smem)",
+                        "fp64_pipe_active_pct": ncu.get("sm__pipe_fp64_cycles_active_pct"),
+                        "issue_slots_busy_pct": ncu.get("issue_slots_busy_pct"),
+                        "l1tex_throughput_pct": ncu.get("l1tex_throughput_pct"),
+                        "ncu_round": ncu.get("round")}}
 
     # ---- end to end through the C-ABI host entry (pinned buffers)
     e2e = None
