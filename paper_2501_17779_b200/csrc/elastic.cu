@@ -241,6 +241,110 @@ __device__ __forceinline__ int jmax_of(int i, int n, int W) {
   return min(min(hi1, hi2), n);
 }
 
+// Interpolation offsets (k b) / a of the compile-time step set: constant-
+// evaluated IEEE divisions, the same correctly rounded values dvd() forms.
+struct FrTab {
+  double fr[kMaxSteps][9];
+};
+__host__ __device__ constexpr FrTab make_fr(int W) {
+  FrTab t{};
+  const Steps s = make_steps(W);
+  for (int q = 0; q < s.count; ++q)
+    for (int k = 0; k <= s.a[q]; ++k) t.fr[q][k] = (double)(k * s.b[q]) / (double)s.a[q];
+  return t;
+}
+
+// The DP rows for a compile-time slope bound: dp_step_cost's operand fetches
+// hoisted out of the step loop. Every step into cell (i, j) reads q1 at rows
+// i-kW..i and q2 at columns j-kW..j only, so each thread holds those two
+// windows, the column differences q2[c+1]-q2[c] and (double)(j-c) in
+// registers, and the interpolation base of sample k of step (a, b) is the
+// compile-time offset floor(k b / a) from j-b: (int)((double)(j-b) + kb/a) ==
+// j-b+floor(kb/a) because the fraction is >= 1/a away from an integer and the
+// addition's rounding error is < 2^-32 for any n < 2^20 (the parent matrix
+// alone bounds n far below that). Same operations, same order, same values as
+// step_cost_t; no modulo, no integer/float conversions, no shared loads in the
+// sample loop.
+template <int kW, bool kPow2>
+__device__ __forceinline__ void dp_rows_hoisted(const double2* q1, const double2* q2, int n, double* ring,
+                                                uint8_t* parent, const StepTab& tab, double inv_n) {
+  constexpr Steps kS = make_steps(kW);
+  constexpr FrTab kF = make_fr(kW);
+  const int stride = n + 1;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  auto wrap = [n](int x) { return x < 0 ? 0 : (x >= n ? x - n : x); };  // x < 0: unused slot
+  int ri = 0;  // i % (kW + 1)
+  for (int i = 1; i <= n; ++i) {
+    ri = ri == kW ? 0 : ri + 1;
+    const int lo = jmin_of(i, n, kW), hi = jmax_of(i, n, kW);
+    double* cur = ring + (size_t)ri * stride;
+    const double* prv[kW + 1];
+    double2 q1w[kW + 1];
+#pragma unroll
+    for (int c = 0; c <= kW; ++c) {
+      const int r = ri - c < 0 ? ri - c + kW + 1 : ri - c;
+      prv[c] = ring + (size_t)r * stride;
+      q1w[c] = q1[wrap(i - c)];
+    }
+    for (int j = threadIdx.x; j <= n; j += kT) {
+      double best = inf;
+      uint8_t best_s = 0xff;
+      if (j >= lo && j <= hi) {
+        double2 q2w[kW + 1], dq[kW + 1];
+        double jd[kW + 1];
+#pragma unroll
+        for (int c = 0; c <= kW; ++c) {
+          q2w[c] = q2[wrap(j - c)];
+          jd[c] = (double)(j - c);
+        }
+#pragma unroll
+        for (int c = 1; c <= kW; ++c) dq[c] = make_double2(sub(q2w[c - 1].x, q2w[c].x), sub(q2w[c - 1].y, q2w[c].y));
+        // Branch-free over the steps: an inadmissible predecessor reads as +inf
+        // and inf + cost never compares below best (cost is finite), which is
+        // the reference's `continue` (srv.cpp:214-216) without a divergent
+        // region per step, so the steps' sample chains interleave.
+        double bases[kS.count];
+#pragma unroll
+        for (int s = 0; s < kS.count; ++s) {
+          const int a = kS.a[s], b = kS.b[s];
+          bases[s] = (i - a < 0 || j - b < 0) ? inf : prv[a][max(j - b, 0)];
+        }
+#pragma unroll
+        for (int s = 0; s < kS.count; ++s) {
+          const int a = kS.a[s], b = kS.b[s];
+          const double base = bases[s];
+          const double sq = tab.sq[s];
+          double cost = 0.0;
+#pragma unroll
+          for (int k = 0; k <= a; ++k) {
+            double2 sv;
+            if (k == 0) {
+              sv = q2w[b];
+            } else if (k == a) {
+              sv = q2w[0];
+            } else {
+              const int cu = b - (k * b) / a;
+              const double frac = sub(add(jd[b], kF.fr[s][k]), jd[cu]);
+              sv = make_double2(add(q2w[cu].x, mul(frac, dq[cu].x)), add(q2w[cu].y, mul(frac, dq[cu].y)));
+            }
+            const double2 d = make_double2(sub(q1w[a - k].x, mul(sv.x, sq)), sub(q1w[a - k].y, mul(sv.y, sq)));
+            const double nd = norm2(d);
+            cost = add(cost, (k == 0 || k == a) ? mul(0.5, nd) : nd);
+          }
+          const double cand = add(base, kPow2 ? mul(cost, inv_n) : dvd(cost, (double)n));
+          if (cand < best) {
+            best = cand;
+            best_s = (uint8_t)s;
+          }
+        }
+      }
+      cur[j] = best;
+      parent[(size_t)i * stride + j] = best_s;
+    }
+    __syncthreads();
+  }
+}
+
 // dp_reparam (srv.cpp:180-257) on shared q1, q2 (n samples). ring: (W+1) x
 // (n+1) doubles; parent: (n+1)^2 bytes (shared or global); gamma: n+1.
 // Returns the path energy (thread-uniform); +inf if no admissible path.
@@ -268,6 +372,12 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
   auto row = [&](int i) { return ring + (size_t)(i % (W + 1)) * stride; };
   for (int j = threadIdx.x; j <= n; j += kT) row(0)[j] = j == 0 ? 0.0 : inf;
   __syncthreads();
+  if constexpr (kW > 0) {
+    if (inv_n != 0.0)
+      dp_rows_hoisted<kW, true>(q1, q2, n, ring, parent, tab, inv_n);
+    else
+      dp_rows_hoisted<kW, false>(q1, q2, n, ring, parent, tab, inv_n);
+  } else
   for (int i = 1; i <= n; ++i) {
     const int lo = jmin_of(i, n, W), hi = jmax_of(i, n, W);
     double* cur = row(i);
