@@ -413,7 +413,10 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
     __syncthreads();
   }
   const double e = row(n)[n];
-  // backtrack (thread 0): gamma on the lattice path (srv.cpp:235-255)
+  // Backtrack (srv.cpp:235-255). Thread 0 walks the parent steps and leaves, in
+  // gamma[l] for every row l of the path, the step that covers it (pj, s, k);
+  // the threads then form gamma[pi + k] = (pj + k b / a) / n in parallel (the
+  // walk is a dependent chain of shared loads; the divisions are not).
   if (threadIdx.x == 0) {
     int count = 0;
     for (int a = 1; a <= W; ++a)
@@ -421,7 +424,6 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
     int ok = e != inf;
     if (ok) {
       int i = n, j = n;
-      gamma[n] = 1.0;
       while (i > 0) {
         const uint8_t s = parent[(size_t)i * stride + j];
         if (s == 0xff || s >= count) {
@@ -430,19 +432,25 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
         }
         const int a = tab.a[s], b = tab.b[s];
         const int pi = i - a, pj = j - b;
-        for (int k = 0; k < a; ++k) {
-          const double jj = add((double)pj, dvd((double)(k * b), (double)a));
-          gamma[pi + k] = dvd(jj, (double)n);
-        }
+        for (int k = 0; k < a; ++k) gamma[pi + k] = __longlong_as_double(((long long)pj << 10) | (s << 4) | k);
         i = pi;
         j = pj;
       }
-      gamma[0] = 0.0;
     }
     *cell = ok ? e : inf;
   }
   __syncthreads();
   const double r = *cell;
+  if (r != inf) {
+    for (int l = threadIdx.x; l < n; l += kT) {
+      const long long code = __double_as_longlong(gamma[l]);
+      const int k = (int)(code & 15), s = (int)((code >> 4) & 63), pj = (int)(code >> 10);
+      const int a = tab.a[s], b = tab.b[s];
+      const double jj = add((double)pj, dvd((double)(k * b), (double)a));
+      gamma[l] = l == 0 ? 0.0 : dvd(jj, (double)n);
+    }
+    if (threadIdx.x == 0) gamma[n] = 1.0;
+  }
   __syncthreads();
   return r;
 }
