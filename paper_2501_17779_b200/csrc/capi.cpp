@@ -503,9 +503,11 @@ int cva_resample_batch_host(const double* points, const int64_t* offsets, int64_
 // streams reused across calls (no per-call cudaMalloc of hundreds of MB).
 struct HostCtx {
   int dev = -1;
-  static constexpr int kStreams = 3;
+  static constexpr int kStreams = 3;  // H2D, kernels, D2H
+  static constexpr int kMaxChunks = 16;
   cudaStream_t st[kStreams] = {};
   cudaEvent_t ready = nullptr;
+  cudaEvent_t in_done[kMaxChunks] = {}, k_done[kMaxChunks] = {};
   void* buf[4] = {};
   size_t cap[4] = {};
   ~HostCtx() {
@@ -514,6 +516,10 @@ struct HostCtx {
     for (cudaStream_t x : st)
       if (x) cudaStreamDestroy(x);
     if (ready) cudaEventDestroy(ready);
+    for (int c = 0; c < kMaxChunks; ++c) {
+      if (in_done[c]) cudaEventDestroy(in_done[c]);
+      if (k_done[c]) cudaEventDestroy(k_done[c]);
+    }
   }
   int init() {
     int d = 0;
@@ -527,6 +533,10 @@ struct HostCtx {
         return fail(CVA_CUDA_ERROR, "stream creation failed");
     if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess)
       return fail(CVA_CUDA_ERROR, "event creation failed");
+    for (int c = 0; c < kMaxChunks; ++c)
+      if (cudaEventCreateWithFlags(&in_done[c], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&k_done[c], cudaEventDisableTiming) != cudaSuccess)
+        return fail(CVA_CUDA_ERROR, "event creation failed");
     return CVA_OK;
   }
   void* get(int i, size_t bytes) {
@@ -542,10 +552,13 @@ struct HostCtx {
 };
 thread_local HostCtx t_host;
 
-// Host-buffer fused path, pipelined in chunks of pairs over 3 streams: the
-// H2D copy of chunk i+1, the kernel of chunk i and the D2H copy of chunk i-1
-// overlap (pinned host buffers give the asynchronous copies; pageable ones
-// still work, with less overlap).
+// Host-buffer fused path, pipelined in chunks of pairs over three streams:
+// all H2D copies back to back on one stream (the step is bound by the host ->
+// device link, so it never waits behind a D2H), each chunk's kernel on a
+// second stream once its input has landed, each chunk's D2H on a third once
+// its kernel is done. Up to 16 chunks of >= 256 pairs keep the un-overlapped
+// tail (last chunk's kernel + D2H) small. Pinned host buffers give the
+// asynchronous copies; pageable ones still work, with less overlap.
 int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets, int64_t pairs,
                                     int64_t n_out, int resample, cva_alignment* out,
                                     double* aligned) {
@@ -564,28 +577,36 @@ int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets
   if (!dp || !doff || !dout || (aligned && !dal)) return fail(CVA_BAD_ALLOC, "device allocation failed");
   const int64_t max_n = host_max_n(offsets, 2 * pairs);
   cudaError_t e = cudaMemcpyAsync(doff, offsets, sizeof(int64_t) * (size_t)(2 * pairs + 1),
-                                  cudaMemcpyHostToDevice, h.st[0]);
-  if (e == cudaSuccess) e = cudaEventRecord(h.ready, h.st[0]);
+                                  cudaMemcpyHostToDevice, h.st[0]);  // ahead of chunk 0's input
   if (e != cudaSuccess) return cuda_fail(e, "H2D offsets");
-  const int64_t nchunks = std::min<int64_t>(8, std::max<int64_t>(1, pairs / 256));
+  const int64_t nchunks = std::min<int64_t>(HostCtx::kMaxChunks, std::max<int64_t>(1, pairs / 256));
   const int64_t per = (pairs + nchunks - 1) / nchunks;
+  cudaStream_t sin = h.st[0], sk = h.st[1], sout = h.st[2];
+  for (int64_t c = 0; c < nchunks; ++c) {  // all input copies first, in order
+    const int64_t p0 = c * per, p1 = std::min(pairs, p0 + per);
+    if (p0 >= p1) break;
+    const int64_t a = offsets[2 * p0], b = offsets[2 * p1];
+    e = cudaMemcpyAsync(dp + a, points + 2 * a, sizeof(double2) * (size_t)(b - a), cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess) e = cudaEventRecord(h.in_done[c], sin);
+    if (e != cudaSuccess) return cuda_fail(e, "H2D");
+  }
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t p0 = c * per, p1 = std::min(pairs, p0 + per);
     if (p0 >= p1) break;
-    cudaStream_t s = h.st[c % HostCtx::kStreams];
-    e = cudaStreamWaitEvent(s, h.ready, 0);
-    const int64_t a = offsets[2 * p0], b = offsets[2 * p1];
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(dp + a, points + 2 * a, sizeof(double2) * (size_t)(b - a), cudaMemcpyHostToDevice, s);
-    if (e != cudaSuccess) return cuda_fail(e, "H2D");
+    e = cudaStreamWaitEvent(sk, h.in_done[c], 0);
+    if (e != cudaSuccess) return cuda_fail(e, "stream wait");
     // the kernels index points with the absolute offsets; pass this chunk's slice
     if (int rc = cva_preprocess_align_batch((const double*)dp, doff + 2 * p0, p1 - p0, max_n, n_out, resample,
-                                            dout + p0, aligned ? (double*)(dal + p0 * n_out) : nullptr, s))
+                                            dout + p0, aligned ? (double*)(dal + p0 * n_out) : nullptr, sk))
       return rc;
-    e = cudaMemcpyAsync(out + p0, dout + p0, sizeof(cva_alignment) * (size_t)(p1 - p0), cudaMemcpyDeviceToHost, s);
+    e = cudaEventRecord(h.k_done[c], sk);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, h.k_done[c], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out + p0, dout + p0, sizeof(cva_alignment) * (size_t)(p1 - p0), cudaMemcpyDeviceToHost,
+                          sout);
     if (e == cudaSuccess && aligned)
       e = cudaMemcpyAsync(aligned + 2 * p0 * n_out, dal + p0 * n_out, sizeof(double2) * (size_t)((p1 - p0) * n_out),
-                          cudaMemcpyDeviceToHost, s);
+                          cudaMemcpyDeviceToHost, sout);
     if (e != cudaSuccess) return cuda_fail(e, "D2H");
   }
   for (cudaStream_t s : h.st) {
