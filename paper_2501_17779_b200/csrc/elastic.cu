@@ -254,6 +254,48 @@ __host__ __device__ constexpr FrTab make_fr(int W) {
   return t;
 }
 
+// Offsets of each step's interior samples (k = 1..a-1) in a column's cache.
+struct OffTab {
+  int v[kMaxSteps];
+  int total;
+};
+__host__ __device__ constexpr OffTab make_off(int W) {
+  OffTab t{};
+  const Steps s = make_steps(W);
+  int o = 0;
+  for (int q = 0; q < s.count; ++q) {
+    t.v[q] = o;
+    o += s.a[q] - 1;
+  }
+  t.total = o;
+  return t;
+}
+
+// q2 operand window of column j: q2[(j - c) mod n], q2[j-c+1] - q2[j-c] and
+// (double)(j - c) for c = 0..kW (j - c < 0: unused slots).
+template <int kW>
+__device__ __forceinline__ void column_window(const double2* q2, int n, int j, double2* q2w, double2* dq,
+                                              double* jd) {
+#pragma unroll
+  for (int c = 0; c <= kW; ++c) {
+    const int x = j - c;
+    q2w[c] = q2[x < 0 ? 0 : (x >= n ? x - n : x)];
+    jd[c] = (double)x;
+  }
+#pragma unroll
+  for (int c = 1; c <= kW; ++c) dq[c] = make_double2(sub(q2w[c - 1].x, q2w[c].x), sub(q2w[c - 1].y, q2w[c].y));
+}
+
+// Interior sample k of step (a, b) (0 < k < a) into column j, scaled by
+// sqrt(b/a): dp_step_cost's interpolation (srv.cpp:156-166) at base column
+// j - cu (cu = b - floor(k b / a)) with offset fr = k b / a, then the sq product.
+__device__ __forceinline__ double2 scaled_interior(const double2* q2w, const double2* dq, const double* jd, int b,
+                                                   int cu, double fr, double sq) {
+  const double frac = sub(add(jd[b], fr), jd[cu]);
+  const double2 sv = make_double2(add(q2w[cu].x, mul(frac, dq[cu].x)), add(q2w[cu].y, mul(frac, dq[cu].y)));
+  return make_double2(mul(sv.x, sq), mul(sv.y, sq));
+}
+
 // The DP rows for a compile-time slope bound: dp_step_cost's operand fetches
 // hoisted out of the step loop. Every step into cell (i, j) reads q1 at rows
 // i-kW..i and q2 at columns j-kW..j only, so each thread holds those two
@@ -265,81 +307,113 @@ __host__ __device__ constexpr FrTab make_fr(int W) {
 // alone bounds n far below that). Same operations, same order, same values as
 // step_cost_t; no modulo, no integer/float conversions, no shared loads in the
 // sample loop.
+// A thread's first column (threadIdx.x) is the same in every row and its
+// scaled interior samples do not depend on the row, so they are formed once
+// per DP and kept in registers (kCached cells); only q1's side changes per
+// row. Further columns (n >= kT) take the window path.
+template <int kW, bool kPow2, bool kCached>
+__device__ __forceinline__ void dp_cell(const double2* q2, int n, int i, int j, const double2* q1w,
+                                        const double* const* prv, const double2* Sc, const StepTab& tab,
+                                        double inv_n, double* cur, uint8_t* par) {
+  constexpr Steps kS = make_steps(kW);
+  constexpr FrTab kF = make_fr(kW);
+  constexpr OffTab kO = make_off(kW);
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  double2 q2w[kW + 1], dq[kW + 1];
+  double jd[kW + 1];
+  if constexpr (kCached) {
+#pragma unroll
+    for (int c = 0; c <= kW; ++c) {
+      const int x = j - c;
+      q2w[c] = q2[x < 0 ? 0 : (x >= n ? x - n : x)];
+    }
+  } else {
+    column_window<kW>(q2, n, j, q2w, dq, jd);
+  }
+  // Branch-free over the steps: an inadmissible predecessor reads as +inf and
+  // inf + cost never compares below best (cost is finite), which is the
+  // reference's `continue` (srv.cpp:214-216) without a divergent region per
+  // step, so the steps' sample chains interleave.
+  double best = inf;
+  uint8_t best_s = 0xff;
+#pragma unroll
+  for (int s = 0; s < kS.count; ++s) {
+    const int a = kS.a[s], b = kS.b[s];
+    const double base = (i - a < 0 || j - b < 0) ? inf : prv[a][max(j - b, 0)];
+    const double sq = tab.sq[s];
+    double cost = 0.0;
+#pragma unroll
+    for (int k = 0; k <= a; ++k) {
+      double2 d;
+      if (k == 0 || k == a) {
+        const double2 sv = q2w[k == 0 ? b : 0];
+        d = make_double2(sub(q1w[a - k].x, mul(sv.x, sq)), sub(q1w[a - k].y, mul(sv.y, sq)));
+      } else {
+        double2 S;
+        if constexpr (kCached)
+          S = Sc[kO.v[s] + k - 1];
+        else
+          S = scaled_interior(q2w, dq, jd, b, b - (k * b) / a, kF.fr[s][k], sq);
+        d = make_double2(sub(q1w[a - k].x, S.x), sub(q1w[a - k].y, S.y));
+      }
+      const double nd = norm2(d);
+      cost = add(cost, (k == 0 || k == a) ? mul(0.5, nd) : nd);
+    }
+    const double cand = add(base, kPow2 ? mul(cost, inv_n) : dvd(cost, (double)n));
+    if (cand < best) {
+      best = cand;
+      best_s = (uint8_t)s;
+    }
+  }
+  *cur = best;
+  *par = best_s;
+}
+
 template <int kW, bool kPow2>
 __device__ __forceinline__ void dp_rows_hoisted(const double2* q1, const double2* q2, int n, double* ring,
                                                 uint8_t* parent, const StepTab& tab, double inv_n) {
   constexpr Steps kS = make_steps(kW);
   constexpr FrTab kF = make_fr(kW);
+  constexpr OffTab kO = make_off(kW);
   const int stride = n + 1;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
-  auto wrap = [n](int x) { return x < 0 ? 0 : (x >= n ? x - n : x); };  // x < 0: unused slot
+  const int jc = threadIdx.x;
+  double2 Sc[kO.total];
+  if (jc <= n) {
+    double2 q2w[kW + 1], dq[kW + 1];
+    double jd[kW + 1];
+    column_window<kW>(q2, n, jc, q2w, dq, jd);
+#pragma unroll
+    for (int s = 0; s < kS.count; ++s)
+#pragma unroll
+      for (int k = 1; k < kS.a[s]; ++k)
+        Sc[kO.v[s] + k - 1] =
+            scaled_interior(q2w, dq, jd, kS.b[s], kS.b[s] - (k * kS.b[s]) / kS.a[s], kF.fr[s][k], tab.sq[s]);
+  }
   int ri = 0;  // i % (kW + 1)
   for (int i = 1; i <= n; ++i) {
     ri = ri == kW ? 0 : ri + 1;
     const int lo = jmin_of(i, n, kW), hi = jmax_of(i, n, kW);
     double* cur = ring + (size_t)ri * stride;
+    uint8_t* par = parent + (size_t)i * stride;
     const double* prv[kW + 1];
     double2 q1w[kW + 1];
 #pragma unroll
     for (int c = 0; c <= kW; ++c) {
       const int r = ri - c < 0 ? ri - c + kW + 1 : ri - c;
       prv[c] = ring + (size_t)r * stride;
-      q1w[c] = q1[wrap(i - c)];
+      const int x = i - c;
+      q1w[c] = q1[x < 0 ? 0 : (x >= n ? x - n : x)];
     }
-    for (int j = threadIdx.x; j <= n; j += kT) {
-      double best = inf;
-      uint8_t best_s = 0xff;
-      if (j >= lo && j <= hi) {
-        double2 q2w[kW + 1], dq[kW + 1];
-        double jd[kW + 1];
-#pragma unroll
-        for (int c = 0; c <= kW; ++c) {
-          q2w[c] = q2[wrap(j - c)];
-          jd[c] = (double)(j - c);
-        }
-#pragma unroll
-        for (int c = 1; c <= kW; ++c) dq[c] = make_double2(sub(q2w[c - 1].x, q2w[c].x), sub(q2w[c - 1].y, q2w[c].y));
-        // Branch-free over the steps: an inadmissible predecessor reads as +inf
-        // and inf + cost never compares below best (cost is finite), which is
-        // the reference's `continue` (srv.cpp:214-216) without a divergent
-        // region per step, so the steps' sample chains interleave.
-        double bases[kS.count];
-#pragma unroll
-        for (int s = 0; s < kS.count; ++s) {
-          const int a = kS.a[s], b = kS.b[s];
-          bases[s] = (i - a < 0 || j - b < 0) ? inf : prv[a][max(j - b, 0)];
-        }
-#pragma unroll
-        for (int s = 0; s < kS.count; ++s) {
-          const int a = kS.a[s], b = kS.b[s];
-          const double base = bases[s];
-          const double sq = tab.sq[s];
-          double cost = 0.0;
-#pragma unroll
-          for (int k = 0; k <= a; ++k) {
-            double2 sv;
-            if (k == 0) {
-              sv = q2w[b];
-            } else if (k == a) {
-              sv = q2w[0];
-            } else {
-              const int cu = b - (k * b) / a;
-              const double frac = sub(add(jd[b], kF.fr[s][k]), jd[cu]);
-              sv = make_double2(add(q2w[cu].x, mul(frac, dq[cu].x)), add(q2w[cu].y, mul(frac, dq[cu].y)));
-            }
-            const double2 d = make_double2(sub(q1w[a - k].x, mul(sv.x, sq)), sub(q1w[a - k].y, mul(sv.y, sq)));
-            const double nd = norm2(d);
-            cost = add(cost, (k == 0 || k == a) ? mul(0.5, nd) : nd);
-          }
-          const double cand = add(base, kPow2 ? mul(cost, inv_n) : dvd(cost, (double)n));
-          if (cand < best) {
-            best = cand;
-            best_s = (uint8_t)s;
-          }
-        }
+    for (int j = jc; j <= n; j += kT) {
+      if (j < lo || j > hi) {
+        cur[j] = inf;
+        par[j] = 0xff;
+      } else if (j == jc) {
+        dp_cell<kW, kPow2, true>(q2, n, i, j, q1w, prv, Sc, tab, inv_n, cur + j, par + j);
+      } else {
+        dp_cell<kW, kPow2, false>(q2, n, i, j, q1w, prv, Sc, tab, inv_n, cur + j, par + j);
       }
-      cur[j] = best;
-      parent[(size_t)i * stride + j] = best_s;
     }
     __syncthreads();
   }
