@@ -576,9 +576,15 @@ int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets
   double2* dal = aligned ? (double2*)h.get(3, ab) : nullptr;
   if (!dp || !doff || !dout || (aligned && !dal)) return fail(CVA_BAD_ALLOC, "device allocation failed");
   const int64_t max_n = host_max_n(offsets, 2 * pairs);
+  // Every exit after the first asynchronous call drains the three streams, so
+  // no copy still reads or writes the caller's host buffers after return.
+  auto drain = [&](int rc) {
+    for (cudaStream_t x : h.st) cudaStreamSynchronize(x);
+    return rc;
+  };
   cudaError_t e = cudaMemcpyAsync(doff, offsets, sizeof(int64_t) * (size_t)(2 * pairs + 1),
                                   cudaMemcpyHostToDevice, h.st[0]);  // ahead of chunk 0's input
-  if (e != cudaSuccess) return cuda_fail(e, "H2D offsets");
+  if (e != cudaSuccess) return drain(cuda_fail(e, "H2D offsets"));
   const int64_t nchunks = std::min<int64_t>(HostCtx::kMaxChunks, std::max<int64_t>(1, pairs / 256));
   const int64_t per = (pairs + nchunks - 1) / nchunks;
   cudaStream_t sin = h.st[0], sk = h.st[1], sout = h.st[2];
@@ -588,17 +594,17 @@ int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets
     const int64_t a = offsets[2 * p0], b = offsets[2 * p1];
     e = cudaMemcpyAsync(dp + a, points + 2 * a, sizeof(double2) * (size_t)(b - a), cudaMemcpyHostToDevice, sin);
     if (e == cudaSuccess) e = cudaEventRecord(h.in_done[c], sin);
-    if (e != cudaSuccess) return cuda_fail(e, "H2D");
+    if (e != cudaSuccess) return drain(cuda_fail(e, "H2D"));
   }
   for (int64_t c = 0; c < nchunks; ++c) {
     const int64_t p0 = c * per, p1 = std::min(pairs, p0 + per);
     if (p0 >= p1) break;
     e = cudaStreamWaitEvent(sk, h.in_done[c], 0);
-    if (e != cudaSuccess) return cuda_fail(e, "stream wait");
+    if (e != cudaSuccess) return drain(cuda_fail(e, "stream wait"));
     // the kernels index points with the absolute offsets; pass this chunk's slice
     if (int rc = cva_preprocess_align_batch((const double*)dp, doff + 2 * p0, p1 - p0, max_n, n_out, resample,
                                             dout + p0, aligned ? (double*)(dal + p0 * n_out) : nullptr, sk))
-      return rc;
+      return drain(rc);
     e = cudaEventRecord(h.k_done[c], sk);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, h.k_done[c], 0);
     if (e == cudaSuccess)
@@ -607,13 +613,14 @@ int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets
     if (e == cudaSuccess && aligned)
       e = cudaMemcpyAsync(aligned + 2 * p0 * n_out, dal + p0 * n_out, sizeof(double2) * (size_t)((p1 - p0) * n_out),
                           cudaMemcpyDeviceToHost, sout);
-    if (e != cudaSuccess) return cuda_fail(e, "D2H");
+    if (e != cudaSuccess) return drain(cuda_fail(e, "D2H"));
   }
-  for (cudaStream_t s : h.st) {
-    e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return cuda_fail(e, "preprocess_align_batch_host");
+  cudaError_t first = cudaSuccess;
+  for (cudaStream_t x : h.st) {
+    e = cudaStreamSynchronize(x);
+    if (first == cudaSuccess) first = e;
   }
-  return CVA_OK;
+  return first == cudaSuccess ? CVA_OK : cuda_fail(first, "preprocess_align_batch_host");
 }
 
 int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t row_begin,
