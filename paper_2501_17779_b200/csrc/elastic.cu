@@ -254,6 +254,14 @@ __host__ __device__ constexpr FrTab make_fr(int W) {
   return t;
 }
 
+// (a-1, b-1) of every step, 4 bits per step (W <= 4: at most 11 steps).
+__host__ __device__ constexpr unsigned long long pack_steps(int W) {
+  const Steps s = make_steps(W);
+  unsigned long long v = 0;
+  for (int q = 0; q < s.count; ++q) v |= (unsigned long long)((s.a[q] - 1) | ((s.b[q] - 1) << 2)) << (4 * q);
+  return v;
+}
+
 // Offsets of each step's interior samples (k = 1..a-1) in a column's cache.
 struct OffTab {
   int v[kMaxSteps];
@@ -498,14 +506,25 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
     int ok = e != inf;
     if (ok) {
       int i = n, j = n;
+      const uint8_t* pp = parent + (size_t)n * stride + n;
       while (i > 0) {
-        const uint8_t s = parent[(size_t)i * stride + j];
+        const uint8_t s = *pp;
         if (s == 0xff || s >= count) {
           ok = 0;
           break;
         }
-        const int a = tab.a[s], b = tab.b[s];
+        int a, b;
+        if constexpr (kW > 0 && kW <= 4) {  // (a-1, b-1) of every step in one constant: no table load in the chain
+          constexpr unsigned long long kPack = pack_steps(kW);
+          const int f = (int)((kPack >> (4 * s)) & 15);
+          a = (f & 3) + 1;
+          b = (f >> 2) + 1;
+        } else {
+          a = tab.a[s];
+          b = tab.b[s];
+        }
         const int pi = i - a, pj = j - b;
+        pp -= (size_t)a * stride + b;
         for (int k = 0; k < a; ++k) gamma[pi + k] = __longlong_as_double(((long long)pj << 10) | (s << 4) | k);
         i = pi;
         j = pj;
