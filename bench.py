@@ -487,6 +487,12 @@ def main():
                         "fp64_pipe_active_pct": ncu.get("sm__pipe_fp64_cycles_active_pct"),
                         "issue_slots_busy_pct": ncu.get("issue_slots_busy_pct"),
                         "l1tex_throughput_pct": ncu.get("l1tex_throughput_pct"),
+                        # the kernel's own FP64 work (DADD+DMUL+DFMA thread ops,
+                        # spline + FFTs) at the SMs' FP64 op rate: its compute
+                        # floor, next to the HBM floor the fraction above uses
+                        "fp64_thread_ops_per_pair": (round(ncu["fp64_thread_ops_per_launch"] / pairs)
+                                                     if ncu.get("fp64_thread_ops_per_launch") else None),
+                        "fp64_op_utilisation_pct": ncu.get("fp64_op_utilisation_pct"),
                         "ncu_round": ncu.get("round")}}
 
     # ---- end to end through the C-ABI host entry (pinned buffers)

@@ -75,6 +75,18 @@ def main():
         out["dram_bytes_per_launch"] = int(round((out["dram_read_MB"] + out["dram_write_MB"]) * 1e6))
     if a.algorithmic_bytes:
         out["algorithmic_bytes_per_launch"] = int(a.algorithmic_bytes)
+    # FP64 instruction work of the launch (thread-level DADD + DMUL + DFMA, each
+    # one pipe op) and the time it needs at the SMs' FP64 op rate: the compute
+    # floor of the kernel as written, next to its HBM floor.
+    ops = [num(d.get(f"smsp__sass_thread_inst_executed_op_{o}_pred_on.sum.per_cycle_elapsed", "x"))
+           for o in ("dadd", "dmul", "dfma")]
+    cyc = num(d.get("sm__cycles_elapsed.avg", "x"))
+    peak = num(d.get("sm__sass_thread_inst_executed_op_dfma_pred_on.sum.peak_sustained", "x"))
+    if all(isinstance(x, float) for x in ops + [cyc, peak]) and peak > 0:
+        total = sum(ops) * cyc
+        out["fp64_thread_ops_per_launch"] = int(round(total))
+        out["fp64_op_floor_cycles"] = int(round(total / peak))
+        out["fp64_op_utilisation_pct"] = 100.0 * sum(ops) / peak
     stalls = {}
     for k in hdr:
         m = re.fullmatch(r"smsp__average_warps_issue_stalled_(\w+)_per_issue_active\.ratio", k)
