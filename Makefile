@@ -86,7 +86,7 @@ $(PKG)/libcurvalign.so: $(DROPIN_SRCS) $(wildcard include/curvalign/*.hpp) $(CSR
 # on a GPU by tests/test_gpu_dropin_cpp.py.
 tests/cpp/bin/test_dropin: tests/cpp/test_dropin.cpp $(PKG)/libcurvalign.so
 	@mkdir -p tests/cpp/bin
-	$(CXX) -O2 -std=c++20 -Wall -Iinclude -o $@ $< -L$(PKG) -lcurvalign -lcurvalign_cuda \
+	$(CXX) -O2 -std=c++20 -Wall -pthread -Iinclude -o $@ $< -L$(PKG) -lcurvalign -lcurvalign_cuda \
 	    -Wl,-rpath,'$$ORIGIN/../../../$(PKG)'
 dropin_test: tests/cpp/bin/test_dropin
 

@@ -400,64 +400,6 @@ def dp_reparam(q1, q2, max_slope: int = 4):
     return g[0], float(e[0])
 
 
-def elastic_approach2_batch(c1, c2, max_iters: int = 30, energy_tol: float = 1e-6, max_slope: int = 4,
-                            return_gamma: bool = False):
-    """elastic_distance_approach2 (elastic.cpp:102-174) per pair of preprocessed
-    curves ``(pairs, n, 2)``. Returns a dict of per-pair arrays: distance,
-    energy, t0, theta, iterations, converged, status (+ gamma). numpy in -> numpy
-    out; CUDA tensors in -> CUDA tensors out (stream-ordered)."""
-    lib = _native.load()
-    if _is_cuda_tensor(c1):
-        a, b = c1.contiguous(), c2.contiguous()
-        pairs, n = a.shape[0], a.shape[1]
-        dev = a.device
-        out = {k: torch.empty(pairs, dtype=torch.float64, device=dev) for k in ("distance", "energy", "t0", "theta")}
-        for k in ("iterations", "converged", "status"):
-            out[k] = torch.empty(pairs, dtype=torch.int32, device=dev)
-        g = torch.empty((pairs, n + 1), dtype=torch.float64, device=dev) if return_gamma else None
-        check(lib.cva_elastic_approach2_batch(
-            a.data_ptr(), b.data_ptr(), pairs, n, max_iters, energy_tol, max_slope, out["distance"].data_ptr(),
-            out["energy"].data_ptr(), out["t0"].data_ptr(), out["theta"].data_ptr(), _tptr(g),
-            out["iterations"].data_ptr(), out["converged"].data_ptr(), out["status"].data_ptr(), _stream_of(a)))
-        if return_gamma:
-            out["gamma"] = g
-        return out
-    a, b = _f64c(c1), _f64c(c2)
-    if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 2:
-        raise ValueError("elastic: node count mismatch")
-    pairs, n = a.shape[0], a.shape[1]
-    out = {k: np.empty(pairs) for k in ("distance", "energy", "t0", "theta")}
-    for k in ("iterations", "converged", "status"):
-        out[k] = np.empty(pairs, dtype=np.int32)
-    g = np.empty((pairs, n + 1)) if return_gamma else None
-    check(lib.cva_elastic_approach2_batch_host(
-        _ptr(a), _ptr(b), pairs, n, max_iters, energy_tol, max_slope, out["distance"].ctypes.data,
-        out["energy"].ctypes.data, out["t0"].ctypes.data, out["theta"].ctypes.data,
-        g.ctypes.data if g is not None else 0, out["iterations"].ctypes.data, out["converged"].ctypes.data,
-        out["status"].ctypes.data))
-    if return_gamma:
-        out["gamma"] = g
-    return out
-
-
-def elastic_distance_approach2(c1, c2, max_iters: int = 30, energy_tol: float = 1e-6,
-                               max_slope: int = 4) -> ElasticMatch:
-    """Single pair (reference name and exceptions: ValueError for invalid input,
-    RuntimeError for a DP without admissible path)."""
-    a, b = np.asarray(c1, dtype=np.float64), np.asarray(c2, dtype=np.float64)
-    if a.shape != b.shape:
-        raise ValueError("elastic: node count mismatch")
-    r = elastic_approach2_batch(a[None], b[None], max_iters, energy_tol, max_slope, return_gamma=True)
-    st = int(r["status"][0])
-    if st == _native.CVA_INVALID_ARGUMENT:
-        raise ValueError("elastic: invalid input")
-    if st == _native.CVA_RUNTIME_ERROR:
-        raise RuntimeError("dp: no admissible path")
-    return ElasticMatch(t0=float(r["t0"][0]), theta=float(r["theta"][0]), gamma=r["gamma"][0],
-                        energy=float(r["energy"][0]), distance=float(r["distance"][0]),
-                        iterations=int(r["iterations"][0]), converged=bool(r["converged"][0]))
-
-
 def _elastic_batch(approach, c1, c2, max_iters, energy_tol, max_slope, n_max_approach1, return_gamma):
     lib = _native.load()
     if _is_cuda_tensor(c1):

@@ -199,11 +199,16 @@ int resample_dispatch(const double* points, const int64_t* offsets, int64_t curv
 }
 
 // RAII device buffer for the *_host entry points.
+// Scratch of the synchronous *_host entry points: stream-ordered on the calling
+// host thread's default stream (cudaStreamPerThread), so concurrent callers
+// (the reference's distance_matrix pattern, elastic.cpp:196-234) neither
+// serialise on the legacy stream nor hit cudaFree's device-wide sync.
+const cudaStream_t kHostStream = cudaStreamPerThread;
 struct DevBuf {
   void* p = nullptr;
-  cudaError_t alloc(size_t bytes) { return cudaMalloc(&p, bytes ? bytes : 16); }
+  cudaError_t alloc(size_t bytes) { return scratch_alloc(&p, bytes, kHostStream); }
   ~DevBuf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, kHostStream);
   }
 };
 
@@ -441,7 +446,7 @@ int cva_align_batch_host(const double* c1, const double* c2, int64_t pairs, int6
   if (d1.alloc(cb) || d2.alloc(cb) || dout.alloc(sizeof(cva_alignment) * pairs) ||
       (aligned && dal.alloc(cb)))
     return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = nullptr;
+  cudaStream_t s = kHostStream;
   cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "H2D");
@@ -468,7 +473,7 @@ int preprocess_host_impl(const double* points, const int64_t* offsets, int64_t c
   if (dp.alloc(ib) || doff.alloc(sizeof(int64_t) * (curves + 1)) || dout.alloc(ob) ||
       dst.alloc(sizeof(int32_t) * curves))
     return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = nullptr;
+  cudaStream_t s = kHostStream;
   cudaError_t e = cudaMemcpyAsync(dp.p, points, ib, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(doff.p, offsets, sizeof(int64_t) * (curves + 1), cudaMemcpyHostToDevice, s);
@@ -634,7 +639,7 @@ int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t ro
   if (dc.alloc(sizeof(double2) * (size_t)(count * n)) || de.alloc(sizeof(double) * cells) ||
       dk.alloc(sizeof(int32_t) * cells) || dt.alloc(sizeof(double) * cells))
     return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = nullptr;
+  cudaStream_t s = kHostStream;
   cudaError_t e = cudaMemcpyAsync(dc.p, curves, sizeof(double2) * (size_t)(count * n), cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "H2D");
   if (int rc = cva_allpairs((const double*)dc.p, count, n, row_begin, row_end, (double*)de.p,
@@ -657,7 +662,7 @@ int cva_preprocess_align_uniform_host(const double* c1, const double* c2, int64_
   DevBuf d1, d2, dout, dal;
   if (d1.alloc(cb) || d2.alloc(cb) || dout.alloc(sizeof(cva_alignment) * pairs) || (aligned && dal.alloc(cb)))
     return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = nullptr;
+  cudaStream_t s = kHostStream;
   cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "H2D");
@@ -681,7 +686,7 @@ int cva_srv_align_batch_host(const double* c1, const double* c2, int64_t pairs, 
   if (d1.alloc(cb) || d2.alloc(cb) || dout.alloc(sizeof(cva_alignment) * pairs) ||
       (aligned_q && dal.alloc(cb)))
     return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = nullptr;
+  cudaStream_t s = kHostStream;
   cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "H2D");
@@ -711,7 +716,7 @@ int check_elastic(int64_t pairs, int64_t n, int max_slope, const char* what) {
 
 struct Slab {
   void* p = nullptr;
-  cudaStream_t s = nullptr;
+  cudaStream_t s = kHostStream;
   ~Slab() {
     if (p) cudaFreeAsync(p, s);
   }
@@ -847,7 +852,7 @@ int cva_dp_reparam_batch_host(const double* q1, const double* q2, int64_t pairs,
   if (d1.alloc(cb) || d2.alloc(cb) || dg.alloc(gb) || de.alloc(sizeof(double) * pairs) ||
       ds.alloc(sizeof(int32_t) * pairs))
     return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = nullptr;
+  cudaStream_t s = kHostStream;
   cudaError_t e = cudaMemcpyAsync(d1.p, q1, cb, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, q2, cb, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "H2D");
@@ -877,7 +882,7 @@ int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t
   if (d1.alloc(cb) || d2.alloc(cb) || dv.alloc(4 * vb) || (gamma && dg.alloc(gb)) || di.alloc(3 * ib) ||
       (energy_trace && dt.alloc(tb)))
     return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = nullptr;
+  cudaStream_t s = kHostStream;
   cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "H2D");
@@ -908,7 +913,7 @@ int cva_elastic_distance_matrix_host(const double* curves, int64_t count, int64_
   const size_t cb = sizeof(double2) * (size_t)(count * n), db = sizeof(double) * (size_t)(count * count);
   DevBuf dc, dd;
   if (dc.alloc(cb) || dd.alloc(db)) return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = nullptr;
+  cudaStream_t s = kHostStream;
   cudaError_t e = cudaMemcpyAsync(dc.p, curves, cb, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "H2D");
   if (int rc = cva_elastic_distance_matrix((const double*)dc.p, count, n, method, max_iters, energy_tol, max_slope,
@@ -932,7 +937,7 @@ int cva_elastic_approach1_batch_host(const double* c1, const double* c2, int64_t
   DevBuf d1, d2, dv, dg, di;
   if (d1.alloc(cb) || d2.alloc(cb) || dv.alloc(4 * vb) || (gamma && dg.alloc(gb)) || di.alloc(3 * ib))
     return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = nullptr;
+  cudaStream_t s = kHostStream;
   cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "H2D");

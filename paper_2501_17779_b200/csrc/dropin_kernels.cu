@@ -174,14 +174,18 @@ thread_local std::string t_err;
 
 int err(int st, const char* what, cudaError_t e = cudaSuccess) {
   t_err = std::string(what) + (e != cudaSuccess ? std::string(": ") + cudaGetErrorString(e) : std::string());
+  cudaStreamSynchronize(cudaStreamPerThread);  // no copy of this call still touches the caller's buffers
   return st;
 }
 
+// Single-call utilities run on the calling host thread's default stream
+// (stream-ordered scratch), so concurrent callers do not serialise.
+const cudaStream_t kS = cudaStreamPerThread;
 struct Buf {
   void* p = nullptr;
-  bool alloc(size_t b) { return cudaMalloc(&p, b ? b : 16) == cudaSuccess; }
+  bool alloc(size_t b) { return cudaMallocAsync(&p, b ? b : 16, kS) == cudaSuccess; }
   ~Buf() {
-    if (p) cudaFree(p);
+    if (p) cudaFreeAsync(p, kS);
   }
 };
 
@@ -193,13 +197,14 @@ int have_device() {
 
 int up(Buf& b, const void* h, size_t bytes) {
   if (!b.alloc(bytes)) return err(CVA_BAD_ALLOC, "device allocation failed");
-  cudaError_t e = cudaMemcpy(b.p, h, bytes, cudaMemcpyHostToDevice);
+  cudaError_t e = cudaMemcpyAsync(b.p, h, bytes, cudaMemcpyHostToDevice, kS);
   return e == cudaSuccess ? CVA_OK : err(CVA_CUDA_ERROR, "H2D", e);
 }
 
 int down(void* h, const Buf& b, size_t bytes) {
   cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaMemcpy(h, b.p, bytes, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, b.p, bytes, cudaMemcpyDeviceToHost, kS);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(kS);
   return e == cudaSuccess ? CVA_OK : err(CVA_CUDA_ERROR, "kernel/D2H", e);
 }
 }  // namespace
@@ -223,7 +228,7 @@ int cva_correlation_matrices_host(const double* c1, const double* c2, int64_t n,
   if (int rc = cva::up(a, c1, cb)) return rc;
   if (int rc = cva::up(b, c2, cb)) return rc;
   if (!o.alloc(sizeof(double) * 4 * (size_t)m_count)) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
-  cva::di::corr_kernel<<<(unsigned)m_count, cva::di::kT>>>((const double2*)a.p, (const double2*)b.p, n, m_begin,
+  cva::di::corr_kernel<<<(unsigned)m_count, cva::di::kT, 0, cva::kS>>>((const double2*)a.p, (const double2*)b.p, n, m_begin,
                                                            (double*)o.p);
   return cva::down(out4, o, sizeof(double) * 4 * (size_t)m_count);
 }
@@ -237,7 +242,7 @@ int cva_mismatch_energy_host(const double* c1, const double* c2, int64_t n, int6
   if (int rc = cva::up(a, c1, cb)) return rc;
   if (int rc = cva::up(b, c2, cb)) return rc;
   if (!o.alloc(sizeof(double))) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
-  cva::di::mismatch_kernel<<<1, cva::di::kT>>>((const double2*)a.p, (const double2*)b.p, n, shift, theta,
+  cva::di::mismatch_kernel<<<1, cva::di::kT, 0, cva::kS>>>((const double2*)a.p, (const double2*)b.p, n, shift, theta,
                                                (double*)o.p);
   return cva::down(out, o, sizeof(double));
 }
@@ -248,7 +253,7 @@ int cva_curve_stats_host(const double* xy, int64_t n, double* centroid2, double*
   Buf a, o;
   if (int rc = cva::up(a, xy, sizeof(double2) * (size_t)n)) return rc;
   if (!o.alloc(3 * sizeof(double))) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
-  cva::di::stats_kernel<<<1, cva::di::kT>>>((const double2*)a.p, n, (double*)o.p);
+  cva::di::stats_kernel<<<1, cva::di::kT, 0, cva::kS>>>((const double2*)a.p, n, (double*)o.p);
   double h[3];
   if (int rc = cva::down(h, o, sizeof(h))) return rc;
   if (centroid2) {
@@ -267,12 +272,12 @@ int cva_center_or_normalize_host(const double* xy, int64_t n, int mode, double* 
   const size_t cb = sizeof(double2) * (size_t)n;
   if (int rc = cva::up(a, xy, cb)) return rc;
   if (!o.alloc(cb) || !st.alloc(3 * sizeof(double))) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
-  cva::di::stats_kernel<<<1, cva::di::kT>>>((const double2*)a.p, n, (double*)st.p);
+  cva::di::stats_kernel<<<1, cva::di::kT, 0, cva::kS>>>((const double2*)a.p, n, (double*)st.p);
   double h[3];
   if (int rc = cva::down(h, st, sizeof(h))) return rc;
   if (mode == 2 && !(h[2] > 0.0)) return cva::err(CVA_INVALID_ARGUMENT, "curve: zero length");
   const double gx = mode == 1 ? h[0] : 0.0, gy = mode == 1 ? h[1] : 0.0, sc = mode == 2 ? 1.0 / h[2] : 1.0;
-  cva::di::affine_kernel<<<(unsigned)((n + 255) / 256), 256>>>((const double2*)a.p, n, gx, gy, sc, (double2*)o.p);
+  cva::di::affine_kernel<<<(unsigned)((n + 255) / 256), 256, 0, cva::kS>>>((const double2*)a.p, n, gx, gy, sc, (double2*)o.p);
   return cva::down(out, o, cb);
 }
 
@@ -283,7 +288,7 @@ int cva_arc_length_params_host(const double* xy, int64_t n, double* s, double* t
   if (int rc = cva::up(a, xy, sizeof(double2) * (size_t)n)) return rc;
   if (!so.alloc(sizeof(double) * (size_t)(n + 1)) || !to.alloc(sizeof(double)) || !stt.alloc(sizeof(int)))
     return cva::err(CVA_BAD_ALLOC, "device allocation failed");
-  cva::di::arclen_kernel<<<1, cva::di::kT>>>((const double2*)a.p, (int)n, (double*)so.p, (double*)to.p, (int*)stt.p);
+  cva::di::arclen_kernel<<<1, cva::di::kT, 0, cva::kS>>>((const double2*)a.p, (int)n, (double*)so.p, (double*)to.p, (int*)stt.p);
   int bad = 0;
   if (int rc = cva::down(&bad, stt, sizeof(int))) return rc;
   if (bad) return cva::err(CVA_INVALID_ARGUMENT, "curve: coincident adjacent nodes");
@@ -303,7 +308,7 @@ int cva_spline_solve_host(const double* x, const double* y, int64_t n_knots, dou
   const size_t sm = sizeof(double) * (size_t)((n + 2) & ~1) + 2 * sizeof(double2) * (size_t)n +
                     sizeof(cva::ChunkEnds) * cva::di::kT;
   cudaFuncSetAttribute((const void*)cva::di::spline_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  cva::di::spline_kernel<<<1, cva::di::kT, sm>>>((const double*)dx.p, (const double*)dy.p, n, (double*)dm.p);
+  cva::di::spline_kernel<<<1, cva::di::kT, sm, cva::kS>>>((const double*)dx.p, (const double*)dy.p, n, (double*)dm.p);
   return cva::down(m, dm, sizeof(double) * (size_t)n_knots);
 }
 
@@ -314,7 +319,7 @@ int cva_srv_transform_host(const double* xy, int64_t n, int center, double* q) {
   const size_t cb = sizeof(double2) * (size_t)n;
   if (int rc = cva::up(a, xy, cb)) return rc;
   if (!o.alloc(cb)) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
-  cva::di::srv_kernel<<<1, cva::di::kT>>>((const double2*)a.p, n, center, (double2*)o.p);
+  cva::di::srv_kernel<<<1, cva::di::kT, 0, cva::kS>>>((const double2*)a.p, n, center, (double2*)o.p);
   return cva::down(q, o, cb);
 }
 
@@ -326,7 +331,7 @@ int cva_dft_host(const double* x_complex, int64_t n, int64_t kcount, int sign, d
   Buf a, o;
   if (int rc = cva::up(a, x_complex, sizeof(double2) * (size_t)n)) return rc;
   if (!o.alloc(sizeof(double2) * (size_t)kcount)) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
-  cva::di::dft_kernel<<<(unsigned)kcount, cva::di::kT>>>((const double2*)a.p, n, kcount, sign, scale, (double2*)o.p);
+  cva::di::dft_kernel<<<(unsigned)kcount, cva::di::kT, 0, cva::kS>>>((const double2*)a.p, n, kcount, sign, scale, (double2*)o.p);
   return cva::down(out_complex, o, sizeof(double2) * (size_t)kcount);
 }
 
@@ -355,7 +360,7 @@ int cva_apply_srv_action_host(const double* q, int64_t n, double t0, double thet
   if (int rc = cva::up(g, gamma, sizeof(double) * (size_t)(n + 1))) return rc;
   if (!o.alloc(cb)) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
   cudaError_t e = cva::launch_srv_action((const double2*)a.p, (int)n, t0, theta, (const double*)g.p, (double2*)o.p,
-                                         nullptr);
+                                         cva::kS);
   if (e != cudaSuccess) return cva::err(CVA_CUDA_ERROR, "srv action launch", e);
   return cva::down(out, o, cb);
 }
@@ -374,7 +379,7 @@ int cva_elastic_energy_host(const double* q1, const double* q2, int64_t n, doubl
   if (!t.alloc(sizeof(double) * (size_t)n) || !o.alloc(sizeof(double)))
     return cva::err(CVA_BAD_ALLOC, "device allocation failed");
   cudaError_t e = cva::launch_elastic_energy((const double2*)a.p, (const double2*)b.p, (int)n, t0, theta,
-                                             (const double*)g.p, (double*)t.p, (double*)o.p, nullptr);
+                                             (const double*)g.p, (double*)t.p, (double*)o.p, cva::kS);
   if (e != cudaSuccess) return cva::err(CVA_CUDA_ERROR, "elastic energy launch", e);
   return cva::down(out, o, sizeof(double));
 }
@@ -390,7 +395,7 @@ int cva_dp_step_cost_host(const double* q1, const double* q2, int64_t n, int i0,
   if (int rc = cva::up(b, q2, cb)) return rc;
   if (!o.alloc(sizeof(double))) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
   cudaError_t e = cva::launch_dp_step_cost((const double2*)a.p, (const double2*)b.p, (int)n, i0, j0, di, dj,
-                                           (double*)o.p, nullptr);
+                                           (double*)o.p, cva::kS);
   if (e != cudaSuccess) return cva::err(CVA_CUDA_ERROR, "dp step launch", e);
   return cva::down(out, o, sizeof(double));
 }

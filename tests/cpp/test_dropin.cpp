@@ -10,11 +10,14 @@
 #include <cstdio>
 #include <fstream>
 #include <sstream>
+#include <dirent.h>
+#include <sys/stat.h>
 #include <unistd.h>
 #include <functional>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "curvalign/curve.hpp"
@@ -522,9 +525,61 @@ int main() {
     for (int p = 0; p < 2; ++p) CHECK(r[p].distance == elastic_distance_approach2(a[p], b[p]).distance);
   });
 
+  // ------------------------------------------------- concurrent callers
+  // The reference's functions are pure and re-entrant and distance_matrix calls
+  // align_fft from a thread pool (elastic.cpp:196-234): every thread must get
+  // the answer a lone caller gets.
+  run("concurrent align_fft / preprocess / srv from 8 threads", [&] {
+    std::mt19937_64 rng(77);
+    const int T = 8, per = 6;
+    std::vector<std::pair<Curve, Curve>> in;
+    for (int i = 0; i < T * per; ++i) {
+      const Curve c = preprocess(random_curve(rng, 200 + 37 * i), 256);
+      in.emplace_back(c, shift_rotate(c, (std::size_t)(rng() % 256), 0.1 * i));
+    }
+    std::vector<RigidAlignment> seq, par(in.size());
+    std::vector<Curve> pseq, ppar(in.size());
+    std::vector<RigidAlignment> sseq, spar(in.size());
+    for (const auto& p : in) {
+      seq.push_back(align_fft(p.first, p.second));
+      pseq.push_back(preprocess(p.second, 128));
+      sseq.push_back(align_fft(srv_center(srv_transform(p.first)).q, srv_center(srv_transform(p.second)).q));
+    }
+    std::vector<std::thread> th;
+    std::vector<int> errors(T, 0);
+    for (int t = 0; t < T; ++t)
+      th.emplace_back([&, t] {
+        try {
+          for (int r = 0; r < 3; ++r)
+            for (int i = t; i < (int)in.size(); i += T) {
+              par[i] = align_fft(in[i].first, in[i].second);
+              ppar[i] = preprocess(in[i].second, 128);
+              spar[i] = align_fft(srv_center(srv_transform(in[i].first)).q,
+                                  srv_center(srv_transform(in[i].second)).q);
+            }
+        } catch (...) {
+          errors[t] = 1;
+        }
+      });
+    for (auto& x : th) x.join();
+    for (int t = 0; t < T; ++t) CHECK(errors[t] == 0);
+    auto same = [](const RigidAlignment& a, const RigidAlignment& b) {
+      return a.shift == b.shift && a.t0 == b.t0 && a.rotation.theta() == b.rotation.theta() && a.trace == b.trace &&
+             a.energy == b.energy && a.degenerate == b.degenerate;
+    };
+    for (std::size_t i = 0; i < in.size(); ++i) {
+      CHECK(same(seq[i], par[i]));
+      CHECK(same(sseq[i], spar[i]));
+      bool eq = pseq[i].size() == ppar[i].size();
+      for (std::size_t l = 0; eq && l < pseq[i].size(); ++l)
+        eq = pseq[i].nodes[l].x == ppar[i].nodes[l].x && pseq[i].nodes[l].y == ppar[i].nodes[l].y;
+      CHECK(eq);
+    }
+  });
+
   // --------------------------------------------------------------- file formats
   const std::string tmpdir = "/tmp/cva_dropin_io_" + std::to_string((long)getpid());
-  std::system(("mkdir -p " + tmpdir).c_str());
+  CHECK(mkdir(tmpdir.c_str(), 0700) == 0);
   auto tpath = [&](const char* n) { return tmpdir + "/" + n; };
   auto write_text = [](const std::string& p, const std::string& t) { std::ofstream(p, std::ios::binary) << t; };
   run("io round trips", [&] {  // test_io_cli.cpp:50-72, :110-118
@@ -571,7 +626,12 @@ int main() {
     CHECK(alignment_to_json(r) == "{\"energy\":1e-07,\"shift\":29,\"t0\":0.25,\"theta\":0.5,\"trace\":21.5}");
     CHECK(curve_to_json(Curve{{{1.0, 0.0}, {0.25, 2.0}}}) == "{\"closed\":true,\"nodes\":[[1.0,0.0],[0.25,2.0]]}");
   });
-  std::system(("rm -rf " + tmpdir).c_str());
+  if (DIR* d = opendir(tmpdir.c_str())) {
+    while (dirent* e = readdir(d))
+      if (std::string(e->d_name) != "." && std::string(e->d_name) != "..") std::remove(tpath(e->d_name).c_str());
+    closedir(d);
+  }
+  rmdir(tmpdir.c_str());
 
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
   return g_fail;
