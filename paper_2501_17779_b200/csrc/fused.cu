@@ -84,9 +84,9 @@ __device__ inline void write_bad(cva_alignment* out, int status) {
 
 // Pair p = (curve 2p, curve 2p+1) of the ragged raw batch: preprocess both to
 // N nodes (resample -> center -> normalize, curve.cpp:93-97) and align_fft
-// (rigid_align.cpp:204-208), all on chip. The second curve's resampled nodes
-// are staged in this pair's `aligned` row (L2), which the pair stage then
-// overwrites with the aligned curve.
+// (rigid_align.cpp:204-208), all on chip: the first curve's samples in their
+// own padded buffer, the second's in the resampler's PCR scratch (dead by
+// then), the transforms in the raw-curve region.
 template <int N>
 __global__ void __launch_bounds__(kT, 2)
     resample_align_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off,
@@ -119,15 +119,17 @@ __global__ void __launch_bounds__(kT, 2)
   __syncthreads();  // resample_block's last reads of xy are done
   raw_to_smem(pts + a1, xy, nb, &mbar, 1);
   CVA_MARK(10);
-  const rs::CurveStats B = rs::resample_block<true, false>(xy, nb, s, scr, red, al, N, 11);
+  static_assert(sizeof(double2) * (N + N / 8) <= kScrBytes, "B's padded samples must fit the PCR scratch");
+  double2* Z2 = reinterpret_cast<double2*>(scr);  // B's samples replace the PCR scratch
+  const rs::CurveStats B = rs::resample_block<true, false, true, true>(xy, nb, s, scr, red, Z2, N, 11);
   if (A.bad || B.bad) {
     if (threadIdx.x == 0) write_bad(out + p, CVA_INVALID_ARGUMENT);
     for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
     return;
   }
   __syncthreads();
-  pf::PairIn in{Z1, al, A.centroid, B.centroid, A.inv_len, B.inv_len};
-  pf::pair_stage<false, N, true, 1>(in, bufs, N, tw, out + p, al, red);
+  pf::PairIn in{Z1, Z2, A.centroid, B.centroid, A.inv_len, B.inv_len};
+  pf::pair_stage<false, N, true, 2>(in, bufs, N, tw, out + p, al, red);
 }
 
 // ------------------------------------------------------------- preprocess

@@ -452,7 +452,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     for (int q = 0; q < kMaxPer; ++q) {
       const int j = t + q * kT;
       if (j < N) {
-        const double2 z = in.srv2 ? srv_at(in.srv2, j, N) : in.z2[j];
+        const double2 z = in.srv2 ? srv_at(in.srv2, j, N) : in.z2[kPad == 2 ? j + (j >> 3) : j];
         const double2 p = make_double2((z.x - c.x) * sc, (z.y - c.y) * sc);
         v[q] = make_double2(fma(rot.x, p.x, rot.y * p.y), fma(-rot.y, p.x, rot.x * p.y));
       }

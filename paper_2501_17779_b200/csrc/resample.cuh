@@ -157,7 +157,9 @@ __device__ __forceinline__ double sample_t(int l, int N, double invN) {
 // the knots only): the fused pair kernel measures it while loading its FFT.
 // kPadOut: out is shared memory indexed out[l + (l >> 3)] (one pad slot per
 // 8 samples: the chunk-strided sample stores spread over all banks).
-template <bool kPow2, bool kLen = true, bool kPadOut = false>
+// kOutInScr: out may alias scr (>= N + N/8 double2): the PCR scratch is dead
+// once phase 3 has read its boundary values, so the samples go there.
+template <bool kPow2, bool kLen = true, bool kPadOut = false, bool kOutInScr = false>
 __device__ inline CurveStats resample_block(const double2* xy, int n, double* L, double* scr,
                                             double2* red, double2* out, const int N,
                                             const int pb = 0 /* phase-stamp base */) {
@@ -399,8 +401,10 @@ __device__ inline CurveStats resample_block(const double2* xy, int n, double* L,
 
     // ---- phase 3: interior re-solve + fused evaluation
     double2 cacc = make_double2(0, 0);
+    double2 mub = make_double2(0, 0);
+    if (own) mub = MB[t + 1 == K ? 0 : t + 1];
+    if constexpr (kOutInScr) bar_sync();  // out aliases scr (W, MB): every read above is done
     if (own) {
-      const double2 mub = MB[t + 1 == K ? 0 : t + 1];
       // forward with known boundary values, in place (R[j] <- g_j): each row
       // reads its left spacing from the knots and g_{j-1} from R[j-1], so no
       // value rotates through the data-dependent guard
