@@ -77,7 +77,8 @@ int cva_abi_version(void);
 const char* cva_last_error(void);
 /* Number of visible CUDA devices (0 when none); never fails. */
 int cva_device_count(void);
-/* Largest raw node count a single curve may have in the resampling kernels. */
+/* Largest raw node count a single curve may have in the resampling entry points
+ * (INT32_MAX: curves beyond shared memory are solved in global scratch). */
 int64_t cva_max_resample_nodes(void);
 
 /* ---------------------------------------------------------------------------

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <map>
 #include <new>
+#include <climits>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -131,14 +132,6 @@ cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
   return cudaMallocAsync(p, bytes ? bytes : 16, s);
 }
 
-int check_resample_nmax(int64_t nmax, int64_t n_out, size_t smem) {
-  if (nmax > cva::max_chunked_nodes() || smem > (size_t)smem_limit())
-    return fail(CVA_UNSUPPORTED, "resample: curve has more raw nodes than the shared-memory "
-                                 "resampler holds (n_in=" + std::to_string(nmax) +
-                                     ", n_out=" + std::to_string(n_out) + ")");
-  return CVA_OK;
-}
-
 int64_t host_max_n(const int64_t* offsets, int64_t curves) {
   int64_t m = 0;
   for (int64_t c = 0; c < curves; ++c) m = std::max(m, offsets[c + 1] - offsets[c]);
@@ -158,6 +151,25 @@ int device_max_n(const int64_t* d_offsets, int64_t curves, cudaStream_t s, int64
 int finish(cudaError_t e, const char* what) {
   if (e != cudaSuccess) return cuda_fail(e, what);
   return CVA_OK;
+}
+
+// General resampler for raw curves the v2 kernel does not hold: the v1
+// shared-memory kernel when the curve and its solver arrays fit shared memory,
+// else the same solver on per-CTA global slabs (any n_in, any n_out).
+int resample_general(const double* points, const int64_t* offsets, int64_t curves, int nmax, int64_t n_out,
+                     int center_normalize, double* out, int32_t* status, cudaStream_t s) {
+  const size_t smem = cva::resample_smem_bytes(nmax, (int)n_out);
+  if (nmax <= cva::max_chunked_nodes() && smem <= (size_t)smem_limit())
+    return finish(cva::launch_preprocess_resample((const double2*)points, offsets, curves, nmax, (int)n_out,
+                                                  center_normalize, (double2*)out, status, s),
+                  "preprocess launch");
+  void* slab = nullptr;
+  const size_t bytes = cva::resample_global_slab_bytes(nmax) * (size_t)cva::resample_global_grid(curves);
+  if (scratch_alloc(&slab, bytes, s) != cudaSuccess) return fail(CVA_BAD_ALLOC, "resample slab allocation failed");
+  cudaError_t e = cva::launch_preprocess_resample_global((const double2*)points, offsets, curves, nmax, (int)n_out,
+                                                         center_normalize, (double2*)out, status, slab, s);
+  cudaFreeAsync(slab, s);
+  return finish(e, "preprocess (global slab) launch");
 }
 
 int large_align(const double* c1, const double* c2, int64_t pairs, int64_t n, int normalize,
@@ -190,12 +202,7 @@ int resample_dispatch(const double* points, const int64_t* offsets, int64_t curv
     return finish(cva::launch_v2_preprocess((const double2*)points, offsets, curves, (int)n_out,
                                             center_normalize, (double2*)out, status, s),
                   "preprocess launch");
-  if (int rc = check_resample_nmax(nmax, n_out, cva::resample_smem_bytes(nmax, (int)n_out)))
-    return rc;
-  return finish(cva::launch_preprocess_resample((const double2*)points, offsets, curves, nmax,
-                                                (int)n_out, center_normalize, (double2*)out,
-                                                status, s),
-                "preprocess launch");
+  return resample_general(points, offsets, curves, nmax, n_out, center_normalize, out, status, s);
 }
 
 // RAII device buffer for the *_host entry points.
@@ -226,7 +233,7 @@ int cva_device_count(void) {
   return n;
 }
 
-int64_t cva_max_resample_nodes(void) { return cva::max_chunked_nodes(); }
+int64_t cva_max_resample_nodes(void) { return INT32_MAX; }  // beyond shared memory: global slabs
 
 int cva_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
                     cva_alignment* out, double* aligned, void* stream) {
@@ -303,15 +310,10 @@ int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int
   if (nmax <= cva::v2_max_raw_nodes()) {
     const size_t ab = sizeof(double2) * (size_t)(pairs * n_out);
     if (cva::v2_resample_align_supported((int)n_out)) {
-      // fused kernel; the aligned rows double as the second curve's staging buffer
-      void* ws = nullptr;
-      if (!aligned && scratch_alloc(&ws, ab, s) != cudaSuccess)
-        return fail(CVA_BAD_ALLOC, "scratch allocation failed");
-      cudaError_t e = cva::launch_v2_resample_align((const double2*)points, offsets, pairs,
-                                                    (int)n_out, tw, out,
-                                                    aligned ? (double2*)aligned : (double2*)ws, s);
-      if (ws) cudaFreeAsync(ws, s);
-      return finish(e, "resample_align launch");
+      // fused kernel (aligned may be null: results only)
+      return finish(cva::launch_v2_resample_align((const double2*)points, offsets, pairs, (int)n_out, tw, out,
+                                                  (double2*)aligned, s),
+                    "resample_align launch");
     }
     // other N: preprocess into scratch, then align
     void* ws = nullptr;
@@ -328,16 +330,15 @@ int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int
     return finish(e, "preprocess+align launch");
   }
   // raw curves beyond the v2 resampler: general resampler into scratch, then align
-  if (int rc = check_resample_nmax(nmax, n_out, cva::resample_smem_bytes(nmax, (int)n_out)))
-    return rc;
   void* ws = nullptr;
   if (scratch_alloc(&ws, 2 * sizeof(double2) * (size_t)(pairs * n_out), s) != cudaSuccess)
     return fail(CVA_BAD_ALLOC, "scratch allocation failed");
-  cudaError_t e = cva::launch_preprocess_resample((const double2*)points, offsets, 2 * pairs, nmax,
-                                                  (int)n_out, 1, (double2*)ws, nullptr, s);
-  if (e == cudaSuccess)
-    e = cva::launch_v2_align_interleaved((const double2*)ws, pairs, (int)n_out, tw, out,
-                                         (double2*)aligned, s);
+  if (int rc = resample_general(points, offsets, 2 * pairs, nmax, n_out, 1, (double*)ws, nullptr, s)) {
+    cudaFreeAsync(ws, s);
+    return rc;
+  }
+  cudaError_t e = cva::launch_v2_align_interleaved((const double2*)ws, pairs, (int)n_out, tw, out,
+                                                   (double2*)aligned, s);
   cudaFreeAsync(ws, s);
   return finish(e, "preprocess+align launch");
 }

@@ -103,11 +103,12 @@ __global__ void __launch_bounds__(kT, 2)
   const int64_t p = blockIdx.x;
   const int64_t a0 = off[2 * p], a1 = off[2 * p + 1], b1 = off[2 * p + 2];
   const int na = (int)(a1 - a0), nb = (int)(b1 - a1);
-  double2* al = aligned + p * N;
+  double2* al = aligned ? aligned + p * N : nullptr;  // null: results only
   if (threadIdx.x == 0) prefetch_l2(pts + a1, nb * (int)sizeof(double2));
   if (na < 4 || nb < 4 || na > rs::kNMax || nb > rs::kNMax) {  // validate_curve(c, 4)
     if (threadIdx.x == 0) write_bad(out + p, CVA_INVALID_ARGUMENT);
-    for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
+    if (al)
+      for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
     return;
   }
   CVA_MARK(0);
@@ -124,7 +125,8 @@ __global__ void __launch_bounds__(kT, 2)
   const rs::CurveStats B = rs::resample_block<true, false, true, true>(xy, nb, s, scr, red, Z2, N, 11);
   if (A.bad || B.bad) {
     if (threadIdx.x == 0) write_bad(out + p, CVA_INVALID_ARGUMENT);
-    for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
+    if (al)
+      for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
     return;
   }
   __syncthreads();

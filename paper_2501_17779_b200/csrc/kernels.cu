@@ -71,7 +71,8 @@ struct ResampleSmem {
 // Returns block-uniform status.
 __device__ inline int block_resample_preprocess(const double2* __restrict__ raw, int n, int n_out,
                                                 const ResampleSmem& R, double2* out_sm,
-                                                double2* red, bool center_normalize = true) {
+                                                double2* red, bool center_normalize = true,
+                                                double* cpv_g = nullptr) {
   if (n < 4 || n_out < 8) return kInvalid;  // validate_curve(c, 4), n_out >= 8 (curve.cpp:68-69)
   load_curve(raw, R.xy, n);
   __syncthreads();
@@ -79,7 +80,7 @@ __device__ inline int block_resample_preprocess(const double2* __restrict__ raw,
   if (bad) return kInvalid;
   block_arc_length(R.xy, n, R.s, red, &bad);
   if (bad) return kInvalid;
-  block_spline_solve(R.s, R.xy, R.m, n, R.ends, red);
+  block_spline_solve(R.s, R.xy, R.m, n, R.ends, red, cpv_g);
   block_spline_eval(R.s, R.xy, R.m, n, n_out, out_sm);
   if (center_normalize) block_center_normalize(out_sm, n_out, red, &bad);
   return bad ? kInvalid : kOk;
@@ -143,6 +144,31 @@ __global__ void __launch_bounds__(kThreads)
     fill_nan(o, n_out);
   }
   if (status && threadIdx.x == 0) status[c] = st;
+}
+
+// The same resample -> center -> normalize for raw curves too long for shared
+// memory (any n >= 4, any n_out >= 8): the solver's arrays live in a per-CTA
+// slab of global memory (L2-resident: 48 B per raw node) and the samples are
+// written straight to `out`. A grid-stride loop over curves reuses the slabs.
+__global__ void __launch_bounds__(kThreads)
+    preprocess_resample_global_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off,
+                                      int64_t curves, int nmax, int n_out, int center_normalize,
+                                      double2* __restrict__ out, int32_t* __restrict__ status, char* slab,
+                                      size_t slab_bytes) {
+  __shared__ double2 red[kRedSlots];
+  char* base = slab + (size_t)blockIdx.x * slab_bytes;
+  ResampleSmem R;
+  R.carve(base, nmax);
+  double* cpv = reinterpret_cast<double*>(base + ResampleSmem::bytes(nmax));
+  for (int64_t c = blockIdx.x; c < curves; c += gridDim.x) {
+    const int64_t b0 = off[c];
+    const int n = (int)(off[c + 1] - b0);
+    double2* o = out + c * n_out;
+    const int st = block_resample_preprocess(pts + b0, n, n_out, R, o, red, center_normalize != 0, cpv);
+    if (st != kOk) fill_nan(o, n_out);
+    if (status && threadIdx.x == 0) status[c] = st;
+    __syncthreads();  // the slab is reused by the next curve
+  }
 }
 
 // center + normalize in place in global memory (no resampling; any n >= 3).
@@ -340,5 +366,25 @@ cudaError_t launch_srv_align(const double2* c1, const double2* c2, int64_t pairs
 }
 
 int max_chunked_nodes() { return kThreads * kMaxChunk; }
+
+size_t resample_global_slab_bytes(int nmax) {
+  return (ResampleSmem::bytes(nmax) + sizeof(double) * (size_t)nmax + 255) & ~size_t(255);
+}
+int resample_global_grid(int64_t curves) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return (int)(curves < 4 * (int64_t)sms ? curves : 4 * (int64_t)sms);
+}
+cudaError_t launch_preprocess_resample_global(const double2* pts, const int64_t* off, int64_t curves, int nmax,
+                                              int n_out, int center_normalize, double2* out, int32_t* status,
+                                              void* slab, cudaStream_t s) {
+  const int grid = resample_global_grid(curves);
+  if (grid == 0) return cudaSuccess;
+  preprocess_resample_global_kernel<<<grid, kThreads, 0, s>>>(pts, off, curves, nmax, n_out, center_normalize, out,
+                                                              status, (char*)slab,
+                                                              resample_global_slab_bytes(nmax));
+  return cudaGetLastError();
+}
 
 }  // namespace cva

@@ -109,9 +109,12 @@ struct ChunkEnds {  // values at the first / last interior knot of a chunk
 };
 
 // Solve the periodic spline system for m[0..n) (both coordinates). On entry m is
-// scratch; `ends` holds >= K ChunkEnds (K <= blockDim.x). n >= 4, n <= K * kMaxChunk.
+// scratch; `ends` holds >= K ChunkEnds (K <= blockDim.x). n >= 4, n <= K * kMaxChunk
+// unless cpv_g is given (then any n).
+// cpv_g: optional n-double scratch (global) for the phase-3 pivot ratios; null
+// = a per-thread local array (chunks of <= kMaxChunk knots).
 __device__ inline void block_spline_solve(const double* s, const double2* xy, double2* m, int n,
-                                          ChunkEnds* ends, double2* red) {
+                                          ChunkEnds* ends, double2* red, double* cpv_g = nullptr) {
   const int T = blockDim.x, t = threadIdx.x;
   const int K = spline_chunks(n, T);
 
@@ -238,7 +241,8 @@ __device__ inline void block_spline_solve(const double* s, const double2* xy, do
     const int a = (int)(((long long)t * n) / K), b = (int)(((long long)(t + 1) * n) / K);
     const int L = b - 2;
     const double2 wl = m[a == 0 ? n - 1 : a - 1], wr = m[b - 1];
-    double cpv[kMaxChunk];
+    double cpv_l[kMaxChunk];
+    double* cpv = cpv_g ? cpv_g + a : cpv_l;
     double hm = knot_h(s, n, a - 1), hi = knot_h(s, n, a);
     double ib = 1.0 / (2.0 * (hm + hi));
     double2 r = m[a];

@@ -452,3 +452,72 @@ def test_misaligned_curve_buffer_rejected(cuda):
                                         out.data_ptr(), None, torch.cuda.current_stream().cuda_stream)
     assert rc == _native.CVA_INVALID_ARGUMENT and b"16-byte aligned" in lib.cva_last_error()
     torch.cuda.synchronize()
+
+
+def test_c1_fused_mixed_invalid_pairs(cuda):
+    """Invalid pairs inside a fused C1 batch (validate_curve, curve.cpp:11-14,
+    :58) fail alone: status CVA_INVALID_ARGUMENT and NaN results for them, the
+    other pairs bitwise what a clean batch gives; with and without the aligned
+    output (results only)."""
+    pts, offs, _, _ = synth.ragged_pairs(77, 8, 1024)
+    curves = [pts[offs[i]:offs[i + 1]].copy() for i in range(16)]
+    bad = list(curves)
+    bad[3] = curves[3][:3]                     # pair 1: too few nodes
+    d = curves[4].copy()
+    d[10] = d[9]
+    bad[4] = d                                 # pair 2: coincident nodes
+    nn = curves[9].copy()
+    nn[5, 1] = np.inf
+    bad[9] = nn                                # pair 4: non-finite node
+    p_bad, o_bad = cva.ragged(bad)
+    p_ok, o_ok = cva.ragged(curves)
+    r_ok, a_ok = cva.preprocess_align_batch(p_ok, o_ok, 1024, return_aligned=True)
+    r_bad, a_bad = cva.preprocess_align_batch(p_bad, o_bad, 1024, return_aligned=True)
+    r_only, _ = cva.preprocess_align_batch(p_bad, o_bad, 1024, return_aligned=False)
+    assert (r_ok["status"] == 0).all()
+    for p in range(8):
+        if p in (1, 2, 4):
+            assert r_bad[p]["status"] == _native.CVA_INVALID_ARGUMENT
+            assert np.isnan(r_bad[p]["theta"]) and np.isnan(a_bad[p]).all()
+        else:
+            assert r_bad[p] == r_ok[p]
+            np.testing.assert_array_equal(a_bad[p], a_ok[p])
+    for f in ("shift", "status"):
+        np.testing.assert_array_equal(r_only[f], r_bad[f])
+    np.testing.assert_array_equal(r_only["energy"], r_bad["energy"])
+
+
+def test_c1_raw_curves_beyond_shared_memory(cuda, oracle):
+    """Raw curves longer than the fused kernel holds (> 3072 nodes) take the
+    general resampler and the same alignment; results match the oracle."""
+    rng = np.random.default_rng(5)
+    curves = []
+    for n_in in (3500, 800, 5000, 4100):
+        phi = np.sort(rng.uniform(0, 2 * PI, n_in))
+        r = 1 + 0.25 * np.cos(5 * phi + rng.uniform(0, 6)) + 0.1 * np.sin(2 * phi)
+        curves.append(np.stack([r * np.cos(phi), r * np.sin(phi)], 1))
+    pts, offs = cva.ragged(curves)
+    res, al = cva.preprocess_align_batch(pts, offs, 1024, return_aligned=True)
+    ro, ao = oracle.batch(pts, offs, 1024, mode=0, threads=2, aligned=True)
+    for p in range(2):
+        c1 = oracle.preprocess(curves[2 * p], 1024)
+        c2 = oracle.preprocess(curves[2 * p + 1], 1024)
+        check_pair(res[p], ro[p], c1, c2, al[p], ao[p])
+
+
+@pytest.mark.parametrize("n_in", [4700, 9000, 20000])
+def test_resample_raw_curves_beyond_shared_memory(cuda, oracle, n_in):
+    """The reference resamples any node count (curve.cpp:67-91). Curves whose
+    solver arrays exceed shared memory (> ~4.6 K nodes at n_out = 1024, or more
+    than 256 x 32 knots) run the same partition solver on global scratch."""
+    rng = np.random.default_rng(n_in)
+    phi = (np.arange(n_in) + rng.uniform(-0.4, 0.4, n_in)) * (2 * PI / n_in)
+    r = 1 + 0.3 * np.cos(7 * phi + 0.5) + 0.05 * np.sin(31 * phi)
+    raw = np.stack([r * np.cos(phi), r * np.sin(phi)], 1)
+    for n_out in (64, 1024, 4096):
+        got = cva.resample_uniform(raw, n_out)
+        want = oracle.resample_uniform(raw, n_out)
+        assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max()
+    got = cva.preprocess(raw, 1024)
+    want = oracle.preprocess(raw, 1024)
+    assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max()
