@@ -114,7 +114,9 @@ int cva_resample_batch(const double* points, const int64_t* offsets, int64_t cur
  * the ragged raw batch; preprocess both to n_out nodes (resample != 0;
  * proj/src/curve.cpp:93-97) then align_fft (proj/src/rigid_align.cpp:204-208),
  * the sequence of cmd_align / run_align (proj/src/cli.cpp:41-44, :99). aligned
- * (nullable): pairs x n_out points. */
+ * (nullable): pairs x n_out points. Any raw node count and any n_out >= 8:
+ * n_out = 512 / 1024 with raw curves <= 3072 nodes run one fused kernel, other
+ * sizes preprocess into scratch and align (multi-pass beyond n_out = 2048). */
 int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int64_t pairs,
                                int64_t max_n_in, int64_t n_out, int resample,
                                cva_alignment* out, double* aligned, void* stream);
@@ -129,7 +131,8 @@ int cva_preprocess_align_uniform(const double* c1, const double* c2, int64_t pai
 /* SRV-space alignment: align_fft(srv_center(srv_transform(c1)).q,
  * srv_center(srv_transform(c2)).q) (proj/src/srv.cpp:71-98; the (t0,R) step
  * pattern of proj/src/elastic.cpp:138-139). aligned_q (nullable): the rotated,
- * shifted centered SRV of c2. Requires n >= 8. */
+ * shifted centered SRV of c2. Requires n >= 8; any n (n <= 2048 fused on chip,
+ * larger n: SRV curves in scratch, then the multi-pass alignment). */
 int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
                         cva_alignment* out, double* aligned_q, void* stream);
 

@@ -299,12 +299,33 @@ int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int
                 "preprocess_align: resample=0 takes equal-size pairs; use "
                 "cva_preprocess_align_uniform");
   if (n_out < 8) return fail(CVA_INVALID_ARGUMENT, "resample: need at least 8 output nodes");
-  if (int rc = check_small_fft(n_out)) return rc;
+  if (int rc = check_fft_size(n_out)) return rc;
   if (int rc = require_device()) return rc;
   cudaStream_t s = (cudaStream_t)stream;
   if (max_n_in <= 0)
     if (int rc = device_max_n(offsets, 2 * pairs, s, &max_n_in)) return rc;
   const int nmax = (int)std::max<int64_t>(max_n_in, 4);
+  if (!small_fft(n_out)) {
+    // beyond the shared-memory transforms: preprocess every curve, split the
+    // pairs' rows into two arrays, then the multi-pass alignment (any N)
+    const size_t row = sizeof(double2) * (size_t)n_out;
+    void* ws = nullptr;
+    if (scratch_alloc(&ws, 4 * row * (size_t)pairs, s) != cudaSuccess)
+      return fail(CVA_BAD_ALLOC, "scratch allocation failed");
+    char* prep = (char*)ws;
+    char* ab = prep + 2 * row * (size_t)pairs;
+    int rc = resample_dispatch(points, offsets, 2 * pairs, nmax, n_out, 1, (double*)prep, nullptr, s);
+    for (int h = 0; h < 2 && rc == CVA_OK; ++h) {
+      const cudaError_t e = cudaMemcpy2DAsync(ab + h * row * (size_t)pairs, row, prep + h * row, 2 * row, row,
+                                              (size_t)pairs, cudaMemcpyDeviceToDevice, s);
+      if (e != cudaSuccess) rc = cuda_fail(e, "de-interleave");
+    }
+    if (rc == CVA_OK)
+      rc = cva_align_batch((const double*)ab, (const double*)(ab + row * (size_t)pairs), pairs, n_out, out,
+                           aligned, stream);
+    cudaFreeAsync(ws, s);
+    return rc;
+  }
   const double2* tw = nullptr;
   if (int rc = get_twiddles(cva::v2_fft_len((int)n_out), s, &tw)) return rc;
   if (nmax <= cva::v2_max_raw_nodes()) {
@@ -376,13 +397,26 @@ int cva_preprocess_align_uniform(const double* c1, const double* c2, int64_t pai
 int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
                         cva_alignment* out, double* aligned_q, void* stream) {
   if (n < 8) return fail(CVA_INVALID_ARGUMENT, "curve: too few nodes");  // srv.cpp:72
-  if (int rc = check_small_fft(n)) return rc;
+  if (int rc = check_fft_size(n)) return rc;
   if (pairs < 0) return fail(CVA_INVALID_ARGUMENT, "srv: negative pair count");
   if (pairs == 0) return CVA_OK;
   if (!c1 || !c2 || !out) return fail(CVA_INVALID_ARGUMENT, "srv: null pointer");
   if (!a16(c1) || !a16(c2) || !a16(aligned_q)) return misaligned("srv");
   if (int rc = require_device()) return rc;
   cudaStream_t s = (cudaStream_t)stream;
+  if (!small_fft(n)) {  // SRV curves into scratch, then the multi-pass alignment (any N)
+    const size_t rows = sizeof(double2) * (size_t)(pairs * n);
+    void* ws = nullptr;
+    if (scratch_alloc(&ws, 2 * rows, s) != cudaSuccess) return fail(CVA_BAD_ALLOC, "scratch allocation failed");
+    double2* q1 = (double2*)ws;
+    double2* q2 = q1 + pairs * n;
+    cudaError_t e = cva::launch_v2_srv_center((const double2*)c1, pairs, (int)n, q1, s);
+    if (e == cudaSuccess) e = cva::launch_v2_srv_center((const double2*)c2, pairs, (int)n, q2, s);
+    int rc = e == cudaSuccess ? CVA_OK : cuda_fail(e, "srv launch");
+    if (rc == CVA_OK) rc = cva_align_batch((const double*)q1, (const double*)q2, pairs, n, out, aligned_q, stream);
+    cudaFreeAsync(ws, s);
+    return rc;
+  }
   const double2* tw = nullptr;
   if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
   return finish(cva::launch_v2_srv_align((const double2*)c1, (const double2*)c2, pairs, (int)n, tw, out,
@@ -679,7 +713,7 @@ int cva_preprocess_align_uniform_host(const double* c1, const double* c2, int64_
 int cva_srv_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
                              cva_alignment* out, double* aligned_q) {
   if (n < 8) return fail(CVA_INVALID_ARGUMENT, "curve: too few nodes");
-  if (int rc = check_small_fft(n)) return rc;
+  if (int rc = check_fft_size(n)) return rc;
   if (pairs <= 0) return pairs == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative pair count");
   if (int rc = require_device()) return rc;
   const size_t cb = sizeof(double) * 2 * (size_t)(pairs * n);

@@ -301,6 +301,33 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
   pf::pair_stage<kIP, kN, false, 2>(in, bufs, N, tw, out + p, al, red);
 }
 
+// srv_center(srv_transform(c)) of one curve per CTA into global memory, any
+// N (srv.cpp:71-98): the large-N SRV alignment feeds these to the multi-pass
+// transforms. A curve with a non-finite node becomes NaN (its pair then
+// reports CVA_INVALID_ARGUMENT, like validate_curve).
+__global__ void __launch_bounds__(kT) srv_center_kernel(const double2* __restrict__ c, int N, double2* __restrict__ q) {
+  __shared__ double2 red[16];
+  const int64_t k = blockIdx.x;
+  const double2* x = c + k * N;
+  double2* o = q + k * N;
+  double mx = 0.0, my = 0.0, nf = 0.0;
+  for (int l = threadIdx.x; l < N; l += kT) {
+    const double2 u = x[l];
+    nf += (isfinite(u.x) && isfinite(u.y)) ? 0.0 : 1.0;
+    const double2 v = pf::srv_at(x, l, N);
+    o[l] = v;
+    mx += v.x;
+    my += v.y;
+  }
+  rs::block_sum3(mx, my, nf, red);
+  const double invn = 1.0 / (double)N;
+  const double2 m = nf != 0.0 ? make_double2(qnan(), qnan()) : make_double2(invn * mx, invn * my);
+  for (int l = threadIdx.x; l < N; l += kT) {  // each thread rewrites only its own entries
+    const double2 v = o[l];
+    o[l] = make_double2(v.x - m.x, v.y - m.y);
+  }
+}
+
 }  // namespace v2
 
 // ------------------------------------------------------------ launchers
@@ -475,4 +502,11 @@ cudaError_t launch_v2_srv_align(const double2* c1, const double2* c2, int64_t pa
   return launch_srv_n<false, 0>(c1, c2, pairs, N, tw, out, aligned, sm, s);
 }
 
+}  // namespace cva
+
+namespace cva {
+cudaError_t launch_v2_srv_center(const double2* c, int64_t curves, int N, double2* q, cudaStream_t s) {
+  if (curves > 0) v2::srv_center_kernel<<<(unsigned)curves, v2::kT, 0, s>>>(c, N, q);
+  return cudaGetLastError();
+}
 }  // namespace cva

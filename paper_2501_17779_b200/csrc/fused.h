@@ -45,6 +45,8 @@ cudaError_t launch_allpairs(const double2* za, const double2* zb, const double* 
                             int64_t row_begin, int64_t row_end, const double2* tw, double* energy,
                             int32_t* shift, double* theta, double2* dm, cudaStream_t s);
 
+// srv_center(srv_transform(c)) per curve, any N (global in/out)
+cudaError_t launch_v2_srv_center(const double2* c, int64_t curves, int N, double2* q, cudaStream_t s);
 cudaError_t launch_v2_srv_align(const double2* c1, const double2* c2, int64_t pairs, int N,
                                 const double2* tw, cva_alignment* out, double2* aligned, cudaStream_t s);
 

@@ -521,3 +521,25 @@ def test_resample_raw_curves_beyond_shared_memory(cuda, oracle, n_in):
     got = cva.preprocess(raw, 1024)
     want = oracle.preprocess(raw, 1024)
     assert np.abs(got - want).max() <= 1e-11 * np.abs(want).max()
+
+
+def test_large_n_out_and_srv_beyond_shared_memory(cuda, oracle):
+    """preprocess_align with n_out beyond the shared-memory transforms, and the
+    SRV alignment at N = 4096: same answers as the step-by-step path
+    (preprocess, srv_transform + srv_center, align_fft) on the oracle."""
+    pts, offs, _, _ = synth.ragged_pairs(31, 3, 1024)
+    res, al = cva.preprocess_align_batch(pts, offs, 4096, return_aligned=True)
+    for p in range(3):
+        c1 = oracle.preprocess(pts[offs[2 * p]:offs[2 * p + 1]], 4096)
+        c2 = oracle.preprocess(pts[offs[2 * p + 1]:offs[2 * p + 2]], 4096)
+        r = oracle.align(c1, c2)
+        check_pair(res[p], r, c1, c2)
+    s1, s2, _, _, _ = synth.srv_pairs(32, 3, 4096)
+    res, alq = cva.srv_align_batch(s1, s2, return_aligned=True)
+    small, _ = cva.srv_align_batch(s1[:, ::2].copy(), s2[:, ::2].copy())  # N = 2048 fused kernel still fine
+    assert (small["status"] == 0).all()
+    for p in range(3):
+        q1 = oracle.srv_center(oracle.srv_transform(s1[p]))
+        q2 = oracle.srv_center(oracle.srv_transform(s2[p]))
+        r = oracle.align(q1, q2)
+        check_pair(res[p], r, q1, q2)
