@@ -1,19 +1,16 @@
 // sm_100a kernels of the curve-alignment hot path and their host launchers.
 //
-//   tw_init_kernel              twiddle table w_N^k = exp(-2 pi i k / N) (sincospi)
-//   align_kernel                align_fft on pre-sampled pairs       (rigid_align.cpp:204-208)
-//   preprocess_resample_kernel  resample -> center -> normalize       (curve.cpp:93-97)
-//   preprocess_center_kernel    center -> normalize (resample=false)   (curve.cpp:93-97)
-//   preprocess_align_kernel     fused C1 path: both preprocesses + align_fft of one pair
-//   srv_align_kernel            srv_transform -> srv_center -> align_fft (srv.cpp:71-98)
+//   tw_init_kernel                     twiddle table w_N^k = exp(-2 pi i k / N) (sincospi)
+//   preprocess_resample_kernel         resample -> center -> normalize (curve.cpp:93-97), one
+//                                      curve per CTA in shared memory (raw curves the v2
+//                                      resampler of fused.cu does not hold, up to ~4.6 K nodes)
+//   preprocess_resample_global_kernel  the same on per-CTA global slabs (any node count)
+//   preprocess_center_kernel           center -> normalize (resample=false)
 //
-// One CTA per pair (or per curve); all intermediate data stays in shared memory,
-// so each pair reads its raw input from HBM once and writes only its result and
-// aligned curve.
+// The alignment itself runs in fused.cu / largen.cu / allpairs.cu.
 #include <cuda_runtime.h>
 
 #include "../../include/curvalign_cuda.h"
-#include "align.cuh"
 #include "cva_common.cuh"
 #include "fft.cuh"
 #include "kernels.h"
@@ -86,43 +83,11 @@ __device__ inline int block_resample_preprocess(const double2* __restrict__ raw,
   return bad ? kInvalid : kOk;
 }
 
-__device__ inline void write_bad_alignment(cva_alignment* out, int status) {
-  cva_alignment r;
-  r.shift = 0;
-  r.t0 = 0.0;
-  r.theta = qnan();
-  r.trace = qnan();
-  r.energy = qnan();
-  r.degenerate = 0;
-  r.status = status;
-  *out = r;
-}
-
 __device__ inline void fill_nan(double2* g, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) g[i] = make_double2(qnan(), qnan());
 }
 
 // ------------------------------------------------------------------ kernels
-
-__global__ void __launch_bounds__(kThreads) align_kernel(const double2* __restrict__ c1,
-                                                         const double2* __restrict__ c2, int N,
-                                                         const double2* __restrict__ tw,
-                                                         cva_alignment* __restrict__ out,
-                                                         double2* __restrict__ aligned) {
-  extern __shared__ __align__(16) char smem_raw[];
-  __shared__ double2 red[kRedSlots];
-  double2* A = reinterpret_cast<double2*>(smem_raw);
-  double2* B = A + N;
-  double2* C = B + N;
-  double2* D = C + N;
-  const int64_t p = blockIdx.x;
-  load_curve(c1 + p * N, A, N);
-  load_curve(c2 + p * N, B, N);
-  __syncthreads();
-  const double s1 = block_sum_norm2(A, N, red);
-  const double s2 = block_sum_norm2(B, N, red);
-  block_align_tail(A, B, C, D, N, tw, s1, s2, out + p, aligned ? aligned + p * N : nullptr, red);
-}
 
 __global__ void __launch_bounds__(kThreads)
     preprocess_resample_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off,
@@ -211,102 +176,10 @@ __global__ void __launch_bounds__(kThreads)
   if (status && threadIdx.x == 0) status[c] = bad ? kInvalid : kOk;
 }
 
-__global__ void __launch_bounds__(kThreads)
-    preprocess_align_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off,
-                            int nmax, int N, const double2* __restrict__ tw,
-                            cva_alignment* __restrict__ out, double2* __restrict__ aligned) {
-  extern __shared__ __align__(16) char smem_raw[];
-  __shared__ double2 red[kRedSlots];
-  double2* Z1 = reinterpret_cast<double2*>(smem_raw);
-  double2* Z2 = Z1 + N;
-  char* work = reinterpret_cast<char*>(Z2 + N);  // resample arrays, later FFT scratch
-  ResampleSmem R;
-  R.carve(work, nmax);
-  const int64_t p = blockIdx.x;
-  const int64_t a0 = off[2 * p], a1 = off[2 * p + 1], b1 = off[2 * p + 2];
-  int st = block_resample_preprocess(pts + a0, (int)(a1 - a0), N, R, Z1, red);
-  if (st == kOk) st = block_resample_preprocess(pts + a1, (int)(b1 - a1), N, R, Z2, red);
-  double2* al = aligned ? aligned + p * N : nullptr;
-  if (st != kOk) {
-    if (threadIdx.x == 0) write_bad_alignment(out + p, st);
-    if (al) fill_nan(al, N);
-    return;
-  }
-  const double s1 = block_sum_norm2(Z1, N, red);
-  const double s2 = block_sum_norm2(Z2, N, red);
-  double2* W1 = reinterpret_cast<double2*>(work);
-  double2* W2 = W1 + N;
-  block_align_tail(Z1, Z2, W1, W2, N, tw, s1, s2, out + p, al, red);
-}
-
-// q_l = d_l / sqrt(|d_l|), d_l = (N/2)(c[l+1] - c[l-1]); 0 if |d_l| < 1e-8 N (srv.cpp:71-88)
-__device__ inline void block_srv(const double2* c, double2* q, int N) {
-  const double nn = (double)N;
-  const double eps = 1e-8 * nn;
-  for (int l = threadIdx.x; l < N; l += blockDim.x) {
-    const double2 nx = c[l + 1 == N ? 0 : l + 1], pv = c[l == 0 ? N - 1 : l - 1];
-    const double2 d = make_double2((nn / 2.0) * (nx.x - pv.x), (nn / 2.0) * (nx.y - pv.y));
-    const double mag = sqrt(fma(d.x, d.x, d.y * d.y));
-    q[l] = mag < eps ? make_double2(0.0, 0.0) : cscale(d, 1.0 / sqrt(mag));
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) srv_align_kernel(const double2* __restrict__ c1,
-                                                             const double2* __restrict__ c2, int N,
-                                                             const double2* __restrict__ tw,
-                                                             cva_alignment* __restrict__ out,
-                                                             double2* __restrict__ aligned) {
-  extern __shared__ __align__(16) char smem_raw[];
-  __shared__ double2 red[kRedSlots];
-  double2* A = reinterpret_cast<double2*>(smem_raw);
-  double2* B = A + N;
-  double2* Q1 = B + N;
-  double2* Q2 = Q1 + N;
-  const int64_t p = blockIdx.x;
-  load_curve(c1 + p * N, A, N);
-  load_curve(c2 + p * N, B, N);
-  __syncthreads();
-  const int bad = block_any_nonfinite(A, N, red) | block_any_nonfinite(B, N, red);
-  double2* al = aligned ? aligned + p * N : nullptr;
-  if (bad) {
-    if (threadIdx.x == 0) write_bad_alignment(out + p, kInvalid);
-    if (al) fill_nan(al, N);
-    return;
-  }
-  block_srv(A, Q1, N);
-  block_srv(B, Q2, N);
-  __syncthreads();
-  // srv_center (srv.cpp:90-98)
-  double2 m1 = make_double2(0, 0), m2 = make_double2(0, 0);
-  for (int l = threadIdx.x; l < N; l += blockDim.x) {
-    m1 = cadd(m1, Q1[l]);
-    m2 = cadd(m2, Q2[l]);
-  }
-  m1 = block_sum2(m1, red);
-  m2 = block_sum2(m2, red);
-  const double invn = 1.0 / (double)N;
-  m1 = cscale(m1, invn);
-  m2 = cscale(m2, invn);
-  for (int l = threadIdx.x; l < N; l += blockDim.x) {
-    Q1[l] = csub(Q1[l], m1);
-    Q2[l] = csub(Q2[l], m2);
-  }
-  __syncthreads();
-  const double s1 = block_sum_norm2(Q1, N, red);
-  const double s2 = block_sum_norm2(Q2, N, red);
-  block_align_tail(Q1, Q2, A, B, N, tw, s1, s2, out + p, al, red);
-}
-
 // ------------------------------------------------------------ host launchers
 
-size_t align_smem_bytes(int N) { return 4 * sizeof(double2) * (size_t)N; }
 size_t resample_smem_bytes(int nmax, int n_out) {
   return ResampleSmem::bytes(nmax) + sizeof(double2) * (size_t)n_out;
-}
-size_t preprocess_align_smem_bytes(int nmax, int N) {
-  const size_t work = ResampleSmem::bytes(nmax);
-  const size_t fft_scratch = 2 * sizeof(double2) * (size_t)N;
-  return 2 * sizeof(double2) * (size_t)N + (work > fft_scratch ? work : fft_scratch);
 }
 
 static cudaError_t set_smem(const void* fn, size_t bytes) {
@@ -315,15 +188,6 @@ static cudaError_t set_smem(const void* fn, size_t bytes) {
 
 cudaError_t launch_tw_init(double2* tw, int N, cudaStream_t s) {
   tw_init_kernel<<<(N + 255) / 256, 256, 0, s>>>(tw, N);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_align(const double2* c1, const double2* c2, int64_t pairs, int N,
-                         const double2* tw, cva_alignment* out, double2* aligned, cudaStream_t s) {
-  const size_t sm = align_smem_bytes(N);
-  cudaError_t e = set_smem((const void*)align_kernel, sm);
-  if (e != cudaSuccess) return e;
-  align_kernel<<<(unsigned)pairs, kThreads, sm, s>>>(c1, c2, N, tw, out, aligned);
   return cudaGetLastError();
 }
 
@@ -341,27 +205,6 @@ cudaError_t launch_preprocess_resample(const double2* pts, const int64_t* off, i
 cudaError_t launch_preprocess_center(const double2* pts, const int64_t* off, int64_t curves,
                                      double2* out, int32_t* status, cudaStream_t s) {
   preprocess_center_kernel<<<(unsigned)curves, kThreads, 0, s>>>(pts, off, out, status);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_preprocess_align(const double2* pts, const int64_t* off, int64_t pairs,
-                                    int nmax, int N, const double2* tw, cva_alignment* out,
-                                    double2* aligned, cudaStream_t s) {
-  const size_t sm = preprocess_align_smem_bytes(nmax, N);
-  cudaError_t e = set_smem((const void*)preprocess_align_kernel, sm);
-  if (e != cudaSuccess) return e;
-  preprocess_align_kernel<<<(unsigned)pairs, kThreads, sm, s>>>(pts, off, nmax, N, tw, out,
-                                                                 aligned);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_srv_align(const double2* c1, const double2* c2, int64_t pairs, int N,
-                             const double2* tw, cva_alignment* out, double2* aligned,
-                             cudaStream_t s) {
-  const size_t sm = align_smem_bytes(N);
-  cudaError_t e = set_smem((const void*)srv_align_kernel, sm);
-  if (e != cudaSuccess) return e;
-  srv_align_kernel<<<(unsigned)pairs, kThreads, sm, s>>>(c1, c2, N, tw, out, aligned);
   return cudaGetLastError();
 }
 

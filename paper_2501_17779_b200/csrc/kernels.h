@@ -9,9 +9,7 @@
 
 namespace cva {
 
-size_t align_smem_bytes(int N);
 size_t resample_smem_bytes(int nmax, int n_out);
-size_t preprocess_align_smem_bytes(int nmax, int N);
 int max_chunked_nodes();
 // raw curves beyond shared memory: per-CTA global slabs (bytes per CTA, CTAs)
 size_t resample_global_slab_bytes(int nmax);
@@ -21,18 +19,9 @@ cudaError_t launch_preprocess_resample_global(const double2* pts, const int64_t*
                                               void* slab, cudaStream_t s);
 
 cudaError_t launch_tw_init(double2* tw, int N, cudaStream_t s);
-cudaError_t launch_align(const double2* c1, const double2* c2, int64_t pairs, int N,
-                         const double2* tw, cva_alignment* out, double2* aligned, cudaStream_t s);
 cudaError_t launch_preprocess_resample(const double2* pts, const int64_t* off, int64_t curves,
                                        int nmax, int n_out, int center_normalize, double2* out,
                                        int32_t* status, cudaStream_t s);
 cudaError_t launch_preprocess_center(const double2* pts, const int64_t* off, int64_t curves,
                                      double2* out, int32_t* status, cudaStream_t s);
-cudaError_t launch_preprocess_align(const double2* pts, const int64_t* off, int64_t pairs,
-                                    int nmax, int N, const double2* tw, cva_alignment* out,
-                                    double2* aligned, cudaStream_t s);
-cudaError_t launch_srv_align(const double2* c1, const double2* c2, int64_t pairs, int N,
-                             const double2* tw, cva_alignment* out, double2* aligned,
-                             cudaStream_t s);
-
 }  // namespace cva
