@@ -120,6 +120,27 @@ def main():
     seconds = np.tile(prep, (len(rows), 1, 1))
     dummy = np.ones((len(rows) * M, 1, 2))
     summary["c2_rows"] = compare(g, ro, dummy, dummy, firsts, seconds)
+
+    # E1: every ordered pair of the 64 curves, approach 2 (elastic.cpp:102-174),
+    # both sides on the same (reference-preprocessed) curves. Not bitwise (the
+    # rigid steps use the FFT correlation): agreement to rounding, same path.
+    if reference_available():
+        cfg = synth.CONFIGS["e1"]
+        M, N = cfg["curves"], cfg["N"]
+        pts, offs = synth.ragged_curves(a.seed, M)
+        prep = np.stack([lib.preprocess(pts[offs[c]:offs[c + 1]], N, True) for c in range(M)])
+        d_gpu = cva.elastic_distance_matrix(prep)
+        cells = np.arange(M * M)
+        r = lib.elastic_approach2_batch(prep[cells // M], prep[cells % M], threads=threads)
+        d_ref = r["distance"].reshape(M, M)
+        g2 = cva.elastic_approach2_batch(prep[cells // M], prep[cells % M])
+        rel = np.abs(d_gpu - d_ref) / np.maximum(np.abs(d_ref), 1e-300)
+        summary["e1"] = {"pairs": int(M * M), "max_distance_rel": float(rel.max()),
+                         "median_distance_rel": float(np.median(rel)),
+                         "iterations_equal": int((g2["iterations"] == r["iterations"]).sum()),
+                         "t0_equal": int((g2["t0"] == r["t0"]).sum()),
+                         "max_dtheta": float(np.abs(wrap(g2["theta"] - r["theta"])).max()),
+                         "matrix_equals_pair_batch": bool(np.array_equal(d_gpu.ravel(), g2["distance"]))}
     print(json.dumps(summary, indent=1))
 
 
