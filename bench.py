@@ -336,7 +336,7 @@ def run_secondary(args):
         units = M * M  # every rank computes the whole matrix (weak scaling: replicas)
         workload = E1_WORKLOAD
         l2 = "inputs L2-resident (64 curves); the DP is compute-bound"
-        bound = "none"
+        bound = "fp64ops"
     else:
         cfg = synth.CONFIGS["c4"]
         P, N = cfg["pairs"], cfg["N"]
@@ -373,8 +373,22 @@ def run_secondary(args):
     total_units = units * world
     value = total_units / (ms_step * 1e-3)
     launch_s = (ms / args.steps) * 1e-3
-    if bound == "none":
-        roof = None
+    if bound == "fp64ops":
+        # FP64 thread ops (DADD + DMUL + DFMA) of the elastic kernel from its ncu
+        # capture, per launch, against the FP64 op rate the probe measured
+        # (dependent DFMA chains: TFLOP/s / 2 = T ops/s)
+        prof = os.path.join(ROOT, "profiles", "r2h_e1_elastic_ncu_summary.json")
+        ops = None
+        if os.path.exists(prof):
+            with open(prof) as f:
+                ops = json.load(f).get("fp64_thread_ops_per_launch")
+        ach = ops / launch_s / 1e12 if ops else None
+        peak_ops = fp64 / 2 if fp64 else None
+        roof = {"bound": "fp64", "achieved": ach, "peak": peak_ops, "unit": "T FP64 ops/s",
+                "frac": ach / peak_ops if ach and peak_ops else None, "traffic": None,
+                "peak_source": "measured here (cva_probe_fp64_tflops / 2)",
+                "note": "DADD+DMUL+DFMA thread ops of the elastic kernel per launch (ncu, "
+                        "profiles/r2h_e1_elastic_ncu_summary.json); the DP has no FFT-style flop model"}
     elif bound == "fp64":
         ach = units * flops_unit / launch_s / 1e12
         roof = {"bound": "fp64", "achieved": ach, "peak": fp64, "unit": "TFLOP/s", "frac": ach / fp64 if fp64 else None,
