@@ -97,7 +97,9 @@ int cva_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n
  * resample != 0: periodic-cubic-spline arc-length resampling to n_out nodes,
  * then center, then normalize; out is curves x n_out points.
  * resample == 0: center + normalize only; out has the input's ragged layout.
- * max_n_in: largest curve size in the batch (host-known; bounds shared memory).
+ * max_n_in: largest curve size in the batch (host-known; sizes the kernels'
+ *   scratch), or 0 to have it computed from the offsets; a curve longer than a
+ *   positive max_n_in is reported CVA_INVALID_ARGUMENT in status (never read).
  * status (nullable): per-curve cva_status. */
 int cva_preprocess_batch(const double* points, const int64_t* offsets, int64_t curves,
                          int64_t max_n_in, int64_t n_out, int resample, double* out,

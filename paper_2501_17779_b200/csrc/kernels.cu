@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(kThreads)
   const int64_t c = blockIdx.x;
   const int64_t b0 = off[c];
   const int n = (int)(off[c + 1] - b0);
-  const int st = block_resample_preprocess(pts + b0, n, n_out, R, obuf, red, center_normalize != 0);
+  // a curve above the caller's max_n_in would overrun the carved arrays: invalid
+  const int st = n > nmax ? kInvalid : block_resample_preprocess(pts + b0, n, n_out, R, obuf, red, center_normalize != 0);
   double2* o = out + c * n_out;
   if (st == kOk) {
     for (int i = threadIdx.x; i < n_out; i += blockDim.x) o[i] = obuf[i];
@@ -129,7 +130,8 @@ __global__ void __launch_bounds__(kThreads)
     const int64_t b0 = off[c];
     const int n = (int)(off[c + 1] - b0);
     double2* o = out + c * n_out;
-    const int st = block_resample_preprocess(pts + b0, n, n_out, R, o, red, center_normalize != 0, cpv);
+    const int st = n > nmax ? kInvalid : block_resample_preprocess(pts + b0, n, n_out, R, o, red,
+                                                                   center_normalize != 0, cpv);
     if (st != kOk) fill_nan(o, n_out);
     if (status && threadIdx.x == 0) status[c] = st;
     __syncthreads();  // the slab is reused by the next curve

@@ -543,3 +543,28 @@ def test_large_n_out_and_srv_beyond_shared_memory(cuda, oracle):
         q2 = oracle.srv_center(oracle.srv_transform(s2[p]))
         r = oracle.align(q1, q2)
         check_pair(res[p], r, q1, q2)
+
+
+def test_max_n_in_hint_below_a_curve(cuda, oracle):
+    """max_n_in sizes the kernels' scratch: a curve longer than a positive hint
+    is reported invalid (never read past its scratch); 0 computes the bound."""
+    import torch
+
+    rng = np.random.default_rng(9)
+    curves = []
+    for n_in in (500, 4000, 800):
+        phi = (np.arange(n_in) + rng.uniform(-0.3, 0.3, n_in)) * (2 * PI / n_in)
+        r = 1 + 0.2 * np.cos(3 * phi)
+        curves.append(np.stack([r * np.cos(phi), r * np.sin(phi)], 1))
+    pts, offs = cva.ragged(curves)
+    dp, do = torch.from_numpy(pts).cuda(), torch.from_numpy(offs).cuda()
+    want = [oracle.preprocess(c, 256) for c in curves]
+    for hint, ok in ((1000, [0, 1, 0]), (3500, [0, 1, 0]), (0, [0, 0, 0]), (4000, [0, 0, 0])):
+        out, st = cva.preprocess_batch(dp, do, 256, max_n_in=hint)
+        st, out = st.cpu().numpy(), out.cpu().numpy()
+        assert list(st) == ok, (hint, st)
+        for c in range(3):
+            if ok[c] == 0:
+                assert np.abs(out[c] - want[c]).max() <= 1e-11 * np.abs(want[c]).max()
+            else:
+                assert np.isnan(out[c]).all()
