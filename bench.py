@@ -292,13 +292,21 @@ def run_secondary(args):
         k = torch.empty((r1 - r0, M), dtype=torch.int32, device=dev)
         th = torch.empty((r1 - r0, M), dtype=torch.float64, device=dev)
 
+        if world > 1:  # the assembled matrices on every rank (one NCCL all-gather each)
+            assert M % world == 0
+            full = [torch.empty((M, M), dtype=x.dtype, device=dev) for x in (e, k, th)]
+
         def step():
             _native.check(lib.cva_preprocess_batch(dp.data_ptr(), do.data_ptr(), M, mx, N, 1, prep.data_ptr(), 0,
                                                    stream.cuda_stream))
             _native.check(lib.cva_allpairs(prep.data_ptr(), M, N, r0, r1, e.data_ptr(), k.data_ptr(), th.data_ptr(),
                                            stream.cuda_stream))
+            if world > 1:
+                for dst, src in zip(full, (e, k, th)):
+                    dist.all_gather_into_tensor(dst, src)
         units = (r1 - r0) * M
-        workload = f"C2: all ordered pairs of {M} curves (raw n_in~U{{300..3000}}), N={N}, rows sharded"
+        workload = (f"C2: all ordered pairs of {M} curves (raw n_in~U{{300..3000}}), N={N}, rows sharded, "
+                    "matrices all-gathered (NCCL) inside the step when N > 1")
         l2 = "spectra (16.8 MB) L2-resident by design (reused by every cell); 4.2 M cells of output per step"
         flops_unit = 5 * N * math.log2(N)
         bound = "fp64"
