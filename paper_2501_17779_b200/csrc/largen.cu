@@ -127,12 +127,29 @@ __global__ void __launch_bounds__(kT)
   double2 acc = make_double2(0, 0);
   double len = 0.0;
   int nf = 0;
-  for (int i = blockIdx.x * kT + threadIdx.x; i < N; i += kStatBlocks * kT) {
-    const double2 p0 = __ldg(&z[i]), p1 = __ldg(&z[i + 1 == N ? 0 : i + 1]);
-    nf |= !(isfinite(p0.x) && isfinite(p0.y));
-    acc = cadd(acc, p0);
-    const double dx = p1.x - p0.x, dy = p1.y - p0.y;
-    len += sqrt(fma(dx, dx, dy * dy));
+  // kU strided elements per thread per round, all loads issued before use (the
+  // pass streams the chunk's curves from HBM: memory-level parallelism)
+  constexpr int kU = 4;
+  constexpr int kS = kStatBlocks * kT;
+  for (int i0 = blockIdx.x * kT + threadIdx.x; i0 < N; i0 += kU * kS) {
+    double2 p0[kU], p1[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int i = i0 + u * kS;
+      if (i < N) {
+        p0[u] = __ldg(&z[i]);
+        p1[u] = __ldg(&z[i + 1 == N ? 0 : i + 1]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      if (i0 + u * kS < N) {
+        nf |= !(isfinite(p0[u].x) && isfinite(p0[u].y));
+        acc = cadd(acc, p0[u]);
+        const double dx = p1[u].x - p0[u].x, dy = p1[u].y - p0[u].y;
+        len += sqrt(fma(dx, dx, dy * dy));
+      }
+    }
   }
   nf = block_or(nf, red);
   acc = block_sum2(acc, red);
