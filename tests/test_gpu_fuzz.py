@@ -1,9 +1,11 @@
 """Seeded random sweep over sizes and shapes (GPU vs the oracle): raw node
 counts 4..5000, output sizes 8..4096 (powers of two and not), random star
 shapes with uneven node spacing, random planted shift / rotation; the fused and
-split preprocess+align paths, the SRV alignment and the uniform alignment. The
-acceptance rule is tests/test_gpu_parity.py's (shift identical up to a
-documented near-tie, theta 1e-10, coordinates and energy 1e-10 relative).
+split preprocess+align paths, the SRV alignment and the uniform alignment
+(acceptance rule of tests/test_gpu_parity.py: shift identical up to a
+documented near-tie, theta 1e-10, coordinates and energy 1e-10 relative); and
+the elastic DP (bitwise the reference compiled in place, random n and slope
+bound) and approach 2 (rounding-level, same iteration counts).
 """
 import numpy as np
 import pytest
@@ -88,3 +90,40 @@ def test_random_srv_align(cuda, oracle, seed):
         q = q2[(np.arange(n) + int(want["shift"])) % n]
         wal = np.stack([cth * q[:, 0] + sth * q[:, 1], -sth * q[:, 0] + cth * q[:, 1]], 1)
         check_pair(res[p], want, q1, q2, alq[p], wal)
+
+
+# ---------------------------------------------------------------- elastic
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_random_dp_bitwise(cuda, reference, seed):
+    """dp_reparam on random SRV pairs (random n, slope bound, shapes, scales):
+    bitwise the reference's gamma and energy."""
+    ref = reference
+    rng = np.random.default_rng(4000 + seed)
+    n = int(rng.choice([8, 16, 24, 64, 100, 128, 200, 256, 512]))
+    w = int(rng.choice([1, 2, 3, 4, 4, 4, 5]))
+    pairs = 3
+    q1 = np.stack([ref.srv_transform(ref.preprocess(star(rng, 600, 9), n)) for _ in range(pairs)])
+    q2 = np.stack([ref.srv_transform(ref.preprocess(star(rng, 700, 9), n)) for _ in range(pairs)])
+    g, e, st = cva.dp_reparam_batch(q1, q2, w)
+    rg, re_, rst = ref.dp_reparam_batch(q1, q2, w)
+    np.testing.assert_array_equal(st, rst)
+    ok = st == 0
+    np.testing.assert_array_equal(g[ok], rg[ok])
+    np.testing.assert_array_equal(e[ok], re_[ok])
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_approach2(cuda, reference, seed):
+    ref = reference
+    rng = np.random.default_rng(5000 + seed)
+    n = int(rng.choice([32, 64, 100, 128, 256]))
+    pairs = 4
+    c1 = np.stack([ref.preprocess(star(rng, 500, 9), n) for _ in range(pairs)])
+    c2 = np.stack([ref.preprocess(star(rng, 650, 9), n) for _ in range(pairs)])
+    g = cva.elastic_approach2_batch(c1, c2)
+    r = ref.elastic_approach2_batch(c1, c2)
+    np.testing.assert_array_equal(g["status"], r["status"])
+    np.testing.assert_allclose(g["distance"], r["distance"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_array_equal(g["iterations"], r["iterations"])
