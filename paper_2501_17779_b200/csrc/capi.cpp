@@ -544,7 +544,13 @@ int cva_resample_batch_host(const double* points, const int64_t* offsets, int64_
 struct HostCtx {
   int dev = -1;
   static constexpr int kStreams = 3;  // H2D, kernels, D2H
-  static constexpr int kMaxChunks = 16;
+#ifndef CVA_HOST_MAX_CHUNKS
+#define CVA_HOST_MAX_CHUNKS 16
+#endif
+#ifndef CVA_HOST_MIN_CHUNK
+#define CVA_HOST_MIN_CHUNK 256
+#endif
+  static constexpr int kMaxChunks = CVA_HOST_MAX_CHUNKS;
   cudaStream_t st[kStreams] = {};
   cudaEvent_t ready = nullptr;
   cudaEvent_t in_done[kMaxChunks] = {}, k_done[kMaxChunks] = {};
@@ -625,7 +631,7 @@ int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets
   cudaError_t e = cudaMemcpyAsync(doff, offsets, sizeof(int64_t) * (size_t)(2 * pairs + 1),
                                   cudaMemcpyHostToDevice, h.st[0]);  // ahead of chunk 0's input
   if (e != cudaSuccess) return drain(cuda_fail(e, "H2D offsets"));
-  const int64_t nchunks = std::min<int64_t>(HostCtx::kMaxChunks, std::max<int64_t>(1, pairs / 256));
+  const int64_t nchunks = std::min<int64_t>(HostCtx::kMaxChunks, std::max<int64_t>(1, pairs / CVA_HOST_MIN_CHUNK));
   const int64_t per = (pairs + nchunks - 1) / nchunks;
   cudaStream_t sin = h.st[0], sk = h.st[1], sout = h.st[2];
   for (int64_t c = 0; c < nchunks; ++c) {  // all input copies first, in order
