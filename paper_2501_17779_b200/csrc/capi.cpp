@@ -61,7 +61,7 @@ int get_twiddles(int n, cudaStream_t stream, const double2** out) {
     return CVA_OK;
   }
   double2* tw = nullptr;
-  e = cudaMalloc(&tw, sizeof(double2) * (size_t)n);
+  e = cudaMalloc(&tw, sizeof(double2) * (size_t)(n + cva::twiddle_extra(n)));
   if (e != cudaSuccess) return fail(CVA_BAD_ALLOC, "twiddle table allocation failed");
   e = cva::launch_tw_init(tw, n, stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(stream);

@@ -14,6 +14,7 @@
 #include "cva_common.cuh"
 #include "fft.cuh"
 #include "kernels.h"
+#include "pairfft.cuh"
 #include "spline.cuh"
 
 namespace cva {
@@ -30,6 +31,23 @@ __global__ void tw_init_kernel(double2* tw, int N) {
     // exp(-2 pi i k / N) = cospi(2k/N) - i sinpi(2k/N); 2k/N exact for N = 2^p
     sincospi(2.0 * (double)k / (double)N, &s, &c);
     tw[k] = make_double2(c, -s);
+  }
+}
+
+// Pass twiddle tables after the length-N table (layout: pairfft.cuh ptw_off),
+// copied from it entry by entry. One CTA; N <= 2048.
+__global__ void ptw_fill_kernel(double2* tw, int N) {
+  for (int h = 0; h < 2; ++h) {
+    int off = N + (h ? pf::ptw_until<128>(N, N) : 0);
+    for (int Ns = 1; Ns < N;) {
+      const int R = h ? pf::plan_radix<256>(N, Ns) : pf::plan_radix<128>(N, Ns);
+      if (Ns > 1) {
+        const int tws = N / (Ns * R);
+        for (int k = threadIdx.x; k < (R - 1) * Ns; k += blockDim.x) tw[off + k] = tw[(k / Ns + 1) * (k % Ns) * tws];
+        off += (R - 1) * Ns;
+      }
+      Ns *= R;
+    }
   }
 }
 
@@ -190,7 +208,12 @@ static cudaError_t set_smem(const void* fn, size_t bytes) {
 
 cudaError_t launch_tw_init(double2* tw, int N, cudaStream_t s) {
   tw_init_kernel<<<(N + 255) / 256, 256, 0, s>>>(tw, N);
+  if (twiddle_extra(N)) ptw_fill_kernel<<<1, 256, 0, s>>>(tw, N);  // after the table (same stream)
   return cudaGetLastError();
+}
+
+int twiddle_extra(int N) {
+  return (N >= 4 && N <= 2048 && (N & (N - 1)) == 0) ? pf::ptw_len(N) : 0;
 }
 
 cudaError_t launch_preprocess_resample(const double2* pts, const int64_t* off, int64_t curves,

@@ -71,32 +71,6 @@ __device__ __forceinline__ void pass(Src src, double2* dst, int N, int Ns,
   }
 }
 
-// Compile-time pass: N, Ns, the butterfly count per thread and every index
-// stride are constants.
-template <int R, int NT, int N, int Ns, typename Src>
-__device__ __forceinline__ void pass_ct(Src src, double2* dst, const double2* __restrict__ tw, int g) {
-  constexpr int nb = N / R;
-  constexpr int tws = N / (Ns * R);
-#pragma unroll
-  for (int j0 = 0; j0 < nb; j0 += NT) {
-    const int j = j0 + g;
-    if (nb % NT == 0 || j < nb) {
-      double2 v[R];
-      const int jm = j & (Ns - 1);
-#pragma unroll
-      for (int r = 0; r < R; ++r) v[r] = src(j + r * nb);
-      if (Ns > 1) {
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&tw[r * jm * tws]));
-      }
-      dft_r<R>(v);
-      const int base = (j - jm) * R + jm;
-#pragma unroll
-      for (int r = 0; r < R; ++r) dst[pad(base + r * Ns)] = v[dft_slot<R>(r)];
-    }
-  }
-}
-
 // Radix plan: radix 8 while it keeps every thread of the group busy, then 4 / 2
 // (1024 points, 128 threads: 8 x 8 x 8 x 2). Radix 16 was measured slower here
 // (register spills at the 128-register cap, half the threads idle).
@@ -110,6 +84,52 @@ template <int NT>
 #endif
 __host__ __device__ constexpr int plan_radix(int N, int Ns) {
   return ((N / Ns) % 8 == 0 && N / NT >= CVA_R8_MIN) ? 8 : ((N / Ns) % 4 == 0 ? 4 : 2);
+}
+
+
+// Pass twiddle tables, stored after the length-N table of W_N^k: for every
+// pass (R, Ns > 1) of the NT = 128 plan, then of the NT = 256 plan, the
+// values W_N^(r jm N/(Ns R)) laid out [r - 1][jm] (copied from the table, so
+// bitwise the same values): a warp's twiddle load of one r reads consecutive
+// entries (4 lines) instead of entries r*tws apart (up to 8r lines).
+template <int NT>
+__host__ __device__ constexpr int ptw_until(int N, int Ns_stop) {
+  int s = 0;
+  for (int Ns = 1; Ns < N && Ns < Ns_stop; Ns *= plan_radix<NT>(N, Ns))
+    if (Ns > 1) s += (plan_radix<NT>(N, Ns) - 1) * Ns;
+  return s;
+}
+__host__ __device__ constexpr int ptw_len(int N) { return ptw_until<128>(N, N) + ptw_until<256>(N, N); }
+template <int NT>
+__host__ __device__ constexpr int ptw_off(int N, int Ns) {
+  return N + (NT == 256 ? ptw_until<128>(N, N) : 0) + ptw_until<NT>(N, Ns);
+}
+
+// Compile-time pass: N, Ns, the butterfly count per thread and every index
+// stride are constants.
+template <int R, int NT, int N, int Ns, typename Src>
+__device__ __forceinline__ void pass_ct(Src src, double2* dst, const double2* __restrict__ tw, int g) {
+  static_assert(NT == 128 || NT == 256, "pass twiddle tables exist for the 128- and 256-thread plans");
+  constexpr int nb = N / R;
+  const double2* __restrict__ pt = tw + ptw_off<NT>(N, Ns);  // this pass's [r - 1][jm] table
+#pragma unroll
+  for (int j0 = 0; j0 < nb; j0 += NT) {
+    const int j = j0 + g;
+    if (nb % NT == 0 || j < nb) {
+      double2 v[R];
+      const int jm = j & (Ns - 1);
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r] = src(j + r * nb);
+      if (Ns > 1) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&pt[(r - 1) * Ns + jm]));
+      }
+      dft_r<R>(v);
+      const int base = (j - jm) * R + jm;
+#pragma unroll
+      for (int r = 0; r < R; ++r) dst[pad(base + r * Ns)] = v[dft_slot<R>(r)];
+    }
+  }
 }
 
 // Forward FFT of compile-time length N by NT threads, first pass through src,
