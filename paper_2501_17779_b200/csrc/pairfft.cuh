@@ -31,24 +31,6 @@ __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// W_N^e (0 <= e < N, N a power of two >= 4) from the first quadrant of the
-// length-N table: W^(f + q N/4) = (-i)^q W^f, a swap and sign flips (exact), so
-// a transform's twiddle loads touch N/4 entries instead of N. Used by the
-// M = 2048 in-place passes (C4: the 32 KB table competes for the L1 left next
-// to two CTAs' shared memory; 0.672 -> 0.648 ms); at M <= 1024 the extra
-// selects cost more than the smaller footprint saves.
-template <int N>
-__device__ __forceinline__ double2 tw_quad(const double2* __restrict__ tw, int e) {
-  constexpr int Q = N / 4;
-  const double2 w = __ldg(&tw[e & (Q - 1)]);
-  const int q = e / Q;  // 0..3
-  const double x = (q & 1) ? w.y : w.x, y = (q & 1) ? w.x : w.y;
-  const long long sx = (q == 2 || q == 3) ? (long long)0x8000000000000000ULL : 0;
-  const long long sy = (q == 1 || q == 2) ? (long long)0x8000000000000000ULL : 0;
-  return make_double2(__longlong_as_double(__double_as_longlong(x) ^ sx),
-                      __longlong_as_double(__double_as_longlong(y) ^ sy));
-}
-
 // One Stockham pass (see fft.cuh) reading through a functor (runtime N, Ns).
 template <int R, int NT, typename Src>
 __device__ __forceinline__ void pass(Src src, double2* dst, int N, int Ns,
@@ -193,7 +175,10 @@ __device__ __forceinline__ void pass_ip(Src src, double2* buf, const double2* __
   constexpr int nb = M / R;
   constexpr int B = nb / NT;  // butterflies per thread
   static_assert(B >= 1 && B * R <= 16, "in-place pass keeps <= 16 values per thread");
-  constexpr int tws = M / (Ns * R);
+  // the 8, 8, 8, 4 sequence is also the 128- and 256-thread plan of M = 2048,
+  // so the pass twiddle tables of ptw_off apply
+  static_assert(R == plan_radix<NT>(M, Ns), "in-place sequence must match the table plan");
+  const double2* __restrict__ pt = tw + ptw_off<NT>(M, Ns);
   double2 v[B][R];
 #pragma unroll
   for (int b = 0; b < B; ++b) {
@@ -203,7 +188,7 @@ __device__ __forceinline__ void pass_ip(Src src, double2* buf, const double2* __
     for (int r = 0; r < R; ++r) v[b][r] = src(j + r * nb);
     if (Ns > 1) {
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], tw_quad<M>(tw, r * jm * tws));
+      for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], __ldg(&pt[(r - 1) * Ns + jm]));
     }
   }
   sync();
