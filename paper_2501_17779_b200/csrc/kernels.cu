@@ -37,10 +37,11 @@ __global__ void tw_init_kernel(double2* tw, int N) {
 // Pass twiddle tables after the length-N table (layout: pairfft.cuh ptw_off),
 // copied from it entry by entry. One CTA; N <= 2048.
 __global__ void ptw_fill_kernel(double2* tw, int N) {
-  for (int h = 0; h < 2; ++h) {
-    int off = N + (h ? pf::ptw_until<128>(N, N) : 0);
+  for (int h = 0; h < 3; ++h) {  // 128-thread, 256-thread, one-warp plans
+    int off = h == 0 ? pf::ptw_off<128>(N, 1) : h == 1 ? pf::ptw_off<256>(N, 1) : pf::ptw_off_warp(N, 1);
     for (int Ns = 1; Ns < N;) {
-      const int R = h ? pf::plan_radix<256>(N, Ns) : pf::plan_radix<128>(N, Ns);
+      const int R = h == 0 ? pf::plan_radix<128>(N, Ns) : h == 1 ? pf::plan_radix<256>(N, Ns)
+                                                                 : pf::plan_radix_warp(N, Ns);
       if (Ns > 1) {
         const int tws = N / (Ns * R);
         for (int k = threadIdx.x; k < (R - 1) * Ns; k += blockDim.x) tw[off + k] = tw[(k / Ns + 1) * (k % Ns) * tws];

@@ -333,16 +333,19 @@ __host__ __device__ constexpr int vstride() {
 
 template <int L, int Ns>
 __host__ __device__ constexpr int radix_at() {
-  return ((L / Ns) % 8 == 0 && L / 8 >= 32) ? 8 : ((L / Ns) % 4 == 0 ? 4 : 2);
+  return pf::plan_radix_warp(L, Ns);  // the plan the pass twiddle tables are laid out for
 }
 
 // One in-place Stockham pass of radix R on a length-L shared vector by one warp.
-// Twiddles of the sub-transform: W_L^k = tw[k * twstride] (tw: length-M table).
+// tw: the length-L table of get_twiddles (twstride 1); the pass reads its
+// twiddles W_L^(r jm L/(Ns R)) from the table's one-warp pass tables
+// ([r - 1][jm], pairfft.cuh ptw_off_warp: consecutive entries per warp load).
 template <int L, int R, int Ns>
 __device__ __forceinline__ void wpass(double2* x, const double2* __restrict__ tw, int twstride, int lane) {
   constexpr int nb = L / R;
   constexpr int B = (nb + 31) / 32;
-  constexpr int tws = L / (Ns * R);
+  (void)twstride;  // always 1: sub-transform tables of their own length
+  const double2* __restrict__ pt = tw + pf::ptw_off_warp(L, Ns);
   double2 v[B][R];
 #pragma unroll
   for (int b = 0; b < B; ++b) {
@@ -353,7 +356,7 @@ __device__ __forceinline__ void wpass(double2* x, const double2* __restrict__ tw
       for (int r = 0; r < R; ++r) v[b][r] = x[padL(j + r * nb)];
       if (Ns > 1) {
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], __ldg(&tw[(r * jm * tws) * twstride]));
+        for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], __ldg(&pt[(r - 1) * Ns + jm]));
       }
     }
   }

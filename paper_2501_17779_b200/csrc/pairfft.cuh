@@ -81,10 +81,27 @@ __host__ __device__ constexpr int ptw_until(int N, int Ns_stop) {
     if (Ns > 1) s += (plan_radix<NT>(N, Ns) - 1) * Ns;
   return s;
 }
-__host__ __device__ constexpr int ptw_len(int N) { return ptw_until<128>(N, N) + ptw_until<256>(N, N); }
+// One warp per transform (largen.cu four-step sub-transforms): radix 8 while
+// every lane has a butterfly, then 4 / 2.
+__host__ __device__ constexpr int plan_radix_warp(int N, int Ns) {
+  return ((N / Ns) % 8 == 0 && N / 8 >= 32) ? 8 : ((N / Ns) % 4 == 0 ? 4 : 2);
+}
+__host__ __device__ constexpr int ptw_until_warp(int N, int Ns_stop) {
+  int s = 0;
+  for (int Ns = 1; Ns < N && Ns < Ns_stop; Ns *= plan_radix_warp(N, Ns))
+    if (Ns > 1) s += (plan_radix_warp(N, Ns) - 1) * Ns;
+  return s;
+}
+// layout after the length-N table: [128-thread plan][256-thread plan][warp plan]
+__host__ __device__ constexpr int ptw_len(int N) {
+  return ptw_until<128>(N, N) + ptw_until<256>(N, N) + ptw_until_warp(N, N);
+}
 template <int NT>
 __host__ __device__ constexpr int ptw_off(int N, int Ns) {
   return N + (NT == 256 ? ptw_until<128>(N, N) : 0) + ptw_until<NT>(N, Ns);
+}
+__host__ __device__ constexpr int ptw_off_warp(int N, int Ns) {
+  return N + ptw_until<128>(N, N) + ptw_until<256>(N, N) + ptw_until_warp(N, Ns);
 }
 
 // Compile-time pass: N, Ns, the butterfly count per thread and every index
