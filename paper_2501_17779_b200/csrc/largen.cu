@@ -429,12 +429,19 @@ __global__ void __launch_bounds__(kT)
   wfft<M1>(sm + w * VS, twS, 1, lane);
   __syncthreads();
   double2* u = U + sidx * (int64_t)M;
+  // a thread's column n2 is fixed and its k1 advance by kT / kCT per round, so
+  // W_M^(n2 k1) is a geometric sequence: two table reads per thread instead of
+  // two scattered reads per element (rounding drift <= a few ulps over the
+  // M1 kCT / kT rounds)
+  const int cn2 = c0 + (int)threadIdx.x % kCT;
+  const int k10 = (int)threadIdx.x / kCT;
+  double2 wt = tw_m(lo, hi, cn2 * k10);
+  const double2 wstep = tw_m(lo, hi, (cn2 * (kT / kCT)) & (M - 1));
 #pragma unroll
   for (int it = 0; it < M1 * kCT / kT; ++it) {
-    const int idx = threadIdx.x + it * kT;
-    const int k1 = idx / kCT, c = idx % kCT;
-    const int n2 = c0 + c;
-    u[(int64_t)k1 * M2 + n2] = cmul(sm[c * VS + padL(k1)], tw_m(lo, hi, n2 * k1));
+    const int k1 = k10 + it * (kT / kCT);
+    u[(int64_t)k1 * M2 + cn2] = cmul(sm[(cn2 - c0) * VS + padL(k1)], wt);
+    wt = cmul(wt, wstep);
   }
 }
 
@@ -469,8 +476,14 @@ __global__ void __launch_bounds__(kT, 2)
   wfft<M2>(x, twS, 1, lane);
   const int k1 = r0 + w;
   double2* g = G + p * (int64_t)M + (int64_t)k1 * M2;
+  // W_M^(k1 (i0 + lane)): geometric in i0 (step W_M^(32 k1)), see f1_kernel
+  double2 wt = tw_m(lo, hi, k1 * lane);
+  const double2 wstep = tw_m(lo, hi, (32 * k1) & (M - 1));
 #pragma unroll
-  for (int i0 = 0; i0 < M2; i0 += 32) g[i0 + lane] = cmul(x[padL(i0 + lane)], tw_m(lo, hi, k1 * (i0 + lane)));
+  for (int i0 = 0; i0 < M2; i0 += 32) {
+    g[i0 + lane] = cmul(x[padL(i0 + lane)], wt);
+    wt = cmul(wt, wstep);
+  }
 }
 
 // Column pass of the correlation transform: F[m2 + M2 m1] (natural order) and
