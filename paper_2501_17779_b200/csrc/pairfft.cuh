@@ -243,13 +243,15 @@ struct PairIn {
 };
 
 // q_l = d_l / sqrt(|d_l|), d_l = (N/2)(c[l+1] - c[l-1]); 0 if |d_l| < 1e-8 N (srv.cpp:71-88)
+// (MUFU-seeded sqrt / reciprocal with one correction step, <= 1 ulp each: the
+// IEEE sqrt and division slow paths were a visible share of the C4 kernel)
 __device__ __forceinline__ double2 srv_at(const double2* c, int l, int N) {
   const double nn = (double)N;
   const double2 nx = c[l + 1 == N ? 0 : l + 1], pv = c[l == 0 ? N - 1 : l - 1];
   const double2 d = make_double2((nn / 2.0) * (nx.x - pv.x), (nn / 2.0) * (nx.y - pv.y));
-  const double mag = sqrt(fma(d.x, d.x, d.y * d.y));
+  const double mag = fsqrt(fma(d.x, d.x, d.y * d.y));
   if (mag < 1e-8 * nn) return make_double2(0.0, 0.0);
-  const double r = 1.0 / sqrt(mag);
+  const double r = frcp(fsqrt(mag));
   return make_double2(r * d.x, r * d.y);
 }
 
