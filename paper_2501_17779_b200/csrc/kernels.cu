@@ -34,6 +34,15 @@ __global__ void tw_init_kernel(double2* tw, int N) {
   }
 }
 
+// Layout checks (N = 1024: plan 8, 8, 8, 2 for 128 and 256 threads and for one
+// warp; tables of 7 x 8, 7 x 64 and 1 x 512 entries after the W_N table).
+static_assert(pf::ptw_off<128>(1024, 8) == 1024 && pf::ptw_off<128>(1024, 64) == 1024 + 56 &&
+                  pf::ptw_off<128>(1024, 512) == 1024 + 56 + 448,
+              "pass table offsets, 128-thread plan");
+static_assert(pf::ptw_off<256>(1024, 8) == 1024 + 1016 && pf::ptw_off_warp(1024, 8) == 1024 + 2 * 1016 &&
+                  pf::ptw_len(1024) == 3 * 1016,
+              "pass table offsets, 256-thread and one-warp plans");
+
 // Pass twiddle tables after the length-N table (layout: pairfft.cuh ptw_off),
 // copied from it entry by entry. One CTA; N <= 2048.
 __global__ void ptw_fill_kernel(double2* tw, int N) {
