@@ -34,14 +34,21 @@ __global__ void tw_init_kernel(double2* tw, int N) {
   }
 }
 
-// Layout checks (N = 1024: plan 8, 8, 8, 2 for 128 and 256 threads and for one
-// warp; tables of 7 x 8, 7 x 64 and 1 x 512 entries after the W_N table).
+// Layout checks (N = 1024: plan 8, 8, 8, 2 for 128 threads and for one warp,
+// tables of 7 x 8, 7 x 64 and 1 x 512 entries after the W_N table; 256 threads:
+// radix 8 only with CVA_R8_MIN <= 4).
 static_assert(pf::ptw_off<128>(1024, 8) == 1024 && pf::ptw_off<128>(1024, 64) == 1024 + 56 &&
                   pf::ptw_off<128>(1024, 512) == 1024 + 56 + 448,
               "pass table offsets, 128-thread plan");
+#if CVA_R8_MIN <= 4
 static_assert(pf::ptw_off<256>(1024, 8) == 1024 + 1016 && pf::ptw_off_warp(1024, 8) == 1024 + 2 * 1016 &&
                   pf::ptw_len(1024) == 3 * 1016,
               "pass table offsets, 256-thread and one-warp plans");
+#else  // 256 threads: radix 4 x 5 (3 x 4, 3 x 16, 3 x 64, 3 x 256 entries)
+static_assert(pf::ptw_off<256>(1024, 4) == 1024 + 1016 &&
+                  pf::ptw_off_warp(1024, 8) == 1024 + 1016 + 3 * (4 + 16 + 64 + 256),
+              "pass table offsets, 256-thread and one-warp plans");
+#endif
 
 // Pass twiddle tables after the length-N table (layout: pairfft.cuh ptw_off),
 // copied from it entry by entry. One CTA; N <= 2048.

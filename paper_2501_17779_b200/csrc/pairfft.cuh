@@ -57,12 +57,12 @@ __device__ __forceinline__ void pass(Src src, double2* dst, int N, int Ns,
 // (1024 points, 128 threads: 8 x 8 x 8 x 2). Radix 16 was measured slower here
 // (register spills at the 128-register cap, half the threads idle).
 template <int NT>
-// Radix 8 also when it leaves up to half of the threads idle in that pass
-// (the 1024-point correlation transform on 256 threads: 8, 8, 8, 2 -> 4
-// passes instead of 5 radix-4 ones; measured 1.4 % faster on the fused C1
-// kernel).
+// CVA_R8_MIN: radix 8 only when every thread has a butterfly (N / NT >= 8).
+// With scattered twiddle loads, 4 (radix 8 with half the threads idle in the
+// 1024-point correlation transform: 4 passes instead of 5) was 1.4 % faster;
+// with the per-pass twiddle tables, 8 is 0.35 % faster.
 #ifndef CVA_R8_MIN
-#define CVA_R8_MIN 4
+#define CVA_R8_MIN 8
 #endif
 __host__ __device__ constexpr int plan_radix(int N, int Ns) {
   return ((N / Ns) % 8 == 0 && N / NT >= CVA_R8_MIN) ? 8 : ((N / Ns) % 4 == 0 ? 4 : 2);
