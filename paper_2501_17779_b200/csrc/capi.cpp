@@ -1,3 +1,4 @@
+#include <cstdlib>
 // extern "C" entry points of libcurvalign_cuda.so (declared in include/curvalign_cuda.h).
 //
 // Host-side validation mirrors the reference's std::invalid_argument checks
@@ -221,6 +222,15 @@ struct DevBuf {
 
 }  // namespace
 
+// CVA_FUSED=v2 selects the round-2 fused C1 kernel (A/B measurements).
+static bool use_v2_fused() {
+  static const bool v2 = [] {
+    const char* e = std::getenv("CVA_FUSED");
+    return e != nullptr && std::strcmp(e, "v2") == 0;
+  }();
+  return v2;
+}
+
 extern "C" {
 
 int cva_abi_version(void) { return CVA_ABI_VERSION; }
@@ -328,6 +338,11 @@ int cva_preprocess_align_batch(const double* points, const int64_t* offsets, int
   }
   const double2* tw = nullptr;
   if (int rc = get_twiddles(cva::v2_fft_len((int)n_out), s, &tw)) return rc;
+  if (nmax <= cva::v3_max_raw_nodes() && cva::v3_resample_align_supported((int)n_out) && !use_v2_fused()) {
+    return finish(cva::launch_v3_resample_align((const double2*)points, offsets, pairs, (int)n_out, tw, out,
+                                                (double2*)aligned, s),
+                  "resample_align launch");
+  }
   if (nmax <= cva::v2_max_raw_nodes()) {
     const size_t ab = sizeof(double2) * (size_t)(pairs * n_out);
     if (cva::v2_resample_align_supported((int)n_out)) {

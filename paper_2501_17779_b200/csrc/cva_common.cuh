@@ -52,6 +52,17 @@ __device__ __forceinline__ double fsqrt(double x) {
   return x > 0.0 ? y : (x == 0.0 ? 0.0 : __longlong_as_double(0x7ff8000000000000ULL));
 }
 
+// sqrt without the zero / negative select (no branch in the SASS): x == 0 or
+// x = inf give NaN (MUFU seed inf / 0); callers test the argument or result.
+__device__ __forceinline__ double fsqrt_nb(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x * r, r, 1.0);
+  r = fma(r * e, fma(0.375, e, 0.5), r);
+  const double y = x * r;
+  return fma(fma(-y, y, x), 0.5 * r, y);
+}
+
 // --------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

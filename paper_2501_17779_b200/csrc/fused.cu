@@ -1,3 +1,4 @@
+#include <cstdlib>
 // v2 sm_100a kernels (256 threads, 2 CTAs per SM): the fused C1 path and the
 // shared-memory preprocess / align / SRV-align kernels built from resample.cuh
 // and pairfft.cuh. kernels.cu keeps the general v1 kernels for sizes outside
@@ -9,6 +10,7 @@
 #include "pairfft.cuh"
 #include "prof.cuh"
 #include "resample.cuh"
+#include "resample3.cuh"
 
 #ifdef CVA_PHASE_TIMING
 extern "C" int cva_debug_set_prof(long long* p) {
@@ -330,6 +332,74 @@ __global__ void __launch_bounds__(kT) srv_center_kernel(const double2* __restric
 
 }  // namespace v2
 
+// ------------------------------------------------------------ fused C1 (v3)
+
+namespace v3 {
+
+// Shared memory: [XY | S] (rs3::kRawBytes, reused by the four FFT buffers),
+// scratch (PCR; curve B's samples in its first 16 KB; the interval map at
+// rs3::kMapOff), curve A's samples.
+constexpr size_t kZ1Off = rs3::kRawBytes + rs3::kScrBytes;
+template <int N>
+constexpr size_t smem_bytes() {
+  return kZ1Off + sizeof(double2) * N;
+}
+static_assert(4 * sizeof(double2) * pf::padded_len(1024) <= rs3::kRawBytes, "FFT buffers fit the raw region");
+
+// Pair p = (curve 2p, curve 2p+1) of the ragged raw batch: preprocess both to
+// N nodes (resample -> center -> normalize, curve.cpp:93-97) and align_fft
+// (rigid_align.cpp:204-208), all on chip.
+template <int N>
+__global__ void __launch_bounds__(rs3::kT, 2)
+    resample_align_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off,
+                          const double2* __restrict__ tw, cva_alignment* __restrict__ out,
+                          double2* aligned) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double2 red[16];
+  double2* XY = reinterpret_cast<double2*>(smem);
+  double* S = reinterpret_cast<double*>(smem + rs3::kXYBytes);
+  double* scr = reinterpret_cast<double*>(smem + rs3::kRawBytes);
+  double2* Z1 = reinterpret_cast<double2*>(smem + kZ1Off);
+  double2* Z2 = reinterpret_cast<double2*>(scr);  // B's samples replace the PCR scratch
+
+  const int64_t p = blockIdx.x;
+  const int64_t a0 = off[2 * p], a1 = off[2 * p + 1], b1 = off[2 * p + 2];
+  const int na = (int)(a1 - a0), nb = (int)(b1 - a1);
+  double2* al = aligned ? aligned + p * N : nullptr;  // null: results only
+  if (threadIdx.x == 0) v2::prefetch_l2(pts + a1, nb * (int)sizeof(double2));
+  if (na < 4 || nb < 4 || na > rs3::kNMax || nb > rs3::kNMax) {  // validate_curve(c, 4)
+    if (threadIdx.x == 0) v2::write_bad(out + p, CVA_INVALID_ARGUMENT);
+    if (al)
+      for (int l = threadIdx.x; l < N; l += rs3::kT) al[l] = make_double2(v2::qnan(), v2::qnan());
+    return;
+  }
+  CVA_MARK(0);
+  rs3::load_raw(pts + a0, XY, na);
+  rs3::cp_async_wait();
+  __syncthreads();
+  CVA_MARK(1);
+  const rs3::Stats A = rs3::resample_curve<N>(pts + a0, XY, S, scr, Z1, red, na, 2);
+  __syncthreads();  // A's last reads of XY / S / the map are done
+  rs3::load_raw(pts + a1, XY, nb);
+  rs3::cp_async_wait();
+  __syncthreads();
+  CVA_MARK(10);
+  const rs3::Stats B = rs3::resample_curve<N>(pts + a1, XY, S, scr, Z2, red, nb, 11);
+  const int bad = A.bad | B.bad;
+  const double2 cA = A.centroid, cB = B.centroid;
+  if (bad) {
+    if (threadIdx.x == 0) v2::write_bad(out + p, CVA_INVALID_ARGUMENT);
+    if (al)
+      for (int l = threadIdx.x; l < N; l += rs3::kT) al[l] = make_double2(v2::qnan(), v2::qnan());
+    return;
+  }
+  __syncthreads();
+  pf::PairIn in{Z1, Z2, cA, cB, 1.0, 1.0};
+  pf::pair_stage<false, N, true, 0>(in, reinterpret_cast<double2*>(smem), N, tw, out + p, al, red);
+}
+
+}  // namespace v3
+
 // ------------------------------------------------------------ launchers
 
 namespace {
@@ -411,6 +481,33 @@ cudaError_t launch_v2_resample_align(const double2* pts, const int64_t* off, int
     v2::resample_align_kernel<512><<<(unsigned)pairs, v2::kT, sm, s>>>(pts, off, tw, out, aligned);
   else
     v2::resample_align_kernel<1024><<<(unsigned)pairs, v2::kT, sm, s>>>(pts, off, tw, out, aligned);
+  return cudaGetLastError();
+}
+
+
+bool v3_resample_align_supported(int N) { return N == 512 || N == 1024; }
+int v3_max_raw_nodes() { return rs3::kNMax; }
+
+cudaError_t launch_v3_resample_align(const double2* pts, const int64_t* off, int64_t pairs, int N,
+                                     const double2* tw, cva_alignment* out, double2* aligned,
+                                     cudaStream_t s) {
+  // CVA_SMEM_PAD=<bytes> (measurement only): extra dynamic shared memory per CTA,
+  // e.g. to run one CTA per SM
+  static const size_t pad = [] {
+    const char* e = std::getenv("CVA_SMEM_PAD");
+    return e ? (size_t)std::strtoul(e, nullptr, 10) : (size_t)0;
+  }();
+  if (N == 512) {
+    const size_t sm = v3::smem_bytes<512>() + pad;
+    cudaError_t e = set_smem((const void*)v3::resample_align_kernel<512>, sm);
+    if (e != cudaSuccess) return e;
+    v3::resample_align_kernel<512><<<(unsigned)pairs, rs3::kT, sm, s>>>(pts, off, tw, out, aligned);
+  } else {
+    const size_t sm = v3::smem_bytes<1024>() + pad;
+    cudaError_t e = set_smem((const void*)v3::resample_align_kernel<1024>, sm);
+    if (e != cudaSuccess) return e;
+    v3::resample_align_kernel<1024><<<(unsigned)pairs, rs3::kT, sm, s>>>(pts, off, tw, out, aligned);
+  }
   return cudaGetLastError();
 }
 

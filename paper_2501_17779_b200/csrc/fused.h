@@ -19,6 +19,11 @@ bool v2_resample_align_supported(int N);
 cudaError_t launch_v2_resample_align(const double2* pts, const int64_t* off, int64_t pairs, int N,
                                      const double2* tw, cva_alignment* out, double2* aligned,
                                      cudaStream_t s);
+bool v3_resample_align_supported(int N);
+int v3_max_raw_nodes();
+cudaError_t launch_v3_resample_align(const double2* pts, const int64_t* off, int64_t pairs, int N,
+                                     const double2* tw, cva_alignment* out, double2* aligned,
+                                     cudaStream_t s);
 cudaError_t launch_v2_preprocess(const double2* pts, const int64_t* off, int64_t curves, int n_out,
                                  int center_normalize, double2* out, int32_t* status,
                                  cudaStream_t s);

@@ -40,13 +40,12 @@ __global__ void tw_init_kernel(double2* tw, int N) {
 static_assert(pf::ptw_off<128>(1024, 8) == 1024 && pf::ptw_off<128>(1024, 64) == 1024 + 56 &&
                   pf::ptw_off<128>(1024, 512) == 1024 + 56 + 448,
               "pass table offsets, 128-thread plan");
-#if CVA_R8_MIN <= 4
-static_assert(pf::ptw_off<256>(1024, 8) == 1024 + 1016 && pf::ptw_off_warp(1024, 8) == 1024 + 2 * 1016 &&
+#if CVA_R8_MIN <= 4  // all three plans are 8, 8, 8, 2 at N = 1024: one shared set of tables
+static_assert(pf::ptw_off<256>(1024, 8) == 1024 && pf::ptw_off_warp(1024, 512) == 1024 + 56 + 448 &&
                   pf::ptw_len(1024) == 3 * 1016,
               "pass table offsets, 256-thread and one-warp plans");
 #else  // 256 threads: radix 4 x 5 (3 x 4, 3 x 16, 3 x 64, 3 x 256 entries)
-static_assert(pf::ptw_off<256>(1024, 4) == 1024 + 1016 &&
-                  pf::ptw_off_warp(1024, 8) == 1024 + 1016 + 3 * (4 + 16 + 64 + 256),
+static_assert(pf::ptw_off<256>(1024, 4) == 1024 + 1016 && pf::ptw_off_warp(1024, 8) == 1024,
               "pass table offsets, 256-thread and one-warp plans");
 #endif
 

@@ -61,6 +61,9 @@ template <int NT>
 // With scattered twiddle loads, 4 (radix 8 with half the threads idle in the
 // 1024-point correlation transform: 4 passes instead of 5) was 1.4 % faster;
 // with the per-pass twiddle tables, 8 is 0.35 % faster.
+// Radix 8 for the 256-thread transform too (4: its pass tables are then the
+// 128-thread plan's, 16 KB of twiddles per pair instead of 32 KB) measured
+// slower in round 3 (align kernel 111 -> 132 us): half the threads idle.
 #ifndef CVA_R8_MIN
 #define CVA_R8_MIN 8
 #endif
@@ -92,16 +95,30 @@ __host__ __device__ constexpr int ptw_until_warp(int N, int Ns_stop) {
     if (Ns > 1) s += (plan_radix_warp(N, Ns) - 1) * Ns;
   return s;
 }
-// layout after the length-N table: [128-thread plan][256-thread plan][warp plan]
+// layout after the length-N table: [128-thread plan][256-thread plan][warp plan];
+// a plan equal to an earlier one (same radix sequence) reads that one's tables
+// (its own region is left unused).
+__host__ __device__ constexpr bool plan256_is_128(int N) {
+  for (int Ns = 1; Ns < N; Ns *= plan_radix<128>(N, Ns))
+    if (plan_radix<128>(N, Ns) != plan_radix<256>(N, Ns)) return false;
+  return true;
+}
+__host__ __device__ constexpr bool planwarp_is_128(int N) {
+  for (int Ns = 1; Ns < N; Ns *= plan_radix<128>(N, Ns))
+    if (plan_radix<128>(N, Ns) != plan_radix_warp(N, Ns)) return false;
+  return true;
+}
 __host__ __device__ constexpr int ptw_len(int N) {
   return ptw_until<128>(N, N) + ptw_until<256>(N, N) + ptw_until_warp(N, N);
 }
 template <int NT>
 __host__ __device__ constexpr int ptw_off(int N, int Ns) {
-  return N + (NT == 256 ? ptw_until<128>(N, N) : 0) + ptw_until<NT>(N, Ns);
+  return NT == 256 && !plan256_is_128(N) ? N + ptw_until<128>(N, N) + ptw_until<256>(N, Ns)
+                                         : N + ptw_until<128>(N, Ns);
 }
 __host__ __device__ constexpr int ptw_off_warp(int N, int Ns) {
-  return N + ptw_until<128>(N, N) + ptw_until<256>(N, N) + ptw_until_warp(N, Ns);
+  return planwarp_is_128(N) ? N + ptw_until<128>(N, Ns)
+                            : N + ptw_until<128>(N, N) + ptw_until<256>(N, N) + ptw_until_warp(N, Ns);
 }
 
 // Compile-time pass: N, Ns, the butterfly count per thread and every index
@@ -139,6 +156,7 @@ __device__ __forceinline__ double2* group_fft_ct(Src src, double2* dst, double2*
   constexpr int R = plan_radix<NT>(N, Ns);
   pass_ct<R, NT, N, Ns>(src, dst, tw, g);
   sync();
+  CVA_MARK(40 + (NT == 256 ? 8 : 0) + (Ns == 1 ? 0 : Ns == 8 ? 1 : Ns == 64 ? 2 : Ns == 512 ? 3 : Ns == 4 ? 4 : Ns == 16 ? 5 : Ns == 256 ? 6 : 7));
   if constexpr (Ns * R < N) {
     auto next = [dst](int i) { return dst[pad(i)]; };
     return group_fft_ct<NT, N, Ns * R>(next, other, dst, tw, g, sync);
@@ -325,7 +343,9 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
           const int k1 = k + 1 == N ? 0 : k + 1;
           const double2 o = src[padded ? k1 + (k1 >> 3) : k1];
           const double dx = o.x - q.x, dy = o.y - q.y;
-          len += fsqrt(fma(dx, dx, dy * dy));
+          const double e2 = fma(dx, dx, dy * dy);
+          const double e = fsqrt_nb(e2);  // branch-free; a zero edge adds 0
+          len += e2 == 0.0 ? 0.0 : e;  // NaN / inf edges propagate (flagged below)
         }
       }
       return z;
