@@ -350,41 +350,15 @@ int or_correlation_all_shifts_naive(const double* c1, const double* c2, int64_t 
 /* proj/src/fft.cpp:81-95: n/2+1 unnormalised bins of exp(-2 pi i jk/n) */
 int or_real_dft(const double* in, int64_t n, double* out) {
   if (n < 2) return OR_INVALID;
-  double* buf = (double*)malloc(sizeof(double) * 2 * n);
-  if (!buf) return OR_BAD_ALLOC;
-  for (int64_t j = 0; j < n; ++j) {
-    buf[2 * j] = in[j];
-    buf[2 * j + 1] = 0.0;
-  }
-  if (offt_dft(buf, (size_t)n, -1)) {
-    free(buf);
-    return OR_BAD_ALLOC;
-  }
-  memcpy(out, buf, sizeof(double) * 2 * (size_t)(n / 2 + 1));
-  free(buf);
-  return OR_OK;
+  return offt_r2c(in, (size_t)n, out) ? OR_BAD_ALLOC : OR_OK;
 }
 
 /* proj/src/fft.cpp:97-114: Hermitian half-spectrum back to n reals, scaled 1/n */
 int or_real_idft(const double* spec, int64_t n_bins, int64_t n, double* out) {
   if (n < 1 || n_bins != n / 2 + 1) return OR_INVALID;
-  double* buf = (double*)malloc(sizeof(double) * 2 * n);
-  if (!buf) return OR_BAD_ALLOC;
-  for (int64_t k = 0; k <= n / 2; ++k) {
-    buf[2 * k] = spec[2 * k];
-    buf[2 * k + 1] = spec[2 * k + 1];
-  }
-  for (int64_t k = n / 2 + 1; k < n; ++k) {
-    buf[2 * k] = spec[2 * (n - k)];
-    buf[2 * k + 1] = -spec[2 * (n - k) + 1];
-  }
-  if (offt_dft(buf, (size_t)n, +1)) {
-    free(buf);
-    return OR_BAD_ALLOC;
-  }
+  if (offt_c2r(spec, (size_t)n, out)) return OR_BAD_ALLOC;
   const double scale = 1.0 / (double)n;
-  for (int64_t j = 0; j < n; ++j) out[j] = buf[2 * j] * scale;
-  free(buf);
+  for (int64_t j = 0; j < n; ++j) out[j] = out[j] * scale;
   return OR_OK;
 }
 

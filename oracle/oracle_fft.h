@@ -24,6 +24,13 @@ extern "C" {
  * success, -1 on allocation failure. */
 int offt_dft(double* data, size_t n, int sign);
 
+/* Real input x[0..n) -> n/2+1 unnormalised bins of exp(-2 pi i jk/n) (FFTW
+ * r2c), and back (FFTW c2r: unnormalised, Hermitian input of n/2+1 bins).
+ * Power-of-two n >= 4 go through one n/2-point complex transform with
+ * per-n cached twiddles; thread-safe. 0 on success, -1 on failure. */
+int offt_r2c(const double* in, size_t n, double* out_bins);
+int offt_c2r(const double* bins, size_t n, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,6 +1,9 @@
 /* TEST INFRASTRUCTURE ONLY — FFTW3-API stand-in for compiling the reference's
  * own fft.cpp (/root/reference/proj/src/fft.cpp) into oracle/_ref. See fftw3.h
- * for the transform definitions restated here.
+ * for the transform definitions restated here. The transforms are
+ * oracle_fft.c's offt_r2c / offt_c2r: per-n cached twiddles and one half-length
+ * complex transform per real transform (about what an FFTW_ESTIMATE plan
+ * does), so the CPU baseline is not handicapped by the stand-in.
  */
 #include "fftw3.h"
 
@@ -46,36 +49,11 @@ fftw_plan fftw_plan_dft_c2r_1d(int n, fftw_complex* in, double* out, unsigned fl
 }
 
 void fftw_execute_dft_r2c(const fftw_plan p, double* in, fftw_complex* out) {
-  const size_t n = (size_t)p->n;
-  double* buf = (double*)malloc(sizeof(double) * 2 * n);
-  if (!buf) abort();
-  for (size_t j = 0; j < n; ++j) {
-    buf[2 * j] = in[j];
-    buf[2 * j + 1] = 0.0;
-  }
-  if (offt_dft(buf, n, -1) != 0) abort();
-  for (size_t k = 0; k <= n / 2; ++k) {
-    out[k][0] = buf[2 * k];
-    out[k][1] = buf[2 * k + 1];
-  }
-  free(buf);
+  if (offt_r2c(in, (size_t)p->n, &out[0][0]) != 0) abort();
 }
 
 void fftw_execute_dft_c2r(const fftw_plan p, fftw_complex* in, double* out) {
-  const size_t n = (size_t)p->n;
-  double* buf = (double*)malloc(sizeof(double) * 2 * n);
-  if (!buf) abort();
-  for (size_t k = 0; k <= n / 2; ++k) {
-    buf[2 * k] = in[k][0];
-    buf[2 * k + 1] = in[k][1];
-  }
-  for (size_t k = n / 2 + 1; k < n; ++k) { /* Hermitian extension */
-    buf[2 * k] = in[n - k][0];
-    buf[2 * k + 1] = -in[n - k][1];
-  }
-  if (offt_dft(buf, n, +1) != 0) abort();
-  for (size_t j = 0; j < n; ++j) out[j] = buf[2 * j];
-  free(buf);
+  if (offt_c2r(&in[0][0], (size_t)p->n, out) != 0) abort();
 }
 
 void fftw_destroy_plan(fftw_plan p) { free(p); }

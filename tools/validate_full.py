@@ -22,45 +22,8 @@ import paper_2501_17779_b200 as cva  # noqa: E402
 from paper_2501_17779_b200 import synth  # noqa: E402
 from pyoracle import Oracle, Reference, reference_available  # noqa: E402
 
-PI = np.pi
-
-
-def wrap(a):
-    return (np.asarray(a) + PI) % (2 * PI) - PI
-
-
-def tau(c1, c2, m):
-    z1 = c1[:, 0] + 1j * c1[:, 1]
-    z2 = np.roll(c2[:, 0] + 1j * c2[:, 1], -m)
-    return abs(np.sum(np.conj(z1) * z2)) / len(z1)
-
-
-def compare(res, ro, al, ao, firsts, seconds):
-    n = firsts.shape[1]
-    out = {"pairs": int(len(res)), "status_ok": int((res["status"] == 0).sum()), "shift_equal": 0,
-           "near_ties": 0, "violations": 0, "max_dtheta": 0.0, "max_coord_rel": 0.0, "max_energy_rel": 0.0}
-    for p in range(len(res)):
-        g, r = res[p], ro[p]
-        c1, c2 = firsts[p], seconds[p]
-        if int(g["shift"]) != int(r["shift"]):
-            t1, t2 = tau(c1, c2, int(g["shift"])), tau(c1, c2, int(r["shift"]))
-            if abs(t1 - t2) <= 1e-12 * max(t1, t2):
-                out["near_ties"] += 1
-            else:
-                out["violations"] += 1
-            continue
-        out["shift_equal"] += 1
-        dth = abs(float(wrap(float(g["theta"]) - float(r["theta"]))))
-        out["max_dtheta"] = max(out["max_dtheta"], dth)
-        scale = (np.sum(c1 ** 2) + np.sum(c2 ** 2)) / n
-        er = abs(float(g["energy"]) - float(r["energy"])) / max(float(r["energy"]), 1e-4 * scale)
-        out["max_energy_rel"] = max(out["max_energy_rel"], er)
-        cr = np.abs(al[p] - ao[p]).max() / np.abs(ao[p]).max()
-        out["max_coord_rel"] = max(out["max_coord_rel"], float(cr))
-        if dth > 1e-10 or cr > 1e-10 or abs(float(g["energy"]) - float(r["energy"])) > (
-                1e-10 * float(r["energy"]) + 1e-14 * scale):
-            out["violations"] += 1
-    return out
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from parity_rule import compare, wrap  # noqa: E402
 
 
 def main():
