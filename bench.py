@@ -462,6 +462,7 @@ def count_kernels(step):
     from torch.profiler import ProfilerActivity, profile
 
     try:
+        step()  # first-call setup (twiddle tables, workspaces) is not a step
         torch.cuda.synchronize()
         with profile(activities=[ProfilerActivity.CUDA], acc_events=True) as prof:
             step()
