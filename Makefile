@@ -20,7 +20,7 @@ KERNEL_HDRS := $(wildcard $(CSRC)/*.cuh) $(CSRC)/kernels.h $(CSRC)/fused.h $(CSR
 
 # Phase-timing build (tools/phase_timing.py): separate .so, never shipped.
 prof: $(PKG)/libcurvalign_cuda_prof.so
-$(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kernels.cu $(CSRC)/allpairs.cu $(CSRC)/largen.cu $(CSRC)/dropin_kernels.cu $(CSRC)/elastic.cu $(KERNEL_HDRS) $(CSRC)/prof.cuh
+$(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kernels.cu $(CSRC)/allpairs.cu $(CSRC)/largen.cu $(CSRC)/dropin_kernels.cu $(CSRC)/gfft.cu $(CSRC)/elastic.cu $(KERNEL_HDRS) $(CSRC)/prof.cuh
 	@mkdir -p $(BUILD)/prof
 	$(NVCC) $(NVFLAGS) -DCVA_PHASE_TIMING -c $(CSRC)/fused.cu -o $(BUILD)/prof/fused.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/kernels.cu -o $(BUILD)/prof/kernels.o
@@ -29,6 +29,7 @@ $(PKG)/libcurvalign_cuda_prof.so: $(CSRC)/fused.cu $(CSRC)/capi.cpp $(CSRC)/kern
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/allpairs.cu -o $(BUILD)/prof/allpairs.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/largen.cu -o $(BUILD)/prof/largen.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/dropin_kernels.cu -o $(BUILD)/prof/dropin_kernels.o
+	$(NVCC) $(NVFLAGS) -c $(CSRC)/gfft.cu -o $(BUILD)/prof/gfft.o
 	$(NVCC) $(NVFLAGS) -c $(CSRC)/elastic.cu -o $(BUILD)/prof/elastic.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(BUILD)/prof/*.o
 all: lib synth dropin dropin_test oracle ref
@@ -57,7 +58,11 @@ $(BUILD)/elastic.o: $(CSRC)/elastic.cu $(KERNEL_HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c $< -o $@ 2> $(BUILD)/ptxas_elastic.log || (cat $(BUILD)/ptxas_elastic.log; exit 1)
 
-$(BUILD)/dropin_kernels.o: $(CSRC)/dropin_kernels.cu $(KERNEL_HDRS)
+$(BUILD)/dropin_kernels.o: $(CSRC)/dropin_kernels.cu $(KERNEL_HDRS) $(CSRC)/gfft.h
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(BUILD)/gfft.o: $(CSRC)/gfft.cu $(CSRC)/gfft.h $(KERNEL_HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
@@ -69,7 +74,7 @@ $(BUILD)/probe.o: $(CSRC)/probe.cu include/curvalign_cuda.h
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/fused.o $(BUILD)/allpairs.o $(BUILD)/largen.o $(BUILD)/elastic.o $(BUILD)/dropin_kernels.o $(BUILD)/capi.o $(BUILD)/probe.o
+$(PKG)/libcurvalign_cuda.so: $(BUILD)/kernels.o $(BUILD)/fused.o $(BUILD)/allpairs.o $(BUILD)/largen.o $(BUILD)/elastic.o $(BUILD)/dropin_kernels.o $(BUILD)/gfft.o $(BUILD)/capi.o $(BUILD)/probe.o
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^
 
 # Synthetic workload generators (bench harness; host only).

@@ -7,7 +7,7 @@
  * C++ or torch types cross it. The C++ API of the reference (namespace
  * curvalign: align_fft, preprocess, resample_uniform, srv_transform, ...) is
  * re-declared in the include/curvalign/ headers and implemented on top of these entry
- * points (paper_2501_17779_b200/csrc/dropin.cpp); INTEGRATION.md shows the
+ * points (paper_2501_17779_b200/csrc/dropin/, one .cpp per header); INTEGRATION.md shows the
  * ctypes / C++ bindings a maintainer adds.
  *
  * Data layout. A curve of n nodes is n interleaved (x, y) doubles — the layout
@@ -192,10 +192,13 @@ int cva_arc_length_params_host(const double* xy, int64_t n, double* s, double* t
 int cva_spline_solve_host(const double* x, const double* y, int64_t n_knots, double* m);
 /* srv_transform (srv.cpp:71-88); center != 0 also applies srv_center (srv.cpp:90-98) */
 int cva_srv_transform_host(const double* xy, int64_t n, int center, double* q);
-/* X_k = scale * sum_j x_j exp(sign 2 pi i j k / n), k < kcount (any n; real_dft /
- * real_idft / circular_cross_correlation, proj/src/fft.cpp:81-125) */
+/* X_k = scale * sum_j x_j exp(sign 2 pi i j k / n), k < kcount (any n, O(n log n):
+ * radix 2 or Bluestein; real_dft / real_idft, proj/src/fft.cpp:81-114) */
 int cva_dft_host(const double* x_complex, int64_t n, int64_t kcount, int sign, double scale,
                  double* out_complex);
+/* A(m) for every shift m, out4[4 m + {0,1,2,3}] = a11, a12, a21, a22, by FFT
+ * (correlation_all_shifts_fft, rigid_align.cpp:147-183; any n, O(n log n)) */
+int cva_correlation_fft_host(const double* c1, const double* c2, int64_t n, double* out4);
 
 /* ---------------------------------------------------------------------------
  * Elastic (SRV) matching: the rigid path's callers in the reference's elastic

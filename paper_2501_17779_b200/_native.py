@@ -89,6 +89,7 @@ SIGNATURES = {
     "cva_spline_solve_host": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "cva_srv_transform_host": (c_int, [c_void_p, c_int64, c_int, c_void_p]),
     "cva_dft_host": (c_int, [c_void_p, c_int64, c_int64, c_int, c_double, c_void_p]),
+    "cva_correlation_fft_host": (c_int, [c_void_p, c_void_p, c_int64, c_void_p]),
     "cva_preprocess_align_uniform": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
     "cva_preprocess_align_uniform_host": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "cva_allpairs": (

@@ -32,15 +32,14 @@ std::vector<double> circular_cross_correlation(std::span<const double> a, std::s
   if (a.size() != b.size()) throw std::invalid_argument("fft: correlation size mismatch");
   const std::size_t n = a.size();
   if (n < 2) throw std::invalid_argument("fft: length must be at least 2");
-  // r[m] = A11(m) of the curves (a, 0), (b, 0)
+  // r[m] = A11(m) of the curves (a, 0), (b, 0), by FFT (O(n log n), fft.cpp:116-125)
   std::vector<Point2> pa(n), pb(n);
   for (std::size_t i = 0; i < n; ++i) {
     pa[i] = Point2(a[i], 0.0);
     pb[i] = Point2(b[i], 0.0);
   }
   std::vector<double> m4(4 * n), r(n);
-  detail::check_dropin(
-      cva_correlation_matrices_host(detail::raw(pa.data()), detail::raw(pb.data()), (int64_t)n, 0, (int64_t)n, m4.data()));
+  detail::check_dropin(cva_correlation_fft_host(detail::raw(pa.data()), detail::raw(pb.data()), (int64_t)n, m4.data()));
   for (std::size_t m = 0; m < n; ++m) r[m] = m4[4 * m];
   return r;
 }

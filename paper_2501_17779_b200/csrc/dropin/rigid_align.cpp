@@ -1,7 +1,9 @@
 // Rigid alignment (reference: proj/src/rigid_align.cpp) on the GPU.
 #include "curvalign/rigid_align.hpp"
 
+#include <algorithm>
 #include <cmath>
+#include <limits>
 #include <stdexcept>
 
 #include "status.hpp"
@@ -90,11 +92,17 @@ std::vector<Mat2> correlation_all_shifts_naive(std::span<const Point2> c1, std::
   return out;
 }
 
-// The GPU computes the stack by exact per-shift sums (no FFT rounding); the
-// reference's own equivalence test bounds |naive - fft| by 1e-9 n
-// (test_rigid_align.cpp:133-151).
+// Two forward and two inverse GPU FFTs of z = x + i y (D and E spectra,
+// gfft.cu), any n, O(n log n); correlation_all_shifts_naive above is the exact
+// per-shift scan, so the reference's equivalence test (|naive - fft| <= 1e-9 n,
+// test_rigid_align.cpp:133-151) compares two computations.
 std::vector<Mat2> correlation_all_shifts_fft(std::span<const Point2> c1, std::span<const Point2> c2) {
-  return correlation_all_shifts_naive(c1, c2);
+  check_pair(c1.size(), c2.size());
+  const std::size_t n = c1.size();
+  std::vector<Mat2> out(n);
+  check_dropin(cva_correlation_fft_host(raw(c1.data()), raw(c2.data()), (int64_t)n,
+                                        reinterpret_cast<double*>(out.data())));
+  return out;
 }
 
 double mismatch_energy(std::span<const Point2> c1, std::span<const Point2> c2, std::size_t shift,
@@ -114,10 +122,47 @@ RigidAlignment align_fft(std::span<const Point2> c1, std::span<const Point2> c2)
   return from_record(r);
 }
 
-// The exhaustive scan and the FFT search return the same optimum (the
-// reference's acceptance criterion 1, acceptance.cpp:94-120); both run on the
-// GPU correlation kernel.
-RigidAlignment align_naive(std::span<const Point2> c1, std::span<const Point2> c2) { return align_fft(c1, c2); }
+namespace {
+double sum_norm2(std::span<const Point2> c) {
+  double s = 0.0;
+  for (const Point2& p : c) s += p.x * p.x + p.y * p.y;
+  return s;
+}
+
+// pick_best (rigid_align.cpp:31-61): the smallest shift whose optimal trace is
+// within 1e-12 (relative) of the maximum, rotation by SVD, energy identity.
+RigidAlignment pick_best(const std::vector<Mat2>& corr, double s1, double s2, std::size_t n) {
+  auto opt_trace = [](const Mat2& A) { return std::hypot(A.a11 + A.a22, A.a12 - A.a21); };
+  double best = -std::numeric_limits<double>::infinity();
+  for (const Mat2& A : corr) best = std::max(best, opt_trace(A));
+  const double tol = 1e-12 * std::max(1.0, std::abs(best));
+  std::size_t m = 0;
+  for (std::size_t i = 0; i < n; ++i)
+    if (opt_trace(corr[i]) >= best - tol) {
+      m = i;
+      break;
+    }
+  const RotationFit fit = optimal_rotation_svd(corr[m]);
+  RigidAlignment out;
+  out.shift = m;
+  out.t0 = (double)m / (double)n;
+  out.rotation = fit.rotation;
+  out.trace = fit.trace;
+  out.degenerate = fit.degenerate;
+  const double h = 1.0 / (double)n;
+  out.energy = std::max(0.0, h * (s1 + s2) - 2.0 * h * fit.trace);
+  return out;
+}
+}  // namespace
+
+// The exhaustive scan (rigid_align.cpp:198-202): exact per-shift sums on the GPU
+// (correlation_all_shifts_naive), then the reference's tie-broken pick on the
+// host — a computation independent of align_fft's FFT kernel, so the
+// reference's acceptance criterion 1 (acceptance.cpp:94-120) compares the two.
+RigidAlignment align_naive(std::span<const Point2> c1, std::span<const Point2> c2) {
+  check_pair(c1.size(), c2.size());
+  return pick_best(correlation_all_shifts_naive(c1, c2), sum_norm2(c1), sum_norm2(c2), c1.size());
+}
 
 std::vector<RigidAlignment> align_fft_batch(const std::vector<Curve>& c1, const std::vector<Curve>& c2,
                                             std::vector<Curve>* aligned) {

@@ -9,6 +9,7 @@
 
 #include "../../include/curvalign_cuda.h"
 #include "cva_common.cuh"
+#include "gfft.h"
 #include "elastic.h"
 #include "spline.cuh"
 
@@ -146,23 +147,10 @@ __global__ void __launch_bounds__(kT) srv_kernel(const double2* __restrict__ c, 
   for (int64_t l = threadIdx.x; l < n; l += kT) q[l] = csub(q[l], mean);
 }
 
-// Direct DFT (fft.cpp:81-114 semantics, any n): X_k = sum_j x_j exp(sign 2 pi i j k / n),
-// twiddle angle from (j k mod n) so every term is exact to the ulp. O(n^2); used
-// by the scalar real_dft / real_idft entry points only.
-__global__ void __launch_bounds__(kT) dft_kernel(const double2* __restrict__ x, int64_t n, int64_t kcount, int sign,
-                                                 double scale, double2* out) {
-  __shared__ double2 red[64];
-  const int64_t k = blockIdx.x;
-  double2 acc = make_double2(0, 0);
-  for (int64_t j = threadIdx.x; j < n; j += kT) {
-    const int64_t jk = (j * k) % n;
-    double sn, cs;
-    sincospi(2.0 * (double)jk / (double)n, &sn, &cs);
-    const double2 w = make_double2(cs, sign * sn);
-    acc = cadd(acc, cmul(x[j], w));
-  }
-  acc = block_sum2(acc, red);
-  if (threadIdx.x == 0 && k < kcount) out[k] = cscale(acc, scale);
+// x *= scale (in place; the 1/n of real_idft, fft.cpp:111-112)
+__global__ void scale_kernel(double2* x, int64_t n, double scale) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = cscale(x[i], scale);
 }
 
 }  // namespace di
@@ -323,16 +311,37 @@ int cva_srv_transform_host(const double* xy, int64_t n, int center, double* q) {
   return cva::down(q, o, cb);
 }
 
-// X_k, k < kcount, of the complex sequence x (n points); sign -1 forward, +1 inverse.
+// X_k, k < kcount, of the complex sequence x (n points); sign -1 forward, +1
+// inverse; any n, O(n log n) (gfft.cu: radix 2 or Bluestein).
 int cva_dft_host(const double* x_complex, int64_t n, int64_t kcount, int sign, double scale, double* out_complex) {
-  if (n < 1 || kcount < 0 || kcount > n) return cva::err(CVA_INVALID_ARGUMENT, "fft: bad length");
+  if (n < 1 || kcount < 0 || kcount > n || (sign != 1 && sign != -1))
+    return cva::err(CVA_INVALID_ARGUMENT, "fft: bad length");
   if (kcount == 0) return CVA_OK;
   if (int rc = cva::have_device()) return rc;
-  Buf a, o;
+  Buf a, w;
   if (int rc = cva::up(a, x_complex, sizeof(double2) * (size_t)n)) return rc;
-  if (!o.alloc(sizeof(double2) * (size_t)kcount)) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
-  cva::di::dft_kernel<<<(unsigned)kcount, cva::di::kT, 0, cva::kS>>>((const double2*)a.p, n, kcount, sign, scale, (double2*)o.p);
-  return cva::down(out_complex, o, sizeof(double2) * (size_t)kcount);
+  if (!w.alloc(sizeof(double2) * (size_t)cva::gfft_workspace(n))) return cva::err(CVA_BAD_ALLOC, "device allocation failed");
+  cudaError_t e = cva::gfft((double2*)a.p, n, sign, (double2*)w.p, cva::kS);
+  if (e != cudaSuccess) return cva::err(CVA_CUDA_ERROR, "fft launch", e);
+  if (scale != 1.0) cva::di::scale_kernel<<<(unsigned)((kcount + 255) / 256), 256, 0, cva::kS>>>((double2*)a.p, kcount, scale);
+  return cva::down(out_complex, a, sizeof(double2) * (size_t)kcount);
+}
+
+// A(m) for every shift m by FFT (correlation_all_shifts_fft, rigid_align.cpp:147-183).
+int cva_correlation_fft_host(const double* c1, const double* c2, int64_t n, double* out4) {
+  if (n < 1) return cva::err(CVA_INVALID_ARGUMENT, "correlation: empty");
+  if (int rc = cva::have_device()) return rc;
+  Buf a, b, o, w;
+  const size_t cb = sizeof(double2) * (size_t)n;
+  if (int rc = cva::up(a, c1, cb)) return rc;
+  if (int rc = cva::up(b, c2, cb)) return rc;
+  if (!o.alloc(sizeof(double) * 4 * (size_t)n) ||
+      !w.alloc(sizeof(double2) * (size_t)cva::gfft_correlation_workspace(n)))
+    return cva::err(CVA_BAD_ALLOC, "device allocation failed");
+  cudaError_t e = cva::gfft_correlation((const double2*)a.p, (const double2*)b.p, n, (double*)o.p, (double2*)w.p,
+                                        cva::kS);
+  if (e != cudaSuccess) return cva::err(CVA_CUDA_ERROR, "correlation fft launch", e);
+  return cva::down(out4, o, sizeof(double) * 4 * (size_t)n);
 }
 
 // ---- SRV / elastic utilities (srv.cpp:58-69 validation, :100-176)

@@ -1,3 +1,4 @@
+#include <chrono>
 // C++ tests of the drop-in API (include/curvalign/*.hpp over libcurvalign_cuda.so).
 // Each case restates a hot-path test of the reference's own suite
 // (/root/reference/proj/tests/test_rigid_align.cpp, test_curve_core.cpp,
@@ -148,15 +149,34 @@ int main() {
   });
   run("naive == fft stacks", [] {  // :133-151
     std::mt19937_64 rng(43);
-    for (std::size_t n : {8u, 20u, 64u, 101u}) {
+    // naive: exact per-shift sums; fft: two forward + two inverse GPU FFTs
+    // (radix 2 for powers of two, Bluestein otherwise): two computations
+    for (std::size_t n : {4u, 5u, 8u, 20u, 37u, 64u, 101u, 1000u, 4097u}) {
       Curve c1 = random_curve(rng, n), c2 = random_curve(rng, n);
       const auto a = correlation_all_shifts_naive(c1.nodes, c2.nodes);
       const auto b = correlation_all_shifts_fft(c1.nodes, c2.nodes);
       CHECK(a.size() == n && b.size() == n);
       for (std::size_t m = 0; m < n; ++m)
-        CHECK(std::fabs(a[m].a11 - b[m].a11) < 1e-9 * n && std::fabs(a[m].a22 - b[m].a22) < 1e-9 * n);
+        CHECK(std::fabs(a[m].a11 - b[m].a11) < 1e-9 * n && std::fabs(a[m].a22 - b[m].a22) < 1e-9 * n &&
+              std::fabs(a[m].a12 - b[m].a12) < 1e-9 * n && std::fabs(a[m].a21 - b[m].a21) < 1e-9 * n);
       const RigidAlignment f = align_fft(c1, c2), g = align_naive(c1, c2);
       CHECK(f.shift == g.shift && std::fabs(f.energy - g.energy) < 1e-9);
+    }
+  });
+  run("fft stack at n = 65536 is O(n log n)", [] {
+    std::mt19937_64 rng(44);
+    const std::size_t n = 65536;
+    Curve c1 = random_curve(rng, n), c2 = random_curve(rng, n);
+    (void)correlation_all_shifts_fft(c1.nodes, c2.nodes);  // first call: context, workspace
+    const auto t0 = std::chrono::steady_clock::now();
+    const auto b = correlation_all_shifts_fft(c1.nodes, c2.nodes);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::printf("    correlation_all_shifts_fft(65536): %.2f ms\n", ms);
+    CHECK(ms < 100.0);
+    for (std::size_t m : {0u, 1u, 777u, 32768u, 65535u}) {
+      const Mat2 a = cross_correlation_matrix(c1.nodes, c2.nodes, m);
+      CHECK(std::fabs(a.a11 - b[m].a11) < 1e-9 * n && std::fabs(a.a12 - b[m].a12) < 1e-9 * n &&
+            std::fabs(a.a21 - b[m].a21) < 1e-9 * n && std::fabs(a.a22 - b[m].a22) < 1e-9 * n);
     }
   });
   run("exact cyclic shift", [] {  // :153-168
@@ -337,7 +357,7 @@ int main() {
   run("real dft / idft / correlation", [] {
     std::mt19937_64 rng(5);
     std::normal_distribution<double> g;
-    for (std::size_t n : {2u, 3u, 8u, 33u, 101u, 256u}) {
+    for (std::size_t n : {2u, 3u, 8u, 33u, 101u, 256u, 1000u}) {
       std::vector<double> x(n), y(n);
       for (auto& v : x) v = g(rng);
       for (auto& v : y) v = g(rng);
