@@ -112,25 +112,36 @@ int check_small_fft(int64_t n) {
 
 // Stream-ordered scratch (cudaMallocAsync on the call's stream, freed after the
 // kernels on the same stream): safe for concurrent calls on different streams.
-// The device's default pool keeps freed blocks cached.
+// Scratch comes from this library's own stream-ordered pool per device (freed
+// blocks stay cached up to kPoolKeep bytes; the process-wide default pool and
+// its release threshold are left to the application).
+constexpr uint64_t kPoolKeep = uint64_t(2) << 30;
 std::mutex g_pool_mu;
-std::map<int, bool> g_pool_ready;
+std::map<int, cudaMemPool_t> g_pools;
 
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
   int dev = 0;
-  cudaGetDevice(&dev);
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  cudaMemPool_t pool = nullptr;
   {
     std::lock_guard<std::mutex> lock(g_pool_mu);
-    if (!g_pool_ready[dev]) {
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-      }
-      g_pool_ready[dev] = true;
+    auto it = g_pools.find(dev);
+    if (it == g_pools.end()) {
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = dev;
+      e = cudaMemPoolCreate(&pool, &props);
+      if (e != cudaSuccess) return e;
+      uint64_t thr = kPoolKeep;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      g_pools[dev] = pool;
+    } else {
+      pool = it->second;
     }
   }
-  return cudaMallocAsync(p, bytes ? bytes : 16, s);
+  return cudaMallocFromPoolAsync(p, bytes ? bytes : 16, pool, s);
 }
 
 int64_t host_max_n(const int64_t* offsets, int64_t curves) {
@@ -830,20 +841,48 @@ int cva_elastic_approach2_batch(const double* c1, const double* c2, int64_t pair
   return elastic_launch(c1, c2, pairs, 0, n, max_iters, energy_tol, max_slope, o, (cudaStream_t)stream);
 }
 
+// Approach 1 keeps per-item results until the per-pair pick. With gamma wanted
+// (independent pairs only: distance matrices pass gamma = null), the items'
+// gammas would need pairs * n * (n + 1) doubles, so the pairs run in chunks
+// whose scratch stays below kA1ScratchCap.
 static int approach1_launch(const double* A, const double* B, int64_t pairs, int64_t k, int64_t n, int max_slope,
                             const cva::ElasticOut& o, cudaStream_t s) {
-  const int64_t items = pairs * n;
+  constexpr size_t kA1ScratchCap = size_t(1) << 30;
+  const bool gamma = o.gamma != nullptr;
+  int64_t chunk = pairs;
+  if (gamma && k == 0) {
+    const size_t per_pair = cva::elastic_a1_scratch(1, (int)n, true);
+    chunk = std::max<int64_t>(1, std::min<int64_t>(pairs, (int64_t)(kA1ScratchCap / per_pair)));
+  }
+  const int64_t items = chunk * n;
   const int grid = cva::elastic_items_grid(items, (int)n, max_slope);
   Slab slab, scratch;
   slab.s = scratch.s = s;
   const size_t per = cva::elastic_parent_slab(items, (int)n, max_slope);
   if (per && scratch_alloc(&slab.p, per * (size_t)grid, s) != cudaSuccess)
     return fail(CVA_BAD_ALLOC, "elastic: parent scratch allocation failed");
-  if (scratch_alloc(&scratch.p, cva::elastic_a1_scratch(pairs, (int)n), s) != cudaSuccess)
+  if (scratch_alloc(&scratch.p, cva::elastic_a1_scratch(chunk, (int)n, gamma), s) != cudaSuccess)
     return fail(CVA_BAD_ALLOC, "elastic: scratch allocation failed");
-  return finish(cva::launch_elastic_approach1((const double2*)A, (const double2*)B, pairs, k, (int)n, max_slope,
-                                              (uint8_t*)slab.p, grid, scratch.p, o, s),
-                "elastic approach1 launch");
+  for (int64_t p0 = 0; p0 < pairs; p0 += chunk) {
+    const int64_t cp = std::min(chunk, pairs - p0);
+    cva::ElasticOut oc = o;
+    if (p0) {  // independent pairs: offset inputs and outputs (k == 0 here)
+      oc.distance += p0;
+      oc.energy += p0;
+      oc.t0 += p0;
+      oc.theta += p0;
+      oc.gamma += p0 * (n + 1);
+      oc.iterations += p0;
+      oc.converged += p0;
+      oc.status += p0;
+    }
+    const cudaError_t e = cva::launch_elastic_approach1((const double2*)A + p0 * n, (const double2*)B + p0 * n, cp,
+                                                        k, (int)n, max_slope, (uint8_t*)slab.p,
+                                                        cva::elastic_items_grid(cp * n, (int)n, max_slope),
+                                                        scratch.p, oc, s);
+    if (e != cudaSuccess) return finish(e, "elastic approach1 launch");
+  }
+  return finish(cudaSuccess, "elastic approach1 launch");
 }
 
 static int check_a1(int64_t n, int64_t n_max) {

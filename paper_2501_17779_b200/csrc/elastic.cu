@@ -905,7 +905,8 @@ __global__ void __launch_bounds__(kT, CVA_EL_MINB)
         }
       }
     }
-    for (int l = threadIdx.x; l <= n; l += kT) item_gamma[it * (n + 1) + l] = status == CVA_OK ? S.gd[l] : qnan;
+    if (item_gamma)  // only when the caller wants gamma (not for distance matrices)
+      for (int l = threadIdx.x; l <= n; l += kT) item_gamma[it * (n + 1) + l] = status == CVA_OK ? S.gd[l] : qnan;
     if (threadIdx.x == 0) {
       item_e[it] = e;
       item_theta[it] = th;
@@ -1081,9 +1082,11 @@ static cudaError_t launch_a1(const double2* A, const double2* B, int64_t pairs, 
   return cudaGetLastError();
 }
 
-size_t elastic_a1_scratch(int64_t pairs, int n) {
+// Per item (pair, shift): energy, theta, status, and the item's gamma only
+// when the caller asked for gamma (n + 1 doubles per item).
+size_t elastic_a1_scratch(int64_t pairs, int n, bool gamma) {
   const int64_t items = pairs * n;
-  return (size_t)items * (2 * sizeof(double) + sizeof(int32_t) + sizeof(double) * (n + 1)) + 1024;
+  return (size_t)items * (2 * sizeof(double) + sizeof(int32_t) + (gamma ? sizeof(double) * (n + 1) : 0)) + 1024;
 }
 
 cudaError_t launch_elastic_approach1(const double2* A, const double2* B, int64_t pairs, int64_t matrix_k, int n,
@@ -1092,8 +1095,8 @@ cudaError_t launch_elastic_approach1(const double2* A, const double2* B, int64_t
   const int64_t items = pairs * n;
   double* ie = (double*)scratch;
   double* ith = ie + items;
-  double* ig = ith + items;
-  int32_t* ist = (int32_t*)(ig + items * (n + 1));
+  double* ig = out.gamma ? ith + items : nullptr;
+  int32_t* ist = (int32_t*)(ith + items + (out.gamma ? items * (n + 1) : 0));
   cudaError_t e;
   if (W == 4) {
     switch (n) {

@@ -39,7 +39,7 @@ cudaError_t launch_elastic_approach2(const double2* A, const double2* B, int64_t
                                      const ElasticOut& out, cudaStream_t s);
 
 // approach 1: scratch bytes for pairs x n work items; grid for those items
-size_t elastic_a1_scratch(int64_t pairs, int n);
+size_t elastic_a1_scratch(int64_t pairs, int n, bool gamma);
 int elastic_items_grid(int64_t items, int n, int W);
 cudaError_t launch_elastic_approach1(const double2* A, const double2* B, int64_t pairs, int64_t matrix_k, int n,
                                      int W, uint8_t* slab, int grid, void* scratch, const ElasticOut& out,
