@@ -1,3 +1,4 @@
+#include <algorithm>
 #include <cstdlib>
 // v2 sm_100a kernels (256 threads, 2 CTAs per SM): the fused C1 path and the
 // shared-memory preprocess / align / SRV-align kernels built from resample.cuh
@@ -351,8 +352,8 @@ static_assert(4 * sizeof(double2) * pf::padded_len(1024) <= rs3::kRawBytes, "FFT
 // (rigid_align.cpp:204-208), all on chip.
 template <int N>
 __global__ void __launch_bounds__(rs3::kT, 2)
-    resample_align_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off,
-                          const double2* __restrict__ tw, cva_alignment* __restrict__ out,
+    resample_align_kernel(const double2* __restrict__ pts, const int64_t* __restrict__ off, int64_t pairs,
+                          int64_t ahead, const double2* __restrict__ tw, cva_alignment* __restrict__ out,
                           double2* aligned) {
   extern __shared__ __align__(16) char smem[];
   __shared__ double2 red[16];
@@ -362,11 +363,21 @@ __global__ void __launch_bounds__(rs3::kT, 2)
   double2* Z1 = reinterpret_cast<double2*>(smem + kZ1Off);
   double2* Z2 = reinterpret_cast<double2*>(scr);  // B's samples replace the PCR scratch
 
+  // one CTA per pair; the CTA that starts `ahead` pairs later (about one wave
+  // of resident CTAs) finds its raw curves in L2: prefetch them now
   const int64_t p = blockIdx.x;
   const int64_t a0 = off[2 * p], a1 = off[2 * p + 1], b1 = off[2 * p + 2];
   const int na = (int)(a1 - a0), nb = (int)(b1 - a1);
   double2* al = aligned ? aligned + p * N : nullptr;  // null: results only
-  if (threadIdx.x == 0) v2::prefetch_l2(pts + a1, nb * (int)sizeof(double2));
+  if (threadIdx.x == rs3::kT - 32) {  // a thread of the last warp (idle in most phases)
+    v2::prefetch_l2(pts + a1, nb * (int)sizeof(double2));
+    const int64_t q = p + ahead;
+    if (ahead > 0 && q < pairs) {
+      const int64_t c0 = off[2 * q], c2 = off[2 * q + 2];
+      const int64_t cn = c2 - c0 < (1 << 20) ? c2 - c0 : (1 << 20);
+      v2::prefetch_l2(pts + c0, (int)cn * (int)sizeof(double2));
+    }
+  }
   if (na < 4 || nb < 4 || na > rs3::kNMax || nb > rs3::kNMax) {  // validate_curve(c, 4)
     if (threadIdx.x == 0) v2::write_bad(out + p, CVA_INVALID_ARGUMENT);
     if (al)
@@ -385,16 +396,14 @@ __global__ void __launch_bounds__(rs3::kT, 2)
   __syncthreads();
   CVA_MARK(10);
   const rs3::Stats B = rs3::resample_curve<N>(pts + a1, XY, S, scr, Z2, red, nb, 11);
-  const int bad = A.bad | B.bad;
-  const double2 cA = A.centroid, cB = B.centroid;
-  if (bad) {
+  if (A.bad | B.bad) {
     if (threadIdx.x == 0) v2::write_bad(out + p, CVA_INVALID_ARGUMENT);
     if (al)
       for (int l = threadIdx.x; l < N; l += rs3::kT) al[l] = make_double2(v2::qnan(), v2::qnan());
     return;
   }
   __syncthreads();
-  pf::PairIn in{Z1, Z2, cA, cB, 1.0, 1.0};
+  pf::PairIn in{Z1, Z2, A.centroid, B.centroid, 1.0, 1.0};
   pf::pair_stage<false, N, true, 0>(in, reinterpret_cast<double2*>(smem), N, tw, out + p, al, red);
 }
 
@@ -488,6 +497,23 @@ cudaError_t launch_v2_resample_align(const double2* pts, const int64_t* off, int
 bool v3_resample_align_supported(int N) { return N == 512 || N == 1024; }
 int v3_max_raw_nodes() { return rs3::kNMax; }
 
+// One CTA per pair; each prefetches (into L2) the pair one wave of resident
+// CTAs ahead.
+template <int N>
+static cudaError_t launch_v3_n(const double2* pts, const int64_t* off, int64_t pairs, const double2* tw,
+                               cva_alignment* out, double2* aligned, size_t sm, cudaStream_t s) {
+  const void* fn = (const void*)v3::resample_align_kernel<N>;
+  cudaError_t e = set_smem(fn, sm);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, rs3::kT, sm);
+  const int64_t ahead = (int64_t)std::max(1, sms) * std::max(1, per);
+  v3::resample_align_kernel<N><<<(unsigned)pairs, rs3::kT, sm, s>>>(pts, off, pairs, ahead, tw, out, aligned);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_v3_resample_align(const double2* pts, const int64_t* off, int64_t pairs, int N,
                                      const double2* tw, cva_alignment* out, double2* aligned,
                                      cudaStream_t s) {
@@ -497,18 +523,9 @@ cudaError_t launch_v3_resample_align(const double2* pts, const int64_t* off, int
     const char* e = std::getenv("CVA_SMEM_PAD");
     return e ? (size_t)std::strtoul(e, nullptr, 10) : (size_t)0;
   }();
-  if (N == 512) {
-    const size_t sm = v3::smem_bytes<512>() + pad;
-    cudaError_t e = set_smem((const void*)v3::resample_align_kernel<512>, sm);
-    if (e != cudaSuccess) return e;
-    v3::resample_align_kernel<512><<<(unsigned)pairs, rs3::kT, sm, s>>>(pts, off, tw, out, aligned);
-  } else {
-    const size_t sm = v3::smem_bytes<1024>() + pad;
-    cudaError_t e = set_smem((const void*)v3::resample_align_kernel<1024>, sm);
-    if (e != cudaSuccess) return e;
-    v3::resample_align_kernel<1024><<<(unsigned)pairs, rs3::kT, sm, s>>>(pts, off, tw, out, aligned);
-  }
-  return cudaGetLastError();
+  if (pairs <= 0) return cudaSuccess;
+  if (N == 512) return launch_v3_n<512>(pts, off, pairs, tw, out, aligned, v3::smem_bytes<512>() + pad, s);
+  return launch_v3_n<1024>(pts, off, pairs, tw, out, aligned, v3::smem_bytes<1024>() + pad, s);
 }
 
 cudaError_t launch_v2_preprocess(const double2* pts, const int64_t* off, int64_t curves, int n_out,
