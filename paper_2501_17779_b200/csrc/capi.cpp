@@ -184,6 +184,23 @@ int resample_general(const double* points, const int64_t* offsets, int64_t curve
   return finish(e, "preprocess (global slab) launch");
 }
 
+#ifndef CVA_LARGE_TWO_STREAMS
+#define CVA_LARGE_TWO_STREAMS 1
+#endif
+
+// This host thread's side stream on the current device (non-blocking, kept).
+cudaStream_t side_stream() {
+  thread_local std::map<int, cudaStream_t> streams;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  streams[dev] = st;
+  return st;
+}
+
 int large_align(const double* c1, const double* c2, int64_t pairs, int64_t n, int normalize,
                 cva_alignment* out, double* aligned, const double2* tw, cudaStream_t s) {
   // four-step twiddle tables (sub-transform lengths and the two-level W_M)
@@ -195,13 +212,48 @@ int large_align(const double* c1, const double* c2, int64_t pairs, int64_t n, in
     if (int rc = get_twiddles(M / m1, s, &fst.s2)) return rc;
     if (int rc = get_twiddles(M / 256, s, &fst.hi)) return rc;
   }
-  const int64_t chunk = std::min<int64_t>(pairs, cva::large_chunk_pairs((int)n));
-  void* ws = nullptr;
-  if (scratch_alloc(&ws, cva::large_workspace_bytes(chunk, (int)n), s) != cudaSuccess)
-    return fail(CVA_BAD_ALLOC, "large-N workspace allocation failed");
-  cudaError_t e = cva::launch_large_align((const double2*)c1, (const double2*)c2, pairs, (int)n, normalize, tw,
-                                          m1 ? &fst : nullptr, out, (double2*)aligned, ws, chunk, s);
-  cudaFreeAsync(ws, s);
+  // Chunks of pairs alternate between the caller's stream and a side stream
+  // (forked / joined with events), each with its own workspace: the small
+  // tail kernels of chunk c (candidate / pick / aligned output, a few dozen
+  // CTAs) run under the transforms of chunk c + 1. Two chunks in flight share
+  // the L2, so each is half the single-stream chunk.
+  const int64_t full = cva::large_chunk_pairs((int)n);
+  const bool two = CVA_LARGE_TWO_STREAMS && pairs > full / 2 && full >= 2;
+  const int64_t chunk = std::min<int64_t>(pairs, two ? std::max<int64_t>(1, full / 2) : full);
+  void* ws[2] = {nullptr, nullptr};
+  for (int i = 0; i < (two ? 2 : 1); ++i)
+    if (scratch_alloc(&ws[i], cva::large_workspace_bytes(chunk, (int)n), s) != cudaSuccess) {
+      if (ws[0]) cudaFreeAsync(ws[0], s);
+      return fail(CVA_BAD_ALLOC, "large-N workspace allocation failed");
+    }
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaError_t e = cudaSuccess;
+  if (two) {
+    side = side_stream();
+    if (!side || cudaEventCreateWithFlags(&fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&join, cudaEventDisableTiming) != cudaSuccess) {
+      e = cudaErrorUnknown;
+    } else {
+      e = cudaEventRecord(fork, s);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side, fork, 0);
+    }
+  }
+  for (int64_t p0 = 0, c = 0; p0 < pairs && e == cudaSuccess; p0 += chunk, ++c) {
+    const int64_t P = std::min(chunk, pairs - p0);
+    const bool alt = two && (c & 1);
+    e = cva::launch_large_align((const double2*)c1 + p0 * n, (const double2*)c2 + p0 * n, P, (int)n, normalize, tw,
+                                m1 ? &fst : nullptr, out + p0, aligned ? (double2*)aligned + p0 * n : nullptr,
+                                ws[alt ? 1 : 0], chunk, alt ? side : s);
+  }
+  if (two && side) {
+    if (e == cudaSuccess) e = cudaEventRecord(join, side);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, join, 0);
+  }
+  if (fork) cudaEventDestroy(fork);
+  if (join) cudaEventDestroy(join);
+  for (void* w : ws)
+    if (w) cudaFreeAsync(w, s);
   return finish(e, "large-N align launch");
 }
 
