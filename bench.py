@@ -475,6 +475,24 @@ def count_kernels(step):
         return None
 
 
+def graph_of(step):
+    """One step captured as a CUDA graph; returns its replay on the current stream."""
+    import torch
+
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        step()  # warm on the capture stream (first-call setup is not capturable)
+    torch.cuda.current_stream().wait_stream(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        step()
+    torch.cuda.synchronize()
+    graph_of.keep = g
+    return g.replay
+
+
 def wall_max(seconds, world, dist, local):
     import torch
 
@@ -499,7 +517,9 @@ def run_gpu(args):
     dev = torch.device("cuda", local)
     lib = _native.load()
     stream = torch.cuda.current_stream(dev)
-    sptr = stream.cuda_stream
+
+    def cs():  # the current stream at call time (a graph capture switches it)
+        return torch.cuda.current_stream(dev).cuda_stream
     fp64 = ctypes_probe(lib)
     cfg = synth.CONFIGS[args.config]
     strong = args.config == "c1" and args.scaling == "strong"
@@ -521,7 +541,7 @@ def run_gpu(args):
 
         def step():
             _native.check(lib.cva_preprocess_align_batch(dp.data_ptr(), do.data_ptr(), pairs, max_n, N, 1,
-                                                         out.data_ptr(), al.data_ptr(), sptr))
+                                                         out.data_ptr(), al.data_ptr(), cs()))
         units = pairs
         bytes_launch = algorithmic_bytes_c1(offs, p0, p1, N)
         flops_launch = pairs * 3 * 5 * N * math.log2(N)
@@ -545,11 +565,11 @@ def run_gpu(args):
 
         def prep_step():
             _native.check(lib.cva_preprocess_batch(dp.data_ptr(), do.data_ptr(), M, mx, N, 1, prep.data_ptr(), 0,
-                                                   sptr))
+                                                   cs()))
         if world > 1:
             def fill(rb, re, e, k, th):
                 _native.check(lib.cva_allpairs(prep.data_ptr(), M, N, rb, re, e.data_ptr(), k.data_ptr(),
-                                               th.data_ptr(), sptr))
+                                               th.data_ptr(), cs()))
             gat = AllPairsGather(M, fill, chunks=4, dst=0)
 
             def step():
@@ -564,7 +584,7 @@ def run_gpu(args):
             def step():
                 prep_step()
                 _native.check(lib.cva_allpairs(prep.data_ptr(), M, N, 0, M, e.data_ptr(), k.data_ptr(),
-                                               th.data_ptr(), sptr))
+                                               th.data_ptr(), cs()))
             launches_per_step = 2
         units = (r1 - r0) * M
         flops_unit = 5 * N * math.log2(N)
@@ -591,7 +611,7 @@ def run_gpu(args):
         host_fn = lib.cva_preprocess_align_uniform_host if args.config == "c3" else lib.cva_srv_align_batch_host
 
         def step():
-            _native.check(dev_fn(d1.data_ptr(), d2.data_ptr(), P, N, out.data_ptr(), al.data_ptr(), sptr))
+            _native.check(dev_fn(d1.data_ptr(), d2.data_ptr(), P, N, out.data_ptr(), al.data_ptr(), cs()))
         units = P
         bytes_launch = P * (16 * 2 * N + 16 * N + 48)
         bound = "hbm"
@@ -612,9 +632,9 @@ def run_gpu(args):
 
         def step():
             _native.check(lib.cva_preprocess_batch(dp.data_ptr(), do.data_ptr(), M, mx, N, 1, prep.data_ptr(), 0,
-                                                   sptr))
+                                                   cs()))
             _native.check(lib.cva_elastic_distance_matrix(prep.data_ptr(), M, N, 2, 30, 1e-6, 4, 512, d.data_ptr(),
-                                                          sptr))
+                                                          cs()))
         units = M * M  # every rank computes the whole matrix (replicas)
         bound = "fp64ops"
         launches_per_step = 2
@@ -630,7 +650,11 @@ def run_gpu(args):
 
     launches_per_step = count_kernels(step) or launches_per_step
 
-    ms_max, ms_own, clocks = time_steps(step, args.steps, args.warmup, stream, local, world, dist)
+    # multi-kernel steps replay as one CUDA graph (same kernels, no launch gaps);
+    # the NCCL gathers of C2 at N > 1 stay eager
+    use_graph = args.config in ("c2", "c3", "e1") and world == 1
+    timed = graph_of(step) if use_graph else step
+    ms_max, ms_own, clocks = time_steps(timed, args.steps, args.warmup, stream, local, world, dist)
     if args.config == "c1":
         res = cva.decode_results(out)
         assert (res["status"] == 0).all(), "kernel reported invalid pairs"
@@ -711,7 +735,7 @@ def run_gpu(args):
                        "l2": ("inputs larger than L2" if args.config in ("c1", "c3", "c4")
                               else "spectra / curves L2-resident by design")},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
-            "clocks": clocks, "kernels": getattr(count_kernels, "names", None),
+            "clocks": clocks, "kernels": getattr(count_kernels, "names", None), "cuda_graph": use_graph,
         }
         if args.config == "c1":
             line["config"].update({"pairs_per_gpu": units, "N": cfg["N"], "n_in": [300, 3000],
