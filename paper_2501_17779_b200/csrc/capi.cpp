@@ -102,13 +102,6 @@ int check_fft_size(int64_t n) {
   return CVA_OK;
 }
 
-int check_small_fft(int64_t n) {
-  if (int rc = check_fft_size(n)) return rc;
-  if (!small_fft(n))
-    return fail(CVA_UNSUPPORTED, "this entry point's shared-memory kernels cover N <= 2048 "
-                                 "(powers of two) and N <= 1024 otherwise");
-  return CVA_OK;
-}
 
 // Stream-ordered scratch (cudaMallocAsync on the call's stream, freed after the
 // kernels on the same stream): safe for concurrent calls on different streams.
@@ -504,7 +497,7 @@ int cva_srv_align_batch(const double* c1, const double* c2, int64_t pairs, int64
 
 int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_begin, int64_t row_end,
                  double* energy, int32_t* shift, double* theta, void* stream) {
-  if (int rc = check_small_fft(n)) return rc;
+  if (int rc = check_fft_size(n)) return rc;
   if (count < 0 || row_begin < 0 || row_end > count || row_begin > row_end)
     return fail(CVA_INVALID_ARGUMENT, "allpairs: bad row range");
   if (row_end == row_begin || count == 0) return CVA_OK;
@@ -515,6 +508,32 @@ int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_beg
   const int M = cva::v2_fft_len((int)n);
   const double2* tw = nullptr;
   if (int rc = get_twiddles(M, s, &tw)) return rc;
+  if (!small_fft(n)) {
+    // beyond the shared-memory kernels: each row i is a batch of `count` pairs
+    // (curve i, curve j) through the large-N pair path (multi-pass transforms)
+    void* ws = nullptr;
+    const size_t rep = sizeof(double2) * (size_t)(count * n);
+    if (scratch_alloc(&ws, rep + sizeof(cva_alignment) * (size_t)count, s) != cudaSuccess)
+      return fail(CVA_BAD_ALLOC, "scratch allocation failed");
+    double2* row = (double2*)ws;
+    cva_alignment* rec = (cva_alignment*)((char*)ws + rep);
+    int rc = CVA_OK;
+    for (int64_t i = row_begin; i < row_end && rc == CVA_OK; ++i) {
+      const int64_t o = (i - row_begin) * count;
+      cudaError_t e = cva::launch_broadcast_curve((const double2*)curves + i * n, n, count, row, s);
+      if (e != cudaSuccess) {
+        rc = cuda_fail(e, "allpairs broadcast");
+        break;
+      }
+      rc = large_align((const double*)row, curves, count, n, 0, rec, nullptr, tw, s);
+      if (rc == CVA_OK) {
+        e = cva::launch_unpack_row(rec, count, energy + o, shift + o, theta + o, s);
+        if (e != cudaSuccess) rc = cuda_fail(e, "allpairs unpack");
+      }
+    }
+    cudaFreeAsync(ws, s);
+    return rc;
+  }
   if (cva::allpairs_fast_supported((int)n)) {
     // spectra once per curve (kept L2-resident), then one warp per cell
     void* ws = nullptr;
@@ -749,7 +768,7 @@ int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets
 
 int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t row_begin,
                       int64_t row_end, double* energy, int32_t* shift, double* theta) {
-  if (int rc = check_small_fft(n)) return rc;
+  if (int rc = check_fft_size(n)) return rc;
   if (count < 0 || row_begin < 0 || row_end > count || row_begin > row_end)
     return fail(CVA_INVALID_ARGUMENT, "allpairs: bad row range");
   if (int rc = require_device()) return rc;

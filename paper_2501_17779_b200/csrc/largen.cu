@@ -1,3 +1,4 @@
+#include <algorithm>
 // Large-N alignment (BASELINE config C3: N = 65536; any N whose transform
 // length exceeds the shared-memory pair kernels, e.g. the reference tests'
 // N = 4097). A curve is 1 MB at N = 65536, beyond one CTA's shared memory, so
@@ -777,6 +778,22 @@ cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pai
     e = cudaGetLastError();
   }
   return e;
+}
+
+namespace ln {
+__global__ void broadcast_kernel(const double2* __restrict__ c, int64_t n, int64_t copies, double2* __restrict__ out) {
+  const int64_t total = n * copies;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = c[i % n];
+}
+}  // namespace ln
+
+// out[k * n + l] = c[l], k < copies (one row of an all-pairs matrix as a pair batch)
+cudaError_t launch_broadcast_curve(const double2* c, int64_t n, int64_t copies, double2* out, cudaStream_t s) {
+  const int64_t total = n * copies;
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
+  ln::broadcast_kernel<<<(unsigned)std::max<int64_t>(1, blocks), 256, 0, s>>>(c, n, copies, out);
+  return cudaGetLastError();
 }
 
 size_t curve_stats_workspace(int64_t curves) {

@@ -12,6 +12,7 @@ namespace cva {
 // Workspace for `chunk` pairs of N-node curves and the pair count per chunk
 // that keeps the chunk's working set L2-resident.
 size_t large_workspace_bytes(int64_t chunk, int N);
+cudaError_t launch_broadcast_curve(const double2* c, int64_t n, int64_t copies, double2* out, cudaStream_t s);
 int64_t large_chunk_pairs(int N);
 
 // Twiddle tables of the four-step path (4096 <= M <= 65536, M = M1 x M2):

@@ -568,3 +568,25 @@ def test_max_n_in_hint_below_a_curve(cuda, oracle):
                 assert np.abs(out[c] - want[c]).max() <= 1e-11 * np.abs(want[c]).max()
             else:
                 assert np.isnan(out[c]).all()
+
+
+@pytest.mark.parametrize("n", [2049, 3000, 4096])
+def test_allpairs_beyond_shared_memory(cuda, oracle, n):
+    """cva_allpairs for N beyond the shared-memory kernels (rows through the
+    large-N pair path) against align_fft per cell (the reference accepts any N,
+    rigid_align.cpp:18-21)."""
+    rng = np.random.default_rng(n)
+    m = 5
+    t = np.linspace(0, 2 * np.pi, n, endpoint=False)
+    base = np.stack([np.stack([np.cos(t) * (1 + 0.2 * np.cos(3 * t + p)), np.sin(t) * (1 + 0.1 * np.sin(5 * t + p))],
+                              axis=1) for p in rng.uniform(0, 6, m)])
+    base[2] = np.roll(base[0], 777, 0)  # an exact shifted copy
+    e, k, th = cva.allpairs(base, 1, 4)
+    assert e.shape == (3, m)
+    for r in range(3):
+        for j in range(m):
+            want = oracle.align(base[1 + r], base[j])
+            g = np.zeros(1, dtype=_native.ALIGNMENT_DTYPE)[0]
+            g["shift"], g["theta"], g["energy"] = k[r, j], th[r, j], e[r, j]
+            g["trace"], g["t0"] = want["trace"], int(k[r, j]) / n
+            check_pair(g, want, base[1 + r], base[j])
