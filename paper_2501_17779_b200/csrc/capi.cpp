@@ -95,6 +95,9 @@ int smem_limit() {
 constexpr int64_t kMaxLargeN = 1 << 22;
 
 bool small_fft(int64_t n) { return n <= 2048 && cva::v2_fft_len((int)n) <= 2048; }
+// the pair-alignment kernels (launch_v2_align*): shared-memory transforms up to
+// M = 2048, and the 512-thread in-place kernel for M = 4096
+bool pair_fft(int64_t n) { return small_fft(n) || (n <= 4096 && cva::v2_fft_len((int)n) == 4096); }
 
 int check_fft_size(int64_t n) {
   if (n < 4) return fail(CVA_INVALID_ARGUMENT, "align: need at least 4 nodes");
@@ -312,7 +315,7 @@ int cva_align_batch(const double* c1, const double* c2, int64_t pairs, int64_t n
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
   if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
-  if (!small_fft(n)) return large_align(c1, c2, pairs, n, 0, out, aligned, tw, s);
+  if (!pair_fft(n)) return large_align(c1, c2, pairs, n, 0, out, aligned, tw, s);
   return finish(cva::launch_v2_align((const double2*)c1, (const double2*)c2, pairs, (int)n, tw,
                                      out, (double2*)aligned, s),
                 "align launch");
@@ -447,7 +450,7 @@ int cva_preprocess_align_uniform(const double* c1, const double* c2, int64_t pai
   cudaStream_t s = (cudaStream_t)stream;
   const double2* tw = nullptr;
   if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
-  if (!small_fft(n)) return large_align(c1, c2, pairs, n, 1, out, aligned, tw, s);
+  if (!pair_fft(n)) return large_align(c1, c2, pairs, n, 1, out, aligned, tw, s);
   // shared-memory path: per-curve stats, then the pair kernel normalising on load
   void* ws = nullptr;
   const size_t nb = sizeof(double4) * (size_t)(2 * pairs), bb = sizeof(int32_t) * (size_t)(2 * pairs);
@@ -508,7 +511,7 @@ int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_beg
   const int M = cva::v2_fft_len((int)n);
   const double2* tw = nullptr;
   if (int rc = get_twiddles(M, s, &tw)) return rc;
-  if (!small_fft(n)) {
+  if (!pair_fft(n)) {
     // beyond the shared-memory kernels: each row i is a batch of `count` pairs
     // (curve i, curve j) through the large-N pair path (multi-pass transforms)
     void* ws = nullptr;

@@ -213,6 +213,40 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
                           aligned ? aligned + p * N : nullptr, red);
 }
 
+// align_fft for transform length M = 4096 (non-power-of-two N in (1024, 2048],
+// zero-padded per pairfft.cuh fft_len, and N = 4096): 512 threads, one CTA per
+// SM, the two forward transforms in place on 256-thread halves, the
+// correlation transform in place on all 512 (147 KB of shared memory).
+// Same parameters as align_kernel.
+constexpr int kT4 = 512;
+__global__ void __launch_bounds__(kT4, 1)
+    align4k_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
+                   int64_t stride1, int64_t stride2, const double2* __restrict__ tw,
+                   cva_alignment* __restrict__ out, double2* aligned, const double4* __restrict__ norm1,
+                   const double4* __restrict__ norm2, const int32_t* __restrict__ bad1,
+                   const int32_t* __restrict__ bad2) {
+  extern __shared__ __align__(16) char smem[];
+  __shared__ double2 red[32];
+  static_assert(pf::plan_is_128<kT4>(4096), "the 512-thread plan reads the 128-thread tables");
+  const int64_t p = blockIdx.x;
+  pf::PairIn in{c1 + p * stride1, c2 + p * stride2, make_double2(0, 0), make_double2(0, 0), 1.0, 1.0};
+  if (norm1) {
+    if (bad1[p] || bad2[p]) {
+      if (threadIdx.x == 0) write_bad(out + p, CVA_INVALID_ARGUMENT);
+      if (aligned)
+        for (int l = threadIdx.x; l < N; l += kT4) aligned[p * N + l] = make_double2(qnan(), qnan());
+      return;
+    }
+    const double4 a = norm1[p], b = norm2[p];
+    in.g1 = make_double2(a.x, a.y);
+    in.sc1 = a.z;
+    in.g2 = make_double2(b.x, b.y);
+    in.sc2 = b.z;
+  }
+  pf::pair_stage<true, 0, false, 0, kT4, 4096>(in, reinterpret_cast<double2*>(smem), N, tw, out + p,
+                                                aligned ? aligned + p * N : nullptr, red);
+}
+
 // ------------------------------------------------------------------- SRV
 
 // SRV alignment (srv_transform -> srv_center -> align_fft, the (t0,R) step of
@@ -441,6 +475,13 @@ static cudaError_t launch_align_kernel(unsigned grid, size_t sm, cudaStream_t s,
                                        const double2* c2, int N, int64_t st1, int64_t st2, const double2* tw,
                                        cva_alignment* out, double2* aligned, const double4* n1, const double4* n2,
                                        const int32_t* b1, const int32_t* b2) {
+  if (pf::fft_len(N) == 4096) {
+    const size_t sm4 = 2 * sizeof(double2) * (size_t)pf::padded_len(4096);
+    cudaError_t e = set_smem((const void*)v2::align4k_kernel, sm4);
+    if (e != cudaSuccess) return e;
+    v2::align4k_kernel<<<grid, v2::kT4, sm4, s>>>(c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
+    return cudaGetLastError();
+  }
   switch (N) {
     case 2048: return launch_align_n<2048>(grid, sm, s, c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);
     case 1024: return launch_align_n<1024>(grid, sm, s, c1, c2, N, st1, st2, tw, out, aligned, n1, n2, b1, b2);

@@ -229,7 +229,7 @@ cudaError_t launch_tw_init(double2* tw, int N, cudaStream_t s) {
 }
 
 int twiddle_extra(int N) {
-  return (N >= 4 && N <= 2048 && (N & (N - 1)) == 0) ? pf::ptw_len(N) : 0;
+  return (N >= 4 && N <= 4096 && (N & (N - 1)) == 0) ? pf::ptw_len(N) : 0;
 }
 
 cudaError_t launch_preprocess_resample(const double2* pts, const int64_t* off, int64_t curves,

@@ -112,6 +112,14 @@ __host__ __device__ constexpr int ptw_len(int N) {
   return ptw_until<128>(N, N) + ptw_until<256>(N, N) + ptw_until_warp(N, N);
 }
 template <int NT>
+__host__ __device__ constexpr bool plan_is_128(int N) {
+  for (int Ns = 1; Ns < N; Ns *= plan_radix<128>(N, Ns))
+    if (plan_radix<128>(N, Ns) != plan_radix<NT>(N, Ns)) return false;
+  return true;
+}
+// NT = 512 (the M = 4096 pair kernel) reads the 128-thread plan's tables, which
+// its radix sequence must equal (checked where it is used)
+template <int NT>
 __host__ __device__ constexpr int ptw_off(int N, int Ns) {
   return NT == 256 && !plan256_is_128(N) ? N + ptw_until<128>(N, N) + ptw_until<256>(N, Ns)
                                          : N + ptw_until<128>(N, Ns);
@@ -213,6 +221,7 @@ __device__ __forceinline__ void pass_ip(Src src, double2* buf, const double2* __
   // the 8, 8, 8, 4 sequence is also the 128- and 256-thread plan of M = 2048,
   // so the pass twiddle tables of ptw_off apply
   static_assert(R == plan_radix<NT>(M, Ns), "in-place sequence must match the table plan");
+  static_assert(NT == 128 || NT == 256 || plan_is_128<NT>(M), "pass twiddle tables exist for this plan");
   const double2* __restrict__ pt = tw + ptw_off<NT>(M, Ns);
   double2 v[B][R];
 #pragma unroll
@@ -237,6 +246,18 @@ __device__ __forceinline__ void pass_ip(Src src, double2* buf, const double2* __
     for (int r = 0; r < R; ++r) buf[pad(base + r * Ns)] = v[b][dft_slot<R>(r)];
   }
   sync();
+}
+
+// In-place transform of compile-time length M by NT threads with the table
+// plan (plan_radix<NT>): M = 2048 gives 8, 8, 8, 4, M = 4096 8, 8, 8, 8.
+template <int NT, int M, int Ns = 1, typename Src, typename Sync>
+__device__ __forceinline__ void fft_ip_ct(Src src, double2* buf, const double2* __restrict__ tw, int g, Sync sync) {
+  constexpr int R = plan_radix<NT>(M, Ns);
+  pass_ip<R, NT, M, Ns>(src, buf, tw, g, sync);
+  if constexpr (Ns * R < M) {
+    auto next = [buf](int i) { return buf[pad(i)]; };
+    fft_ip_ct<NT, M, Ns * R>(next, buf, tw, g, sync);
+  }
 }
 
 template <int NT, typename Src, typename Sync>
@@ -296,8 +317,9 @@ __host__ __device__ inline int fft_len(int N) {
 // Runs the pair stage. bufs: 4 * padded_len(M) double2 of shared memory (distinct from
 // the inputs), M = fft_len(N), tw the length-M twiddle table. out: this pair's
 // result (written by thread 0). aligned: this pair's aligned curve (may alias
-// in.z2: all reads happen before any write). red: >= 16 double2 shared.
-// Requires blockDim.x == 256, N >= 4, M <= 2048.
+// in.z2: all reads happen before any write). red: >= kCT / 16 double2 shared.
+// Requires blockDim.x == kCT (256, or 512 for the in-place M = 4096 kernel),
+// N >= 4, M <= 2048 (M = kIPM with kInPlace).
 // kInPlace: 2 * padded_len(M) buffers instead of 4; requires M == 2048.
 // kN: compile-time N (a power of two) or 0 for a runtime N.
 // kLenOnLoad: in.sc1 / in.sc2 are ignored; each curve's polygon length is
@@ -307,12 +329,13 @@ __host__ __device__ inline int fft_len(int N) {
 // is not finite and > 0 marks the pair invalid (preprocess: curve.cpp:41-48).
 // kPad: 1 = in.z1 is shared memory in the padded layout z1[l + (l >> 3)]
 // (the resampler's and the transform buffers' layout); 2 = in.z1 and in.z2 both.
-template <bool kInPlace = false, int kN = 0, bool kLenOnLoad = false, int kPad = 0>
+template <bool kInPlace = false, int kN = 0, bool kLenOnLoad = false, int kPad = 0, int kCT = kT, int kIPM = 2048>
 __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
                                   const double2* __restrict__ tw, cva_alignment* out,
                                   double2* aligned, double2* red) {
   const int t = threadIdx.x;
-  const int grp = t / kHalf, g = t % kHalf;
+  constexpr int kH = kCT / 2;  // threads per forward transform
+  const int grp = t / kH, g = t % kH;
   if constexpr (kN > 0) N = kN;
   const int M = kN > 0 ? kN : fft_len(N);
   const int NP = padded_len(M);
@@ -350,28 +373,28 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       }
       return z;
     };
-    auto sync = [grp]() { named_sync(1 + grp, kHalf); };
+    auto sync = [grp]() { named_sync(1 + grp, kH); };
     if constexpr (kInPlace) {
-      fft2048_ip<kHalf>(load, grp == 0 ? B0 : B2, tw, g, sync);
+      fft_ip_ct<kH, kIPM>(load, grp == 0 ? B0 : B2, tw, g, sync);
       X = grp == 0 ? B0 : B2;
     } else {
       if constexpr (kN > 0)
-        X = group_fft_ct<kHalf, kN>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, tw, g, sync);
+        X = group_fft_ct<kH, kN>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, tw, g, sync);
       else
-        X = group_fft<kHalf>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, M, tw, g, sync);
+        X = group_fft<kH>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, M, tw, g, sync);
     }
   }
   PairScale psc{in.sc1, in.sc2};
   if constexpr (kLenOnLoad) {
-    __shared__ double s_len[kT / 32];
+    __shared__ double s_len[kCT / 32];
     len = warp_sum(len);
     if ((t & 31) == 0) s_len[t >> 5] = len;
     __syncthreads();
     double l1 = 0.0, l2 = 0.0;
 #pragma unroll
-    for (int w = 0; w < kT / 64; ++w) {
+    for (int w = 0; w < kCT / 64; ++w) {
       l1 += s_len[w];
-      l2 += s_len[kT / 64 + w];
+      l2 += s_len[kCT / 64 + w];
     }
     if (!(l1 > 0.0) || !isfinite(l1) || !(l2 > 0.0) || !isfinite(l2)) {  // curve.cpp:44-46
       if (t == 0) {
@@ -385,7 +408,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       }
       if (aligned != nullptr) {
         __syncthreads();  // in.z2 may alias `aligned`
-        for (int l = t; l < N; l += kT) aligned[l] = make_double2(qnan(), qnan());
+        for (int l = t; l < N; l += kCT) aligned[l] = make_double2(qnan(), qnan());
       }
       return;
     }
@@ -406,7 +429,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       const double2 v = cmulconj(X1[pad(k)], X2[pad(k)]);
       return kLenOnLoad ? cscale(v, s12) : v;
     };
-    fft2048_ip<kT>(prod, B0, tw, t, sync_all);
+    fft_ip_ct<kCT, kIPM>(prod, B0, tw, t, sync_all);
     F = B0;
   } else {
     // group 0's result is B0 or B1, group 1's is B2 or B3 (same pass count)
@@ -421,9 +444,9 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       return kLenOnLoad ? cscale(v, s12) : v;
     };
     if constexpr (kN > 0)
-      F = group_fft_ct<kT, kN>(prod, F0, F1, tw, t, sync_all);
+      F = group_fft_ct<kCT, kN>(prod, F0, F1, tw, t, sync_all);
     else
-      F = group_fft<kT>(prod, F0, F1, M, tw, t, sync_all);
+      F = group_fft<kCT>(prod, F0, F1, M, tw, t, sync_all);
   }
 
   CVA_MARK(21);
@@ -438,7 +461,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   double best2 = -1.0;
 #pragma unroll
   for (int q = 0; q < kMaxPer; ++q) {
-    const int k = t + q * kT;
+    const int k = t + q * kCT;
     mag2[q] = -1.0;
     if (k < N) {
       const double2 f = F[pad(k)];
@@ -457,16 +480,16 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   }
   if (lane == 0) {
     red[wid] = make_double2(best2, s1);
-    red[8 + wid].x = s2;
+    red[kCT / 32 + wid].x = s2;
   }
   __syncthreads();
   best2 = -1.0;
   s1 = s2 = 0.0;
 #pragma unroll
-  for (int w = 0; w < kT / 32; ++w) {
+  for (int w = 0; w < kCT / 32; ++w) {
     best2 = fmax(best2, red[w].x);
     s1 += red[w].y;
-    s2 += red[8 + w].x;
+    s2 += red[kCT / 32 + w].x;
   }
   if constexpr (kLenOnLoad) {  // sums of |z - c|^2 -> of |(z - c) / len|^2
     s1 *= psc.sc1 * psc.sc1;
@@ -479,15 +502,15 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   int cand = INT_MAX;
 #pragma unroll
   for (int q = kMaxPer - 1; q >= 0; --q)
-    if (mag2[q] >= thr2 && t + q * kT < N) cand = t + q * kT;  // smallest k of this thread
+    if (mag2[q] >= thr2 && t + q * kCT < N) cand = t + q * kCT;  // smallest k of this thread
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
-  __shared__ int s_cand[8];
+  __shared__ int s_cand[kCT / 32];
   if (lane == 0) s_cand[wid] = cand;
   __syncthreads();
   int m = INT_MAX;
 #pragma unroll
-  for (int w = 0; w < kT / 32; ++w) m = min(m, s_cand[w]);
+  for (int w = 0; w < kCT / 32; ++w) m = min(m, s_cand[w]);
   const bool ok = isfinite(best) && best2 >= 0.0 && m != INT_MAX;
   // rotation straight from D_m: (cos, sin) = (Re D, Im D) / |D| (every thread)
   double2 rot = make_double2(qnan(), qnan());
@@ -512,7 +535,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     const double sc = psc.sc2;
 #pragma unroll
     for (int q = 0; q < kMaxPer; ++q) {
-      const int j = t + q * kT;
+      const int j = t + q * kCT;
       if (j < N) {
         const double2 z = in.srv2 ? srv_at(in.srv2, j, N) : in.z2[kPad == 2 ? j + (j >> 3) : j];
         const double2 p = make_double2((z.x - c.x) * sc, (z.y - c.y) * sc);
@@ -523,7 +546,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     const int mm = ok ? m : 0;
 #pragma unroll
     for (int q = 0; q < kMaxPer; ++q) {
-      const int j = t + q * kT;
+      const int j = t + q * kCT;
       if (j < N) {
         int l = j - mm;
         if (l < 0) l += N;

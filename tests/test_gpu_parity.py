@@ -103,7 +103,7 @@ def test_random_pairs_match_reference(cuda, n):  # test_rigid_align.cpp:133-151
     check_pair(res[0], g[f"rand{n}_res_naive"][0], a, b)
 
 
-@pytest.mark.parametrize("n", [4, 5, 6, 7, 9, 33, 37, 48, 60, 96, 100, 127, 255, 256, 257, 1000, 1023, 2048])
+@pytest.mark.parametrize("n", [4, 5, 6, 7, 9, 33, 37, 48, 60, 96, 100, 127, 255, 256, 257, 1000, 1023, 1025, 2000, 2047, 2048])
 def test_any_n_matches_oracle(cuda, oracle, n):
     """Any N >= 4 (the reference's FFTW path takes any length; its
     tests use N = 20, 33, 40, 48, 60, 96, 100, 101, 127, 255): non-powers of two
