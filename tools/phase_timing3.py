@@ -30,8 +30,8 @@ for it in range(3):
                                                  al.data_ptr(), s))
 torch.cuda.synchronize()
 t = prof.cpu().numpy().astype(np.float64)
-names = {0: "start", 1: "load A", 2: "A arc length", 3: "A phase1", 4: "A pcr", 5: "A p3+map", 6: "A eval+sum",
-         10: "load B", 11: "B arc length", 12: "B phase1", 13: "B pcr", 14: "B p3+map", 15: "B eval+sum",
+names = {0: "start", 1: "load A", 2: "A sweep+scan", 3: "A xchg", 4: "A pcr", 5: "A p3+map", 6: "A eval+sum",
+         10: "load B", 11: "B sweep+scan", 12: "B xchg", 13: "B pcr", 14: "B p3+map", 15: "B eval+sum",
          20: "2 FFTs", 21: "3rd FFT", 23: "argmax+aligned out"}
 order = [0, 1, 2, 3, 4, 5, 6, 10, 11, 12, 13, 14, 15, 20, 21, 23]
 tot = 0
@@ -41,8 +41,8 @@ for a, b in zip(order, order[1:]):
     print(f"{names[b]:20s} {d.mean():9.0f} cycles (p50 {np.median(d):8.0f})")
 print(f"{'total':20s} {tot:9.0f} cycles per CTA; n_in mean {np.diff(offs).mean():.0f}")
 
-sub = [(1, 30, "A p0 edges"), (30, 32, "A p0 scan+div"), (32, 33, "A p0 knots"), (33, 2, "A p0 barrier"),
-       (2, 34, "A p1 loop"), (34, 3, "A p1 xchg barrier"), (4, 37, "A p3 fwd"), (37, 38, "A p3 bwd"),
+sub = [(1, 34, "A merged sweep"), (34, 2, "A scan+knots"), (2, 3, "A xchg barrier"), (4, 37, "A p3 fwd"),
+       (37, 38, "A p3 bwd"),
        (38, 5, "A p3 barrier"), (5, 35, "A map scan"), (35, 36, "A eval"), (36, 6, "A block sum")]
 print("-- curve A sub-phases (thread 0's clock)")
 for a, b, nm in sub:
