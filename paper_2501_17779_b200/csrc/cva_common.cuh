@@ -54,13 +54,14 @@ __device__ __forceinline__ double fsqrt(double x) {
 
 // sqrt without the zero / negative select (no branch in the SASS): x == 0 or
 // x = inf give NaN (MUFU seed inf / 0); callers test the argument or result.
+// x times the refined rsqrt (~2^-56): within ~1 ulp, no Heron step (used for
+// polygon lengths, sums of many edges).
 __device__ __forceinline__ double fsqrt_nb(double x) {
   double r;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
   const double e = fma(-x * r, r, 1.0);
   r = fma(r * e, fma(0.375, e, 0.5), r);
-  const double y = x * r;
-  return fma(fma(-y, y, x), 0.5 * r, y);
+  return x * r;
 }
 
 // --------------------------------------------------------------- reductions
