@@ -222,7 +222,10 @@ int cva_dp_reparam_batch_host(const double* q1, const double* q2, int64_t pairs,
  * iterations, converged, status, energy_trace (nullable, pairs x (max_iters+1):
  * ElasticMatch::energy_trace, NaN after the last iteration). The GPU always uses the FFT correlation
  * (use_fft = true); ElasticOptions defaults: max_iters 30, energy_tol 1e-6,
- * max_slope 4. Supports 8 <= n <= 1024 (non-powers of two <= 512). */
+ * max_slope 4. Supports 8 <= n <= 2^20 and 1 <= max_slope <= 20; n <= 1024
+ * (non-powers of two <= 512) with max_slope <= 8 run the shared-memory
+ * kernels, anything else slab mode (per-CTA global working set, direct
+ * correlation for the rigid steps). */
 int cva_elastic_approach2_batch(const double* c1, const double* c2, int64_t pairs, int64_t n,
                                 int max_iters, double energy_tol, int max_slope, double* distance,
                                 double* energy, double* t0, double* theta, double* gamma,

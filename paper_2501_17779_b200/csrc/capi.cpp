@@ -850,8 +850,8 @@ int check_elastic(int64_t pairs, int64_t n, int max_slope, const char* what) {
   if (max_slope < 1) return fail(CVA_INVALID_ARGUMENT, "dp: max_slope must be >= 1");  // srv.cpp:131
   if (n > 1 << 20 || !cva::elastic_supported((int)n, max_slope))
     return fail(CVA_UNSUPPORTED, std::string(what) +
-                                     ": supported sizes are 8 <= n <= 1024 (powers of two; other n <= 512), "
-                                     "max_slope <= 8");
+                                     ": supported sizes are 8 <= n <= 2^20 and max_slope <= 20 (beyond 20 the "
+                                     "reference's 8-bit parent indices wrap)");
   return CVA_OK;
 }
 
@@ -885,8 +885,9 @@ int cva_dp_reparam_batch(const double* q1, const double* q2, int64_t pairs, int6
 
 static int elastic_launch(const double* A, const double* B, int64_t pairs, int64_t k, int64_t n, int max_iters,
                           double energy_tol, int max_slope, const cva::ElasticOut& o, cudaStream_t s) {
-  const double2* tw = nullptr;
-  if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
+  const double2* tw = nullptr;  // slab mode aligns by the direct correlation (no transform)
+  if (!cva::elastic_slab_mode((int)n, max_slope))
+    if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
   const int grid = cva::elastic_grid(pairs, (int)n, max_slope);
   Slab slab;
   slab.s = s;

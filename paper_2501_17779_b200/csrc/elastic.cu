@@ -37,7 +37,8 @@ namespace el {
 
 constexpr int kT = 256;
 constexpr double kGridSnap = 1e-9;  // srv.cpp:14
-constexpr int kMaxSteps = 64;
+constexpr int kMaxSteps = 64;   // shared step table (W <= 8: 43 steps)
+constexpr int kMaxSlope = 20;   // 255 steps: parent indices stay below the 0xff sentinel (srv.cpp:222)
 #ifndef CVA_EL_MINB
 #define CVA_EL_MINB 2
 #endif
@@ -178,10 +179,19 @@ __host__ __device__ constexpr Steps make_steps(int W) {
 // Per-step constants of dp_step_cost, formed once per CTA with the reference's
 // operations: sq = sqrt((double)b / a) and the interpolation offsets
 // (double)(k b) / a, so the per-cell work has no division or square root.
+// StepTab: shared-memory table for W <= 8; StepView: the table the DP reads,
+// either that one or a per-CTA global table (slab mode, W up to kMaxSlope).
 struct StepTab {
   double sq[kMaxSteps];
   double fr[kMaxSteps][9];
   int a[kMaxSteps], b[kMaxSteps];
+};
+struct StepView {
+  double* sq;
+  double* fr;  // count x frs
+  int frs;
+  int* a;
+  int* b;
 };
 
 // dp_step_cost (srv.cpp:145-176) with q1, q2 in shared memory. sq, fr: the
@@ -321,7 +331,7 @@ __device__ __forceinline__ double2 scaled_interior(const double2* q2w, const dou
 // row. Further columns (n >= kT) take the window path.
 template <int kW, bool kPow2, bool kCached>
 __device__ __forceinline__ void dp_cell(const double2* q2, int n, int i, int j, const double2* q1w,
-                                        const double* const* prv, const double2* Sc, const StepTab& tab,
+                                        const double* const* prv, const double2* Sc, const double* sqt,
                                         double inv_n, double* cur, uint8_t* par) {
   constexpr Steps kS = make_steps(kW);
   constexpr FrTab kF = make_fr(kW);
@@ -348,7 +358,7 @@ __device__ __forceinline__ void dp_cell(const double2* q2, int n, int i, int j, 
   for (int s = 0; s < kS.count; ++s) {
     const int a = kS.a[s], b = kS.b[s];
     const double base = (i - a < 0 || j - b < 0) ? inf : prv[a][max(j - b, 0)];
-    const double sq = tab.sq[s];
+    const double sq = sqt[s];
     double cost = 0.0;
 #pragma unroll
     for (int k = 0; k <= a; ++k) {
@@ -379,7 +389,7 @@ __device__ __forceinline__ void dp_cell(const double2* q2, int n, int i, int j, 
 
 template <int kW, bool kPow2>
 __device__ __forceinline__ void dp_rows_hoisted(const double2* q1, const double2* q2, int n, double* ring,
-                                                uint8_t* parent, const StepTab& tab, double inv_n) {
+                                                uint8_t* parent, const double* sqt, double inv_n) {
   constexpr Steps kS = make_steps(kW);
   constexpr FrTab kF = make_fr(kW);
   constexpr OffTab kO = make_off(kW);
@@ -396,7 +406,7 @@ __device__ __forceinline__ void dp_rows_hoisted(const double2* q1, const double2
 #pragma unroll
       for (int k = 1; k < kS.a[s]; ++k)
         Sc[kO.v[s] + k - 1] =
-            scaled_interior(q2w, dq, jd, kS.b[s], kS.b[s] - (k * kS.b[s]) / kS.a[s], kF.fr[s][k], tab.sq[s]);
+            scaled_interior(q2w, dq, jd, kS.b[s], kS.b[s] - (k * kS.b[s]) / kS.a[s], kF.fr[s][k], sqt[s]);
   }
   int ri = 0;  // i % (kW + 1)
   for (int i = 1; i <= n; ++i) {
@@ -418,33 +428,36 @@ __device__ __forceinline__ void dp_rows_hoisted(const double2* q1, const double2
         cur[j] = inf;
         par[j] = 0xff;
       } else if (j == jc) {
-        dp_cell<kW, kPow2, true>(q2, n, i, j, q1w, prv, Sc, tab, inv_n, cur + j, par + j);
+        dp_cell<kW, kPow2, true>(q2, n, i, j, q1w, prv, Sc, sqt, inv_n, cur + j, par + j);
       } else {
-        dp_cell<kW, kPow2, false>(q2, n, i, j, q1w, prv, Sc, tab, inv_n, cur + j, par + j);
+        dp_cell<kW, kPow2, false>(q2, n, i, j, q1w, prv, Sc, sqt, inv_n, cur + j, par + j);
       }
     }
     __syncthreads();
   }
 }
 
-// dp_reparam (srv.cpp:180-257) on shared q1, q2 (n samples). ring: (W+1) x
-// (n+1) doubles; parent: (n+1)^2 bytes (shared or global); gamma: n+1.
-// Returns the path energy (thread-uniform); +inf if no admissible path.
+// dp_reparam (srv.cpp:180-257) on q1, q2 (n samples; shared memory, or the
+// CTA's global slab in slab mode). ring: (W+1) x (n+1) doubles; parent:
+// (n+1)^2 bytes (shared or global); gamma: n+1. gtab: null = the shared step
+// table (W <= 8), else a global StepView with room for W's steps. Returns the
+// path energy (thread-uniform); +inf if no admissible path.
 template <int kW>
 __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wrt, double* ring,
-                             uint8_t* parent, double* gamma, double* cell) {
+                             uint8_t* parent, double* gamma, double* cell, const StepView* gtab = nullptr) {
   const int W = kW > 0 ? kW : Wrt;
   const int stride = n + 1;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   const double inv_n = (n & (n - 1)) == 0 ? dvd(1.0, (double)n) : 0.0;
-  __shared__ StepTab tab;
+  __shared__ StepTab stab;
+  const StepView tab = gtab ? *gtab : StepView{stab.sq, &stab.fr[0][0], 9, stab.a, stab.b};
   {
     int s = 0;
     for (int a = 1; a <= W; ++a)
       for (int b = 1; b <= W; ++b)
         if (gcd_i(a, b) == 1) {
           if (threadIdx.x == s) {
-            step_consts(a, b, &tab.sq[s], tab.fr[s]);
+            step_consts(a, b, &tab.sq[s], tab.fr + (size_t)s * tab.frs);
             tab.a[s] = a;
             tab.b[s] = b;
           }
@@ -456,9 +469,9 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
   __syncthreads();
   if constexpr (kW > 0) {
     if (inv_n != 0.0)
-      dp_rows_hoisted<kW, true>(q1, q2, n, ring, parent, tab, inv_n);
+      dp_rows_hoisted<kW, true>(q1, q2, n, ring, parent, tab.sq, inv_n);
     else
-      dp_rows_hoisted<kW, false>(q1, q2, n, ring, parent, tab, inv_n);
+      dp_rows_hoisted<kW, false>(q1, q2, n, ring, parent, tab.sq, inv_n);
   } else
   for (int i = 1; i <= n; ++i) {
     const int lo = jmin_of(i, n, W), hi = jmax_of(i, n, W);
@@ -472,7 +485,8 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
           if (pi < 0 || pj < 0) return;
           const double base = row(pi)[pj];
           if (base == inf) return;
-          const double cand = add(base, step_cost_t(q1, q2, n, pi, pj, a, b, tab.sq[s], tab.fr[s], inv_n));
+          const double cand =
+              add(base, step_cost_t(q1, q2, n, pi, pj, a, b, tab.sq[s], tab.fr + (size_t)s * tab.frs, inv_n));
           if (cand < best) {
             best = cand;
             best_s = (uint8_t)s;
@@ -525,7 +539,7 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
         }
         const int pi = i - a, pj = j - b;
         pp -= (size_t)a * stride + b;
-        for (int k = 0; k < a; ++k) gamma[pi + k] = __longlong_as_double(((long long)pj << 10) | (s << 4) | k);
+        for (int k = 0; k < a; ++k) gamma[pi + k] = __longlong_as_double(((long long)pj << 16) | (s << 8) | k);
         i = pi;
         j = pj;
       }
@@ -537,7 +551,7 @@ __device__ double dp_reparam(const double2* q1, const double2* q2, int n, int Wr
   if (r != inf) {
     for (int l = threadIdx.x; l < n; l += kT) {
       const long long code = __double_as_longlong(gamma[l]);
-      const int k = (int)(code & 15), s = (int)((code >> 4) & 63), pj = (int)(code >> 10);
+      const int k = (int)(code & 255), s = (int)((code >> 8) & 255), pj = (int)(code >> 16);
       const int a = tab.a[s], b = tab.b[s];
       const double jj = add((double)pj, dvd((double)(k * b), (double)a));
       gamma[l] = l == 0 ? 0.0 : dvd(jj, (double)n);
@@ -596,10 +610,13 @@ struct Smem {
 
 __host__ __device__ inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
-// Layout shared by the host size query and the kernel.
-__host__ __device__ inline size_t smem_layout(int n, int W, bool parent_in_smem, char* base, Smem* S) {
+// Layout shared by the host size query and the kernel. Slab mode (fft ==
+// false): the same arrays in the CTA's global slab, without the transform
+// buffers (the rigid steps run the direct correlation, align_direct).
+__host__ __device__ inline size_t smem_layout(int n, int W, bool parent_in_smem, char* base, Smem* S,
+                                              bool fft_bufs = true) {
   const int M = pf::fft_len(n);
-  const size_t fft = 4 * sizeof(double2) * (size_t)pf::padded_len(M);
+  const size_t fft = fft_bufs ? 4 * sizeof(double2) * (size_t)pf::padded_len(M) : 0;
   const size_t dp = align_up(sizeof(double) * (size_t)(W + 1) * (n + 1)) +
                     (parent_in_smem ? align_up((size_t)(n + 1) * (n + 1)) : 0);
   const size_t scratch = fft > dp ? fft : dp;
@@ -642,24 +659,193 @@ __host__ __device__ inline size_t smem_layout(int n, int W, bool parent_in_smem,
   return off;
 }
 
+// Slab mode (n or W beyond the shared-memory kernels): every per-pair array,
+// the dp ring, the parent matrix and the step table live in a per-CTA slab of
+// global memory (L2-resident for moderate n); shared memory keeps only the
+// reduction cells. Returns the slab bytes per CTA.
+__host__ __device__ inline int step_count(int W) {
+  int c = 0;
+  for (int a = 1; a <= W; ++a)
+    for (int b = 1; b <= W; ++b) c += gcd_i(a, b) == 1;
+  return c;
+}
+__host__ __device__ inline size_t slab_layout(int n, int W, char* base, Smem* S, uint8_t** parent, StepView* tv,
+                                              double2** D) {
+  size_t off = smem_layout(n, W, false, base, S, false);
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += align_up(bytes);
+    return base ? base + o : nullptr;
+  };
+  const int cnt = step_count(W);
+  char* par = take((size_t)(n + 1) * (n + 1));
+  char* d = take(sizeof(double2) * (size_t)n);
+  char* sq = take(sizeof(double) * cnt);
+  char* fr = take(sizeof(double) * (size_t)cnt * (W + 1));
+  char* a = take(sizeof(int) * cnt);
+  char* b = take(sizeof(int) * cnt);
+  if (base) {
+    *parent = (uint8_t*)par;
+    *D = (double2*)d;
+    *tv = StepView{(double*)sq, (double*)fr, W + 1, (int*)a, (int*)b};
+  }
+  return off;
+}
+
+// align_fft(a, b) (rigid_align.cpp:204-208) by the direct correlation: D_m =
+// sum_l conj(a_l) b_{(l+m) mod n} for every shift m, each thread summing its
+// shifts in order of l, then the pair stage's selection on |D_m| (max, the
+// reference's tie band, smallest shift in the band; theta = arg D_m). Used in
+// slab mode, where n is past the shared-memory transforms and the DP costs
+// O(n^2 W^2) per iteration anyway. D: n double2 of scratch.
+__device__ cva_alignment align_direct(const double2* a, const double2* b, int n, double2* D, double2* red) {
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  double s1 = 0.0, s2 = 0.0;
+  for (int l = t; l < n; l += kT) {
+    s1 = fma(a[l].x, a[l].x, fma(a[l].y, a[l].y, s1));
+    s2 = fma(b[l].x, b[l].x, fma(b[l].y, b[l].y, s2));
+  }
+  constexpr int kB = 4;  // shifts per pass of a thread: one read of a_l feeds kB products
+  double best2 = -1.0;
+  for (int m0 = t; m0 < n; m0 += kB * kT) {
+    double2 acc[kB];
+    int j[kB];
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      acc[q] = make_double2(0.0, 0.0);
+      j[q] = m0 + q * kT;
+      if (j[q] >= n) j[q] -= n;  // padding lanes (discarded) stay in range
+    }
+    for (int l = 0; l < n; ++l) {
+      const double2 x = a[l];
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+        const double2 y = b[j[q]];
+        acc[q].x = fma(x.x, y.x, fma(x.y, y.y, acc[q].x));
+        acc[q].y = fma(x.x, y.y, fma(-x.y, y.x, acc[q].y));
+        j[q] = j[q] + 1 == n ? 0 : j[q] + 1;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kB; ++q) {
+      const int m = m0 + q * kT;
+      if (m < n) {
+        D[m] = acc[q];
+        best2 = fmax(best2, fma(acc[q].x, acc[q].x, acc[q].y * acc[q].y));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    best2 = fmax(best2, __shfl_xor_sync(0xffffffffu, best2, o));
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  __shared__ double r3[3][kT / 32];
+  __shared__ int s_cand[kT / 32];
+  if (lane == 0) {
+    r3[0][wid] = best2;
+    r3[1][wid] = s1;
+    r3[2][wid] = s2;
+  }
+  __syncthreads();
+  best2 = -1.0;
+  s1 = s2 = 0.0;
+#pragma unroll
+  for (int w = 0; w < kT / 32; ++w) {
+    best2 = fmax(best2, r3[0][w]);
+    s1 += r3[1][w];
+    s2 += r3[2][w];
+  }
+  const double best = sqrt(best2);  // NaN if the correlation is not finite
+  const double thr = best - pf::kTieRelTol * fmax(1.0, fabs(best));
+  const double thr2 = thr > 0.0 ? thr * thr : -1.0;
+  int cand = INT_MAX;
+  for (int m = t; m < n; m += kT) {  // own entries: written by this thread above
+    const double2 d = D[m];
+    if (fma(d.x, d.x, d.y * d.y) >= thr2) {
+      cand = m;
+      break;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
+  if (lane == 0) s_cand[wid] = cand;
+  __syncthreads();
+  int m = INT_MAX;
+#pragma unroll
+  for (int w = 0; w < kT / 32; ++w) m = min(m, s_cand[w]);
+  const bool ok = isfinite(best) && best2 >= 0.0 && m != INT_MAX;
+  cva_alignment r;
+  if (!ok) {
+    r.shift = 0;
+    r.t0 = 0.0;
+    r.theta = r.trace = r.energy = pf::qnan();
+    r.degenerate = 0;
+    r.status = CVA_INVALID_ARGUMENT;  // non-finite correlation (rigid_align.cpp:83)
+  } else {
+    const double2 dm = D[m];  // written by thread m % kT before the barrier above
+    const double trace = sqrt(fma(dm.x, dm.x, dm.y * dm.y));
+    const int degenerate = trace == 0.0;
+    const double invN = 1.0 / (double)n;
+    double e = invN * (s1 + s2) - 2.0 * invN * trace;  // rigid_align.cpp:56-59
+    if (e < 0.0) e = 0.0;
+    r.shift = m;
+    r.t0 = (double)m / (double)n;
+    r.theta = degenerate ? 0.0 : atan2(dm.y, dm.x);
+    r.trace = trace;
+    r.energy = e;
+    r.degenerate = degenerate;
+    r.status = CVA_OK;
+  }
+  __syncthreads();  // D and the reduction cells are reused by the next call
+  return r;
+}
+
 __device__ __forceinline__ void load_curve(const double2* src, double2* dst, int n) {
   for (int l = threadIdx.x; l < n; l += kT) dst[l] = src[l];
 }
 
+// Per-CTA working set: shared memory (with the parents there or in the slab),
+// or, in slab mode, the CTA's slab with only the cells in shared memory.
+struct Work {
+  Smem S;
+  uint8_t* parent;
+  StepView tv;
+  const StepView* tvp;  // null: the shared step table
+  double2* D;           // slab mode: align_direct scratch
+};
+template <bool kSlab>
+__device__ __forceinline__ void setup_work(Work& w, char* smem, int n, int W, int parent_in_smem,
+                                           uint8_t* parent_slab) {
+  if constexpr (kSlab) {
+    const size_t per = slab_layout(n, W, nullptr, nullptr, nullptr, nullptr, nullptr);
+    slab_layout(n, W, (char*)parent_slab + (size_t)blockIdx.x * per, &w.S, &w.parent, &w.tv, &w.D);
+    w.S.cell = (double*)smem;
+    w.S.rec = (cva_alignment*)(smem + 64);
+    w.tvp = &w.tv;
+  } else {
+    smem_layout(n, W, parent_in_smem != 0, smem, &w.S);
+    w.parent = parent_in_smem ? w.S.parent : parent_slab + (size_t)blockIdx.x * (n + 1) * (n + 1);
+    w.tvp = nullptr;
+    w.D = nullptr;
+  }
+}
+
 // Batched dp_reparam on SRV pairs (q1, q2: pairs x n).
-template <int kW>
+template <int kW, bool kSlab = false>
 __global__ void __launch_bounds__(kT, CVA_EL_MINB)
     dp_kernel(const double2* __restrict__ q1, const double2* __restrict__ q2, int64_t pairs, int n, int W,
               int parent_in_smem, uint8_t* parent_slab, double* gamma, double* energy, int32_t* status) {
   extern __shared__ __align__(16) char smem[];
-  Smem S;
-  smem_layout(n, W, parent_in_smem != 0, smem, &S);
-  uint8_t* parent = parent_in_smem ? S.parent : parent_slab + (size_t)blockIdx.x * (n + 1) * (n + 1);
+  Work wk;
+  setup_work<kSlab>(wk, smem, n, W, parent_in_smem, parent_slab);
+  Smem& S = wk.S;
   for (int64_t p = blockIdx.x; p < pairs; p += gridDim.x) {
     load_curve(q1 + p * n, S.q1, n);
     load_curve(q2 + p * n, S.q2, n);
     __syncthreads();
-    const double e = dp_reparam<kW>(S.q1, S.q2, n, W, S.ring, parent, S.gd, S.cell);
+    const double e = dp_reparam<kW>(S.q1, S.q2, n, W, S.ring, wk.parent, S.gd, S.cell, wk.tvp);
     const bool ok = isfinite(e);
     for (int l = threadIdx.x; l <= n; l += kT)
       gamma[p * (n + 1) + l] = ok ? S.gd[l] : __longlong_as_double(0x7ff8000000000000LL);
@@ -687,7 +873,7 @@ __device__ __forceinline__ cva_alignment align(const double2* a, const double2* 
 // elastic_distance_approach2 per pair. Pair p matches c2 onto c1 where
 // matrix_k == 0: c1 = A + p n, c2 = B + p n; else (distance matrix of
 // matrix_k curves A): c1 = A + (p / k) n, c2 = A + (p % k) n.
-template <int kN, int kW>
+template <int kN, int kW, bool kSlab = false>
 __global__ void __launch_bounds__(kT, CVA_EL_MINB)
     elastic_kernel(const double2* __restrict__ A, const double2* __restrict__ B, int64_t pairs, int64_t matrix_k,
                    int n_rt, ElasticParams prm, int parent_in_smem, uint8_t* parent_slab, const double2* tw,
@@ -696,15 +882,28 @@ __global__ void __launch_bounds__(kT, CVA_EL_MINB)
   __shared__ double2 red[16];
   const int n = kN > 0 ? kN : n_rt;
   const int W = kW > 0 ? kW : prm.max_slope;
-  Smem S;
-  smem_layout(n, W, parent_in_smem != 0, smem, &S);
-  uint8_t* parent = parent_in_smem ? S.parent : parent_slab + (size_t)blockIdx.x * (n + 1) * (n + 1);
+  Work wk;
+  setup_work<kSlab>(wk, smem, n, W, parent_in_smem, parent_slab);
+  Smem& S = wk.S;
+  uint8_t* parent = wk.parent;
   const double qnan = __longlong_as_double(0x7ff8000000000000LL);
+  // rigid alignment of two curves held in S (align_fft semantics)
+  auto rigid = [&](const double2* a, const double2* b) {
+    if constexpr (kSlab)
+      return align_direct(a, b, n, wk.D, red);
+    else
+      return align<kN>(a, b, n, S, tw, red);
+  };
   for (int64_t p = blockIdx.x; p < pairs; p += gridDim.x) {
     const double2* c1 = matrix_k ? A + (p / matrix_k) * n : A + p * n;
     const double2* c2 = matrix_k ? A + (p % matrix_k) * n : B + p * n;
-    load_curve(c1, S.c1, n);
-    load_curve(c2, S.c2, n);
+    if constexpr (kSlab) {  // read in place (global either way)
+      S.c1 = const_cast<double2*>(c1);
+      S.c2 = const_cast<double2*>(c2);
+    } else {
+      load_curve(c1, S.c1, n);
+      load_curve(c2, S.c2, n);
+    }
     __syncthreads();
     // finite input (validate_curve, curve.cpp:11-14)
     int bad = 0;
@@ -722,7 +921,7 @@ __global__ void __launch_bounds__(kT, CVA_EL_MINB)
       __syncthreads();
       srv_center(S.q1, n, S.q1c, S.cell);
       // rigid pre-alignment of the curves themselves (elastic.cpp:114-117)
-      const cva_alignment pre = align<kN>(S.c1, S.c2, n, S, tw, red);
+      const cva_alignment pre = rigid(S.c1, S.c2);
       if (pre.status != CVA_OK) {
         status = CVA_INVALID_ARGUMENT;
       } else {
@@ -739,7 +938,7 @@ __global__ void __launch_bounds__(kT, CVA_EL_MINB)
             sincos(theta, &s, &c);
             for (int l = threadIdx.x; l < n; l += kT) S.w[l] = action_at(S.q2, n, t0, c, s, S.g, l);
             __syncthreads();
-            const double de = dp_reparam<kW>(S.q1, S.w, n, W, S.ring, parent, S.gd, S.cell);
+            const double de = dp_reparam<kW>(S.q1, S.w, n, W, S.ring, parent, S.gd, S.cell, wk.tvp);
             if (!isfinite(de)) {
               status = CVA_RUNTIME_ERROR;  // srv.cpp:233
               break;
@@ -756,7 +955,7 @@ __global__ void __launch_bounds__(kT, CVA_EL_MINB)
             for (int l = threadIdx.x; l < n; l += kT) S.w[l] = action_at(S.q2, n, t0, 1.0, 0.0, S.g, l);
             __syncthreads();
             srv_center(S.w, n, S.wc, S.cell);
-            const cva_alignment ra = align<kN>(S.q1c, S.wc, n, S, tw, red);
+            const cva_alignment ra = rigid(S.q1c, S.wc);
             if (ra.status != CVA_OK) {
               status = CVA_INVALID_ARGUMENT;
               break;
@@ -833,7 +1032,7 @@ __global__ void __launch_bounds__(kT, CVA_EL_MINB)
 // one DP, and the realised energy at t0 = m / n. Items write (energy, theta,
 // gamma) to scratch; a1_pick_kernel keeps, per pair, the first m with the
 // smallest energy (the reference's strict `e < best` scan over m).
-template <int kN, int kW>
+template <int kN, int kW, bool kSlab = false>
 __global__ void __launch_bounds__(kT, CVA_EL_MINB)
     a1_kernel(const double2* __restrict__ A, const double2* __restrict__ B, int64_t pairs, int64_t matrix_k,
               int n_rt, int Wrt, int parent_in_smem, uint8_t* parent_slab, double* item_e, double* item_theta,
@@ -841,9 +1040,10 @@ __global__ void __launch_bounds__(kT, CVA_EL_MINB)
   extern __shared__ __align__(16) char smem[];
   const int n = kN > 0 ? kN : n_rt;
   const int W = kW > 0 ? kW : Wrt;
-  Smem S;
-  smem_layout(n, W, parent_in_smem != 0, smem, &S);
-  uint8_t* parent = parent_in_smem ? S.parent : parent_slab + (size_t)blockIdx.x * (n + 1) * (n + 1);
+  Work wk;
+  setup_work<kSlab>(wk, smem, n, W, parent_in_smem, parent_slab);
+  Smem& S = wk.S;
+  uint8_t* parent = wk.parent;
   const double qnan = __longlong_as_double(0x7ff8000000000000LL);
   const int64_t items = pairs * n;
   for (int64_t it = blockIdx.x; it < items; it += gridDim.x) {
@@ -851,8 +1051,13 @@ __global__ void __launch_bounds__(kT, CVA_EL_MINB)
     const int m = (int)(it % n);
     const double2* c1 = matrix_k ? A + (p / matrix_k) * n : A + p * n;
     const double2* c2 = matrix_k ? A + (p % matrix_k) * n : B + p * n;
-    load_curve(c1, S.c1, n);
-    load_curve(c2, S.c2, n);
+    if constexpr (kSlab) {
+      S.c1 = const_cast<double2*>(c1);
+      S.c2 = const_cast<double2*>(c2);
+    } else {
+      load_curve(c1, S.c1, n);
+      load_curve(c2, S.c2, n);
+    }
     __syncthreads();
     int bad = 0;
     for (int l = threadIdx.x; l < n; l += kT)
@@ -896,7 +1101,7 @@ __global__ void __launch_bounds__(kT, CVA_EL_MINB)
           S.w[l] = rot_apply(cs, sn, S.q2[lm]);
         }
         __syncthreads();
-        const double de = dp_reparam<kW>(S.q1, S.w, n, W, S.ring, parent, S.gd, S.cell);
+        const double de = dp_reparam<kW>(S.q1, S.w, n, W, S.ring, parent, S.gd, S.cell, wk.tvp);
         if (!isfinite(de)) {
           status = CVA_RUNTIME_ERROR;
         } else {
@@ -1002,61 +1207,87 @@ int resident(const void* fn, size_t smem) {
 }
 }  // namespace
 
-size_t elastic_smem(int n, int W) { return el::smem_layout(n, W, parent_fits(n, W), nullptr, nullptr); }
-bool elastic_supported(int n, int W) {
-  return n >= 8 && W >= 1 && W <= 8 && pf::fft_len(n) <= 1024 &&
-         el::smem_layout(n, W, false, nullptr, nullptr) <= kMaxSmem;
+// Shared-memory kernels: W <= 8 (shared step table), the pair-stage transform
+// (M <= 1024) and the per-pair arrays in shared memory. Anything else the
+// reference accepts runs in slab mode.
+bool elastic_slab_mode(int n, int W) {
+  return !(W <= 8 && pf::fft_len(n) <= 1024 && el::smem_layout(n, W, false, nullptr, nullptr) <= kMaxSmem);
 }
+constexpr size_t kSlabBudget = size_t(4) << 30;  // slab-mode scratch: the grid shrinks to fit
+constexpr size_t kSlabSmem = 256;                // cells + alignment record
+
+size_t elastic_smem(int n, int W) {
+  if (elastic_slab_mode(n, W)) return kSlabSmem;
+  return el::smem_layout(n, W, parent_fits(n, W), nullptr, nullptr);
+}
+bool elastic_supported(int n, int W) { return n >= 8 && n <= (1 << 20) && W >= 1 && W <= el::kMaxSlope; }
 
 size_t elastic_parent_slab(int64_t pairs, int n, int W) {
+  if (elastic_slab_mode(n, W)) return el::slab_layout(n, W, nullptr, nullptr, nullptr, nullptr, nullptr);
   if (parent_fits(n, W)) return 0;
   return (size_t)(n + 1) * (n + 1);  // per CTA; the launcher multiplies by the grid
 }
 
-template <int kW>
+template <int kW, bool kSlab>
 static cudaError_t launch_dp_w(const double2* q1, const double2* q2, int64_t pairs, int n, int W, uint8_t* slab,
                                int grid, double* gamma, double* energy, int32_t* status, cudaStream_t s) {
-  const bool ps = parent_fits(n, W);
-  const size_t sm = el::smem_layout(n, W, ps, nullptr, nullptr);
-  const void* fn = (const void*)el::dp_kernel<kW>;
+  const bool ps = !kSlab && parent_fits(n, W);
+  const size_t sm = elastic_smem(n, W);
+  const void* fn = (const void*)el::dp_kernel<kW, kSlab>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  el::dp_kernel<kW><<<grid, el::kT, sm, s>>>(q1, q2, pairs, n, W, ps ? 1 : 0, slab, gamma, energy, status);
+  el::dp_kernel<kW, kSlab><<<grid, el::kT, sm, s>>>(q1, q2, pairs, n, W, ps ? 1 : 0, slab, gamma, energy, status);
   return cudaGetLastError();
 }
 
 int elastic_grid(int64_t pairs, int n, int W) {
-  const bool ps = parent_fits(n, W);
-  const size_t sm = el::smem_layout(n, W, ps, nullptr, nullptr);
-  // the largest-footprint instance (most static shared memory) bounds all three kernels
-  int r = resident((const void*)el::elastic_kernel<0, 0>, sm);
-  r = std::min(r, resident((const void*)el::dp_kernel<0>, sm));
-  r = std::min(r, resident((const void*)el::a1_kernel<0, 0>, sm));
+  const size_t sm = elastic_smem(n, W);
+  int r;
+  if (elastic_slab_mode(n, W)) {
+    r = resident((const void*)el::elastic_kernel<0, 0, true>, sm);
+    r = std::min(r, resident((const void*)el::dp_kernel<0, true>, sm));
+    r = std::min(r, resident((const void*)el::a1_kernel<0, 0, true>, sm));
+    const size_t per = elastic_parent_slab(pairs, n, W);
+    r = (int)std::max<size_t>(1, std::min<size_t>((size_t)r, kSlabBudget / per));
+  } else {
+    // the largest-footprint instance (most static shared memory) bounds all three kernels
+    r = resident((const void*)el::elastic_kernel<0, 0>, sm);
+    r = std::min(r, resident((const void*)el::dp_kernel<0>, sm));
+    r = std::min(r, resident((const void*)el::a1_kernel<0, 0>, sm));
+  }
   return (int)(pairs < r ? pairs : r);
 }
 
 cudaError_t launch_dp_reparam(const double2* q1, const double2* q2, int64_t pairs, int n, int W, uint8_t* slab,
                               int grid, double* gamma, double* energy, int32_t* status, cudaStream_t s) {
-  if (W == 4) return launch_dp_w<4>(q1, q2, pairs, n, W, slab, grid, gamma, energy, status, s);
-  return launch_dp_w<0>(q1, q2, pairs, n, W, slab, grid, gamma, energy, status, s);
+  if (elastic_slab_mode(n, W)) {
+    if (W == 4) return launch_dp_w<4, true>(q1, q2, pairs, n, W, slab, grid, gamma, energy, status, s);
+    return launch_dp_w<0, true>(q1, q2, pairs, n, W, slab, grid, gamma, energy, status, s);
+  }
+  if (W == 4) return launch_dp_w<4, false>(q1, q2, pairs, n, W, slab, grid, gamma, energy, status, s);
+  return launch_dp_w<0, false>(q1, q2, pairs, n, W, slab, grid, gamma, energy, status, s);
 }
 
-template <int kN, int kW>
+template <int kN, int kW, bool kSlab = false>
 static cudaError_t launch_el(const double2* A, const double2* B, int64_t pairs, int64_t k, int n,
                              const ElasticParams& prm, uint8_t* slab, int grid, const double2* tw,
                              const ElasticOut& out, cudaStream_t s) {
-  const bool ps = parent_fits(n, prm.max_slope);
-  const size_t sm = el::smem_layout(n, prm.max_slope, ps, nullptr, nullptr);
-  const void* fn = (const void*)el::elastic_kernel<kN, kW>;
+  const bool ps = !kSlab && parent_fits(n, prm.max_slope);
+  const size_t sm = elastic_smem(n, prm.max_slope);
+  const void* fn = (const void*)el::elastic_kernel<kN, kW, kSlab>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  el::elastic_kernel<kN, kW><<<grid, el::kT, sm, s>>>(A, B, pairs, k, n, prm, ps ? 1 : 0, slab, tw, out);
+  el::elastic_kernel<kN, kW, kSlab><<<grid, el::kT, sm, s>>>(A, B, pairs, k, n, prm, ps ? 1 : 0, slab, tw, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_elastic_approach2(const double2* A, const double2* B, int64_t pairs, int64_t matrix_k, int n,
                                      const ElasticParams& prm, uint8_t* slab, int grid, const double2* tw,
                                      const ElasticOut& out, cudaStream_t s) {
+  if (elastic_slab_mode(n, prm.max_slope)) {
+    if (prm.max_slope == 4) return launch_el<0, 4, true>(A, B, pairs, matrix_k, n, prm, slab, grid, tw, out, s);
+    return launch_el<0, 0, true>(A, B, pairs, matrix_k, n, prm, slab, grid, tw, out, s);
+  }
   if (prm.max_slope == 4) {
     switch (n) {
       case 64: return launch_el<64, 4>(A, B, pairs, matrix_k, n, prm, slab, grid, tw, out, s);
@@ -1069,16 +1300,16 @@ cudaError_t launch_elastic_approach2(const double2* A, const double2* B, int64_t
   return launch_el<0, 0>(A, B, pairs, matrix_k, n, prm, slab, grid, tw, out, s);
 }
 
-template <int kN, int kW>
+template <int kN, int kW, bool kSlab = false>
 static cudaError_t launch_a1(const double2* A, const double2* B, int64_t pairs, int64_t k, int n, int W,
                              uint8_t* slab, int grid, double* ie, double* ith, double* ig, int32_t* ist,
                              cudaStream_t s) {
-  const bool ps = parent_fits(n, W);
-  const size_t sm = el::smem_layout(n, W, ps, nullptr, nullptr);
-  const void* fn = (const void*)el::a1_kernel<kN, kW>;
+  const bool ps = !kSlab && parent_fits(n, W);
+  const size_t sm = elastic_smem(n, W);
+  const void* fn = (const void*)el::a1_kernel<kN, kW, kSlab>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
-  el::a1_kernel<kN, kW><<<grid, el::kT, sm, s>>>(A, B, pairs, k, n, W, ps ? 1 : 0, slab, ie, ith, ig, ist);
+  el::a1_kernel<kN, kW, kSlab><<<grid, el::kT, sm, s>>>(A, B, pairs, k, n, W, ps ? 1 : 0, slab, ie, ith, ig, ist);
   return cudaGetLastError();
 }
 
@@ -1098,7 +1329,10 @@ cudaError_t launch_elastic_approach1(const double2* A, const double2* B, int64_t
   double* ig = out.gamma ? ith + items : nullptr;
   int32_t* ist = (int32_t*)(ith + items + (out.gamma ? items * (n + 1) : 0));
   cudaError_t e;
-  if (W == 4) {
+  if (elastic_slab_mode(n, W)) {
+    e = W == 4 ? launch_a1<0, 4, true>(A, B, pairs, matrix_k, n, W, slab, grid, ie, ith, ig, ist, s)
+               : launch_a1<0, 0, true>(A, B, pairs, matrix_k, n, W, slab, grid, ie, ith, ig, ist, s);
+  } else if (W == 4) {
     switch (n) {
       case 64: e = launch_a1<64, 4>(A, B, pairs, matrix_k, n, W, slab, grid, ie, ith, ig, ist, s); break;
       case 128: e = launch_a1<128, 4>(A, B, pairs, matrix_k, n, W, slab, grid, ie, ith, ig, ist, s); break;

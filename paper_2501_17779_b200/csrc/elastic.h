@@ -25,9 +25,14 @@ struct ElasticOut {
   double* trace;  // nullable: pairs x (max_iters + 1) energies per accepted iteration, NaN-padded
 };
 
+// 8 <= n <= 2^20, 1 <= W <= 20 (255 steps: parent indices below the 0xff
+// sentinel, srv.cpp:203-222). Slab mode: n or W past the shared-memory
+// kernels; per-pair arrays, dp ring and parents in a per-CTA global slab.
 bool elastic_supported(int n, int W);
+bool elastic_slab_mode(int n, int W);
 size_t elastic_smem(int n, int W);
-// Bytes of per-CTA parent scratch in global memory (0: parents fit in shared memory).
+// Bytes of per-CTA scratch in global memory (0: everything fits in shared
+// memory; the parents alone, or in slab mode the whole working set).
 size_t elastic_parent_slab(int64_t pairs, int n, int W);
 int elastic_grid(int64_t pairs, int n, int W);
 

@@ -306,3 +306,73 @@ def test_approach2_iteration_cap_and_tolerance(cuda, reference):
         g = cva.elastic_approach2_batch(c1, c2, max_iters=it, energy_tol=tol)
         r = reference.elastic_approach2_batch(c1, c2, max_iters=it, energy_tol=tol, threads=4)
         _check_vs_reference(g, r)
+
+
+# ------------------------------------------- slab mode (n or W past shared memory)
+# Every per-pair array, the dp ring and the parents in a per-CTA global slab;
+# the rigid steps by the direct correlation (elastic.cu align_direct).
+
+
+@pytest.mark.parametrize("n", [1025, 1100, 2048])
+def test_dp_slab_mode_bitwise(cuda, reference, n):
+    q1, q2 = srv_pair(reference, n, 5)
+    g, e, st = cva.dp_reparam_batch(q1[None], q2[None])
+    rg, re_, rst = reference.dp_reparam_batch(q1[None], q2[None])
+    assert st[0] == rst[0] == 0
+    np.testing.assert_array_equal(g, rg)
+    np.testing.assert_array_equal(e, re_)
+
+
+@pytest.mark.parametrize("w", [9, 12, 20])
+def test_dp_large_slopes_bitwise(cuda, reference, w):
+    pairs = [srv_pair(reference, 48, s) for s in (2, 3)]
+    q1 = np.stack([p[0] for p in pairs])
+    q2 = np.stack([p[1] for p in pairs])
+    g, e, st = cva.dp_reparam_batch(q1, q2, max_slope=w)
+    rg, re_, rst = reference.dp_reparam_batch(q1, q2, max_slope=w)
+    assert (st == 0).all() and (rst == 0).all()
+    np.testing.assert_array_equal(g, rg)
+    np.testing.assert_array_equal(e, re_)
+
+
+def test_dp_slope_beyond_parent_range_unsupported(cuda, reference):
+    q1, q2 = srv_pair(reference, 48, 2)
+    with pytest.raises(Exception, match="max_slope"):
+        cva.dp_reparam_batch(q1[None], q2[None], max_slope=21)
+
+
+@pytest.mark.parametrize("n", [1100, 1536])
+def test_approach2_slab_mode_matches_reference(cuda, reference, n):
+    c1, c2 = _pairs(reference, n, 2, seed0=91)
+    g = cva.elastic_approach2_batch(c1, c2, max_iters=4, return_gamma=True)
+    r = reference.elastic_approach2_batch(c1, c2, max_iters=4, threads=2, gamma=True)
+    _check_vs_reference(g, r)
+    np.testing.assert_allclose(g["t0"], r["t0"], atol=1e-9)
+    assert (g["gamma"][:, 0] == 0).all() and (g["gamma"][:, -1] == 1).all()
+
+
+def test_approach2_slab_mode_small_n_agrees_with_shared_kernel(cuda, reference):
+    """W = 9 forces slab mode at n = 64 (direct correlation, global step
+    table); the same pairs at W = 9 against the reference, and W = 4 slab vs
+    shared cannot be compared (different W), so the check is the reference."""
+    c1, c2 = _pairs(reference, 64, 4, seed0=101)
+    g = cva.elastic_approach2_batch(c1, c2, max_slope=9)
+    r = reference.elastic_approach2_batch(c1, c2, max_slope=9, threads=4)
+    _check_vs_reference(g, r)
+
+
+def test_distance_matrix_slab_mode(cuda, reference):
+    curves = np.stack([prep(reference, f, 1030, s) for s, f in enumerate(["bumps", "clover", "limacon"], 1)])
+    d = cva.elastic_distance_matrix(curves, 2, max_iters=3)
+    i, j = np.meshgrid(np.arange(3), np.arange(3), indexing="ij")
+    r = reference.elastic_approach2_batch(curves[i.ravel()], curves[j.ravel()], max_iters=3, threads=9)
+    np.testing.assert_allclose(d.ravel(), r["distance"], rtol=DIST_RTOL, atol=1e-12)
+
+
+def test_approach1_slab_mode_matches_reference(cuda, reference):
+    c1, c2 = _pairs(reference, 40, 2, seed0=111)
+    g = cva.elastic_approach1_batch(c1, c2, max_slope=9)
+    r = reference.elastic_approach1_batch(c1, c2, max_slope=9, threads=2)
+    assert (g["status"] == 0).all() and (r["status"] == 0).all()
+    np.testing.assert_allclose(g["distance"], r["distance"], rtol=DIST_RTOL, atol=1e-12)
+    np.testing.assert_array_equal(g["t0"], r["t0"])
