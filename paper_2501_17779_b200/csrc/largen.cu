@@ -160,11 +160,11 @@ __global__ void __launch_bounds__(kT)
     part[(int64_t)blockIdx.y * kStatBlocks + blockIdx.x] = make_double4(acc.x, acc.y, len, nf ? 1.0 : 0.0);
 }
 
-__global__ void stats_final(const double4* __restrict__ part, int64_t curves, int N, int normalize,
-                            CurveNorm* norm, int32_t* bad) {
-  const int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+// One warp: curve c's partials -> its CurveNorm and bad flag (every lane
+// returns them; fixed reduction order, so every caller forms the same values).
+__device__ __forceinline__ CurveNorm norm_of(const double4* __restrict__ part, int64_t c, int N, int normalize,
+                                             int* bad) {
   const int lane = threadIdx.x & 31;
-  if (c >= curves) return;
   double4 v = lane < kStatBlocks ? part[c * kStatBlocks + lane] : make_double4(0, 0, 0, 0);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -173,15 +173,26 @@ __global__ void stats_final(const double4* __restrict__ part, int64_t curves, in
     v.z += __shfl_xor_sync(0xffffffffu, v.z, o);
     v.w += __shfl_xor_sync(0xffffffffu, v.w, o);
   }
+  CurveNorm cn{make_double2(0.0, 0.0), 1.0};
+  int b = v.w != 0.0;
+  if (normalize) {
+    const double invn = 1.0 / (double)N;
+    cn.g = make_double2(invn * v.x, invn * v.y);
+    b |= !(v.z > 0.0);
+    cn.sc = 1.0 / v.z;
+  }
+  *bad = b;
+  return cn;
+}
+
+__global__ void stats_final(const double4* __restrict__ part, int64_t curves, int N, int normalize,
+                            CurveNorm* norm, int32_t* bad) {
+  const int64_t c = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (c >= curves) return;
+  int b;
+  const CurveNorm cn = norm_of(part, c, N, normalize, &b);
   if (lane == 0) {
-    CurveNorm cn{make_double2(0.0, 0.0), 1.0};
-    int b = v.w != 0.0;
-    if (normalize) {
-      const double invn = 1.0 / (double)N;
-      cn.g = make_double2(invn * v.x, invn * v.y);
-      b |= !(v.z > 0.0);
-      cn.sc = 1.0 / v.z;
-    }
     norm[c] = cn;
     bad[c] = b;
   }
@@ -294,12 +305,25 @@ __global__ void __launch_bounds__(kT)
   const CurveNorm cn = norm2[p];
   const double2* z = c2 + p * N;
   double2* a = aligned + p * N;
-  for (int l = blockIdx.x * kT + threadIdx.x; l < N; l += gridDim.x * kT) {
-    int64_t j = l + m;
-    if (j >= N) j -= N;
-    const double2 q = __ldg(&z[j]);
-    const double2 v = make_double2((q.x - cn.g.x) * cn.sc, (q.y - cn.g.y) * cn.sc);
-    a[l] = make_double2(fma(r.x, v.x, r.y * v.y), fma(-r.y, v.x, r.x * v.y));
+  constexpr int kU = 4;  // loads of kU rounds in flight before their stores
+  const int step = gridDim.x * kT;
+  for (int l0 = blockIdx.x * kT + threadIdx.x; l0 < N; l0 += kU * step) {
+    double2 q[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int l = l0 + u * step;
+      int64_t j = l + m;
+      if (j >= N) j -= N;
+      q[u] = l < N ? __ldg(&z[j]) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int l = l0 + u * step;
+      if (l < N) {
+        const double2 v = make_double2((q[u].x - cn.g.x) * cn.sc, (q[u].y - cn.g.y) * cn.sc);
+        a[l] = make_double2(fma(r.x, v.x, r.y * v.y), fma(-r.y, v.x, r.x * v.y));
+      }
+    }
   }
 }
 
@@ -315,6 +339,9 @@ __global__ void __launch_bounds__(kT)
 //              Z[k1 + M1 k2]), the product Z1 conj(Z2), its row FFT and twiddle
 //              W_M^{k1 m2}                   -> G[k1][m2]
 //   p2_kernel  column FFTs of G: F[m2 + M2 m1] in natural order, + block max
+//   pick_kernel tie-broken argmax + shift / rotation / energy (one CTA per pair)
+// f1_kernel also reduces the stats partials into each curve's norm (no
+// stats_final launch): per chunk, stats_partial, f1, fp, p2, pick, aligned.
 // The product's transform is a forward FFT over the spectral index
 // k = k1 + M1 k2 (D = conj(FFT(Z1 conj Z2)) / M, as in pairfft.cuh), which is
 // why the second step of the forward transforms and the first of the third
@@ -393,33 +420,56 @@ __device__ __forceinline__ void wfft(double2* x, const double2* __restrict__ tw,
 // Column pass of the forward transforms. grid (M2 / kCT, 2 P): sequence s < P is
 // curve 1 of pair s (the a = [z1', 0...] form), s >= P curve 2 of pair s - P
 // (b = [z2', z2', 0...]). Writes U[s][k1 M2 + n2] and sum |z'|^2 partials.
+// The curve's CurveNorm comes from the stats partials (stats_final's reduction,
+// done by warp 0 of every CTA of the curve; the first CTA also stores it and the
+// bad flag for the pick and aligned-output kernels).
 template <int M1>
 __global__ void __launch_bounds__(kT)
     f1_kernel(const double2* __restrict__ z1, const double2* __restrict__ z2, int64_t P, int N, int M2,
               const double2* __restrict__ twS, const double2* __restrict__ lo, const double2* __restrict__ hi,
-              const CurveNorm* __restrict__ n1, const CurveNorm* __restrict__ n2, double2* U, double* sq1,
-              double* sq2) {
+              const double4* __restrict__ part, int normalize, CurveNorm* norm, int32_t* bad, double2* U,
+              double* sq1, double* sq2) {
   constexpr int VS = vstride<M1>();
   __shared__ __align__(16) double2 sm[kCT * VS];
   __shared__ double2 red[64];
+  __shared__ CurveNorm s_cn;
   const int M = M1 * M2;
   const int64_t sidx = blockIdx.y;
   const bool second = sidx >= P;
   const int64_t p = second ? sidx - P : sidx;
   const double2* z = (second ? z2 : z1) + p * N;
-  const CurveNorm cn = (second ? n2 : n1)[p];
   const int lim = (!second || M == N) ? N : 2 * N;
   const int c0 = blockIdx.x * kCT;
+  constexpr int kLd = M1 * kCT / kT;
+  double2 q[kLd];  // the tile's nodes, all loads in flight before the norm is formed
+#pragma unroll
+  for (int it = 0; it < kLd; ++it) {
+    const int idx = threadIdx.x + it * kT;
+    const int n = M2 * (idx / kCT) + c0 + idx % kCT;
+    q[it] = n < lim ? __ldg(&z[n < N ? n : n - N]) : make_double2(0.0, 0.0);
+  }
+  if (threadIdx.x < 32) {  // curve sidx: curve 1s then curve 2s, as stats_partial numbers them
+    int b;
+    const CurveNorm c = norm_of(part, sidx, N, normalize, &b);
+    if (threadIdx.x == 0) {
+      s_cn = c;
+      if (blockIdx.x == 0) {
+        norm[sidx] = c;
+        bad[sidx] = b;
+      }
+    }
+  }
+  __syncthreads();
+  const CurveNorm cn = s_cn;
   double sq = 0.0;
 #pragma unroll
-  for (int it = 0; it < M1 * kCT / kT; ++it) {  // all loads of the tile in flight
+  for (int it = 0; it < kLd; ++it) {
     const int idx = threadIdx.x + it * kT;
     const int n1i = idx / kCT, c = idx % kCT;
     const int n = M2 * n1i + c0 + c;
     double2 v = make_double2(0.0, 0.0);
     if (n < lim) {
-      const double2 q = __ldg(&z[n < N ? n : n - N]);
-      v = make_double2((q.x - cn.g.x) * cn.sc, (q.y - cn.g.y) * cn.sc);
+      v = make_double2((q[it].x - cn.g.x) * cn.sc, (q[it].y - cn.g.y) * cn.sc);
       if (n < N) sq = fma(v.x, v.x, fma(v.y, v.y, sq));
     }
     sm[c * VS + padL(n1i)] = v;
@@ -463,8 +513,11 @@ __global__ void __launch_bounds__(kT, 2)
   for (int h = 0; h < 2; ++h) {
     const double2* u = U + (h ? P + p : p) * (int64_t)M + (int64_t)(r0 + w) * M2;
     double2* x = smv + (h * kRT + w) * VS;
+    double2 q[M2 / 32];  // the row's loads in flight before the shared stores
 #pragma unroll
-    for (int i0 = 0; i0 < M2; i0 += 32) x[padL(i0 + lane)] = __ldg(&u[i0 + lane]);
+    for (int i0 = 0; i0 < M2; i0 += 32) q[i0 / 32] = __ldg(&u[i0 + lane]);
+#pragma unroll
+    for (int i0 = 0; i0 < M2; i0 += 32) x[padL(i0 + lane)] = q[i0 / 32];
     __syncwarp();
     wfft<M2>(x, twS, 1, lane);
   }
@@ -500,11 +553,17 @@ __global__ void __launch_bounds__(kT)
   const int64_t p = blockIdx.y;
   const int c0 = blockIdx.x * kCT;
   const double2* g = G + p * (int64_t)M;
+  constexpr int kLd = M1 * kCT / kT;
+  double2 q[kLd];  // every load in flight before the shared stores
 #pragma unroll
-  for (int it = 0; it < M1 * kCT / kT; ++it) {
+  for (int it = 0; it < kLd; ++it) {
     const int idx = threadIdx.x + it * kT;
-    const int k1 = idx / kCT, c = idx % kCT;
-    sm[c * VS + padL(k1)] = __ldg(&g[(int64_t)k1 * M2 + c0 + c]);
+    q[it] = __ldg(&g[(int64_t)(idx / kCT) * M2 + c0 + idx % kCT]);
+  }
+#pragma unroll
+  for (int it = 0; it < kLd; ++it) {
+    const int idx = threadIdx.x + it * kT;
+    sm[(idx % kCT) * VS + padL(idx / kCT)] = q[it];
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -524,12 +583,16 @@ __global__ void __launch_bounds__(kT)
   mx = block_max(mx, red);
   if (threadIdx.x == 0) bmax[p * gridDim.x + blockIdx.x] = mx;
 }
-// Tie-band candidate of the four-step layout (one CTA per pair): global max
-// from the column-tile maxima, then only tiles whose maximum reaches the band
-// are scanned (usually one) for the smallest m with |F_m|^2 >= thr^2.
+// Tie-band pick of the four-step layout, one CTA per pair: global max from the
+// column-tile maxima, then only tiles whose maximum reaches the band are
+// scanned (usually one) for the smallest m with |F_m|^2 >= thr^2; then, in
+// warp 0, lpick_kernel's work for the pair (shift, rotation, trace, energy),
+// so the candidate never goes through global memory and there is one launch.
 template <int M1>
 __global__ void __launch_bounds__(kT)
-    cand_kernel(const double2* __restrict__ F, int N, int M2, const double* __restrict__ bmax, int* cand_out) {
+    pick_kernel(const double2* __restrict__ F, int N, int M2, const double* __restrict__ bmax,
+                const double* __restrict__ sq1, const double* __restrict__ sq2, const int32_t* bad1,
+                const int32_t* bad2, cva_alignment* out, double2* rot) {
   __shared__ double2 red[64];
   const int64_t p = blockIdx.x;
   const int nt = M2 / kCT, M = M1 * M2;
@@ -553,7 +616,48 @@ __global__ void __launch_bounds__(kT)
     }
   }
   cand = block_min_int(cand, red);
-  if (threadIdx.x == 0) cand_out[p] = isfinite(best) && best2 >= 0.0 ? cand : INT_MAX;
+  if (threadIdx.x >= 32) return;
+  // lpick_kernel for pair p (one candidate, nt sum-of-squares partials)
+  const int m = isfinite(best) && best2 >= 0.0 ? cand : INT_MAX;
+  const int lane = threadIdx.x;
+  double s1 = 0.0, s2 = 0.0;
+  for (int b = lane; b < nt; b += 32) {
+    s1 += sq1[p * nt + b];
+    s2 += sq2[p * nt + b];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+  }
+  if (lane != 0) return;
+  const double invM = 1.0 / (double)M, invN = 1.0 / (double)N;
+  cva_alignment r;
+  if (bad1[p] || bad2[p] || m == INT_MAX) {
+    r.shift = 0;
+    r.t0 = 0.0;
+    r.theta = r.trace = r.energy = qnan();
+    r.degenerate = 0;
+    r.status = CVA_INVALID_ARGUMENT;
+    rot[p] = make_double2(qnan(), qnan());
+  } else {
+    const double2 v = f[m];
+    const double a2 = fma(v.x, v.x, v.y * v.y);
+    const double trace = sqrt(a2) * invM;
+    const int degenerate = trace == 0.0;
+    double e = invN * (s1 + s2) - 2.0 * invN * trace;
+    if (e < 0.0) e = 0.0;
+    r.shift = m;
+    r.t0 = (double)m / (double)N;
+    r.theta = degenerate ? 0.0 : atan2(-v.y, v.x);
+    r.trace = trace;
+    r.energy = e;
+    r.degenerate = degenerate;
+    r.status = CVA_OK;
+    const double ia = degenerate ? 0.0 : 1.0 / sqrt(a2);
+    rot[p] = degenerate ? make_double2(1.0, 0.0) : make_double2(v.x * ia, -v.y * ia);
+  }
+  out[p] = r;
 }
 }  // namespace fs
 
@@ -633,10 +737,10 @@ int four_step_m1_impl(int M) {
 
 template <int M1>
 cudaError_t f1_launch(const double2* z1, const double2* z2, int64_t P, int N, int M2, const FourStepTw& t,
-                      const ln::CurveNorm* n1, const ln::CurveNorm* n2, double2* U, double* q1, double* q2,
-                      cudaStream_t s) {
+                      const double4* part, int normalize, ln::CurveNorm* norm, int32_t* bad, double2* U, double* q1,
+                      double* q2, cudaStream_t s) {
   ln::fs::f1_kernel<M1><<<dim3((unsigned)(M2 / ln::fs::kCT), (unsigned)(2 * P)), ln::fs::kT, 0, s>>>(
-      z1, z2, P, N, M2, t.s1, t.lo, t.hi, n1, n2, U, q1, q2);
+      z1, z2, P, N, M2, t.s1, t.lo, t.hi, part, normalize, norm, bad, U, q1, q2);
   return cudaGetLastError();
 }
 template <int M1>
@@ -659,14 +763,14 @@ cudaError_t fp_launch(const double2* U, int64_t P, int M1, const FourStepTw& t, 
 
 // The three passes of one chunk; F in natural order, bmax / sq partials per tile.
 cudaError_t four_step(int M1, const double2* z1, const double2* z2, int64_t P, int N, const FourStepTw& t,
-                      const ln::CurveNorm* n1, const ln::CurveNorm* n2, double2* U, double2* G, double2* F,
-                      double* q1, double* q2, double* bmax, cudaStream_t s) {
+                      const double4* part, int normalize, ln::CurveNorm* norm, int32_t* bad, double2* U, double2* G,
+                      double2* F, double* q1, double* q2, double* bmax, cudaStream_t s) {
   const int M = pf::fft_len(N), M2 = M / M1;
   cudaError_t e;
   switch (M1) {
-    case 64: e = f1_launch<64>(z1, z2, P, N, M2, t, n1, n2, U, q1, q2, s); break;
-    case 128: e = f1_launch<128>(z1, z2, P, N, M2, t, n1, n2, U, q1, q2, s); break;
-    default: e = f1_launch<256>(z1, z2, P, N, M2, t, n1, n2, U, q1, q2, s); break;
+    case 64: e = f1_launch<64>(z1, z2, P, N, M2, t, part, normalize, norm, bad, U, q1, q2, s); break;
+    case 128: e = f1_launch<128>(z1, z2, P, N, M2, t, part, normalize, norm, bad, U, q1, q2, s); break;
+    default: e = f1_launch<256>(z1, z2, P, N, M2, t, part, normalize, norm, bad, U, q1, q2, s); break;
   }
   if (e != cudaSuccess) return e;
   switch (M2) {
@@ -739,15 +843,24 @@ cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pai
     ln::CurveNorm *n1 = nn, *n2 = nn + P;
     int32_t *b1 = bb, *b2 = bb + P;
     ln::stats_partial<<<dim3(ln::kStatBlocks, (unsigned)(2 * P)), ln::kT, 0, s>>>(z1, N, spp, z2, P);
-    ln::stats_final<<<(unsigned)((2 * P + 7) / 8), 256, 0, s>>>(spp, 2 * P, N, normalize, nn, bb);
     double2* F = nullptr;
-    int nbmax = nblk, nsq = sqn;
-    if (fm1) {  // four-step: U = A|B (2P sequences, adjacent), G = C, F = D
-      e = four_step(fm1, z1, z2, P, N, *fst, n1, n2, A, C, D, q1, q2, bmax, s);
+    const int nbmax = nblk, nsq = sqn;
+    if (fm1) {  // four-step: U = A|B (2P sequences, adjacent), G = C, F = D; f1 forms the norms
+      e = four_step(fm1, z1, z2, P, N, *fst, spp, normalize, nn, bb, A, C, D, q1, q2, bmax, s);
       if (e != cudaSuccess) break;
-      F = D;
-      nbmax = nsq = (M / fm1) / ln::fs::kCT;
+      const int M2 = M / fm1;
+      switch (fm1) {  // argmax + pick in one kernel
+        case 64: ln::fs::pick_kernel<64><<<(unsigned)P, ln::kT, 0, s>>>(D, N, M2, bmax, q1, q2, b1, b2, out + p0, rot); break;
+        case 128: ln::fs::pick_kernel<128><<<(unsigned)P, ln::kT, 0, s>>>(D, N, M2, bmax, q1, q2, b1, b2, out + p0, rot); break;
+        default: ln::fs::pick_kernel<256><<<(unsigned)P, ln::kT, 0, s>>>(D, N, M2, bmax, q1, q2, b1, b2, out + p0, rot); break;
+      }
+      if (aligned)
+        ln::aligned_kernel<<<dim3((unsigned)((N + 4 * ln::kT - 1) / (4 * ln::kT)), (unsigned)P), ln::kT, 0, s>>>(
+            z2, N, n2, out + p0, rot, aligned + p0 * N);
+      e = cudaGetLastError();
+      continue;
     } else {
+      ln::stats_final<<<(unsigned)((2 * P + 7) / 8), 256, 0, s>>>(spp, 2 * P, N, normalize, nn, bb);
       double2 *Z1 = nullptr, *Z2 = nullptr;
       e = fft_many<ln::kLoadA>(z1, nullptr, A, B, M, N, tw, n1, P, q1, s, &Z1);
       if (e == cudaSuccess) e = fft_many<ln::kLoadB>(z2, nullptr, C, D, M, N, tw, n2, P, q2, s, &Z2);
@@ -758,19 +871,8 @@ cudaError_t launch_large_align(const double2* c1, const double2* c2, int64_t pai
       if (e != cudaSuccess) break;
       ln::lmax_kernel<<<dim3((unsigned)nblk, (unsigned)P), ln::kT, 0, s>>>(F, M, N, bmax);
     }
-    int ncand = nblk;
-    if (fm1) {
-      const int M2 = M / fm1;
-      switch (fm1) {
-        case 64: ln::fs::cand_kernel<64><<<(unsigned)P, ln::kT, 0, s>>>(F, N, M2, bmax, bcand); break;
-        case 128: ln::fs::cand_kernel<128><<<(unsigned)P, ln::kT, 0, s>>>(F, N, M2, bmax, bcand); break;
-        default: ln::fs::cand_kernel<256><<<(unsigned)P, ln::kT, 0, s>>>(F, N, M2, bmax, bcand); break;
-      }
-      ncand = 1;
-    } else {
-      ln::lcand_kernel<<<dim3((unsigned)nblk, (unsigned)P), ln::kT, 0, s>>>(F, M, N, bmax, nbmax, bcand);
-    }
-    ln::lpick_kernel<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(F, M, N, bcand, ncand, q1, q2, nsq, b1, b2, P, out + p0,
+    ln::lcand_kernel<<<dim3((unsigned)nblk, (unsigned)P), ln::kT, 0, s>>>(F, M, N, bmax, nbmax, bcand);
+    ln::lpick_kernel<<<(unsigned)((P + 7) / 8), 256, 0, s>>>(F, M, N, bcand, nblk, q1, q2, nsq, b1, b2, P, out + p0,
                                                              rot);
     if (aligned)
       ln::aligned_kernel<<<dim3((unsigned)((N + 4 * ln::kT - 1) / (4 * ln::kT)), (unsigned)P), ln::kT, 0, s>>>(
