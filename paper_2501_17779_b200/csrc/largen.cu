@@ -594,37 +594,51 @@ __global__ void __launch_bounds__(kT)
                 const double* __restrict__ sq1, const double* __restrict__ sq2, const int32_t* bad1,
                 const int32_t* bad2, cva_alignment* out, double2* rot) {
   __shared__ double2 red[64];
+  __shared__ unsigned s_mask;
+  __shared__ double2 s_v;
   const int64_t p = blockIdx.x;
-  const int nt = M2 / kCT, M = M1 * M2;
-  double best2 = -1.0;
-  for (int b = threadIdx.x; b < nt; b += kT) best2 = fmax(best2, bmax[p * nt + b]);
-  best2 = block_max(best2, red);
+  const int nt = M2 / kCT, M = M1 * M2;  // nt <= 32 column tiles
+  const int lane = threadIdx.x & 31;
+  // independent loads first: the tile maxima, and (warp 0) the sum |z'|^2 partials
+  const double tb = (int)threadIdx.x < nt ? bmax[p * nt + threadIdx.x] : -1.0;
+  double s1 = 0.0, s2 = 0.0;
+  if (threadIdx.x < 32)
+    for (int b = lane; b < nt; b += 32) {
+      s1 += sq1[p * nt + b];
+      s2 += sq2[p * nt + b];
+    }
+  const double best2 = block_max(tb, red);
   const double best = sqrt(best2) / (double)M;
   const double thr = best - pf::kTieRelTol * fmax(1.0, fabs(best));
   const double thrM = thr * (double)M;
   const double thr2 = thr > 0.0 ? thrM * thrM : -1.0;
+  if (threadIdx.x < 32) {  // tiles whose maximum reaches the band (usually one)
+    const unsigned msk = __ballot_sync(0xffffffffu, (int)threadIdx.x < nt && tb >= thr2);
+    if (lane == 0) s_mask = msk;
+  }
+  __syncthreads();
   const double2* f = F + p * (int64_t)M;
   int cand = INT_MAX;
-  for (int b = 0; b < nt; ++b) {
-    if (!(bmax[p * nt + b] >= thr2)) continue;  // uniform over the block
+  double2 vc = make_double2(0.0, 0.0);  // F at this thread's candidate
+  for (unsigned msk = s_mask; msk; msk &= msk - 1) {
+    const int b = __ffs(msk) - 1;
     for (int idx = threadIdx.x; idx < M1 * kCT; idx += kT) {
       const int m = (b * kCT + idx % kCT) + M2 * (idx / kCT);
       if (m < N && m < cand) {
         const double2 v = __ldg(&f[m]);
-        if (fma(v.x, v.x, v.y * v.y) >= thr2) cand = m;
+        if (fma(v.x, v.x, v.y * v.y) >= thr2) {
+          cand = m;
+          vc = v;
+        }
       }
     }
   }
-  cand = block_min_int(cand, red);
+  const int cmin = block_min_int(cand, red);
+  if (cand == cmin && cand != INT_MAX) s_v = vc;  // one thread scanned index cmin
+  __syncthreads();
   if (threadIdx.x >= 32) return;
-  // lpick_kernel for pair p (one candidate, nt sum-of-squares partials)
-  const int m = isfinite(best) && best2 >= 0.0 ? cand : INT_MAX;
-  const int lane = threadIdx.x;
-  double s1 = 0.0, s2 = 0.0;
-  for (int b = lane; b < nt; b += 32) {
-    s1 += sq1[p * nt + b];
-    s2 += sq2[p * nt + b];
-  }
+  // lpick_kernel's work for pair p (one candidate, nt sum-of-squares partials)
+  const int m = isfinite(best) && best2 >= 0.0 ? cmin : INT_MAX;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     s1 += __shfl_xor_sync(0xffffffffu, s1, o);
@@ -641,7 +655,7 @@ __global__ void __launch_bounds__(kT)
     r.status = CVA_INVALID_ARGUMENT;
     rot[p] = make_double2(qnan(), qnan());
   } else {
-    const double2 v = f[m];
+    const double2 v = s_v;
     const double a2 = fma(v.x, v.x, v.y * v.y);
     const double trace = sqrt(a2) * invM;
     const int degenerate = trace == 0.0;
