@@ -571,29 +571,6 @@ int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_beg
 
 // ------------------------------------------------------------- host entries
 
-int cva_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
-                         cva_alignment* out, double* aligned) {
-  if (int rc = check_fft_size(n)) return rc;
-  if (pairs <= 0) return pairs == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative pair count");
-  if (int rc = require_device()) return rc;
-  const size_t cb = sizeof(double) * 2 * (size_t)(pairs * n);
-  DevBuf d1, d2, dout, dal;
-  if (d1.alloc(cb) || d2.alloc(cb) || dout.alloc(sizeof(cva_alignment) * pairs) ||
-      (aligned && dal.alloc(cb)))
-    return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = kHostStream;
-  cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D");
-  if (int rc = cva_align_batch((const double*)d1.p, (const double*)d2.p, pairs, n,
-                               (cva_alignment*)dout.p, aligned ? (double*)dal.p : nullptr, s))
-    return rc;
-  e = cudaMemcpyAsync(out, dout.p, sizeof(cva_alignment) * pairs, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && aligned) e = cudaMemcpyAsync(aligned, dal.p, cb, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  return finish(e, "align_batch_host");
-}
-
 namespace {
 // resample: 0 = center+normalize, 1 = resample+center+normalize, 2 = resample only
 int preprocess_host_impl(const double* points, const int64_t* offsets, int64_t curves,
@@ -793,52 +770,94 @@ int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t ro
   return finish(e, "allpairs_host");
 }
 
+// Host-buffer paths over pairs of uniform curves (c1, c2: pairs x n each),
+// pipelined like cva_preprocess_align_batch_host: every chunk's H2D copies on
+// one stream, its kernels on a second once they have landed, its results back
+// on a third, with the grow-only per-thread device buffers (no per-call
+// cudaMalloc). Chunks of >= ~4 MB of input per curve array; at large N a
+// chunk holds whole internal chunks of the L2-chunked path (large_chunk_pairs).
+}  // extern "C" (the helper below is a template)
+namespace {
+template <class Launch>
+int uniform_pairs_host(const double* c1, const double* c2, int64_t pairs, int64_t n, cva_alignment* out,
+                       double* aligned, Launch launch, const char* what) {
+  if (pairs <= 0) return pairs == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative pair count");
+  if (int rc = require_device()) return rc;
+  if (int rc = t_host.init()) return rc;
+  HostCtx& h = t_host;
+  const size_t cb = sizeof(double2) * (size_t)(pairs * n);
+  double2* d1 = (double2*)h.get(0, cb);
+  double2* d2 = (double2*)h.get(1, cb);
+  cva_alignment* dout = (cva_alignment*)h.get(2, sizeof(cva_alignment) * (size_t)pairs);
+  double2* dal = aligned ? (double2*)h.get(3, cb) : nullptr;
+  if (!d1 || !d2 || !dout || (aligned && !dal)) return fail(CVA_BAD_ALLOC, "device allocation failed");
+  auto drain = [&](int rc) {
+    for (cudaStream_t x : h.st) cudaStreamSynchronize(x);
+    return rc;
+  };
+  const int64_t min_chunk = std::max<int64_t>(1, (int64_t(4) << 20) / (16 * n));
+  const int64_t nchunks = std::min<int64_t>(HostCtx::kMaxChunks, std::max<int64_t>(1, pairs / min_chunk));
+  int64_t per = (pairs + nchunks - 1) / nchunks;
+  if (!pair_fft(n)) {  // whole internal chunks of the large-N path
+    const int64_t g = std::max<int64_t>(1, cva::large_chunk_pairs((int)n));
+    per = std::min<int64_t>(pairs, (per + g - 1) / g * g);
+  }
+  cudaStream_t sin = h.st[0], sk = h.st[1], sout = h.st[2];
+  cudaError_t e = cudaSuccess;
+  int64_t used = 0;
+  for (int64_t p0 = 0, c = 0; p0 < pairs; p0 += per, ++c) {  // all input copies first, in order
+    const size_t bytes = sizeof(double2) * (size_t)(std::min(per, pairs - p0) * n);
+    e = cudaMemcpyAsync(d1 + p0 * n, c1 + 2 * p0 * n, bytes, cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d2 + p0 * n, c2 + 2 * p0 * n, bytes, cudaMemcpyHostToDevice, sin);
+    if (e == cudaSuccess) e = cudaEventRecord(h.in_done[c], sin);
+    if (e != cudaSuccess) return drain(cuda_fail(e, "H2D"));
+    used = c + 1;
+  }
+  for (int64_t c = 0; c < used; ++c) {
+    const int64_t p0 = c * per, np = std::min(per, pairs - p0);
+    e = cudaStreamWaitEvent(sk, h.in_done[c], 0);
+    if (e != cudaSuccess) return drain(cuda_fail(e, "stream wait"));
+    if (int rc = launch((const double*)(d1 + p0 * n), (const double*)(d2 + p0 * n), np, n, dout + p0,
+                        aligned ? (double*)(dal + p0 * n) : nullptr, sk))
+      return drain(rc);
+    e = cudaEventRecord(h.k_done[c], sk);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, h.k_done[c], 0);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(out + p0, dout + p0, sizeof(cva_alignment) * (size_t)np, cudaMemcpyDeviceToHost, sout);
+    if (e == cudaSuccess && aligned)
+      e = cudaMemcpyAsync(aligned + 2 * p0 * n, dal + p0 * n, sizeof(double2) * (size_t)(np * n),
+                          cudaMemcpyDeviceToHost, sout);
+    if (e != cudaSuccess) return drain(cuda_fail(e, "D2H"));
+  }
+  cudaError_t first = cudaSuccess;
+  for (cudaStream_t x : h.st) {
+    e = cudaStreamSynchronize(x);
+    if (first == cudaSuccess) first = e;
+  }
+  return first == cudaSuccess ? CVA_OK : cuda_fail(first, what);
+}
+}  // namespace
+extern "C" {
+
+int cva_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                         cva_alignment* out, double* aligned) {
+  if (int rc = check_fft_size(n)) return rc;
+  return uniform_pairs_host(c1, c2, pairs, n, out, aligned, cva_align_batch, "align_batch_host");
+}
+
 int cva_preprocess_align_uniform_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
                                       cva_alignment* out, double* aligned) {
   if (n < 4) return fail(CVA_INVALID_ARGUMENT, "align: need at least 4 nodes");
   if (int rc = check_fft_size(n)) return rc;
-  if (pairs <= 0) return pairs == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative pair count");
-  if (int rc = require_device()) return rc;
-  const size_t cb = sizeof(double) * 2 * (size_t)(pairs * n);
-  DevBuf d1, d2, dout, dal;
-  if (d1.alloc(cb) || d2.alloc(cb) || dout.alloc(sizeof(cva_alignment) * pairs) || (aligned && dal.alloc(cb)))
-    return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = kHostStream;
-  cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D");
-  if (int rc = cva_preprocess_align_uniform((const double*)d1.p, (const double*)d2.p, pairs, n,
-                                            (cva_alignment*)dout.p, aligned ? (double*)dal.p : nullptr, s))
-    return rc;
-  e = cudaMemcpyAsync(out, dout.p, sizeof(cva_alignment) * pairs, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && aligned) e = cudaMemcpyAsync(aligned, dal.p, cb, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  return finish(e, "preprocess_align_uniform_host");
+  return uniform_pairs_host(c1, c2, pairs, n, out, aligned, cva_preprocess_align_uniform,
+                            "preprocess_align_uniform_host");
 }
 
 int cva_srv_align_batch_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
                              cva_alignment* out, double* aligned_q) {
   if (n < 8) return fail(CVA_INVALID_ARGUMENT, "curve: too few nodes");
   if (int rc = check_fft_size(n)) return rc;
-  if (pairs <= 0) return pairs == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative pair count");
-  if (int rc = require_device()) return rc;
-  const size_t cb = sizeof(double) * 2 * (size_t)(pairs * n);
-  DevBuf d1, d2, dout, dal;
-  if (d1.alloc(cb) || d2.alloc(cb) || dout.alloc(sizeof(cva_alignment) * pairs) ||
-      (aligned_q && dal.alloc(cb)))
-    return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = kHostStream;
-  cudaError_t e = cudaMemcpyAsync(d1.p, c1, cb, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(d2.p, c2, cb, cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D");
-  if (int rc = cva_srv_align_batch((const double*)d1.p, (const double*)d2.p, pairs, n,
-                                   (cva_alignment*)dout.p, aligned_q ? (double*)dal.p : nullptr, s))
-    return rc;
-  e = cudaMemcpyAsync(out, dout.p, sizeof(cva_alignment) * pairs, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && aligned_q)
-    e = cudaMemcpyAsync(aligned_q, dal.p, cb, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  return finish(e, "srv_align_batch_host");
+  return uniform_pairs_host(c1, c2, pairs, n, out, aligned_q, cva_srv_align_batch, "srv_align_batch_host");
 }
 
 // ------------------------------------------------------------- elastic (SRV) matching
