@@ -571,51 +571,6 @@ int cva_allpairs(const double* curves, int64_t count, int64_t n, int64_t row_beg
 
 // ------------------------------------------------------------- host entries
 
-namespace {
-// resample: 0 = center+normalize, 1 = resample+center+normalize, 2 = resample only
-int preprocess_host_impl(const double* points, const int64_t* offsets, int64_t curves,
-                         int64_t n_out, int resample, double* out, int32_t* status) {
-  if (curves <= 0) return curves == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative curve count");
-  if (int rc = require_device()) return rc;
-  const int64_t total = offsets[curves] - offsets[0];
-  if (offsets[0] != 0) return fail(CVA_INVALID_ARGUMENT, "offsets[0] must be 0");
-  const size_t ib = sizeof(double) * 2 * (size_t)total;
-  const size_t ob = resample ? sizeof(double) * 2 * (size_t)(curves * n_out) : ib;
-  DevBuf dp, doff, dout, dst;
-  if (dp.alloc(ib) || doff.alloc(sizeof(int64_t) * (curves + 1)) || dout.alloc(ob) ||
-      dst.alloc(sizeof(int32_t) * curves))
-    return fail(CVA_BAD_ALLOC, "device allocation failed");
-  cudaStream_t s = kHostStream;
-  cudaError_t e = cudaMemcpyAsync(dp.p, points, ib, cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(doff.p, offsets, sizeof(int64_t) * (curves + 1), cudaMemcpyHostToDevice, s);
-  if (e != cudaSuccess) return cuda_fail(e, "H2D");
-  const int rc = resample == 2
-                     ? cva_resample_batch((const double*)dp.p, (const int64_t*)doff.p, curves,
-                                          host_max_n(offsets, curves), n_out, (double*)dout.p,
-                                          (int32_t*)dst.p, s)
-                     : cva_preprocess_batch((const double*)dp.p, (const int64_t*)doff.p, curves,
-                                            host_max_n(offsets, curves), n_out, resample,
-                                            (double*)dout.p, (int32_t*)dst.p, s);
-  if (rc) return rc;
-  e = cudaMemcpyAsync(out, dout.p, ob, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess && status)
-    e = cudaMemcpyAsync(status, dst.p, sizeof(int32_t) * curves, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  return finish(e, "preprocess_batch_host");
-}
-}  // namespace
-
-int cva_preprocess_batch_host(const double* points, const int64_t* offsets, int64_t curves,
-                              int64_t n_out, int resample, double* out, int32_t* status) {
-  return preprocess_host_impl(points, offsets, curves, n_out, resample ? 1 : 0, out, status);
-}
-
-int cva_resample_batch_host(const double* points, const int64_t* offsets, int64_t curves,
-                            int64_t n_out, double* out, int32_t* status) {
-  return preprocess_host_impl(points, offsets, curves, n_out, 2, out, status);
-}
-
 // Per-thread, per-device host-path context: grow-only device buffers and
 // streams reused across calls (no per-call cudaMalloc of hundreds of MB).
 struct HostCtx {
@@ -674,6 +629,60 @@ struct HostCtx {
   }
 };
 thread_local HostCtx t_host;
+
+namespace {
+// resample: 0 = center+normalize, 1 = resample+center+normalize, 2 = resample only
+int preprocess_host_impl(const double* points, const int64_t* offsets, int64_t curves,
+                         int64_t n_out, int resample, double* out, int32_t* status) {
+  if (curves <= 0) return curves == 0 ? CVA_OK : fail(CVA_INVALID_ARGUMENT, "negative curve count");
+  if (int rc = require_device()) return rc;
+  const int64_t total = offsets[curves] - offsets[0];
+  if (offsets[0] != 0) return fail(CVA_INVALID_ARGUMENT, "offsets[0] must be 0");
+  const size_t ib = sizeof(double) * 2 * (size_t)total;
+  const size_t ob = resample ? sizeof(double) * 2 * (size_t)(curves * n_out) : ib;
+  // the grow-only per-thread buffers of the other host paths (no per-call cudaMalloc)
+  if (int rc = t_host.init()) return rc;
+  HostCtx& h = t_host;
+  void* dp = h.get(0, ib);
+  void* doff = h.get(1, sizeof(int64_t) * (curves + 1));
+  void* dout = h.get(2, ob);
+  void* dst = h.get(3, sizeof(int32_t) * curves);
+  if (!dp || !doff || !dout || !dst) return fail(CVA_BAD_ALLOC, "device allocation failed");
+  cudaStream_t s = h.st[1];
+  auto drain = [&](int rc) {
+    cudaStreamSynchronize(s);
+    return rc;
+  };
+  cudaError_t e = cudaMemcpyAsync(dp, points, ib, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(doff, offsets, sizeof(int64_t) * (curves + 1), cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) return drain(cuda_fail(e, "H2D"));
+  const int rc = resample == 2
+                     ? cva_resample_batch((const double*)dp, (const int64_t*)doff, curves,
+                                          host_max_n(offsets, curves), n_out, (double*)dout,
+                                          (int32_t*)dst, s)
+                     : cva_preprocess_batch((const double*)dp, (const int64_t*)doff, curves,
+                                            host_max_n(offsets, curves), n_out, resample,
+                                            (double*)dout, (int32_t*)dst, s);
+  if (rc) return drain(rc);
+  e = cudaMemcpyAsync(out, dout, ob, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && status)
+    e = cudaMemcpyAsync(status, dst, sizeof(int32_t) * curves, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  return finish(e, "preprocess_batch_host");
+}
+}  // namespace
+
+int cva_preprocess_batch_host(const double* points, const int64_t* offsets, int64_t curves,
+                              int64_t n_out, int resample, double* out, int32_t* status) {
+  return preprocess_host_impl(points, offsets, curves, n_out, resample ? 1 : 0, out, status);
+}
+
+int cva_resample_batch_host(const double* points, const int64_t* offsets, int64_t curves,
+                            int64_t n_out, double* out, int32_t* status) {
+  return preprocess_host_impl(points, offsets, curves, n_out, 2, out, status);
+}
+
 
 // Host-buffer fused path, pipelined in chunks of pairs over three streams:
 // all H2D copies back to back on one stream (the step is bound by the host ->
@@ -746,6 +755,9 @@ int cva_preprocess_align_batch_host(const double* points, const int64_t* offsets
   return first == cudaSuccess ? CVA_OK : cuda_fail(first, "preprocess_align_batch_host");
 }
 
+// Host-buffer all-pairs rows: with the warp-per-cell kernel, spectra once, then
+// row chunks whose results go back on a second stream while the next chunk
+// computes (grow-only buffers); other sizes in one call.
 int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t row_begin,
                       int64_t row_end, double* energy, int32_t* shift, double* theta) {
   if (int rc = check_fft_size(n)) return rc;
@@ -753,6 +765,57 @@ int cva_allpairs_host(const double* curves, int64_t count, int64_t n, int64_t ro
     return fail(CVA_INVALID_ARGUMENT, "allpairs: bad row range");
   if (int rc = require_device()) return rc;
   const int64_t cells = (row_end - row_begin) * count;
+  if (cells > 0 && pair_fft(n) && cva::allpairs_fast_supported((int)n)) {
+    if (int rc = t_host.init()) return rc;
+    HostCtx& h = t_host;
+    const int M = cva::v2_fft_len((int)n);
+    const int64_t rows = row_end - row_begin;
+    const int64_t nchunks = std::min<int64_t>(HostCtx::kMaxChunks, std::max<int64_t>(1, rows / 64));
+    const int64_t per = (rows + nchunks - 1) / nchunks;
+    double2* dc = (double2*)h.get(0, sizeof(double2) * (size_t)(count * n));
+    double* de = (double*)h.get(1, sizeof(double) * (size_t)cells);
+    int32_t* dk = (int32_t*)h.get(2, sizeof(int32_t) * (size_t)cells);
+    double* dt = (double*)h.get(3, sizeof(double) * (size_t)cells);
+    if (!dc || !de || !dk || !dt) return fail(CVA_BAD_ALLOC, "device allocation failed");
+    cudaStream_t sk = h.st[1], sout = h.st[2];
+    auto drain = [&](int rc) {
+      for (cudaStream_t x : h.st) cudaStreamSynchronize(x);
+      return rc;
+    };
+    const double2* tw = nullptr;
+    if (int rc = get_twiddles(M, sk, &tw)) return drain(rc);
+    const size_t zbytes = sizeof(double2) * (size_t)(count * M);
+    const size_t sbytes = (sizeof(double) * (size_t)count + 255) & ~size_t(255);
+    void* ws = nullptr;
+    if (scratch_alloc(&ws, zbytes + sbytes + cva::allpairs_scratch_cells(per, count), sk) != cudaSuccess)
+      return drain(fail(CVA_BAD_ALLOC, "scratch allocation failed"));
+    double2* za = (double2*)ws;
+    double* ss = (double*)((char*)ws + zbytes);
+    double2* dm = (double2*)((char*)ws + zbytes + sbytes);
+    cudaError_t e = cudaMemcpyAsync(dc, curves, sizeof(double2) * (size_t)(count * n), cudaMemcpyHostToDevice, sk);
+    if (e == cudaSuccess) e = cva::launch_spectra(dc, count, (int)n, tw, za, za, ss, sk);
+    for (int64_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+      const int64_t r0 = row_begin + c * per, r1 = std::min(row_end, r0 + per);
+      if (r0 >= r1) break;
+      const int64_t o = (r0 - row_begin) * count, nc = (r1 - r0) * count;
+      e = cva::launch_allpairs(za, za, ss, count, r0, r1, tw, de + o, dk + o, dt + o, dm, sk);
+      if (e == cudaSuccess) e = cudaEventRecord(h.k_done[c], sk);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(sout, h.k_done[c], 0);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(energy + o, de + o, sizeof(double) * (size_t)nc, cudaMemcpyDeviceToHost, sout);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(shift + o, dk + o, sizeof(int32_t) * (size_t)nc, cudaMemcpyDeviceToHost, sout);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(theta + o, dt + o, sizeof(double) * (size_t)nc, cudaMemcpyDeviceToHost, sout);
+    }
+    cudaFreeAsync(ws, sk);
+    cudaError_t first = e;
+    for (cudaStream_t x : h.st) {
+      const cudaError_t f = cudaStreamSynchronize(x);
+      if (first == cudaSuccess) first = f;
+    }
+    return first == cudaSuccess ? CVA_OK : cuda_fail(first, "allpairs_host");
+  }
   DevBuf dc, de, dk, dt;
   if (dc.alloc(sizeof(double2) * (size_t)(count * n)) || de.alloc(sizeof(double) * cells) ||
       dk.alloc(sizeof(int32_t) * cells) || dt.alloc(sizeof(double) * cells))
