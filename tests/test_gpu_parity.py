@@ -167,6 +167,45 @@ def test_c3_full_size(cuda, oracle):
         check_pair(res[p], want, u, v, al[p], wal)
 
 
+@pytest.mark.parametrize("n", [4096, 8192, 65536])
+@pytest.mark.parametrize("offset", [(0.0, 0.0), (3.0e3, -7.0e3)])
+def test_large_n_off_origin(cuda, oracle, n, offset):
+    """Large-N path (four-step transforms) on curves away from the origin,
+    normalised (preprocess_align_uniform: the centroid comes from the stats
+    pass) and raw (align_fft_batch). The offset is kept where the reference's
+    own sequential centroid sum stays well inside the 1e-10 bar (at 1e6 and
+    N = 65536 its rounding alone moves the normalised coordinates by ~1e-10)."""
+    rng = np.random.default_rng(n + 7)
+    phi = 2 * PI * np.arange(n) / n
+    r = 1 + 0.25 * np.cos(3 * phi + 0.3) + 0.05 * np.sin(7 * phi)
+    a = np.stack([r * np.cos(phi), r * np.sin(phi)], 1) * 40.0 + np.array(offset)
+    k = int(rng.integers(0, n))
+    th = -1.1
+    rot = np.array([[np.cos(th), np.sin(th)], [-np.sin(th), np.cos(th)]])
+    b = (np.roll(a, k, 0) - a.mean(0)) @ rot + a.mean(0) + 1e-3 * rng.standard_normal((n, 2))
+    A, B = np.stack([a, b]), np.stack([b, a])
+    raw, al = cva.preprocess_align_uniform(A, B, return_aligned=True)
+    res = cva.decode_results(raw)
+    for p in range(2):
+        u = oracle.preprocess(A[p], 0, resample=False)
+        v = oracle.preprocess(B[p], 0, resample=False)
+        want = oracle.align(u, v)
+        c, sn = np.cos(want["theta"]), np.sin(want["theta"])
+        q = v[(np.arange(n) + int(want["shift"])) % n]
+        wal = np.stack([c * q[:, 0] + sn * q[:, 1], -sn * q[:, 0] + c * q[:, 1]], 1)
+        check_pair(res[p], want, u, v, al[p], wal)
+    # raw curves (no centring) near the origin: far from it the rotation of the
+    # uncentred correlation is ill-conditioned for any implementation
+    A0, B0 = A - np.array(offset), B - np.array(offset) + np.array([5.0, -3.0])
+    res2, al2 = cva.align_fft_batch(A0, B0, return_aligned=True)
+    for p in range(2):
+        want = oracle.align(A0[p], B0[p])
+        c, sn = np.cos(want["theta"]), np.sin(want["theta"])
+        q = B0[p][(np.arange(n) + int(want["shift"])) % n]
+        wal = np.stack([c * q[:, 0] + sn * q[:, 1], -sn * q[:, 0] + c * q[:, 1]], 1)
+        check_pair(res2[p], want, A0[p], B0[p], al2[p], wal)
+
+
 def test_uniform_small_n_matches_split_path(cuda):
     """preprocess_align_uniform at small N equals preprocess(resample=False) + align."""
     c1, c2, _, _ = synth.uniform_pairs(5, 6, 256, sigma=1e-3)
