@@ -27,7 +27,24 @@ namespace cva {
 namespace ap {
 
 constexpr int kWarps = 8;
-constexpr int kRowTile = 4;
+// 8 rows per CTA, one CTA of 8 warps per SM with up to 255 registers: each
+// warp keeps its column's spectrum in registers across the rows (one L1 read
+// per column instead of one per cell; the kernel is bound by L1 / shared
+// wavefronts). 2 CTAs of 128 registers spilled that copy (9.9 ms); with it
+// re-read per cell from L1: 8.85 ms; this: 8.55 ms (C2 step).
+#ifndef CVA_AP_ROWS
+#define CVA_AP_ROWS 8
+#endif
+constexpr int kRowTile = CVA_AP_ROWS;
+#ifndef CVA_AP_ZC_REG
+#define CVA_AP_ZC_REG 1
+#endif
+#ifndef CVA_AP_TW_REG
+#define CVA_AP_TW_REG 0
+#endif
+#ifndef CVA_AP_MINB
+#define CVA_AP_MINB 1
+#endif
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
 
@@ -126,7 +143,7 @@ constexpr int kR = 8;
 constexpr int kB = kM / kR / 32;  // 2
 constexpr int kNB = kM / kR;      // 64
 
-__global__ void __launch_bounds__(kWarps * 32, 2)
+__global__ void __launch_bounds__(kWarps * 32, CVA_AP_MINB)
     allpairs_kernel(const double2* __restrict__ za, const double2* __restrict__ zb,
                     const double* __restrict__ ss, int64_t count, int64_t row_begin, int64_t row_end,
                     int64_t col_chunk, const double2* __restrict__ tw, double* energy,
@@ -152,12 +169,29 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
       s_t3[r - 1][q - 8] = __ldg(&tw[r * (q - 8) * (kM / (64 * kR))]);
   }
   __syncthreads();
+#if CVA_AP_TW_REG
+  // this lane's pass-2 / pass-3 twiddles in registers (the same for every cell)
+  double2 t2r[kR - 1], t3r[kB][kR - 1];
+#pragma unroll
+  for (int r = 1; r < kR; ++r) {
+    t2r[r - 1] = s_t2[r - 1][lane & 7];
+#pragma unroll
+    for (int b = 0; b < kB; ++b) t3r[b][r - 1] = s_t3[r - 1][lane + 32 * b];
+  }
+#endif
   const int64_t j_begin = (int64_t)blockIdx.y * col_chunk;
   const int64_t j_end = min(count, j_begin + col_chunk);
   for (int64_t j = j_begin + warp; j < j_end; j += kWarps) {
-    // the column spectrum is re-read per row through L1 (8 KB per warp)
     const double2* zc = zb + j * kM;
     const double sj = __ldg(&ss[j]);
+#if CVA_AP_ZC_REG
+    // the column spectrum in registers across the CTA's rows (one L1 read per column)
+    double2 cz[kB][kR];
+#pragma unroll
+    for (int b = 0; b < kB; ++b)
+#pragma unroll
+      for (int r = 0; r < kR; ++r) cz[b][r] = __ldg(&zc[lane + 32 * b + r * kNB]);
+#endif
     for (int rr = 0; rr < nrows; ++rr) {
       const double2* zr = rows + rr * kM;
       double2 v[kB][kR];
@@ -165,7 +199,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
 #pragma unroll
       for (int b = 0; b < kB; ++b)
 #pragma unroll
-        for (int r = 0; r < kR; ++r) v[b][r] = cmulconj(zr[lane + 32 * b + r * kNB], __ldg(&zc[lane + 32 * b + r * kNB]));
+        for (int r = 0; r < kR; ++r)
+#if CVA_AP_ZC_REG
+          v[b][r] = cmulconj(zr[lane + 32 * b + r * kNB], cz[b][r]);
+#else
+          v[b][r] = cmulconj(zr[lane + 32 * b + r * kNB], __ldg(&zc[lane + 32 * b + r * kNB]));
+#endif
       warp_compute<kM, kR>(v, 1, lane, tw);
       warp_store<kM, kR>(v, buf, 1, lane);
       __syncwarp();
@@ -174,7 +213,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
 #pragma unroll
       for (int b = 0; b < kB; ++b) {
 #pragma unroll
-        for (int r = 1; r < kR; ++r) v[b][r] = cmul(v[b][r], s_t2[r - 1][lane & 7]);
+        for (int r = 1; r < kR; ++r)
+#if CVA_AP_TW_REG
+          v[b][r] = cmul(v[b][r], t2r[r - 1]);
+#else
+          v[b][r] = cmul(v[b][r], s_t2[r - 1][lane & 7]);
+#endif
         dft_r<kR>(v[b]);
       }
       warp_store<kM, kR>(v, buf, 8, lane);
@@ -183,7 +227,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2)
 #pragma unroll
       for (int b = 0; b < kB; ++b) {
 #pragma unroll
-        for (int r = 1; r < kR; ++r) v[b][r] = cmul(v[b][r], s_t3[r - 1][lane + 32 * b]);
+        for (int r = 1; r < kR; ++r)
+#if CVA_AP_TW_REG
+          v[b][r] = cmul(v[b][r], t3r[b][r - 1]);
+#else
+          v[b][r] = cmul(v[b][r], s_t3[r - 1][lane + 32 * b]);
+#endif
         dft_r<kR>(v[b]);
       }
       // last pass output index of v[b][r]: base + r * 64 with base = j (Ns = 64 = nb)

@@ -8,7 +8,7 @@ mkdir -p build/var_$name
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $*"
 objs=""
-for f in kernels fused allpairs largen elastic dropin_kernels probe; do
+for f in kernels fused allpairs largen elastic dropin_kernels gfft probe; do
   /usr/local/cuda/bin/nvcc $FL -c paper_2501_17779_b200/csrc/$f.cu -o build/var_$name/$f.o &
   objs="$objs build/var_$name/$f.o"
 done
