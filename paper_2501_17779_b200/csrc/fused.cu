@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
   const double m2x = mean[1].x, m2y = mean[1].y;
   const double invn = 1.0 / (double)N;  // srv_center (srv.cpp:90-98)
   pf::PairIn in{qa, qb, make_double2(invn * m1.x, invn * m1.y), make_double2(invn * m2x, invn * m2y), 1.0, 1.0, b};
-  pf::pair_stage<kIP, kN, false, 2>(in, bufs, N, tw, out + p, al, red);
+  pf::pair_stage<kIP, kN, false, 2, kT, 2048, true>(in, bufs, N, tw, out + p, al, red);
 }
 
 // srv_center(srv_transform(c)) of one curve per CTA into global memory, any
@@ -438,7 +438,8 @@ __global__ void __launch_bounds__(rs3::kT, 2)
   }
   __syncthreads();
   pf::PairIn in{Z1, Z2, A.centroid, B.centroid, 1.0, 1.0};
-  pf::pair_stage<false, N, true, 0>(in, reinterpret_cast<double2*>(smem), N, tw, out + p, al, red);
+  pf::pair_stage<false, N, true, 0, rs3::kT, 2048, true>(in, reinterpret_cast<double2*>(smem), N, tw, out + p, al,
+                                                         red);
 }
 
 }  // namespace v3

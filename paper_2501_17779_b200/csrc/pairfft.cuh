@@ -329,7 +329,10 @@ __host__ __device__ inline int fft_len(int N) {
 // is not finite and > 0 marks the pair invalid (preprocess: curve.cpp:41-48).
 // kPad: 1 = in.z1 is shared memory in the padded layout z1[l + (l >> 3)]
 // (the resampler's and the transform buffers' layout); 2 = in.z1 and in.z2 both.
-template <bool kInPlace = false, int kN = 0, bool kLenOnLoad = false, int kPad = 0, int kCT = kT, int kIPM = 2048>
+// kDirectOut: `aligned` never aliases in.z2 (shared z2 or srv2, global output),
+// so the aligned curve is written as it is formed (no register copy, no barrier).
+template <bool kInPlace = false, int kN = 0, bool kLenOnLoad = false, int kPad = 0, int kCT = kT, int kIPM = 2048,
+          bool kDirectOut = false>
 __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
                                   const double2* __restrict__ tw, cva_alignment* out,
                                   double2* aligned, double2* red) {
@@ -529,7 +532,22 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   }
 
   // ---- aligned[l] = R(theta) z2'[(l + m) mod N]  (geometry.hpp:70-73; elastic.cpp:80)
-  if (aligned != nullptr) {
+  if (kDirectOut && aligned != nullptr) {
+    const double2 c = in.g2;
+    const double sc = psc.sc2;
+    const int mm = ok ? m : 0;
+#pragma unroll
+    for (int q = 0; q < kMaxPer; ++q) {
+      const int j = t + q * kCT;
+      if (j < N) {
+        const double2 z = in.srv2 ? srv_at(in.srv2, j, N) : in.z2[kPad == 2 ? j + (j >> 3) : j];
+        const double2 pz = make_double2((z.x - c.x) * sc, (z.y - c.y) * sc);
+        int l = j - mm;
+        if (l < 0) l += N;
+        aligned[l] = make_double2(fma(rot.x, pz.x, rot.y * pz.y), fma(-rot.y, pz.x, rot.x * pz.y));
+      }
+    }
+  } else if (aligned != nullptr) {
     double2 v[kMaxPer];
     const double2 c = in.g2;
     const double sc = psc.sc2;
