@@ -220,9 +220,11 @@ int cva_dp_reparam_batch_host(const double* q1, const double* q2, int64_t pairs,
  * preprocessed curves (pairs x n points each). Outputs per pair: distance,
  * energy, t0, theta (Rotation2 angle), gamma (nullable, pairs x (n+1)),
  * iterations, converged, status, energy_trace (nullable, pairs x (max_iters+1):
- * ElasticMatch::energy_trace, NaN after the last iteration). The GPU always uses the FFT correlation
- * (use_fft = true); ElasticOptions defaults: max_iters 30, energy_tol 1e-6,
- * max_slope 4. Supports 8 <= n <= 2^20 and 1 <= max_slope <= 20; n <= 1024
+ * ElasticMatch::energy_trace, NaN after the last iteration). The rigid steps
+ * use the FFT correlation (ElasticOptions::use_fft = true: align_fft); the
+ * _ex entry points take use_fft, and 0 runs them on the direct per-shift sums
+ * (align_naive, rigid_align.cpp:198-202). ElasticOptions defaults: max_iters
+ * 30, energy_tol 1e-6, use_fft 1, max_slope 4. Supports 8 <= n <= 2^20 and 1 <= max_slope <= 20; n <= 1024
  * (non-powers of two <= 512) with max_slope <= 8 run the shared-memory
  * kernels, anything else slab mode (per-CTA global working set, direct
  * correlation for the rigid steps). */
@@ -236,6 +238,16 @@ int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t
                                      double* energy, double* t0, double* theta, double* gamma,
                                      int32_t* iterations, int32_t* converged, int32_t* status,
                                      double* energy_trace);
+int cva_elastic_approach2_batch_ex(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                   int max_iters, double energy_tol, int max_slope, int use_fft,
+                                   double* distance, double* energy, double* t0, double* theta, double* gamma,
+                                   int32_t* iterations, int32_t* converged, int32_t* status,
+                                   double* energy_trace, void* stream);
+int cva_elastic_approach2_batch_ex_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                        int max_iters, double energy_tol, int max_slope, int use_fft,
+                                        double* distance, double* energy, double* t0, double* theta,
+                                        double* gamma, int32_t* iterations, int32_t* converged, int32_t* status,
+                                        double* energy_trace);
 
 /* elastic_distance_approach1(c1[p], c2[p], opts) (elastic.cpp:62-100): for every
  * start shift m, the Kabsch rotation of the SRV pair, one DP, the realised
@@ -259,6 +271,12 @@ int cva_elastic_distance_matrix(const double* curves, int64_t count, int64_t n, 
                                 void* stream);
 int cva_elastic_distance_matrix_host(const double* curves, int64_t count, int64_t n, int method, int max_iters,
                                      double energy_tol, int max_slope, int64_t n_max_approach1, double* d);
+int cva_elastic_distance_matrix_ex(const double* curves, int64_t count, int64_t n, int method, int max_iters,
+                                   double energy_tol, int max_slope, int use_fft, int64_t n_max_approach1,
+                                   double* d, void* stream);
+int cva_elastic_distance_matrix_ex_host(const double* curves, int64_t count, int64_t n, int method,
+                                        int max_iters, double energy_tol, int max_slope, int use_fft,
+                                        int64_t n_max_approach1, double* d);
 
 /* Single-call SRV utilities behind the C++ drop-in (synchronous, host buffers,
  * GPU compute; failures in cva_dropin_last_error()):

@@ -111,6 +111,16 @@ SIGNATURES = {
         [c_void_p, c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
          c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
     ),
+    "cva_elastic_approach2_batch_ex": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_int, c_void_p, c_void_p, c_void_p,
+         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
+    "cva_elastic_approach2_batch_ex_host": (
+        c_int,
+        [c_void_p, c_void_p, c_int64, c_int64, c_int, c_double, c_int, c_int, c_void_p, c_void_p, c_void_p,
+         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p],
+    ),
     "cva_elastic_approach1_batch": (
         c_int,
         [c_void_p, c_void_p, c_int64, c_int64, c_int, c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
@@ -125,6 +135,10 @@ SIGNATURES = {
                                             c_void_p, c_void_p]),
     "cva_elastic_distance_matrix_host": (c_int, [c_void_p, c_int64, c_int64, c_int, c_int, c_double, c_int,
                                                  c_int64, c_void_p]),
+    "cva_elastic_distance_matrix_ex": (c_int, [c_void_p, c_int64, c_int64, c_int, c_int, c_double, c_int, c_int,
+                                               c_int64, c_void_p, c_void_p]),
+    "cva_elastic_distance_matrix_ex_host": (c_int, [c_void_p, c_int64, c_int64, c_int, c_int, c_double, c_int, c_int,
+                                                    c_int64, c_void_p]),
     "cva_apply_srv_action_host": (c_int, [c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p]),
     "cva_elastic_energy_host": (c_int, [c_void_p, c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p]),
     "cva_dp_step_cost_host": (c_int, [c_void_p, c_void_p, c_int64, c_int, c_int, c_int, c_int, c_void_p]),

@@ -400,7 +400,8 @@ def dp_reparam(q1, q2, max_slope: int = 4):
     return g[0], float(e[0])
 
 
-def _elastic_batch(approach, c1, c2, max_iters, energy_tol, max_slope, n_max_approach1, return_gamma):
+def _elastic_batch(approach, c1, c2, max_iters, energy_tol, max_slope, n_max_approach1, return_gamma,
+                   use_fft=True):
     lib = _native.load()
     if _is_cuda_tensor(c1):
         a, b = c1.contiguous(), c2.contiguous()
@@ -417,8 +418,9 @@ def _elastic_batch(approach, c1, c2, max_iters, energy_tol, max_slope, n_max_app
                                                   *ptrs, _stream_of(a)))
         else:
             tr = torch.empty((pairs, max_iters + 1), dtype=torch.float64, device=dev)
-            check(lib.cva_elastic_approach2_batch(a.data_ptr(), b.data_ptr(), pairs, n, max_iters, energy_tol,
-                                                  max_slope, *ptrs, tr.data_ptr(), _stream_of(a)))
+            check(lib.cva_elastic_approach2_batch_ex(a.data_ptr(), b.data_ptr(), pairs, n, max_iters, energy_tol,
+                                                     max_slope, int(bool(use_fft)), *ptrs, tr.data_ptr(),
+                                                     _stream_of(a)))
             out["energy_trace"] = tr
     else:
         a, b = _f64c(c1), _f64c(c2)
@@ -435,8 +437,8 @@ def _elastic_batch(approach, c1, c2, max_iters, energy_tol, max_slope, n_max_app
             check(lib.cva_elastic_approach1_batch_host(_ptr(a), _ptr(b), pairs, n, max_slope, n_max_approach1, *ptrs))
         else:
             tr = np.empty((pairs, max_iters + 1))
-            check(lib.cva_elastic_approach2_batch_host(_ptr(a), _ptr(b), pairs, n, max_iters, energy_tol, max_slope,
-                                                       *ptrs, tr.ctypes.data))
+            check(lib.cva_elastic_approach2_batch_ex_host(_ptr(a), _ptr(b), pairs, n, max_iters, energy_tol,
+                                                          max_slope, int(bool(use_fft)), *ptrs, tr.ctypes.data))
             out["energy_trace"] = tr
     if return_gamma:
         out["gamma"] = g
@@ -444,13 +446,14 @@ def _elastic_batch(approach, c1, c2, max_iters, energy_tol, max_slope, n_max_app
 
 
 def elastic_approach2_batch(c1, c2, max_iters: int = 30, energy_tol: float = 1e-6, max_slope: int = 4,
-                            return_gamma: bool = False):
+                            return_gamma: bool = False, use_fft: bool = True):
     """elastic_distance_approach2 (elastic.cpp:102-174) per pair of preprocessed
     curves ``(pairs, n, 2)``. Returns a dict of per-pair arrays: distance,
     energy, t0, theta, iterations, converged, status, energy_trace (pairs x
     (max_iters+1), NaN-padded) (+ gamma). numpy in -> numpy out; CUDA tensors in ->
-    CUDA tensors out (stream-ordered)."""
-    return _elastic_batch(2, c1, c2, max_iters, energy_tol, max_slope, 512, return_gamma)
+    CUDA tensors out (stream-ordered). use_fft (ElasticOptions::use_fft): the
+    rigid steps by the FFT correlation (align_fft) or the direct sums (align_naive)."""
+    return _elastic_batch(2, c1, c2, max_iters, energy_tol, max_slope, 512, return_gamma, use_fft)
 
 
 def elastic_approach1_batch(c1, c2, max_slope: int = 4, n_max_approach1: int = 512, return_gamma: bool = False):
@@ -471,13 +474,14 @@ def _match(r):
 
 
 def elastic_distance_approach2(c1, c2, max_iters: int = 30, energy_tol: float = 1e-6,
-                               max_slope: int = 4) -> ElasticMatch:
+                               max_slope: int = 4, use_fft: bool = True) -> ElasticMatch:
     """Single pair (reference name and exceptions: ValueError for invalid input,
     RuntimeError for a DP without admissible path)."""
     a, b = np.asarray(c1, dtype=np.float64), np.asarray(c2, dtype=np.float64)
     if a.shape != b.shape:
         raise ValueError("elastic: node count mismatch")
-    return _match(elastic_approach2_batch(a[None], b[None], max_iters, energy_tol, max_slope, return_gamma=True))
+    return _match(elastic_approach2_batch(a[None], b[None], max_iters, energy_tol, max_slope, return_gamma=True,
+                                          use_fft=use_fft))
 
 
 def elastic_distance_approach1(c1, c2, max_slope: int = 4, n_max_approach1: int = 512) -> ElasticMatch:
@@ -489,7 +493,7 @@ def elastic_distance_approach1(c1, c2, max_slope: int = 4, n_max_approach1: int 
 
 
 def elastic_distance_matrix(curves, method: int = 2, max_iters: int = 30, energy_tol: float = 1e-6,
-                            max_slope: int = 4, n_max_approach1: int = 512):
+                            max_slope: int = 4, n_max_approach1: int = 512, use_fft: bool = True):
     """distance_matrix cells (elastic.cpp:176-236) on already preprocessed curves
     ``(count, n, 2)``: d[i, j] = distance matching curve j onto curve i (method 1:
     approach 1, 2: approach 2), NaN for a failed pair."""
@@ -498,19 +502,19 @@ def elastic_distance_matrix(curves, method: int = 2, max_iters: int = 30, energy
         c = curves.contiguous()
         count, n = c.shape[0], c.shape[1]
         d = torch.empty((count, count), dtype=torch.float64, device=c.device)
-        check(lib.cva_elastic_distance_matrix(c.data_ptr(), count, n, method, max_iters, energy_tol, max_slope,
-                                              n_max_approach1, d.data_ptr(), _stream_of(c)))
+        check(lib.cva_elastic_distance_matrix_ex(c.data_ptr(), count, n, method, max_iters, energy_tol, max_slope,
+                                                 int(bool(use_fft)), n_max_approach1, d.data_ptr(), _stream_of(c)))
         return d
     c = _f64c(curves)
     count, n = c.shape[0], c.shape[1]
     d = np.empty((count, count))
-    check(lib.cva_elastic_distance_matrix_host(_ptr(c), count, n, method, max_iters, energy_tol, max_slope,
-                                               n_max_approach1, d.ctypes.data))
+    check(lib.cva_elastic_distance_matrix_ex_host(_ptr(c), count, n, method, max_iters, energy_tol, max_slope,
+                                                  int(bool(use_fft)), n_max_approach1, d.ctypes.data))
     return d
 
 
 def distance_matrix(curves, n: int, method: int = 2, max_iters: int = 30, energy_tol: float = 1e-6,
-                    max_slope: int = 4, n_max_approach1: int = 512):
+                    max_slope: int = 4, n_max_approach1: int = 512, use_fft: bool = True):
     """distance_matrix(curves, method, n) (elastic.cpp:176-236): raw curves (a
     list of ``(n_i, 2)`` arrays) are preprocessed to n nodes on the GPU, then every
     ordered pair is matched (method 1: approach 1, 2: approach 2)."""
@@ -520,7 +524,7 @@ def distance_matrix(curves, n: int, method: int = 2, max_iters: int = 30, energy
     prep, st = preprocess_batch(pts, offs, n)
     if (st != 0).any():
         raise ValueError("distance_matrix: invalid curve")
-    return elastic_distance_matrix(prep, method, max_iters, energy_tol, max_slope, n_max_approach1)
+    return elastic_distance_matrix(prep, method, max_iters, energy_tol, max_slope, n_max_approach1, use_fft)
 
 
 def apply_srv_action(q, t0: float, theta: float, gamma) -> np.ndarray:

@@ -966,7 +966,7 @@ int cva_dp_reparam_batch(const double* q1, const double* q2, int64_t pairs, int6
 }
 
 static int elastic_launch(const double* A, const double* B, int64_t pairs, int64_t k, int64_t n, int max_iters,
-                          double energy_tol, int max_slope, const cva::ElasticOut& o, cudaStream_t s) {
+                          double energy_tol, int max_slope, int use_fft, const cva::ElasticOut& o, cudaStream_t s) {
   const double2* tw = nullptr;  // slab mode aligns by the direct correlation (no transform)
   if (!cva::elastic_slab_mode((int)n, max_slope))
     if (int rc = get_twiddles(cva::v2_fft_len((int)n), s, &tw)) return rc;
@@ -976,7 +976,7 @@ static int elastic_launch(const double* A, const double* B, int64_t pairs, int64
   const size_t per = cva::elastic_parent_slab(pairs, (int)n, max_slope);
   if (per && scratch_alloc(&slab.p, per * (size_t)grid, s) != cudaSuccess)
     return fail(CVA_BAD_ALLOC, "elastic: parent scratch allocation failed");
-  const cva::ElasticParams prm{max_iters, energy_tol, max_slope};
+  const cva::ElasticParams prm{max_iters, energy_tol, max_slope, use_fft ? 1 : 0};
   return finish(cva::launch_elastic_approach2((const double2*)A, (const double2*)B, pairs, k, (int)n, prm,
                                               (uint8_t*)slab.p, grid, tw, o, s),
                 "elastic launch");
@@ -987,6 +987,15 @@ int cva_elastic_approach2_batch(const double* c1, const double* c2, int64_t pair
                                 double* energy, double* t0, double* theta, double* gamma,
                                 int32_t* iterations, int32_t* converged, int32_t* status,
                                 double* energy_trace, void* stream) {
+  return cva_elastic_approach2_batch_ex(c1, c2, pairs, n, max_iters, energy_tol, max_slope, 1, distance, energy,
+                                        t0, theta, gamma, iterations, converged, status, energy_trace, stream);
+}
+
+int cva_elastic_approach2_batch_ex(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                   int max_iters, double energy_tol, int max_slope, int use_fft,
+                                   double* distance, double* energy, double* t0, double* theta, double* gamma,
+                                   int32_t* iterations, int32_t* converged, int32_t* status,
+                                   double* energy_trace, void* stream) {
   if (int rc = check_elastic(pairs, n, max_slope, "elastic")) return rc;
   if (pairs == 0) return CVA_OK;
   if (!c1 || !c2 || !distance || !energy || !t0 || !theta || !iterations || !converged || !status)
@@ -995,7 +1004,7 @@ int cva_elastic_approach2_batch(const double* c1, const double* c2, int64_t pair
   if (int rc = require_device()) return rc;
   if (max_iters < 0) return fail(CVA_INVALID_ARGUMENT, "elastic: negative max_iters");
   const cva::ElasticOut o{distance, energy, t0, theta, gamma, iterations, converged, status, energy_trace};
-  return elastic_launch(c1, c2, pairs, 0, n, max_iters, energy_tol, max_slope, o, (cudaStream_t)stream);
+  return elastic_launch(c1, c2, pairs, 0, n, max_iters, energy_tol, max_slope, use_fft, o, (cudaStream_t)stream);
 }
 
 // Approach 1 keeps per-item results until the per-pair pick. With gamma wanted
@@ -1067,6 +1076,13 @@ int cva_elastic_approach1_batch(const double* c1, const double* c2, int64_t pair
 int cva_elastic_distance_matrix(const double* curves, int64_t count, int64_t n, int method, int max_iters,
                                 double energy_tol, int max_slope, int64_t n_max_approach1, double* d,
                                 void* stream) {
+  return cva_elastic_distance_matrix_ex(curves, count, n, method, max_iters, energy_tol, max_slope, 1,
+                                        n_max_approach1, d, stream);
+}
+
+int cva_elastic_distance_matrix_ex(const double* curves, int64_t count, int64_t n, int method, int max_iters,
+                                   double energy_tol, int max_slope, int use_fft, int64_t n_max_approach1,
+                                   double* d, void* stream) {
   if (count < 2) return fail(CVA_INVALID_ARGUMENT, "distance_matrix: need at least 2 curves");  // elastic.cpp:181
   if (method != 1 && method != 2) return fail(CVA_INVALID_ARGUMENT, "distance_matrix: method is 1 or 2");
   if (int rc = check_elastic(count * count, n, max_slope, "distance_matrix")) return rc;
@@ -1089,7 +1105,8 @@ int cva_elastic_distance_matrix(const double* curves, int64_t count, int64_t n, 
   cva::ElasticOut o{d, e, e + pairs, e + 2 * pairs, nullptr, (int32_t*)(e + 3 * pairs),
                     (int32_t*)(e + 3 * pairs) + pairs, (int32_t*)(e + 3 * pairs) + 2 * pairs, nullptr};
   const int rc = method == 1 ? approach1_launch(curves, nullptr, pairs, count, n, max_slope, o, s)
-                             : elastic_launch(curves, nullptr, pairs, count, n, max_iters, energy_tol, max_slope, o, s);
+                             : elastic_launch(curves, nullptr, pairs, count, n, max_iters, energy_tol, max_slope, use_fft,
+                                              o, s);
   cudaFreeAsync(ws, s);
   return rc;
 }
@@ -1123,6 +1140,15 @@ int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t
                                      double* energy, double* t0, double* theta, double* gamma,
                                      int32_t* iterations, int32_t* converged, int32_t* status,
                                      double* energy_trace) {
+  return cva_elastic_approach2_batch_ex_host(c1, c2, pairs, n, max_iters, energy_tol, max_slope, 1, distance,
+                                             energy, t0, theta, gamma, iterations, converged, status, energy_trace);
+}
+
+int cva_elastic_approach2_batch_ex_host(const double* c1, const double* c2, int64_t pairs, int64_t n,
+                                        int max_iters, double energy_tol, int max_slope, int use_fft,
+                                        double* distance, double* energy, double* t0, double* theta,
+                                        double* gamma, int32_t* iterations, int32_t* converged, int32_t* status,
+                                        double* energy_trace) {
   if (int rc = check_elastic(pairs, n, max_slope, "elastic")) return rc;
   if (max_iters < 0) return fail(CVA_INVALID_ARGUMENT, "elastic: negative max_iters");
   if (pairs == 0) return CVA_OK;
@@ -1140,10 +1166,10 @@ int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t
   if (e != cudaSuccess) return cuda_fail(e, "H2D");
   double* v = (double*)dv.p;
   int32_t* iv = (int32_t*)di.p;
-  if (int rc = cva_elastic_approach2_batch((const double*)d1.p, (const double*)d2.p, pairs, n, max_iters,
-                                           energy_tol, max_slope, v, v + pairs, v + 2 * pairs, v + 3 * pairs,
-                                           gamma ? (double*)dg.p : nullptr, iv, iv + pairs, iv + 2 * pairs,
-                                           energy_trace ? (double*)dt.p : nullptr, s))
+  if (int rc = cva_elastic_approach2_batch_ex((const double*)d1.p, (const double*)d2.p, pairs, n, max_iters,
+                                              energy_tol, max_slope, use_fft, v, v + pairs, v + 2 * pairs,
+                                              v + 3 * pairs, gamma ? (double*)dg.p : nullptr, iv, iv + pairs,
+                                              iv + 2 * pairs, energy_trace ? (double*)dt.p : nullptr, s))
     return rc;
   double* hv[4] = {distance, energy, t0, theta};
   for (int k = 0; k < 4 && e == cudaSuccess; ++k)
@@ -1159,6 +1185,13 @@ int cva_elastic_approach2_batch_host(const double* c1, const double* c2, int64_t
 
 int cva_elastic_distance_matrix_host(const double* curves, int64_t count, int64_t n, int method, int max_iters,
                                      double energy_tol, int max_slope, int64_t n_max_approach1, double* d) {
+  return cva_elastic_distance_matrix_ex_host(curves, count, n, method, max_iters, energy_tol, max_slope, 1,
+                                             n_max_approach1, d);
+}
+
+int cva_elastic_distance_matrix_ex_host(const double* curves, int64_t count, int64_t n, int method,
+                                        int max_iters, double energy_tol, int max_slope, int use_fft,
+                                        int64_t n_max_approach1, double* d) {
   if (count < 2) return fail(CVA_INVALID_ARGUMENT, "distance_matrix: need at least 2 curves");
   if (int rc = check_elastic(count * count, n, max_slope, "distance_matrix")) return rc;
   if (int rc = require_device()) return rc;
@@ -1168,8 +1201,8 @@ int cva_elastic_distance_matrix_host(const double* curves, int64_t count, int64_
   cudaStream_t s = kHostStream;
   cudaError_t e = cudaMemcpyAsync(dc.p, curves, cb, cudaMemcpyHostToDevice, s);
   if (e != cudaSuccess) return cuda_fail(e, "H2D");
-  if (int rc = cva_elastic_distance_matrix((const double*)dc.p, count, n, method, max_iters, energy_tol, max_slope,
-                                           n_max_approach1, (double*)dd.p, s))
+  if (int rc = cva_elastic_distance_matrix_ex((const double*)dc.p, count, n, method, max_iters, energy_tol,
+                                              max_slope, use_fft, n_max_approach1, (double*)dd.p, s))
     return rc;
   e = cudaMemcpyAsync(d, dd.p, db, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);

@@ -43,10 +43,10 @@ Batch run(const std::vector<Point2>& a, const std::vector<Point2>& b, int64_t pa
   else {
     r.trace_len = o.max_iters + 1;
     r.trace.resize((size_t)pairs * r.trace_len);
-    check(cva_elastic_approach2_batch_host(raw(a.data()), raw(b.data()), pairs, n, o.max_iters, o.energy_tol,
-                                           o.max_slope, r.distance.data(), r.energy.data(), r.t0.data(),
-                                           r.theta.data(), g, r.iterations.data(), r.converged.data(),
-                                           r.status.data(), r.trace.data()));
+    check(cva_elastic_approach2_batch_ex_host(raw(a.data()), raw(b.data()), pairs, n, o.max_iters, o.energy_tol,
+                                              o.max_slope, o.use_fft ? 1 : 0, r.distance.data(), r.energy.data(),
+                                              r.t0.data(), r.theta.data(), g, r.iterations.data(),
+                                              r.converged.data(), r.status.data(), r.trace.data()));
   }
   return r;
 }
@@ -116,9 +116,10 @@ std::vector<std::vector<double>> distance_matrix(const std::vector<Curve>& curve
     prep.insert(prep.end(), p.nodes.begin(), p.nodes.end());
   const std::size_t k = curves.size();
   std::vector<double> d(k * k);
-  check(cva_elastic_distance_matrix_host(raw(prep.data()), (int64_t)k, (int64_t)n,
-                                         method == DistanceMethod::approach1 ? 1 : 2, opts.max_iters, opts.energy_tol,
-                                         opts.max_slope, (int64_t)opts.n_max_approach1, d.data()));
+  check(cva_elastic_distance_matrix_ex_host(raw(prep.data()), (int64_t)k, (int64_t)n,
+                                            method == DistanceMethod::approach1 ? 1 : 2, opts.max_iters,
+                                            opts.energy_tol, opts.max_slope, opts.use_fft ? 1 : 0,
+                                            (int64_t)opts.n_max_approach1, d.data()));
   std::vector<std::vector<double>> out(k, std::vector<double>(k));
   const double secs =
       std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count() / (double)(k * k);

@@ -713,8 +713,7 @@ __device__ cva_alignment align_direct(const double2* a, const double2* b, int n,
 #pragma unroll
     for (int q = 0; q < kB; ++q) {
       acc[q] = make_double2(0.0, 0.0);
-      j[q] = m0 + q * kT;
-      if (j[q] >= n) j[q] -= n;  // padding lanes (discarded) stay in range
+      j[q] = (m0 + q * kT) % n;  // padding lanes (m >= n, discarded) stay in range
     }
     for (int l = 0; l < n; ++l) {
       const double2 x = a[l];
@@ -887,12 +886,15 @@ __global__ void __launch_bounds__(kT, CVA_EL_MINB)
   Smem& S = wk.S;
   uint8_t* parent = wk.parent;
   const double qnan = __longlong_as_double(0x7ff8000000000000LL);
-  // rigid alignment of two curves held in S (align_fft semantics)
+  // rigid alignment of two curves held in S: align_fft, or with use_fft = 0
+  // (and in slab mode) the direct per-shift sums (align_naive's semantics)
   auto rigid = [&](const double2* a, const double2* b) {
-    if constexpr (kSlab)
+    if constexpr (kSlab) {
       return align_direct(a, b, n, wk.D, red);
-    else
+    } else {
+      if (!prm.use_fft) return align_direct(a, b, n, S.fft, red);  // the transform buffers as scratch
       return align<kN>(a, b, n, S, tw, red);
+    }
   };
   for (int64_t p = blockIdx.x; p < pairs; p += gridDim.x) {
     const double2* c1 = matrix_k ? A + (p / matrix_k) * n : A + p * n;

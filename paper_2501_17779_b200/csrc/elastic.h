@@ -11,6 +11,7 @@ struct ElasticParams {
   int max_iters;      // ElasticOptions::max_iters (proj/include/curvalign/elastic.hpp:14)
   double energy_tol;  // ElasticOptions::energy_tol
   int max_slope;      // ElasticOptions::max_slope (DP step bound W)
+  int use_fft = 1;    // ElasticOptions::use_fft: rigid steps by align_fft (1) or the direct sums (0)
 };
 
 struct ElasticOut {

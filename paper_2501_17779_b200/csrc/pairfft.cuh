@@ -460,16 +460,28 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   constexpr int kMaxPer = kInPlace ? 8 : 4;  // N <= 2048 in-place, N <= 1024 otherwise
   const double invN = 1.0 / (double)N;  // h = 1/N (rigid_align.cpp:56)
   const double invM = 1.0 / (double)M;  // D_m = conj(F_m) / M
-  double mag2[kMaxPer];
+  // (the magnitudes are recomputed from shared memory for the band test
+  // rather than held in registers across the block reduction: CVA_MAG_REREAD)
+#ifndef CVA_MAG_REREAD
+#define CVA_MAG_REREAD 1
+#endif
   double best2 = -1.0;
+#if !CVA_MAG_REREAD
+  double mag2[kMaxPer];
+#endif
 #pragma unroll
   for (int q = 0; q < kMaxPer; ++q) {
     const int k = t + q * kCT;
+#if !CVA_MAG_REREAD
     mag2[q] = -1.0;
+#endif
     if (k < N) {
       const double2 f = F[pad(k)];
-      mag2[q] = fma(f.x, f.x, f.y * f.y);
-      best2 = fmax(best2, mag2[q]);
+      const double m2 = fma(f.x, f.x, f.y * f.y);
+#if !CVA_MAG_REREAD
+      mag2[q] = m2;
+#endif
+      best2 = fmax(best2, m2);
     }
   }
   // block max of best2 and sums of s1 / s2 in one exchange
@@ -504,8 +516,17 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   const double thr2 = thr > 0.0 ? thrM * thrM : -1.0;  // |F|^2 >= (thr M)^2  <=>  |D| >= thr
   int cand = INT_MAX;
 #pragma unroll
-  for (int q = kMaxPer - 1; q >= 0; --q)
-    if (mag2[q] >= thr2 && t + q * kCT < N) cand = t + q * kCT;  // smallest k of this thread
+  for (int q = kMaxPer - 1; q >= 0; --q) {
+    const int k = t + q * kCT;
+#if CVA_MAG_REREAD
+    if (k < N) {
+      const double2 f = F[pad(k)];
+      if (fma(f.x, f.x, f.y * f.y) >= thr2) cand = k;  // smallest k of this thread
+    }
+#else
+    if (mag2[q] >= thr2 && k < N) cand = k;  // smallest k of this thread
+#endif
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
   __shared__ int s_cand[kCT / 32];

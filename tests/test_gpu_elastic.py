@@ -376,3 +376,21 @@ def test_approach1_slab_mode_matches_reference(cuda, reference):
     assert (g["status"] == 0).all() and (r["status"] == 0).all()
     np.testing.assert_allclose(g["distance"], r["distance"], rtol=DIST_RTOL, atol=1e-12)
     np.testing.assert_array_equal(g["t0"], r["t0"])
+
+
+@pytest.mark.parametrize("n", [64, 100, 256])
+def test_approach2_naive_correlation_matches_reference(cuda, reference, n):
+    """ElasticOptions::use_fft = false: the rigid steps run on the direct
+    per-shift sums (align_naive, rigid_align.cpp:198-202), on both sides."""
+    c1, c2 = _pairs(reference, n, 4, seed0=121)
+    g = cva.elastic_approach2_batch(c1, c2, use_fft=False)
+    r = reference.elastic_approach2_batch(c1, c2, use_fft=False, threads=4)
+    _check_vs_reference(g, r)
+
+
+def test_distance_matrix_naive_correlation(cuda, reference):
+    curves = np.stack([prep(reference, f, 64, s) for s, f in enumerate(["bumps", "clover", "limacon"], 1)])
+    d = cva.elastic_distance_matrix(curves, 2, use_fft=False)
+    i, j = np.meshgrid(np.arange(3), np.arange(3), indexing="ij")
+    r = reference.elastic_approach2_batch(curves[i.ravel()], curves[j.ravel()], use_fft=False, threads=9)
+    np.testing.assert_allclose(d.ravel(), r["distance"], rtol=DIST_RTOL, atol=1e-12)
