@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
   // one curve at a time (half the live registers): SRV of the raw samples into
   // registers, a barrier (every raw read done), then the padded write in place
   int bad = 0;
-  double2 mean[2];
+  double2 mean0 = make_double2(0, 0), mean1 = make_double2(0, 0);  // (not an array: the loop index is runtime)
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
     double2* qc = h ? qb : qa;
@@ -316,7 +316,10 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
     }
     double mz = 0.0;
     rs::block_sum3(m.x, m.y, mz, red);  // its barriers order every raw read before the writes
-    mean[h] = m;
+    if (h)
+      mean1 = m;
+    else
+      mean0 = m;
 #pragma unroll
     for (int q = 0; q < kMaxPer; ++q) {
       const int l = threadIdx.x + q * kT;
@@ -331,8 +334,8 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
       for (int l = threadIdx.x; l < N; l += kT) al[l] = make_double2(qnan(), qnan());
     return;
   }
-  const double2 m1 = mean[0];
-  const double m2x = mean[1].x, m2y = mean[1].y;
+  const double2 m1 = mean0;
+  const double m2x = mean1.x, m2y = mean1.y;
   const double invn = 1.0 / (double)N;  // srv_center (srv.cpp:90-98)
   pf::PairIn in{qa, qb, make_double2(invn * m1.x, invn * m1.y), make_double2(invn * m2x, invn * m2y), 1.0, 1.0, b};
   pf::pair_stage<kIP, kN, false, 2, kT, 2048, true>(in, bufs, N, tw, out + p, al, red);
