@@ -629,3 +629,18 @@ def test_allpairs_beyond_shared_memory(cuda, oracle, n):
             g["shift"], g["theta"], g["energy"] = k[r, j], th[r, j], e[r, j]
             g["trace"], g["t0"] = want["trace"], int(k[r, j]) / n
             check_pair(g, want, base[1 + r], base[j])
+
+
+@pytest.mark.parametrize("n", [8192, 65536])
+def test_large_n_circle_tie_band(cuda, oracle, n):
+    """A circle against itself: every shift is in the reference's tie band
+    (rigid_align.cpp:31-47), so the smallest index wins; at large N the band
+    spans every column tile of the four-step layout (all tiles scanned)."""
+    phi = 2 * PI * np.arange(n) / n
+    c = np.stack([np.cos(phi), np.sin(phi)], 1)
+    res = cva.align_fft_batch(c[None], c[None])
+    want = oracle.align(c, c)
+    assert int(want["shift"]) == 0
+    check_pair(res[0], want, c, c)
+    r2, _ = cva.preprocess_align_uniform(c[None], c[None])
+    assert int(r2["shift"][0]) == 0 and int(r2["status"][0]) == 0
