@@ -538,6 +538,24 @@ int main() {
     distance_matrix(dup, DistanceMethod::approach2, 64, {}, 1, [&](std::size_t, std::size_t, double, double) { ++calls; });
     CHECK(calls == 4);
   });
+  run("elastic use_fft = false and slab-mode sizes", [] {  // ElasticOptions (elastic.hpp:13-19)
+    const Curve c1 = preprocess(limacon(256), 64), c2 = preprocess(bumps(256), 64);
+    ElasticOptions naive;
+    naive.use_fft = false;
+    const ElasticMatch f = elastic_distance_approach2(c1, c2), g = elastic_distance_approach2(c1, c2, naive);
+    // the two correlations agree to rounding, so the searches end at the same distance
+    CHECK(std::fabs(f.distance - g.distance) <= 1e-9 * f.distance && f.iterations == g.iterations);
+    ElasticOptions steep;  // 9 <= max_slope <= 20 and n > 1024 run with the working set in global memory
+    steep.max_slope = 9;
+    steep.max_iters = 2;
+    const ElasticMatch s9 = elastic_distance_approach2(c1, c2, steep);
+    CHECK(std::isfinite(s9.distance) && s9.distance >= 0.0 && s9.iterations >= 1);
+    const Curve big1 = preprocess(limacon(1500), 1100), big2 = preprocess(bumps(1500), 1100);
+    ElasticOptions two;
+    two.max_iters = 2;
+    const ElasticMatch b = elastic_distance_approach2(big1, big2, two);
+    CHECK(std::isfinite(b.distance) && b.gamma.gamma.size() == 1101 && b.gamma.gamma.back() == 1.0);
+  });
   run("elastic batch == single", [] {
     const std::vector<Curve> a = {preprocess(bumps(200), 64), preprocess(limacon(200), 64)};
     const std::vector<Curve> b = {preprocess(hippopede(200), 64), preprocess(bumps(200), 64)};
