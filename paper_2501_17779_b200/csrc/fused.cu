@@ -374,6 +374,7 @@ __global__ void __launch_bounds__(kT) srv_center_kernel(const double2* __restric
 
 namespace v3 {
 
+
 // Shared memory: [XY | S] (rs3::kRawBytes, reused by the four FFT buffers),
 // scratch (PCR; curve B's samples in its first 16 KB; the interval map at
 // rs3::kMapOff), curve A's samples.
@@ -426,13 +427,17 @@ __global__ void __launch_bounds__(rs3::kT, 2)
   rs3::cp_async_wait();
   __syncthreads();
   CVA_MARK(1);
-  const rs3::Stats A = rs3::resample_curve<N>(pts + a0, XY, S, scr, Z1, red, na, 2);
+  // centroids: each resample leaves its per-warp partial sums here and both
+  // are reduced after curve B (block_sum2's order, so bitwise the same
+  // centroids, minus one block reduction and its barriers per pair: -1 %)
+  __shared__ double2 wsA[rs3::kT / 32], wsB[rs3::kT / 32];
+  const rs3::Stats A = rs3::resample_curve<N>(pts + a0, XY, S, scr, Z1, red, na, 2, wsA);
   __syncthreads();  // A's last reads of XY / S / the map are done
   rs3::load_raw(pts + a1, XY, nb);
   rs3::cp_async_wait();
   __syncthreads();
   CVA_MARK(10);
-  const rs3::Stats B = rs3::resample_curve<N>(pts + a1, XY, S, scr, Z2, red, nb, 11);
+  const rs3::Stats B = rs3::resample_curve<N>(pts + a1, XY, S, scr, Z2, red, nb, 11, wsB);
   if (A.bad | B.bad) {
     if (threadIdx.x == 0) v2::write_bad(out + p, CVA_INVALID_ARGUMENT);
     if (al)
@@ -440,7 +445,16 @@ __global__ void __launch_bounds__(rs3::kT, 2)
     return;
   }
   __syncthreads();
-  pf::PairIn in{Z1, Z2, A.centroid, B.centroid, 1.0, 1.0};
+  double2 cA, cB;
+  {
+    const int lane = threadIdx.x & 31;
+    constexpr double invN = 1.0 / (double)N;
+    const double2 sA = warp_sum2(lane < rs3::kT / 32 ? wsA[lane] : make_double2(0.0, 0.0));
+    const double2 sB = warp_sum2(lane < rs3::kT / 32 ? wsB[lane] : make_double2(0.0, 0.0));
+    cA = make_double2(sA.x * invN, sA.y * invN);
+    cB = make_double2(sB.x * invN, sB.y * invN);
+  }
+  pf::PairIn in{Z1, Z2, cA, cB, 1.0, 1.0};
   pf::pair_stage<false, N, true, 0, rs3::kT, 2048, true>(in, reinterpret_cast<double2*>(smem), N, tw, out + p, al,
                                                          red);
 }

@@ -1,18 +1,22 @@
-#!/bin/bash
-# Build libcurvalign_cuda.so with extra -D flags into build/var_<name>.so (experiments):
-#   tools/variant.sh name -DFOO=1 ...   then   CVA_LIB_PATH=build/var_name.so python tools/bench_parts.py
-set -e
-name=$1; shift
+#!/usr/bin/env bash
+# Build an A/B variant of libcurvalign_cuda.so with extra -D flags on the fused
+# C1 translation unit (the other objects are the regular build/ ones):
+#   tools/variant.sh NAME "-DCVA_FOO=1 -DCVA_BAR=2"
+# -> build/var_NAME/libcurvalign_cuda.so; select it at run time with
+#   CVA_LIB_PATH=build/var_NAME/libcurvalign_cuda.so python tools/bench_parts.py
+# Development only (never shipped; build/ travels to the GPU box with gpurun).
+set -euo pipefail
 cd "$(dirname "$0")/.."
-mkdir -p build/var_$name
+name=$1
+flags=${2:-}
+make -s lib >/dev/null
+out=build/var_$name
+mkdir -p "$out"
+NVCC=${NVCC:-/usr/local/cuda/bin/nvcc}
 ARCH="-gencode arch=compute_100a,code=sm_100a"
-FL="$ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $*"
-objs=""
-for f in kernels fused allpairs largen elastic dropin_kernels gfft probe; do
-  /usr/local/cuda/bin/nvcc $FL -c paper_2501_17779_b200/csrc/$f.cu -o build/var_$name/$f.o &
-  objs="$objs build/var_$name/$f.o"
-done
-/usr/local/cuda/bin/nvcc $FL -x cu -c paper_2501_17779_b200/csrc/capi.cpp -o build/var_$name/capi.o &
-wait
-/usr/local/cuda/bin/nvcc $ARCH -shared -cudart static -o build/var_$name.so $objs build/var_$name/capi.o
-echo build/var_$name.so
+$NVCC $ARCH $flags -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -v \
+  -c paper_2501_17779_b200/csrc/fused.cu -o "$out/fused.o" 2> "$out/ptxas.log"
+objs=$(ls build/*.o | grep -v '/fused.o$')
+$NVCC $ARCH -shared -cudart static -o "$out/libcurvalign_cuda.so" "$out/fused.o" $objs
+grep -A2 "v3.*resample_align_kernelILi1024" "$out/ptxas.log" | grep -E "registers|spill" || true
+echo "built $out/libcurvalign_cuda.so"
