@@ -129,6 +129,45 @@ __host__ __device__ constexpr int ptw_off_warp(int N, int Ns) {
                             : N + ptw_until<128>(N, N) + ptw_until<256>(N, N) + ptw_until_warp(N, Ns);
 }
 
+
+// Twiddles of one butterfly, v[r] *= W^(r e) for r = 1 .. R-1, where the pass
+// table holds W^(r e) at pt[(r - 1) Ns + jm]. With CVA_TW_DERIVE (default)
+// only r = 1, 2, 4 are read and W^3 = W^1 W^2, W^5 = W^1 W^4, W^6 = W^2 W^4,
+// W^7 = W^3 W^4 are formed by products of table values (at most two
+// roundings from sincospi-exact entries, no recurrence): 3 L1 reads per
+// radix-8 butterfly instead of 7, 2 instead of 3 for radix 4 (the pass
+// tables were the top L1 consumer of the transforms: C4 539.9 -> 521.6 us,
+// C1 349.7 -> 347.0 us; profiles/r4_c1_variants.txt). CVA_TW_DERIVE=0 reads
+// every twiddle.
+#ifndef CVA_TW_DERIVE
+#define CVA_TW_DERIVE 1
+#endif
+template <int R>
+__device__ __forceinline__ void twiddle(double2 (&v)[R], const double2* __restrict__ pt, int Ns, int jm) {
+#if CVA_TW_DERIVE
+  if constexpr (R == 8) {
+    const double2 w1 = __ldg(&pt[jm]), w2 = __ldg(&pt[Ns + jm]), w4 = __ldg(&pt[3 * Ns + jm]);
+    const double2 w3 = cmul(w1, w2);
+    v[1] = cmul(v[1], w1);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], w3);
+    v[4] = cmul(v[4], w4);
+    v[5] = cmul(v[5], cmul(w1, w4));
+    v[6] = cmul(v[6], cmul(w2, w4));
+    v[7] = cmul(v[7], cmul(w3, w4));
+    return;
+  } else if constexpr (R == 4) {
+    const double2 w1 = __ldg(&pt[jm]), w2 = __ldg(&pt[Ns + jm]);
+    v[1] = cmul(v[1], w1);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], cmul(w1, w2));
+    return;
+  }
+#endif
+#pragma unroll
+  for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&pt[(r - 1) * Ns + jm]));
+}
+
 // Compile-time pass: N, Ns, the butterfly count per thread and every index
 // stride are constants.
 template <int R, int NT, int N, int Ns, typename Src>
@@ -144,10 +183,7 @@ __device__ __forceinline__ void pass_ct(Src src, double2* dst, const double2* __
       const int jm = j & (Ns - 1);
 #pragma unroll
       for (int r = 0; r < R; ++r) v[r] = src(j + r * nb);
-      if (Ns > 1) {
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&pt[(r - 1) * Ns + jm]));
-      }
+      if (Ns > 1) twiddle<R>(v, pt, Ns, jm);
       dft_r<R>(v);
       const int base = (j - jm) * R + jm;
 #pragma unroll
@@ -230,10 +266,7 @@ __device__ __forceinline__ void pass_ip(Src src, double2* buf, const double2* __
     const int jm = j & (Ns - 1);
 #pragma unroll
     for (int r = 0; r < R; ++r) v[b][r] = src(j + r * nb);
-    if (Ns > 1) {
-#pragma unroll
-      for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], __ldg(&pt[(r - 1) * Ns + jm]));
-    }
+    if (Ns > 1) twiddle<R>(v[b], pt, Ns, jm);
   }
   sync();
 #pragma unroll
