@@ -1,4 +1,4 @@
-"""A/B the fused C1 kernel across library variants built by tools/variant.sh.
+"""A/B the fused C1 kernel (AB_CONFIG=c4: the SRV pair kernel) across library variants built by tools/variant.sh.
 
     python tools/ab_variants.py base jac early ...   (run on the GPU box)
 
@@ -27,18 +27,28 @@ def child(out_path: str, reps: int) -> None:
     from paper_2501_17779_b200 import _native, synth
 
     lib = _native.load()
-    pts, offs, _, _ = synth.ragged_pairs(1, 4096, 1024)
-    dp = torch.from_numpy(pts).cuda()
-    do = torch.from_numpy(offs).cuda()
-    mx = int(np.diff(offs).max())
-    P, N = 4096, 1024
-    out = torch.empty((P, 48), dtype=torch.uint8, device="cuda")
-    al = torch.empty((P, N, 2), dtype=torch.float64, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
+    if os.environ.get("AB_CONFIG", "c1") == "c4":
+        P, N = 8192, 2048
+        a, b, _, _, _ = synth.srv_pairs(1, P, N)
+        da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        out = torch.empty((P, 48), dtype=torch.uint8, device="cuda")
+        al = torch.empty((P, N, 2), dtype=torch.float64, device="cuda")
 
-    def fused():
-        _native.check(lib.cva_preprocess_align_batch(dp.data_ptr(), do.data_ptr(), P, mx, N, 1, out.data_ptr(),
-                                                     al.data_ptr(), s))
+        def fused():
+            _native.check(lib.cva_srv_align_batch(da.data_ptr(), db.data_ptr(), P, N, out.data_ptr(), al.data_ptr(), s))
+    else:
+        pts, offs, _, _ = synth.ragged_pairs(1, 4096, 1024)
+        dp = torch.from_numpy(pts).cuda()
+        do = torch.from_numpy(offs).cuda()
+        mx = int(np.diff(offs).max())
+        P, N = 4096, 1024
+        out = torch.empty((P, 48), dtype=torch.uint8, device="cuda")
+        al = torch.empty((P, N, 2), dtype=torch.float64, device="cuda")
+
+        def fused():
+            _native.check(lib.cva_preprocess_align_batch(dp.data_ptr(), do.data_ptr(), P, mx, N, 1,
+                                                         out.data_ptr(), al.data_ptr(), s))
 
     for _ in range(5):
         fused()
