@@ -194,16 +194,17 @@ __device__ __forceinline__ void pass_ct(Src src, double2* dst, const double2* __
 
 // Forward FFT of compile-time length N by NT threads, first pass through src,
 // ping-ponging dst/other. Returns the buffer holding the spectrum.
-template <int NT, int N, int Ns = 1, typename Src, typename Sync>
+// (kStop: stop before the pass whose Ns is kStop; the default runs all passes)
+template <int NT, int N, int Ns = 1, int kStop = N, typename Src, typename Sync>
 __device__ __forceinline__ double2* group_fft_ct(Src src, double2* dst, double2* other,
                                                  const double2* __restrict__ tw, int g, Sync sync) {
   constexpr int R = plan_radix<NT>(N, Ns);
   pass_ct<R, NT, N, Ns>(src, dst, tw, g);
   sync();
   CVA_MARK(40 + (NT == 256 ? 8 : 0) + (Ns == 1 ? 0 : Ns == 8 ? 1 : Ns == 64 ? 2 : Ns == 512 ? 3 : Ns == 4 ? 4 : Ns == 16 ? 5 : Ns == 256 ? 6 : 7));
-  if constexpr (Ns * R < N) {
+  if constexpr (Ns * R < N && Ns * R < kStop) {
     auto next = [dst](int i) { return dst[pad(i)]; };
-    return group_fft_ct<NT, N, Ns * R>(next, other, dst, tw, g, sync);
+    return group_fft_ct<NT, N, Ns * R, kStop>(next, other, dst, tw, g, sync);
   } else {
     return dst;
   }
@@ -283,13 +284,68 @@ __device__ __forceinline__ void pass_ip(Src src, double2* buf, const double2* __
 
 // In-place transform of compile-time length M by NT threads with the table
 // plan (plan_radix<NT>): M = 2048 gives 8, 8, 8, 4, M = 4096 8, 8, 8, 8.
-template <int NT, int M, int Ns = 1, typename Src, typename Sync>
+template <int NT, int M, int Ns = 1, int kStop = M, typename Src, typename Sync>
 __device__ __forceinline__ void fft_ip_ct(Src src, double2* buf, const double2* __restrict__ tw, int g, Sync sync) {
   constexpr int R = plan_radix<NT>(M, Ns);
   pass_ip<R, NT, M, Ns>(src, buf, tw, g, sync);
-  if constexpr (Ns * R < M) {
+  if constexpr (Ns * R < M && Ns * R < kStop) {
     auto next = [buf](int i) { return buf[pad(i)]; };
-    fft_ip_ct<NT, M, Ns * R>(next, buf, tw, g, sync);
+    fft_ip_ct<NT, M, Ns * R, kStop>(next, buf, tw, g, sync);
+  }
+}
+
+// ---- last forward pass fused into the first pass of the correlation transform
+// The correlation transform's first pass (Ns = 1, radix Rc, butterfly j reads
+// k = j + nbC r) needs exactly the outputs of the forward transforms' last
+// butterflies jb = j + nbC b (b < B), whose outputs are X[jb + NsF r'] (k's
+// r = b + B r'). So thread j runs those B radix-Rf butterflies of both curves
+// from the penultimate spectra, forms conj-products, and does its radix-Rc
+// butterfly: one shared-memory round trip of 2 N points and a barrier fewer.
+template <int NT>
+__host__ __device__ constexpr int last_pass_ns(int N) {
+  int Ns = 1;
+  while (Ns * plan_radix<NT>(N, Ns) < N) Ns *= plan_radix<NT>(N, Ns);
+  return Ns;
+}
+#ifndef CVA_FUSE_LAST
+#define CVA_FUSE_LAST 1
+#endif
+template <int NTf, int NTc, int N>
+struct FusePlan {
+  static constexpr int NsF = last_pass_ns<NTf>(N);
+  static constexpr int Rf = N / NsF;
+  static constexpr int Rc = plan_radix<NTc>(N, 1);
+  static constexpr int nbC = N / Rc;
+  static constexpr int B = NsF >= nbC ? NsF / nbC : 0;
+  static constexpr bool ok = CVA_FUSE_LAST && NsF > 1 && B >= 1 && NsF % nbC == 0 && Rc == Rf * B && nbC <= NTc;
+};
+// v[0 .. Rc) of correlation butterfly j (j < nbC): products of the forward
+// spectra finished from Y1 / Y2 (penultimate Stockham buffers, padded), scaled
+// by s12 when kScale; returned before the radix-Rc DFT.
+template <int NTf, int NTc, int N, bool kScale>
+__device__ __forceinline__ void fused_first_inputs(const double2* Y1, const double2* Y2, double s12,
+                                                   const double2* __restrict__ tw, int j,
+                                                   double2 (&v)[FusePlan<NTf, NTc, N>::Rc]) {
+  using P = FusePlan<NTf, NTc, N>;
+  const double2* __restrict__ ptf = tw + ptw_off<NTf>(N, P::NsF);  // the forward last pass's table
+#pragma unroll
+  for (int b = 0; b < P::B; ++b) {
+    const int jb = j + P::nbC * b;  // forward-last butterfly (jm = jb: jb < NsF)
+    double2 a[P::Rf], c[P::Rf];
+#pragma unroll
+    for (int r = 0; r < P::Rf; ++r) {
+      a[r] = Y1[pad(jb + r * P::NsF)];
+      c[r] = Y2[pad(jb + r * P::NsF)];
+    }
+    twiddle<P::Rf>(a, ptf, P::NsF, jb);
+    twiddle<P::Rf>(c, ptf, P::NsF, jb);
+    dft_r<P::Rf>(a);
+    dft_r<P::Rf>(c);
+#pragma unroll
+    for (int r = 0; r < P::Rf; ++r) {
+      const double2 x = cmulconj(a[dft_slot<P::Rf>(r)], c[dft_slot<P::Rf>(r)]);
+      v[b + P::B * r] = kScale ? cscale(x, s12) : x;
+    }
   }
 }
 
@@ -411,13 +467,16 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     };
     auto sync = [grp]() { named_sync(1 + grp, kH); };
     if constexpr (kInPlace) {
-      fft_ip_ct<kH, kIPM>(load, grp == 0 ? B0 : B2, tw, g, sync);
+      constexpr int stop = FusePlan<kH, kCT, kIPM>::ok ? FusePlan<kH, kCT, kIPM>::NsF : kIPM;
+      fft_ip_ct<kH, kIPM, 1, stop>(load, grp == 0 ? B0 : B2, tw, g, sync);
       X = grp == 0 ? B0 : B2;
     } else {
-      if constexpr (kN > 0)
-        X = group_fft_ct<kH, kN>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, tw, g, sync);
-      else
+      if constexpr (kN > 0) {
+        constexpr int stop = FusePlan<kH, kCT, (kN > 0 ? kN : 2)>::ok ? FusePlan<kH, kCT, (kN > 0 ? kN : 2)>::NsF : kN;
+        X = group_fft_ct<kH, kN, 1, stop>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, tw, g, sync);
+      } else {
         X = group_fft<kH>(load, grp == 0 ? B0 : B2, grp == 0 ? B1 : B3, M, tw, g, sync);
+      }
     }
   }
   PairScale psc{in.sc1, in.sc2};
@@ -465,7 +524,22 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       const double2 v = cmulconj(X1[pad(k)], X2[pad(k)]);
       return kLenOnLoad ? cscale(v, s12) : v;
     };
-    fft_ip_ct<kCT, kIPM>(prod, B0, tw, t, sync_all);
+    using FP = FusePlan<kH, kCT, kIPM>;
+    if constexpr (FP::ok) {  // in place: every load of the fused pass, a barrier, the stores
+      double2 v[FP::Rc];
+      if (t < FP::nbC) fused_first_inputs<kH, kCT, kIPM, kLenOnLoad>(X1, X2, s12, tw, t, v);
+      sync_all();
+      if (t < FP::nbC) {
+        dft_r<FP::Rc>(v);
+#pragma unroll
+        for (int r = 0; r < FP::Rc; ++r) B0[pad(t * FP::Rc + r)] = v[dft_slot<FP::Rc>(r)];
+      }
+      sync_all();
+      auto next = [B0](int i) { return B0[pad(i)]; };
+      fft_ip_ct<kCT, kIPM, FP::Rc>(next, B0, tw, t, sync_all);
+    } else {
+      fft_ip_ct<kCT, kIPM>(prod, B0, tw, t, sync_all);
+    }
     F = B0;
   } else {
     // group 0's result is B0 or B1, group 1's is B2 or B3 (same pass count)
@@ -479,10 +553,29 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       const double2 v = cmulconj(X1[pad(k)], X2[pad(k)]);
       return kLenOnLoad ? cscale(v, s12) : v;
     };
-    if constexpr (kN > 0)
-      F = group_fft_ct<kCT, kN>(prod, F0, F1, tw, t, sync_all);
-    else
+    if constexpr (kN > 0) {
+      using FP = FusePlan<kH, kCT, (kN > 0 ? kN : 2)>;
+      if constexpr (FP::ok) {
+        if (t < FP::nbC) {
+          double2 v[FP::Rc];
+          fused_first_inputs<kH, kCT, kN, kLenOnLoad>(X1, X2, s12, tw, t, v);
+          dft_r<FP::Rc>(v);
+#pragma unroll
+          for (int r = 0; r < FP::Rc; ++r) F0[pad(t * FP::Rc + r)] = v[dft_slot<FP::Rc>(r)];
+        }
+        sync_all();
+        if constexpr (FP::Rc < kN) {
+          auto next = [F0](int i) { return F0[pad(i)]; };
+          F = group_fft_ct<kCT, kN, FP::Rc>(next, F1, F0, tw, t, sync_all);
+        } else {
+          F = F0;
+        }
+      } else {
+        F = group_fft_ct<kCT, kN>(prod, F0, F1, tw, t, sync_all);
+      }
+    } else {
       F = group_fft<kCT>(prod, F0, F1, M, tw, t, sync_all);
+    }
   }
 
   CVA_MARK(21);
