@@ -358,6 +358,40 @@ __device__ inline void fft2048_ip(Src src0, double2* buf, const double2* __restr
   pass_ip<4, NT, 2048, 512>(src, buf, tw, g, sync);
 }
 
+// ---- the correlation transform's last pass into registers
+// Its butterfly j = g + b NT (Ns = N / R >= NT, jm = j) writes outputs
+// k = j + r Ns = g + NT (b + B r): thread g ends up holding exactly the bins
+// k = g + q NT the argmax reads, so they stay in registers (fv[q]) and F is
+// never stored or re-read. CVA_REG_LAST=0 keeps the stored spectrum.
+#ifndef CVA_REG_LAST
+#define CVA_REG_LAST 1
+#endif
+template <int NT, int N>
+struct RegLastPlan {
+  static constexpr int Ns = last_pass_ns<NT>(N);
+  static constexpr int R = N / Ns;
+  static constexpr int B = Ns >= NT ? Ns / NT : 0;
+  static constexpr bool ok = CVA_REG_LAST && Ns > 1 && B >= 1 && Ns % NT == 0;
+};
+template <int NT, int N, int kMax>
+__device__ __forceinline__ void last_pass_regs(const double2* src, const double2* __restrict__ tw, int g,
+                                               double2 (&fv)[kMax]) {
+  using P = RegLastPlan<NT, N>;
+  static_assert(P::B * P::R <= kMax, "bins per thread");
+  const double2* __restrict__ pt = tw + ptw_off<NT>(N, P::Ns);
+#pragma unroll
+  for (int b = 0; b < P::B; ++b) {
+    const int j = g + b * NT;
+    double2 v[P::R];
+#pragma unroll
+    for (int r = 0; r < P::R; ++r) v[r] = src[pad(j + r * P::Ns)];
+    twiddle<P::R>(v, pt, P::Ns, j);
+    dft_r<P::R>(v);
+#pragma unroll
+    for (int r = 0; r < P::R; ++r) fv[b + P::B * r] = v[dft_slot<P::R>(r)];
+  }
+}
+
 __device__ __forceinline__ double qnan() { return __longlong_as_double(0x7ff8000000000000ULL); }
 
 struct PairIn {
@@ -515,7 +549,12 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   CVA_MARK(20);
   // ---- D_m = sum_l conj(z1_l) z2_{l+m} = IDFT(conj Z1 . Z2)_m = conj(FFT(Z1 conj Z2)_m) / N
   auto sync_all = []() { __syncthreads(); };
-  const double2* F;
+  const double2* F = nullptr;
+  constexpr int kMaxPer = kInPlace ? 8 : 4;  // N <= 2048 in-place, N <= 1024 otherwise
+  constexpr int kNc = kInPlace ? kIPM : (kN > 0 ? kN : 2);  // compile-time transform length (if any)
+  constexpr bool kRegLast = (kInPlace || kN > 0) && FusePlan<kH, kCT, kNc>::ok && RegLastPlan<kCT, kNc>::ok &&
+                            RegLastPlan<kCT, kNc>::Ns >= FusePlan<kH, kCT, kNc>::Rc;
+  double2 fv[kMaxPer];  // kRegLast: bins t + q kCT of the correlation spectrum
   if constexpr (kInPlace) {
     const double2* X1 = B0;
     const double2* X2 = B2;
@@ -536,7 +575,13 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       }
       sync_all();
       auto next = [B0](int i) { return B0[pad(i)]; };
-      fft_ip_ct<kCT, kIPM, FP::Rc>(next, B0, tw, t, sync_all);
+      if constexpr (kRegLast) {  // all passes but the last in place, the last into registers
+        if constexpr (FP::Rc < RegLastPlan<kCT, kIPM>::Ns)
+          fft_ip_ct<kCT, kIPM, FP::Rc, RegLastPlan<kCT, kIPM>::Ns>(next, B0, tw, t, sync_all);
+        last_pass_regs<kCT, kIPM>(B0, tw, t, fv);
+      } else {
+        fft_ip_ct<kCT, kIPM, FP::Rc>(next, B0, tw, t, sync_all);
+      }
     } else {
       fft_ip_ct<kCT, kIPM>(prod, B0, tw, t, sync_all);
     }
@@ -564,7 +609,14 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
           for (int r = 0; r < FP::Rc; ++r) F0[pad(t * FP::Rc + r)] = v[dft_slot<FP::Rc>(r)];
         }
         sync_all();
-        if constexpr (FP::Rc < kN) {
+        if constexpr (kRegLast) {  // all passes but the last, then the last into registers
+          const double2* P = F0;
+          if constexpr (FP::Rc < RegLastPlan<kCT, kNc>::Ns) {
+            auto next = [F0](int i) { return F0[pad(i)]; };
+            P = group_fft_ct<kCT, kN, FP::Rc, RegLastPlan<kCT, kNc>::Ns>(next, F1, F0, tw, t, sync_all);
+          }
+          last_pass_regs<kCT, kNc>(P, tw, t, fv);
+        } else if constexpr (FP::Rc < kN) {
           auto next = [F0](int i) { return F0[pad(i)]; };
           F = group_fft_ct<kCT, kN, FP::Rc>(next, F1, F0, tw, t, sync_all);
         } else {
@@ -583,7 +635,6 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   // |D_m| = |F_m| / M. The max and the band test run on squared magnitudes,
   // each thread's |F|^2 values read once into registers; the band threshold is
   // formed exactly as the reference does (on |D|).
-  constexpr int kMaxPer = kInPlace ? 8 : 4;  // N <= 2048 in-place, N <= 1024 otherwise
   const double invN = 1.0 / (double)N;  // h = 1/N (rigid_align.cpp:56)
   const double invM = 1.0 / (double)M;  // D_m = conj(F_m) / M
   // CVA_MAG_REREAD=1 recomputes the magnitudes from shared memory for the band
@@ -603,7 +654,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     mag2[q] = -1.0;
 #endif
     if (k < N) {
-      const double2 f = F[pad(k)];
+      const double2 f = kRegLast ? fv[q] : F[pad(k)];
       const double m2 = fma(f.x, f.x, f.y * f.y);
 #if !CVA_MAG_REREAD
       mag2[q] = m2;
@@ -642,33 +693,52 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
   const double thrM = thr * (double)M;
   const double thr2 = thr > 0.0 ? thrM * thrM : -1.0;  // |F|^2 >= (thr M)^2  <=>  |D| >= thr
   int cand = INT_MAX;
+  double2 fc = make_double2(0.0, 0.0);  // kRegLast: F at this thread's candidate
 #pragma unroll
   for (int q = kMaxPer - 1; q >= 0; --q) {
     const int k = t + q * kCT;
 #if CVA_MAG_REREAD
     if (k < N) {
-      const double2 f = F[pad(k)];
-      if (fma(f.x, f.x, f.y * f.y) >= thr2) cand = k;  // smallest k of this thread
+      const double2 f = kRegLast ? fv[q] : F[pad(k)];
+      if (fma(f.x, f.x, f.y * f.y) >= thr2) {  // smallest k of this thread
+        cand = k;
+        fc = f;
+      }
     }
 #else
-    if (mag2[q] >= thr2 && k < N) cand = k;  // smallest k of this thread
+    if (mag2[q] >= thr2 && k < N) {  // smallest k of this thread
+      cand = k;
+      if constexpr (kRegLast) fc = fv[q];
+    }
 #endif
   }
+  const int cand_t = cand;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) cand = min(cand, __shfl_xor_sync(0xffffffffu, cand, o));
   __shared__ int s_cand[kCT / 32];
+  __shared__ double2 s_fc[kRegLast ? kCT / 32 : 1];
+  if constexpr (kRegLast) {  // the warp's candidate bin travels with its index
+    const unsigned own = __ballot_sync(0xffffffffu, cand_t == cand && cand != INT_MAX);
+    const int src = own ? __ffs(own) - 1 : 0;
+    const double fx = __shfl_sync(0xffffffffu, fc.x, src), fy = __shfl_sync(0xffffffffu, fc.y, src);
+    if (lane == 0) s_fc[wid] = make_double2(fx, fy);
+  }
   if (lane == 0) s_cand[wid] = cand;
   __syncthreads();
-  int m = INT_MAX;
+  int m = INT_MAX, wm = 0;
 #pragma unroll
-  for (int w = 0; w < kCT / 32; ++w) m = min(m, s_cand[w]);
+  for (int w = 0; w < kCT / 32; ++w)
+    if (s_cand[w] < m) {
+      m = s_cand[w];
+      wm = w;
+    }
   const bool ok = isfinite(best) && best2 >= 0.0 && m != INT_MAX;
   // rotation straight from D_m: (cos, sin) = (Re D, Im D) / |D| (every thread)
   double2 rot = make_double2(qnan(), qnan());
   double trace = 0.0;
   double2 fm = make_double2(0.0, 0.0);
   if (ok) {
-    fm = F[pad(m)];
+    fm = kRegLast ? s_fc[wm] : F[pad(m)];
     const double a2 = fma(fm.x, fm.x, fm.y * fm.y);
     trace = sqrt(a2) * invM;
     if (a2 > 0.0) {
