@@ -45,6 +45,28 @@ constexpr int kRowTile = CVA_AP_ROWS;
 #ifndef CVA_AP_MINB
 #define CVA_AP_MINB 1
 #endif
+// twiddles W^3, W^5, W^6, W^7 of the radix-8 passes 2 and 3 formed from
+// W^1, W^2, W^4 (3 shared reads per butterfly instead of 7; the kernel is
+// bound by shared / L1 wavefronts)
+#ifndef CVA_AP_TW_DERIVE
+#define CVA_AP_TW_DERIVE 1
+#endif
+// w[0..6] = W^1..W^7 of one butterfly from the [r - 1][stride] table column
+template <int kStride>
+__device__ __forceinline__ void tw8(const double2 (*t)[kStride], int col, double2 (&w)[7]) {
+#if CVA_AP_TW_DERIVE
+  w[0] = t[0][col];
+  w[1] = t[1][col];
+  w[3] = t[3][col];
+  w[2] = cmul(w[0], w[1]);
+  w[4] = cmul(w[0], w[3]);
+  w[5] = cmul(w[1], w[3]);
+  w[6] = cmul(w[2], w[3]);
+#else
+#pragma unroll
+  for (int r = 0; r < 7; ++r) w[r] = t[r][col];
+#endif
+}
 
 __device__ __forceinline__ int pad(int i) { return i + (i >> 3); }
 
@@ -210,6 +232,10 @@ __global__ void __launch_bounds__(kWarps * 32, CVA_AP_MINB)
       __syncwarp();
       warp_load<kM, kR>(v, buf, lane);
       __syncwarp();
+#if !CVA_AP_TW_REG
+      double2 w2[7];
+      tw8<8>(s_t2, lane & 7, w2);
+#endif
 #pragma unroll
       for (int b = 0; b < kB; ++b) {
 #pragma unroll
@@ -217,7 +243,7 @@ __global__ void __launch_bounds__(kWarps * 32, CVA_AP_MINB)
 #if CVA_AP_TW_REG
           v[b][r] = cmul(v[b][r], t2r[r - 1]);
 #else
-          v[b][r] = cmul(v[b][r], s_t2[r - 1][lane & 7]);
+          v[b][r] = cmul(v[b][r], w2[r - 1]);
 #endif
         dft_r<kR>(v[b]);
       }
@@ -226,12 +252,14 @@ __global__ void __launch_bounds__(kWarps * 32, CVA_AP_MINB)
       warp_load<kM, kR>(v, buf, lane);
 #pragma unroll
       for (int b = 0; b < kB; ++b) {
-#pragma unroll
-        for (int r = 1; r < kR; ++r)
 #if CVA_AP_TW_REG
-          v[b][r] = cmul(v[b][r], t3r[b][r - 1]);
+#pragma unroll
+        for (int r = 1; r < kR; ++r) v[b][r] = cmul(v[b][r], t3r[b][r - 1]);
 #else
-          v[b][r] = cmul(v[b][r], s_t3[r - 1][lane + 32 * b]);
+        double2 w3[7];
+        tw8<64>(s_t3, lane + 32 * b, w3);
+#pragma unroll
+        for (int r = 1; r < kR; ++r) v[b][r] = cmul(v[b][r], w3[r - 1]);
 #endif
         dft_r<kR>(v[b]);
       }

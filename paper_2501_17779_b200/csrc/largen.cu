@@ -382,10 +382,7 @@ __device__ __forceinline__ void wpass(double2* x, const double2* __restrict__ tw
       const int jm = j & (Ns - 1);
 #pragma unroll
       for (int r = 0; r < R; ++r) v[b][r] = x[padL(j + r * nb)];
-      if (Ns > 1) {
-#pragma unroll
-        for (int r = 1; r < R; ++r) v[b][r] = cmul(v[b][r], __ldg(&pt[(r - 1) * Ns + jm]));
-      }
+      if (Ns > 1) pf::twiddle<R>(v[b], pt, Ns, jm);  // (W^3, W^5..7 from W^1, W^2, W^4)
     }
   }
   __syncwarp();
