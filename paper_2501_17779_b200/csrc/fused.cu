@@ -255,6 +255,9 @@ __global__ void __launch_bounds__(kT4, 1)
 // memory into the padded layout the first transform pass reads (the input
 // buffers of that pass: in place at M = 2048, the ping-pong partner
 // otherwise), and the aligned output recomputes q2 from the raw curve (L2).
+#ifndef CVA_SRV_TMA_RAW
+#define CVA_SRV_TMA_RAW 1
+#endif
 template <bool kIP, int kN>
 __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
     srv_align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
@@ -338,6 +341,9 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
   const double m2x = mean1.x, m2y = mean1.y;
   const double invn = 1.0 / (double)N;  // srv_center (srv.cpp:90-98)
   pf::PairIn in{qa, qb, make_double2(invn * m1.x, invn * m1.y), make_double2(invn * m2x, invn * m2y), 1.0, 1.0, b};
+#if CVA_SRV_TMA_RAW
+  in.bar = &mbar;  // phase 0 was the input copies
+#endif
   pf::pair_stage<kIP, kN, false, 2, kT, 2048, true>(in, bufs, N, tw, out + p, al, red);
 }
 

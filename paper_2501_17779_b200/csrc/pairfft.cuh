@@ -402,6 +402,11 @@ struct PairIn {
   // optional: the raw curve whose SRV z2 holds (global memory); the aligned
   // output then recomputes z2[j] = srv_at(srv2, j) because z2 was overwritten
   const double2* srv2 = nullptr;
+  // optional (with srv2, in-place M = 2048 with the fused first pass): a CTA
+  // mbarrier initialised for one arrival whose next phase is 1; the raw curve
+  // srv2 is then copied back into curve 2's transform buffer by TMA once that
+  // buffer is dead, and the aligned output reads it from shared memory
+  uint64_t* bar = nullptr;
 };
 
 // q_l = d_l / sqrt(|d_l|), d_l = (N/2)(c[l+1] - c[l-1]); 0 if |d_l| < 1e-8 N (srv.cpp:71-88)
@@ -568,6 +573,19 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
       double2 v[FP::Rc];
       if (t < FP::nbC) fused_first_inputs<kH, kCT, kIPM, kLenOnLoad>(X1, X2, s12, tw, t, v);
       sync_all();
+      if (kDirectOut && t == 0 && in.srv2 && in.bar && aligned != nullptr) {
+        // B2 is dead from here on: the raw curve 2 comes back into it under
+        // the remaining passes (its SRV is recomputed for the aligned output)
+        const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(in.bar));
+        const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(B2));
+        const uint32_t bytes = (uint32_t)N * 16u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         dst),
+                     "l"(in.srv2), "r"(bytes), "r"(b)
+                     : "memory");
+      }
       if (t < FP::nbC) {
         dft_r<FP::Rc>(v);
 #pragma unroll
@@ -754,11 +772,26 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     const double2 c = in.g2;
     const double sc = psc.sc2;
     const int mm = ok ? m : 0;
+    const double2* raw2 = in.srv2;
+    if constexpr (kInPlace && FusePlan<kH, kCT, kIPM>::ok) {
+      if (in.srv2 && in.bar) {  // the copy issued after the fused first pass (phase 1)
+        const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(in.bar));
+        uint32_t done = 0;
+        do {
+          asm volatile(
+              "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 1;\n selp.u32 %0, 1, 0, p;\n}"
+              : "=r"(done)
+              : "r"(b)
+              : "memory");
+        } while (!done);
+        raw2 = B2;
+      }
+    }
 #pragma unroll
     for (int q = 0; q < kMaxPer; ++q) {
       const int j = t + q * kCT;
       if (j < N) {
-        const double2 z = in.srv2 ? srv_at(in.srv2, j, N) : in.z2[kPad == 2 ? j + (j >> 3) : j];
+        const double2 z = in.srv2 ? srv_at(raw2, j, N) : in.z2[kPad == 2 ? j + (j >> 3) : j];
         const double2 pz = make_double2((z.x - c.x) * sc, (z.y - c.y) * sc);
         int l = j - mm;
         if (l < 0) l += N;
