@@ -412,13 +412,34 @@ struct PairIn {
 // q_l = d_l / sqrt(|d_l|), d_l = (N/2)(c[l+1] - c[l-1]); 0 if |d_l| < 1e-8 N (srv.cpp:71-88)
 // (MUFU-seeded sqrt / reciprocal with one correction step, <= 1 ulp each: the
 // IEEE sqrt and division slow paths were a visible share of the C4 kernel)
+#ifndef CVA_SRV_RSQ2
+#define CVA_SRV_RSQ2 1
+#endif
+// refined reciprocal square root (MUFU seed + one third-order step, ~2^-56)
+__device__ __forceinline__ double rsqrt_ref(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x * r, r, 1.0);
+  return fma(r * e, fma(0.375, e, 0.5), r);
+}
 __device__ __forceinline__ double2 srv_at(const double2* c, int l, int N) {
   const double nn = (double)N;
   const double2 nx = c[l + 1 == N ? 0 : l + 1], pv = c[l == 0 ? N - 1 : l - 1];
   const double2 d = make_double2((nn / 2.0) * (nx.x - pv.x), (nn / 2.0) * (nx.y - pv.y));
+#if CVA_SRV_RSQ2
+  // q = d |d|^(-1/2) from two refined rsqrts: |d| = x rsqrt(x), then
+  // rsqrt(|d|) (each <= ~1 ulp; 9 FP64 operations fewer than sqrt, sqrt and
+  // a reciprocal). x = 0 gives |d| = NaN, which the threshold test maps to 0
+  // like the reference's |d| = 0 < 1e-8 N.
+  const double x = fma(d.x, d.x, d.y * d.y);
+  const double mag = x * rsqrt_ref(x);
+  if (!(mag >= 1e-8 * nn)) return make_double2(0.0, 0.0);
+  const double r = rsqrt_ref(mag);
+#else
   const double mag = fsqrt(fma(d.x, d.x, d.y * d.y));
   if (mag < 1e-8 * nn) return make_double2(0.0, 0.0);
   const double r = frcp(fsqrt(mag));
+#endif
   return make_double2(r * d.x, r * d.y);
 }
 
