@@ -20,8 +20,11 @@ units=${3:-fused}
 mine=""
 skip="^$"
 for u in $units; do
+  src=paper_2501_17779_b200/csrc/$u.cu
+  xcu=""
+  if [ "$u" = capi ]; then src=paper_2501_17779_b200/csrc/capi.cpp; xcu="-x cu"; fi
   $NVCC $ARCH $flags -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -Xptxas -v \
-    -c paper_2501_17779_b200/csrc/$u.cu -o "$out/$u.o" 2>> "$out/ptxas.log"
+    $xcu -c $src -o "$out/$u.o" 2>> "$out/ptxas.log"
   mine="$mine $out/$u.o"
   skip="$skip|/$u.o$"
 done
