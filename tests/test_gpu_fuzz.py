@@ -127,3 +127,44 @@ def test_random_approach2(cuda, reference, seed):
     np.testing.assert_array_equal(g["status"], r["status"])
     np.testing.assert_allclose(g["distance"], r["distance"], rtol=1e-9, atol=1e-12)
     np.testing.assert_array_equal(g["iterations"], r["iterations"])
+
+
+# Every transform plan of the pair stage (pairfft.cuh): compile-time N = 256 ..
+# 2048 (fused last-forward / first-correlation pass, correlation bins kept in
+# registers for the argmax), runtime N with an in-place M = 2048 plan, the
+# M = 4096 kernel, and the SRV kernel with its aligned output (the raw curve 2
+# brought back by TMA in the in-place plan).
+@pytest.mark.parametrize("n", [256, 512, 1024, 2048, 1000, 1500, 2000])
+def test_pair_stage_plans_align(cuda, oracle, n):
+    rng = np.random.default_rng(5000 + n)
+    pairs = 4
+    c1 = np.stack([oracle.preprocess(star(rng, 700, 9), n) for _ in range(pairs)])
+    c2 = np.stack([oracle.preprocess(star(rng, 800, 9), n) for _ in range(pairs)])
+    res, al = cva.align_fft_batch(c1, c2, return_aligned=True)
+    for p in range(pairs):
+        want = oracle.align(c1[p], c2[p])
+        cth, sth = np.cos(want["theta"]), np.sin(want["theta"])
+        q = c2[p][(np.arange(n) + int(want["shift"])) % n]
+        wal = np.stack([cth * q[:, 0] + sth * q[:, 1], -sth * q[:, 0] + cth * q[:, 1]], 1)
+        check_pair(res[p], want, c1[p], c2[p], al[p], wal)
+
+
+@pytest.mark.parametrize("n", [512, 1024, 2048, 1000, 1500])
+@pytest.mark.parametrize("with_aligned", [True, False])
+def test_pair_stage_plans_srv(cuda, oracle, n, with_aligned):
+    rng = np.random.default_rng(6000 + n)
+    pairs = 3
+    c1 = np.stack([oracle.preprocess(star(rng, 900, 10), n) for _ in range(pairs)])
+    c2 = np.stack([oracle.preprocess(star(rng, 1000, 10), n) for _ in range(pairs)])
+    res, alq = cva.srv_align_batch(c1, c2, return_aligned=with_aligned)
+    for p in range(pairs):
+        q1 = oracle.srv_center(oracle.srv_transform(c1[p]))
+        q2 = oracle.srv_center(oracle.srv_transform(c2[p]))
+        want = oracle.align(q1, q2)
+        cth, sth = np.cos(want["theta"]), np.sin(want["theta"])
+        q = q2[(np.arange(n) + int(want["shift"])) % n]
+        wal = np.stack([cth * q[:, 0] + sth * q[:, 1], -sth * q[:, 0] + cth * q[:, 1]], 1)
+        if with_aligned:
+            check_pair(res[p], want, q1, q2, alq[p], wal)
+        else:
+            check_pair(res[p], want, q1, q2)
