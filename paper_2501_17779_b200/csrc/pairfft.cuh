@@ -155,17 +155,17 @@ __device__ __forceinline__ void twiddle(double2 (&v)[R], const double2* __restri
     v[5] = cmul(v[5], cmul(w1, w4));
     v[6] = cmul(v[6], cmul(w2, w4));
     v[7] = cmul(v[7], cmul(w3, w4));
-    return;
   } else if constexpr (R == 4) {
     const double2 w1 = __ldg(&pt[jm]), w2 = __ldg(&pt[Ns + jm]);
     v[1] = cmul(v[1], w1);
     v[2] = cmul(v[2], w2);
     v[3] = cmul(v[3], cmul(w1, w2));
-    return;
-  }
+  } else
 #endif
+  {
 #pragma unroll
-  for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&pt[(r - 1) * Ns + jm]));
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], __ldg(&pt[(r - 1) * Ns + jm]));
+  }
 }
 
 // Compile-time pass: N, Ns, the butterfly count per thread and every index
@@ -480,6 +480,11 @@ __host__ __device__ inline int fft_len(int N) {
 // (the resampler's and the transform buffers' layout); 2 = in.z1 and in.z2 both.
 // kDirectOut: `aligned` never aliases in.z2 (shared z2 or srv2, global output),
 // so the aligned curve is written as it is formed (no register copy, no barrier).
+// Compile-time plans (kN > 0 or kInPlace) run the forward transforms up to
+// their last pass, fuse that pass into the correlation transform's first
+// (FusePlan), and keep the correlation's last-pass bins in registers for the
+// argmax (RegLastPlan); runtime-N out-of-place plans run every pass through
+// shared memory.
 template <bool kInPlace = false, int kN = 0, bool kLenOnLoad = false, int kPad = 0, int kCT = kT, int kIPM = 2048,
           bool kDirectOut = false>
 __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
