@@ -67,8 +67,16 @@ template <int NT>
 #ifndef CVA_R8_MIN
 #define CVA_R8_MIN 8
 #endif
+// CVA_R16_2048: the 128-thread plan of N = 2048 (16 points per thread: the
+// forward transforms of the in-place SRV / N = 2048 pair kernels) is 16, 16, 8
+// instead of 8, 8, 8, 4: one in-place pass fewer, same 16 values per thread.
+#ifndef CVA_R16_2048
+#define CVA_R16_2048 1
+#endif
 __host__ __device__ constexpr int plan_radix(int N, int Ns) {
-  return ((N / Ns) % 8 == 0 && N / NT >= CVA_R8_MIN) ? 8 : ((N / Ns) % 4 == 0 ? 4 : 2);
+  return (CVA_R16_2048 && NT == 128 && N == 2048 && (N / Ns) % 16 == 0)
+             ? 16
+             : (((N / Ns) % 8 == 0 && N / NT >= CVA_R8_MIN) ? 8 : ((N / Ns) % 4 == 0 ? 4 : 2));
 }
 
 
@@ -142,6 +150,9 @@ __host__ __device__ constexpr int ptw_off_warp(int N, int Ns) {
 #ifndef CVA_TW_DERIVE
 #define CVA_TW_DERIVE 1
 #endif
+#ifndef CVA_TW_DERIVE16
+#define CVA_TW_DERIVE16 1
+#endif
 template <int R>
 __device__ __forceinline__ void twiddle(double2 (&v)[R], const double2* __restrict__ pt, int Ns, int jm) {
 #if CVA_TW_DERIVE
@@ -155,6 +166,25 @@ __device__ __forceinline__ void twiddle(double2 (&v)[R], const double2* __restri
     v[5] = cmul(v[5], cmul(w1, w4));
     v[6] = cmul(v[6], cmul(w2, w4));
     v[7] = cmul(v[7], cmul(w3, w4));
+  } else if constexpr (R == 16 && CVA_TW_DERIVE16) {
+    const double2 w1 = __ldg(&pt[jm]), w2 = __ldg(&pt[Ns + jm]), w4 = __ldg(&pt[3 * Ns + jm]),
+                  w8 = __ldg(&pt[7 * Ns + jm]);
+    const double2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
+    v[1] = cmul(v[1], w1);
+    v[2] = cmul(v[2], w2);
+    v[3] = cmul(v[3], w3);
+    v[4] = cmul(v[4], w4);
+    v[5] = cmul(v[5], w5);
+    v[6] = cmul(v[6], w6);
+    v[7] = cmul(v[7], w7);
+    v[8] = cmul(v[8], w8);
+    v[9] = cmul(v[9], cmul(w1, w8));
+    v[10] = cmul(v[10], cmul(w2, w8));
+    v[11] = cmul(v[11], cmul(w3, w8));
+    v[12] = cmul(v[12], cmul(w4, w8));
+    v[13] = cmul(v[13], cmul(w5, w8));
+    v[14] = cmul(v[14], cmul(w6, w8));
+    v[15] = cmul(v[15], cmul(w7, w8));
   } else if constexpr (R == 4) {
     const double2 w1 = __ldg(&pt[jm]), w2 = __ldg(&pt[Ns + jm]);
     v[1] = cmul(v[1], w1);
