@@ -258,6 +258,9 @@ __global__ void __launch_bounds__(kT4, 1)
 #ifndef CVA_SRV_TMA_RAW
 #define CVA_SRV_TMA_RAW 1
 #endif
+#ifndef CVA_SRV_KEEP_Q
+#define CVA_SRV_KEEP_Q 1
+#endif
 template <bool kIP, int kN>
 __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
     srv_align_kernel(const double2* __restrict__ c1, const double2* __restrict__ c2, int N,
@@ -302,6 +305,9 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
   // registers, a barrier (every raw read done), then the padded write in place
   int bad = 0;
   double2 mean0 = make_double2(0, 0), mean1 = make_double2(0, 0);  // (not an array: the loop index is runtime)
+  // the in-place plan brings q2 back by TMA for the aligned output: park it in
+  // this pair's aligned rows (L2-resident, overwritten at the end)
+  double2* const keep = (CVA_SRV_KEEP_Q && CVA_SRV_TMA_RAW && kIP && aligned) ? aligned + p * N : nullptr;
 #pragma unroll 1
   for (int h = 0; h < 2; ++h) {
     double2* qc = h ? qb : qa;
@@ -314,6 +320,7 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
         const double2 u = qc[l];
         bad |= !(isfinite(u.x) && isfinite(u.y));
         x[q] = pf::srv_at(qc, l, N);
+        if (h && keep) keep[l] = x[q];
         m = cadd(m, x[q]);
       }
     }
@@ -343,6 +350,10 @@ __global__ void __launch_bounds__(kT, kIP ? 2 : 3)
   pf::PairIn in{qa, qb, make_double2(invn * m1.x, invn * m1.y), make_double2(invn * m2x, invn * m2y), 1.0, 1.0, b};
 #if CVA_SRV_TMA_RAW
   in.bar = &mbar;  // phase 0 was the input copies
+  if (keep) {  // the generic stores of q2 before the async-proxy read of them
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    in.q2_in_aligned = true;
+  }
 #endif
   pf::pair_stage<kIP, kN, false, 2, kT, 2048, true>(in, bufs, N, tw, out + p, al, red);
 }

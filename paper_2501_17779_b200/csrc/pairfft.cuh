@@ -437,6 +437,10 @@ struct PairIn {
   // srv2 is then copied back into curve 2's transform buffer by TMA once that
   // buffer is dead, and the aligned output reads it from shared memory
   uint64_t* bar = nullptr;
+  // optional (with bar): q2 = SRV(curve 2) already sits in `aligned` (natural
+  // order, written by the caller before the transforms); the TMA then brings
+  // q2 itself back and the aligned output does not recompute it
+  bool q2_in_aligned = false;
 };
 
 // q_l = d_l / sqrt(|d_l|), d_l = (N/2)(c[l+1] - c[l-1]); 0 if |d_l| < 1e-8 N (srv.cpp:71-88)
@@ -639,7 +643,7 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                          dst),
-                     "l"(in.srv2), "r"(bytes), "r"(b)
+                     "l"(in.q2_in_aligned ? (const double2*)aligned : in.srv2), "r"(bytes), "r"(b)
                      : "memory");
       }
       if (t < FP::nbC) {
@@ -847,7 +851,8 @@ __device__ inline void pair_stage(const PairIn& in, double2* bufs, int N,
     for (int q = 0; q < kMaxPer; ++q) {
       const int j = t + q * kCT;
       if (j < N) {
-        const double2 z = in.srv2 ? srv_at(raw2, j, N) : in.z2[kPad == 2 ? j + (j >> 3) : j];
+        const double2 z = in.srv2 ? (raw2 == B2 && in.q2_in_aligned ? B2[j] : srv_at(raw2, j, N))
+                                  : in.z2[kPad == 2 ? j + (j >> 3) : j];
         const double2 pz = make_double2((z.x - c.x) * sc, (z.y - c.y) * sc);
         int l = j - mm;
         if (l < 0) l += N;
